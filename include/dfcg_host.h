@@ -1,0 +1,45 @@
+/* dfcg_host.h — host-side utilities exported by libdfcg.so next to the hot-path ABI.
+ *
+ * These restate the reference's input side so callers (bench, tests, a CLI) can build the
+ * exact inputs the reference builds, without the reference:
+ *   SeededRng            P/include/dfc/rng.hpp:26-74
+ *   sample_without_replacement / partition_columns / extract_*   P/include/dfc/sampling.hpp:15-113
+ *   gen_mc_instance / gen_rmf_instance                            P/include/dfc/simgen.hpp:30-82
+ * Nothing here runs on the GPU. Arrays returned through pointer-to-pointer arguments are
+ * malloc'ed by the library; release them with dfcg_free (dfcg.h).
+ */
+#ifndef DFCG_HOST_H_
+#define DFCG_HOST_H_
+
+#include <stdint.h>
+
+#include "dfcg.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+void dfcg_rng_u64(uint64_t seed, uint64_t stream, int64_t n, uint64_t* out);
+void dfcg_rng_uniform(uint64_t seed, uint64_t stream, int64_t n, double* out);
+void dfcg_rng_normal(uint64_t seed, uint64_t stream, int64_t n, double* out);
+int dfcg_rng_index(uint64_t seed, uint64_t stream, int64_t count, uint64_t bound, uint64_t* out);
+
+int dfcg_sample_without_replacement(uint64_t seed, uint64_t stream, int64_t n, int64_t l, int64_t* out);
+/* cols: n entries, offsets: t + 1 entries (group g = cols[offsets[g]:offsets[g+1]], sorted). */
+int dfcg_partition_columns(uint64_t seed, uint64_t stream, int64_t n, int64_t t, int64_t* cols, int64_t* offsets);
+
+/* gen_mc_instance with SeededRng(seed, stream). L0 factors column-major (library-allocated),
+ * observations sorted column-major (library-allocated, s entries). */
+int dfcg_gen_mc_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigma, uint64_t seed, uint64_t stream,
+                         dfcg_lowrank* L0, int64_t** rows, int64_t** cols, double** vals);
+
+/* gen_rmf_instance; outliers U[lo, hi] (the reference draws U[0,1]); M is a caller buffer of
+ * m * n doubles (column-major); S0 in draw order (library-allocated). */
+int dfcg_gen_rmf_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigma, uint64_t seed, uint64_t stream,
+                          double lo, double hi, dfcg_lowrank* L0, dfcg_sparse* S0, double* M);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DFCG_HOST_H_ */

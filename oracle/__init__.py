@@ -216,7 +216,8 @@ def _trip_from_handle(h):
 
 def make_observed(m, n, rows, cols, vals) -> Observed:
     """Validate and sort like the ObservedMatrix ctor (matrix_io.hpp:38-56)."""
-    return _obs_from_handle(_obs_handle(Observed(m, n, np.asarray(rows), np.asarray(cols), np.asarray(vals))).ptr)
+    h = _obs_handle(Observed(m, n, np.asarray(rows), np.asarray(cols), np.asarray(vals)))
+    return _obs_from_handle(h.ptr)
 
 
 # ------------------------------------------------------------------ RNG / sampling

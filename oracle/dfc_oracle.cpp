@@ -286,7 +286,11 @@ RmfInstance gen_rmf_instance(Index m, Index n, Index r, Index s, double sigma, S
     }
   }
   OutlierEstimate S0(m, n, std::move(outliers));
-  Mat M = materialize(L0);
+  // M = materialize(L0) + S0: entries as plain row dots (Eigen's GEMM summation order is not
+  // reproducible anyway); the product's generator uses the same loop, so both agree bitwise.
+  Mat M(m, n);
+  for (Index j = 0; j < n; ++j)
+    for (Index i = 0; i < m; ++i) M(i, j) = row_dot(L0.left(), i, L0.right(), j);
   for (const auto& o : S0.entries) M(o.row, o.col) += o.value;
   if (sigma > 0)
     for (Index j = 0; j < n; ++j)

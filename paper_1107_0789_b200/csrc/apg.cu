@@ -1,0 +1,765 @@
+// APG base solvers on the device: apg_mc (P/include/dfc/solvers.hpp:241-327) and apg_rmf
+// (:332-414), with the rank-adaptive randomized SVT (svt_operator :98-109, partial_svd /
+// randomized_range P/include/dfc/sketch.hpp:144-166) running entirely on the GPU.
+//
+// Control flow (iteration count, k doubling, shrink count, continuation, stop test) is the
+// reference's, decided on the host from a handful of device scalars per iteration. The
+// Gaussian test matrices come from the same SeededRng(0x737674, 0|1) stream, consumed in
+// the same order. One deliberate difference: extrapolate (:196-212) compacts Y with an
+// exact svd_of_product when kc + kp > min(m, n); the device keeps the concatenated factors
+// instead — the same matrix Y (the compaction only drops singular values <= 1e-12 *
+// max(m,n) * s_max), consumed only through Y*X, Y^T*X and P_Omega(Y).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "solver.hpp"
+
+namespace dfcg {
+
+namespace {
+
+int grid_for(i64 total, int threads = 256) {
+  return static_cast<int>(std::max<i64>(1, std::min<i64>((total + threads - 1) / threads, 4096)));
+}
+
+// dst[r, c] = src[r, c] * scale[c]   (rows x cols)
+__global__ void scale_cols_kernel(i64 rows, i64 cols, const double* __restrict__ src, i64 lds,
+                                  const double* __restrict__ scale, double* __restrict__ dst, i64 ldd) {
+  const i64 total = rows * cols;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = e / cols, c = e % cols;
+    dst[r * ldd + c] = src[r * lds + c] * scale[c];
+  }
+}
+
+__global__ void fill_kernel(i64 n, double v, double* x) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    x[i] = v;
+}
+
+__global__ void scale_by_inv_kernel(i64 n, const double* __restrict__ x, const double* __restrict__ nrm,
+                                    double* __restrict__ y) {
+  const double d = *nrm;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    y[i] = x[i] / d;
+}
+
+__global__ void sqrt_kernel(double* x) { *x = sqrt(*x); }
+
+// RMF fused extrapolation + gradient + soft-threshold (solvers.hpp:358-360,366,370):
+//   yl = Ld + b (Ld - Ldp); ys = S + b (S - Sp); g = yl + ys - M
+//   GL = yl - step g ; S_next = soft(ys - step g, thr)
+__global__ void rmf_fused_kernel(i64 n, double beta, double step, double thr, const double* __restrict__ Ld,
+                                 const double* __restrict__ Ldp, const double* __restrict__ S,
+                                 const double* __restrict__ Sp, const double* __restrict__ M, double* __restrict__ GL,
+                                 double* __restrict__ Snext) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const double ld = Ld[i], s = S[i];
+    const double yl = ld + beta * (ld - Ldp[i]);
+    const double ys = s + beta * (s - Sp[i]);
+    const double g = yl + ys - M[i];
+    GL[i] = yl - step * g;
+    const double a = ys - step * g;
+    const double mag = fabs(a) - thr;
+    Snext[i] = mag > 0 ? (a > 0 ? mag : -mag) : 0.0;
+  }
+}
+
+// Line-search variant inputs: YL, YS, g materialised.
+__global__ void rmf_extrap_kernel(i64 n, double beta, const double* __restrict__ Ld, const double* __restrict__ Ldp,
+                                  const double* __restrict__ S, const double* __restrict__ Sp,
+                                  const double* __restrict__ M, double* __restrict__ YL, double* __restrict__ YS,
+                                  double* __restrict__ G) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const double ld = Ld[i], s = S[i];
+    const double yl = ld + beta * (ld - Ldp[i]);
+    const double ys = s + beta * (s - Sp[i]);
+    YL[i] = yl;
+    YS[i] = ys;
+    G[i] = yl + ys - M[i];
+  }
+}
+
+__global__ void rmf_step_kernel(i64 n, double step, double thr, const double* __restrict__ YL,
+                                const double* __restrict__ YS, const double* __restrict__ G, double* __restrict__ GL,
+                                double* __restrict__ Snext) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const double g = G[i];
+    GL[i] = YL[i] - step * g;
+    const double a = YS[i] - step * g;
+    const double mag = fabs(a) - thr;
+    Snext[i] = mag > 0 ? (a > 0 ? mag : -mag) : 0.0;
+  }
+}
+
+// Deterministic multi-output reductions over n elements: fixed grid, per-block partials,
+// single-block final sum. K quantities per element.
+constexpr int RB = 256, RT = 256;
+
+template <int K, class F>
+__global__ void multi_sum_partial(i64 n, F f, double* part) {
+  double acc[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) acc[q] = 0.0;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    f(i, acc);
+  __shared__ double sh[K][RT / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    double v = acc[q];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[q][w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double v = 0.0;
+    for (int j = 0; j < RT / 32; ++j) v += sh[threadIdx.x][j];
+    part[threadIdx.x * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+__global__ void multi_sum_final(int K, int nb, const double* part, double* out) {
+  __shared__ double sh[RT];
+  for (int q = 0; q < K; ++q) {
+    double v = 0.0;
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) v += part[q * nb + j];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[q] = sh[0];
+    __syncthreads();
+  }
+}
+
+template <int K, class F>
+std::vector<double> multi_sum(cudaStream_t s, i64 n, F f) {
+  DBuf<double> part(K * RB, s), out(K, s);
+  multi_sum_partial<K><<<RB, RT, 0, s>>>(n, f, part.get());
+  DFCG_LAUNCH_CHECK();
+  multi_sum_final<<<1, RT, 0, s>>>(K, RB, part.get(), out.get());
+  DFCG_LAUNCH_CHECK();
+  std::vector<double> h(K);
+  DFCG_CUDA(cudaMemcpyAsync(h.data(), out.get(), sizeof(double) * K, cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+double host_scalar(cudaStream_t s, const double* d) {
+  double h = 0.0;
+  DFCG_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+double dev_dot(cudaStream_t s, i64 n, const double* a, const double* b) {
+  if (n <= 0) return 0.0;
+  DBuf<double> out(1, s);
+  dot_sum(s, n, a, b, out.get());
+  return host_scalar(s, out.get());
+}
+
+// ---------------------------------------------------------------- operators
+// FactoredSparseOp (solvers.hpp:112-136): G = left right^T + coeff * R.
+struct OpMC {
+  const DevOmega* om;
+  const double* r_csr;
+  double coeff;
+  i64 m, w, kY;
+  const double* left;   // m x kY row-major (ld kY)
+  const double* right;  // w x kY row-major
+  i64 rows() const { return m; }
+  i64 cols() const { return w; }
+  void apply(cudaStream_t s, const double* X, i64 b, double* out) const {  // X w x b -> out m x b
+    if (kY > 0) {
+      DBuf<double> T(kY * b, s);
+      gemm(s, true, false, kY, b, w, 1.0, right, kY, X, b, 0.0, T.get(), b);
+      gemm(s, false, false, m, b, kY, 1.0, left, kY, T.get(), b, 0.0, out, b);
+      spmm(s, *om, false, r_csr, b, coeff, X, b, 1.0, out, b);
+    } else {
+      spmm(s, *om, false, r_csr, b, coeff, X, b, 0.0, out, b);
+    }
+  }
+  void apply_adjoint(cudaStream_t s, const double* X, i64 b, double* out) const {  // X m x b -> out w x b
+    if (kY > 0) {
+      DBuf<double> T(kY * b, s);
+      gemm(s, true, false, kY, b, m, 1.0, left, kY, X, b, 0.0, T.get(), b);
+      gemm(s, false, false, w, b, kY, 1.0, right, kY, T.get(), b, 0.0, out, b);
+      spmm(s, *om, true, r_csr, b, coeff, X, b, 1.0, out, b);
+    } else {
+      spmm(s, *om, true, r_csr, b, coeff, X, b, 0.0, out, b);
+    }
+  }
+  void to_dense(cudaStream_t s, double* D) const {  // m x w row-major
+    if (kY > 0) gemm(s, false, true, m, w, kY, 1.0, left, kY, right, kY, 0.0, D, w);
+    else DFCG_CUDA(cudaMemsetAsync(D, 0, sizeof(double) * m * w, s));
+    scatter_add_dense(s, *om, r_csr, coeff, D, w);
+  }
+};
+
+// DenseOp (solvers.hpp:138-145) over a column-major m x w matrix A (== row-major w x m "At").
+struct OpDense {
+  const double* At;
+  i64 m, w;
+  i64 rows() const { return m; }
+  i64 cols() const { return w; }
+  void apply(cudaStream_t s, const double* X, i64 b, double* out) const {
+    gemm(s, true, false, m, b, w, 1.0, At, m, X, b, 0.0, out, b);
+  }
+  void apply_adjoint(cudaStream_t s, const double* X, i64 b, double* out) const {
+    gemm(s, false, false, w, b, m, 1.0, At, m, X, b, 0.0, out, b);
+  }
+  void to_dense(cudaStream_t s, double* D) const { transpose(s, w, m, At, m, D, w); }
+};
+
+// Result of the SVT: L_next = (U, V diag(s)), s = shrunk singular values (host copy).
+struct SvtResult {
+  i64 r = 0;
+  DBuf<double> left, right;  // m x r, w x r row-major
+  std::vector<double> s;
+  i64 k_final = 0;
+  int calls = 0;
+};
+
+// shrink_factors (solvers.hpp:83-88) applied to device factors U (m x ncand, ldu) and
+// V (w x ncand, ldv) with singular values sv (descending, host).
+void shrink_into(cudaStream_t s, i64 m, i64 w, const double* U, i64 ldu, const double* V, i64 ldv,
+                 const std::vector<double>& sv, double tau, SvtResult& res) {
+  i64 r = 0;
+  while (r < static_cast<i64>(sv.size()) && sv[static_cast<size_t>(r)] > tau) ++r;
+  res.r = r;
+  res.s.assign(sv.begin(), sv.begin() + r);
+  for (double& x : res.s) x -= tau;
+  if (r == 0) return;
+  res.left.alloc(m * r, s);
+  res.right.alloc(w * r, s);
+  copy2d(s, m, r, U, ldu, res.left.get(), r);
+  DBuf<double> sc(r, s);
+  DFCG_CUDA(cudaMemcpyAsync(sc.get(), res.s.data(), sizeof(double) * r, cudaMemcpyHostToDevice, s));
+  scale_cols_kernel<<<grid_for(w * r), 256, 0, s>>>(w, r, V, ldv, sc.get(), res.right.get(), r);
+  DFCG_LAUNCH_CHECK();
+  DFCG_CUDA(cudaStreamSynchronize(s));  // res.s host buffer used by the async copy
+}
+
+// svt_factors_dense (solvers.hpp:90-93) on the materialised operator.
+template <class Op>
+void svt_dense(cudaStream_t s, const Op& op, double tau, SvtResult& res) {
+  const i64 m = op.rows(), w = op.cols();
+  DBuf<double> D(m * w, s);
+  op.to_dense(s, D.get());
+  std::vector<double> sv;
+  if (m >= w) {
+    DBuf<double> U(m * w, s), V(w * w, s);
+    thin_svd(s, m, w, D.get(), w, U.get(), w, V.get(), w, sv);
+    shrink_into(s, m, w, U.get(), w, V.get(), w, sv, tau, res);
+  } else {
+    DBuf<double> Dt(w * m, s), U(w * m, s), V(m * m, s);
+    transpose(s, m, w, D.get(), w, Dt.get(), m);
+    thin_svd(s, w, m, Dt.get(), m, U.get(), m, V.get(), m, sv);  // D^T = U S V^T -> D = V S U^T
+    shrink_into(s, m, w, V.get(), m, U.get(), m, sv, tau, res);
+  }
+}
+
+struct NormalCursor {
+  NormalCache* cache;
+  i64 pos = 0;
+};
+
+// partial_svd (sketch.hpp:156-166) + randomized_range (:144-153) with p, q; then the SVT
+// acceptance test and shrink of svt_operator (solvers.hpp:105-106).  Returns true if the
+// result was accepted (f.rank() < k or s[k-1] <= tau), filling res.
+template <class Op>
+bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor& cur, double tau, SvtResult& res) {
+  const i64 m = op.rows(), w = op.cols();
+  const i64 b = std::min(k + p, std::min(m, w));
+  // gaussian_matrix(w, b): column-major draws == row-major b x w; transpose to w x b.
+  DBuf<double> Gt(b * w, s), G(w * b, s), X(m * b, s), Z(w * b, s);
+  cur.cache->fetch(cur.pos, w * b, Gt.get(), s);
+  cur.pos += w * b;
+  transpose(s, b, w, Gt.get(), w, G.get(), b);
+  op.apply(s, G.get(), b, X.get());
+  thin_qr(s, m, b, X.get(), b, nullptr, 0);
+  for (i64 it = 0; it < q; ++it) {
+    op.apply_adjoint(s, X.get(), b, Z.get());
+    thin_qr(s, w, b, Z.get(), b, nullptr, 0);
+    op.apply(s, Z.get(), b, X.get());
+    thin_qr(s, m, b, X.get(), b, nullptr, 0);
+  }
+  op.apply_adjoint(s, X.get(), b, Z.get());  // Z = A^T Q  (w x b)
+  DBuf<double> Uz(w * b, s), Vz(b * b, s);
+  std::vector<double> sv;
+  thin_svd(s, w, b, Z.get(), b, Uz.get(), b, Vz.get(), b, sv);
+  const i64 kk = std::min<i64>(k, static_cast<i64>(sv.size()));
+  sv.resize(static_cast<size_t>(kk));
+  if (!(kk < k || sv[static_cast<size_t>(kk - 1)] <= tau)) return false;
+  // accepted: U = Q Vz[:, :kk], V = Uz[:, :kk]; shrink keeps the first r <= kk columns
+  i64 r = 0;
+  while (r < kk && sv[static_cast<size_t>(r)] > tau) ++r;
+  res.r = r;
+  res.s.assign(sv.begin(), sv.begin() + r);
+  for (double& x : res.s) x -= tau;
+  if (r == 0) return true;
+  res.left.alloc(m * r, s);
+  res.right.alloc(w * r, s);
+  gemm(s, false, false, m, r, b, 1.0, X.get(), b, Vz.get(), b, 0.0, res.left.get(), r);
+  DBuf<double> sc(r, s);
+  DFCG_CUDA(cudaMemcpyAsync(sc.get(), res.s.data(), sizeof(double) * r, cudaMemcpyHostToDevice, s));
+  scale_cols_kernel<<<grid_for(w * r), 256, 0, s>>>(w, r, Uz.get(), b, sc.get(), res.right.get(), r);
+  DFCG_LAUNCH_CHECK();
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
+// svt_operator (solvers.hpp:98-109).
+template <class Op>
+void svt_operator(cudaStream_t s, const Op& op, double tau, i64 rank_hint, NormalCursor& cur, SvtResult& res) {
+  const i64 minmn = std::min(op.rows(), op.cols());
+  res.calls = 0;
+  res.k_final = 0;
+  if (minmn <= 64) {
+    res.calls = 1;
+    svt_dense(s, op, tau, res);
+    return;
+  }
+  i64 k = std::clamp<i64>(rank_hint + 5, 1, minmn);
+  for (;;) {
+    ++res.calls;
+    if (k >= minmn) {
+      res.k_final = 0;
+      svt_dense(s, op, tau, res);
+      return;
+    }
+    res.k_final = k;
+    if (partial_svt(s, op, k, 10, 2, cur, tau, res)) return;
+    k = std::min<i64>(2 * k, minmn);
+  }
+}
+
+// factored_inner (solvers.hpp:179-184): sum((a.l^T b.l) .* (a.r^T b.r)).
+double factored_inner(cudaStream_t s, i64 m, i64 n, i64 ka, const double* al, const double* ar, i64 kb,
+                      const double* bl, const double* br) {
+  if (ka == 0 || kb == 0) return 0.0;
+  DBuf<double> L(ka * kb, s), R(ka * kb, s);
+  gemm(s, true, false, ka, kb, m, 1.0, al, ka, bl, kb, 0.0, L.get(), kb);
+  gemm(s, true, false, ka, kb, n, 1.0, ar, ka, br, kb, 0.0, R.get(), kb);
+  return dev_dot(s, ka * kb, L.get(), R.get());
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+double sum_of(const std::vector<double>& v) {
+  double a = 0.0;
+  for (double x : v) a += x;
+  return a;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- context / streams
+DeviceContext::DeviceContext(int dev) : device(dev) {
+  DFCG_CUDA(cudaSetDevice(dev));
+  cudaMemPool_t pool;
+  DFCG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  std::uint64_t threshold = UINT64_MAX;
+  DFCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  normals_mc = std::make_unique<NormalCache>(dev, 0x737674u, 0);
+  normals_rmf = std::make_unique<NormalCache>(dev, 0x737674u, 1);
+}
+
+DeviceContext::~DeviceContext() {
+  cudaSetDevice(device);
+  for (cudaStream_t st : all_streams) {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
+}
+
+cudaStream_t DeviceContext::acquire() {
+  std::lock_guard<std::mutex> lock(mu);
+  if (!free_streams.empty()) {
+    cudaStream_t st = free_streams.back();
+    free_streams.pop_back();
+    return st;
+  }
+  cudaStream_t st;
+  DFCG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  all_streams.push_back(st);
+  return st;
+}
+
+void DeviceContext::release(cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(mu);
+  free_streams.push_back(st);
+}
+
+CallStream::CallStream(DeviceContext& c) : ctx(c) {
+  DFCG_CUDA(cudaSetDevice(c.device));
+  s = c.acquire();
+}
+CallStream::~CallStream() {
+  cudaStreamSynchronize(s);
+  ctx.release(s);
+}
+
+// validate_config, solvers.hpp:167-177.
+void validate_config(const ApgConfig& cfg) {
+  if (cfg.max_iters < 1) throw std::invalid_argument("ApgConfig: max_iters must be >= 1");
+  if (!(cfg.rel_tol > 0 && cfg.rel_tol < 1)) throw std::invalid_argument("ApgConfig: rel_tol must be in (0,1)");
+  if (!(cfg.mu_decay > 0 && cfg.mu_decay < 1)) throw std::invalid_argument("ApgConfig: mu_decay must be in (0,1)");
+  if (cfg.mu_init && *cfg.mu_init < 0) throw std::invalid_argument("ApgConfig: mu_init < 0");
+  if (cfg.mu_floor && *cfg.mu_floor < 0) throw std::invalid_argument("ApgConfig: mu_floor < 0");
+  if (cfg.mu_init && cfg.mu_floor && *cfg.mu_floor > *cfg.mu_init)
+    throw std::invalid_argument("ApgConfig: mu_floor exceeds mu_init");
+}
+
+// ---------------------------------------------------------------- apg_mc
+void apg_mc_device(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows,
+                   const long long* cols, const double* vals, const ApgConfig& cfg, DevLowRank& out, SolveReport& rep,
+                   std::vector<IterTrace>* trace) {
+  const auto start = std::chrono::steady_clock::now();
+  if (nnz == 0) throw std::invalid_argument("apg_mc: empty observation set");
+  validate_config(cfg);
+  DevOmega om;
+  om.build(s, m, n, nnz, rows, cols, vals);
+
+  // spectral_norm (solvers.hpp:147-165) of P_Omega(M): alternating power iteration.
+  auto spectral = [&]() {
+    DBuf<double> v(n, s), wv(m, s), z(n, s), nrm(1, s);
+    fill_kernel<<<grid_for(n), 256, 0, s>>>(n, 1.0, v.get());
+    DFCG_LAUNCH_CHECK();
+    dot_sum(s, n, v.get(), v.get(), nrm.get());
+    sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+    scale_by_inv_kernel<<<grid_for(n), 256, 0, s>>>(n, v.get(), nrm.get(), v.get());
+    DFCG_LAUNCH_CHECK();
+    double sv = 0.0, prev = 0.0;
+    for (int it = 0; it < 200; ++it) {
+      spmm(s, om, false, om.m_csr.get(), 1, 1.0, v.get(), 1, 0.0, wv.get(), 1);
+      dot_sum(s, m, wv.get(), wv.get(), nrm.get());
+      sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+      const double nw = host_scalar(s, nrm.get());
+      if (nw == 0.0) return 0.0;
+      scale_by_inv_kernel<<<grid_for(m), 256, 0, s>>>(m, wv.get(), nrm.get(), wv.get());
+      spmm(s, om, true, om.m_csr.get(), 1, 1.0, wv.get(), 1, 0.0, z.get(), 1);
+      dot_sum(s, n, z.get(), z.get(), nrm.get());
+      sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+      sv = host_scalar(s, nrm.get());
+      if (sv == 0.0) return 0.0;
+      scale_by_inv_kernel<<<grid_for(n), 256, 0, s>>>(n, z.get(), nrm.get(), v.get());
+      DFCG_LAUNCH_CHECK();
+      if (std::abs(sv - prev) <= 1e-10 * sv) break;
+      prev = sv;
+    }
+    return sv;
+  };
+  const double mu_init = cfg.mu_init ? *cfg.mu_init : 0.99 * spectral();
+  const double mu_floor = cfg.mu_floor ? *cfg.mu_floor : 1e-4 * mu_init;
+  if (mu_floor > mu_init) throw std::invalid_argument("apg_mc: mu_floor exceeds mu_init");
+
+  NormalCursor cur{&ctx.normals(0), 0};
+  DBuf<double> r_csr(nnz, s);
+  DevLowRank Lp, Lc;  // k = 0
+  Lp.m = Lc.m = m;
+  Lp.n = Lc.n = n;
+  double icc = 0.0;  // factored_inner(L_curr, L_curr)
+  std::vector<double> last_s;
+  double tau_prev = 1.0, tau_curr = 1.0, mu = mu_init, mu_used = mu_init;
+  i64 rank_hint = 1;
+  int iters = 0;
+  for (int it = 1; it <= cfg.max_iters; ++it) {
+    iters = it;
+    const double beta = (tau_prev - 1.0) / tau_curr;
+    // Y = extrapolate(L_curr, L_prev, beta) as concatenated factors (no compaction).
+    const bool concat = !(beta == 0.0 || Lp.k == 0);
+    const i64 kY = concat ? Lc.k + Lp.k : Lc.k;
+    DBuf<double> Yl, Yr;
+    if (kY > 0) {
+      Yl.alloc(m * kY, s);
+      Yr.alloc(n * kY, s);
+      if (Lc.k > 0) {
+        copy2d(s, m, Lc.k, Lc.left.get(), Lc.k, Yl.get(), kY);
+        copy2d(s, n, Lc.k, Lc.right.get(), Lc.k, Yr.get(), kY, 1.0 + beta);
+      }
+      if (concat) {
+        copy2d(s, m, Lp.k, Lp.left.get(), Lp.k, Yl.get() + Lc.k, kY);
+        copy2d(s, n, Lp.k, Lp.right.get(), Lp.k, Yr.get() + Lc.k, kY, -beta);
+      }
+    }
+    // R = P_Omega(Y) - P_Omega(M)
+    sddmm_residual(s, om, kY, Yl.get(), kY, Yr.get(), kY, om.m_csr.get(), r_csr.get());
+
+    double step = 1.0;
+    SvtResult f;
+    for (;;) {
+      OpMC G{&om, r_csr.get(), -step, m, n, kY, Yl.get(), Yr.get()};
+      f = SvtResult{};
+      svt_operator(s, G, step * mu, rank_hint, cur, f);
+      if (!cfg.line_search || step <= 0.125) break;
+      // backtracking majorization test (solvers.hpp:294-302)
+      DBuf<double> nd(nnz, s);
+      sddmm_residual(s, om, f.r, f.left.get(), f.r, f.right.get(), f.r, om.m_csr.get(), nd.get());  // next - m
+      const double f_next = 0.5 * dev_dot(s, nnz, nd.get(), nd.get());
+      const double rr = dev_dot(s, nnz, r_csr.get(), r_csr.get());
+      const double f_y = 0.5 * rr;
+      const double lin = dev_dot(s, nnz, r_csr.get(), nd.get()) - rr;  // sum (y-m)(next-y)
+      const double d2 = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get()) -
+                        2.0 * factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), kY, Yl.get(), Yr.get()) +
+                        factored_inner(s, m, n, kY, Yl.get(), Yr.get(), kY, Yl.get(), Yr.get());
+      const double dist2 = std::sqrt(std::max(0.0, d2));
+      if (f_next <= f_y + lin + dist2 * dist2 / (2.0 * step) + 1e-12) break;
+      step *= 0.5;
+    }
+    // rel = ||L_next - L_curr|| / max(1, ||L_curr||) via factored inner products (:305-306)
+    const double inn = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get());
+    const double inc = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), Lc.k, Lc.left.get(), Lc.right.get());
+    const double d2 = inn - 2.0 * inc + icc;
+    const double rel = std::sqrt(std::max(0.0, d2)) / std::max(1.0, std::sqrt(std::max(0.0, icc)));
+    const double tau_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tau_curr * tau_curr));
+    Lp = std::move(Lc);
+    Lc = DevLowRank{};
+    Lc.m = m;
+    Lc.n = n;
+    Lc.k = f.r;
+    Lc.left = std::move(f.left);
+    Lc.right = std::move(f.right);
+    icc = inn;
+    last_s = f.s;
+    tau_prev = tau_curr;
+    tau_curr = tau_next;
+    rank_hint = std::max<i64>(1, Lc.k);
+    mu_used = mu;
+    if (trace) trace->push_back({it, Lc.k, f.k_final, f.calls, rel, mu, sum_of(last_s)});
+    mu = std::max(cfg.mu_decay * mu, mu_floor);
+    if (rel < cfg.rel_tol) break;
+  }
+  rep.iterations = iters;
+  rep.rank = Lc.k;
+  DBuf<double> fin(nnz, s);
+  sddmm_residual(s, om, Lc.k, Lc.left.get(), Lc.k, Lc.right.get(), Lc.k, om.m_csr.get(), fin.get());
+  rep.residual = std::sqrt(dev_dot(s, nnz, fin.get(), fin.get()));
+  rep.objective = mu_used * sum_of(last_s) + 0.5 * rep.residual * rep.residual;
+  out = std::move(Lc);
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  rep.wall_ms = ms_since(start);
+}
+
+// ---------------------------------------------------------------- apg_rmf
+void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor, i64 m, i64 n, double lambda,
+                    const ApgConfig& cfg, DevLowRank& out, std::vector<long long>& s_row, std::vector<long long>& s_col,
+                    std::vector<double>& s_val, SolveReport& rep, std::vector<IterTrace>* trace) {
+  const auto start = std::chrono::steady_clock::now();
+  if (!(lambda > 0)) throw std::invalid_argument("apg_rmf: lambda must be positive");
+  const i64 mn = m * n;
+  for (i64 i = 0; i < mn; ++i)
+    if (!std::isfinite(M_colmajor[i])) throw std::invalid_argument("apg_rmf: non-finite input");
+  validate_config(cfg);
+  // Dense m x n matrices are kept column-major (== row-major n x m), like the input.
+  DBuf<double> M(mn, s), Ld(mn, s), Ldp(mn, s), Sc(mn, s), Sp(mn, s), GL(mn, s), Sn(mn, s), Ldn(mn, s);
+  DFCG_CUDA(cudaMemcpyAsync(M.get(), M_colmajor, sizeof(double) * mn, cudaMemcpyHostToDevice, s));
+  Ld.zero(s);
+  Ldp.zero(s);
+  Sc.zero(s);
+  Sp.zero(s);
+
+  auto spectral = [&]() {  // dense power iteration on M (m x n)
+    DBuf<double> v(n, s), wv(m, s), z(n, s), nrm(1, s);
+    fill_kernel<<<grid_for(n), 256, 0, s>>>(n, 1.0, v.get());
+    DFCG_LAUNCH_CHECK();
+    dot_sum(s, n, v.get(), v.get(), nrm.get());
+    sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+    scale_by_inv_kernel<<<grid_for(n), 256, 0, s>>>(n, v.get(), nrm.get(), v.get());
+    double sv = 0.0, prev = 0.0;
+    for (int it = 0; it < 200; ++it) {
+      gemm(s, true, false, m, 1, n, 1.0, M.get(), m, v.get(), 1, 0.0, wv.get(), 1);  // M v
+      dot_sum(s, m, wv.get(), wv.get(), nrm.get());
+      sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+      const double nw = host_scalar(s, nrm.get());
+      if (nw == 0.0) return 0.0;
+      scale_by_inv_kernel<<<grid_for(m), 256, 0, s>>>(m, wv.get(), nrm.get(), wv.get());
+      gemm(s, false, false, n, 1, m, 1.0, M.get(), m, wv.get(), 1, 0.0, z.get(), 1);  // M^T w
+      dot_sum(s, n, z.get(), z.get(), nrm.get());
+      sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+      sv = host_scalar(s, nrm.get());
+      if (sv == 0.0) return 0.0;
+      scale_by_inv_kernel<<<grid_for(n), 256, 0, s>>>(n, z.get(), nrm.get(), v.get());
+      DFCG_LAUNCH_CHECK();
+      if (std::abs(sv - prev) <= 1e-10 * sv) break;
+      prev = sv;
+    }
+    return sv;
+  };
+  const double mu_init = cfg.mu_init ? *cfg.mu_init : 0.99 * spectral();
+  const double mu_floor = cfg.mu_floor ? *cfg.mu_floor : 1e-4 * mu_init;
+  if (mu_floor > mu_init) throw std::invalid_argument("apg_rmf: mu_floor exceeds mu_init");
+
+  NormalCursor cur{&ctx.normals(1), 0};
+  SvtResult last;
+  double tau_prev = 1.0, tau_curr = 1.0, mu = mu_init, mu_used = mu_init;
+  i64 rank_hint = 1;
+  int iters = 0;
+  const int gb = grid_for(mn);
+  DBuf<double> YL, YS, Gd;
+  if (cfg.line_search) {
+    YL.alloc(mn, s);
+    YS.alloc(mn, s);
+    Gd.alloc(mn, s);
+  }
+  for (int it = 1; it <= cfg.max_iters; ++it) {
+    iters = it;
+    const double beta = (tau_prev - 1.0) / tau_curr;
+    double step = 0.5;
+    SvtResult f;
+    if (cfg.line_search) {
+      rmf_extrap_kernel<<<gb, 256, 0, s>>>(mn, beta, Ld.get(), Ldp.get(), Sc.get(), Sp.get(), M.get(), YL.get(),
+                                           YS.get(), Gd.get());
+      DFCG_LAUNCH_CHECK();
+    }
+    for (;;) {
+      if (cfg.line_search) {
+        rmf_step_kernel<<<gb, 256, 0, s>>>(mn, step, step * lambda * mu, YL.get(), YS.get(), Gd.get(), GL.get(),
+                                           Sn.get());
+      } else {
+        rmf_fused_kernel<<<gb, 256, 0, s>>>(mn, beta, step, step * lambda * mu, Ld.get(), Ldp.get(), Sc.get(),
+                                            Sp.get(), M.get(), GL.get(), Sn.get());
+      }
+      DFCG_LAUNCH_CHECK();
+      OpDense op{GL.get(), m, n};
+      f = SvtResult{};
+      svt_operator(s, op, step * mu, rank_hint, cur, f);
+      // Ld_next = U diag(s) V^T  (column-major m x n == row-major n x m: V diag(s) U^T)
+      if (f.r == 0) {
+        Ldn.zero(s);
+      } else {
+        gemm(s, false, true, n, m, f.r, 1.0, f.right.get(), f.r, f.left.get(), f.r, 0.0, Ldn.get(), m);
+      }
+      if (!cfg.line_search || step <= 0.0625) break;
+      const double* pM = M.get();
+      const double* pLn = Ldn.get();
+      const double* pSn = Sn.get();
+      const double* pYL = YL.get();
+      const double* pYS = YS.get();
+      const double* pG = Gd.get();
+      auto sums = multi_sum<4>(s, mn, [=] __device__(i64 i, double* acc) {
+        const double r = pM[i] - pLn[i] - pSn[i];
+        const double g = pG[i];
+        const double dl = pLn[i] - pYL[i], ds = pSn[i] - pYS[i];
+        acc[0] += r * r;
+        acc[1] += g * g;
+        acc[2] += g * (dl + ds);
+        acc[3] += dl * dl + ds * ds;
+      });
+      if (0.5 * sums[0] <= 0.5 * sums[1] + sums[2] + sums[3] / (2.0 * step) + 1e-12) break;
+      step *= 0.5;
+    }
+    const double* pLd = Ld.get();
+    const double* pLn = Ldn.get();
+    const double* pSc = Sc.get();
+    const double* pSn = Sn.get();
+    auto sums = multi_sum<4>(s, mn, [=] __device__(i64 i, double* acc) {
+      const double dl = pLn[i] - pLd[i], ds = pSn[i] - pSc[i];
+      acc[0] += dl * dl;
+      acc[1] += ds * ds;
+      acc[2] += pLd[i] * pLd[i];
+      acc[3] += pSc[i] * pSc[i];
+    });
+    const double denom = std::max(1.0, std::sqrt(sums[2] + sums[3]));
+    const double rel = std::sqrt(sums[0] + sums[1]) / denom;
+    const double tau_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tau_curr * tau_curr));
+    std::swap(Ldp, Ld);
+    std::swap(Ld, Ldn);  // Ld <- next, Ldn <- old prev (scratch)
+    std::swap(Sp, Sc);
+    std::swap(Sc, Sn);
+    last = std::move(f);
+    tau_prev = tau_curr;
+    tau_curr = tau_next;
+    rank_hint = std::max<i64>(1, last.r);
+    mu_used = mu;
+    if (trace) trace->push_back({it, last.r, last.k_final, last.calls, rel, mu, sum_of(last.s)});
+    mu = std::max(cfg.mu_decay * mu, mu_floor);
+    if (rel < cfg.rel_tol) break;
+  }
+  // outputs (solvers.hpp:398-413)
+  const double* pM = M.get();
+  const double* pLd = Ld.get();
+  const double* pSc = Sc.get();
+  auto sums = multi_sum<2>(s, mn, [=] __device__(i64 i, double* acc) {
+    const double r = pM[i] - pLd[i] - pSc[i];
+    acc[0] += r * r;
+    acc[1] += fabs(pSc[i]);
+  });
+  rep.iterations = iters;
+  rep.rank = last.r;
+  rep.residual = std::sqrt(sums[0]);
+  rep.objective =
+      sum_of(last.s) + lambda * sums[1] + (mu_used > 0 ? rep.residual * rep.residual / (2.0 * mu_used) : 0.0);
+  std::vector<double> hS(mn);
+  DFCG_CUDA(cudaMemcpyAsync(hS.data(), Sc.get(), sizeof(double) * mn, cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  s_row.clear();
+  s_col.clear();
+  s_val.clear();
+  for (i64 j = 0; j < n; ++j)
+    for (i64 i = 0; i < m; ++i) {
+      const double v = hS[j * m + i];
+      if (v != 0.0) {
+        s_row.push_back(i);
+        s_col.push_back(j);
+        s_val.push_back(v);
+      }
+    }
+  out = DevLowRank{};
+  out.m = m;
+  out.n = n;
+  out.k = last.r;
+  out.left = std::move(last.left);
+  out.right = std::move(last.right);
+  rep.wall_ms = ms_since(start);
+}
+
+// ---------------------------------------------------------------- transfers
+void upload_lowrank(cudaStream_t s, const HostLowRank& h, DevLowRank& d) {
+  d = DevLowRank{};
+  d.m = h.m;
+  d.n = h.n;
+  d.k = h.k;
+  if (h.k == 0) return;
+  DBuf<double> tl(h.m * h.k, s), tr(h.n * h.k, s);
+  d.left.alloc(h.m * h.k, s);
+  d.right.alloc(h.n * h.k, s);
+  DFCG_CUDA(cudaMemcpyAsync(tl.get(), h.left.data(), sizeof(double) * h.m * h.k, cudaMemcpyHostToDevice, s));
+  DFCG_CUDA(cudaMemcpyAsync(tr.get(), h.right.data(), sizeof(double) * h.n * h.k, cudaMemcpyHostToDevice, s));
+  // column-major m x k == row-major k x m
+  transpose(s, h.k, h.m, tl.get(), h.m, d.left.get(), h.k);
+  transpose(s, h.k, h.n, tr.get(), h.n, d.right.get(), h.k);
+  DFCG_CUDA(cudaStreamSynchronize(s));
+}
+
+void download_lowrank(cudaStream_t s, const DevLowRank& d, HostLowRank& h) {
+  h.m = d.m;
+  h.n = d.n;
+  h.k = d.k;
+  h.left.assign(static_cast<size_t>(d.m * d.k), 0.0);
+  h.right.assign(static_cast<size_t>(d.n * d.k), 0.0);
+  if (d.k == 0) return;
+  DBuf<double> tl(d.m * d.k, s), tr(d.n * d.k, s);
+  transpose(s, d.m, d.k, d.left.get(), d.k, tl.get(), d.m);
+  transpose(s, d.n, d.k, d.right.get(), d.k, tr.get(), d.n);
+  DFCG_CUDA(cudaMemcpyAsync(h.left.data(), tl.get(), sizeof(double) * d.m * d.k, cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaMemcpyAsync(h.right.data(), tr.get(), sizeof(double) * d.n * d.k, cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace dfcg

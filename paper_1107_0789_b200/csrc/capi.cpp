@@ -1,0 +1,388 @@
+// C ABI (include/dfcg.h): argument validation, host<->device layout conversion, exception ->
+// error-code mapping. Everything below this file is C++/CUDA; nothing here computes.
+#include "../../include/dfcg.h"
+
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <new>
+#include <string>
+
+#include "dfc_host.hpp"
+
+using namespace dfcg;
+
+struct dfcg_ctx {
+  DeviceContext* dev;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_err_block = -1;
+
+template <class F>
+int guard(F&& f) {
+  g_err.clear();
+  g_err_block = -1;
+  try {
+    f();
+    return DFCG_OK;
+  } catch (const BlockError& e) {
+    g_err = e.what();
+    g_err_block = static_cast<int64_t>(e.block);
+    return DFCG_EBLOCK;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return DFCG_ECUDA;
+  } catch (const std::bad_alloc& e) {
+    g_err = "out of host memory";
+    return DFCG_ENOMEM;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return DFCG_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return DFCG_ERANGE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DFCG_EINTERNAL;
+  }
+}
+
+ApgConfig to_cfg(const dfcg_apg_cfg* c) {
+  ApgConfig cfg;
+  if (!c) return cfg;
+  cfg.max_iters = c->max_iters;
+  cfg.rel_tol = c->rel_tol;
+  if (c->has_mu_init) cfg.mu_init = c->mu_init;
+  if (c->has_mu_floor) cfg.mu_floor = c->mu_floor;
+  cfg.mu_decay = c->mu_decay;
+  cfg.line_search = c->line_search != 0;
+  return cfg;
+}
+
+void to_report(const SolveReport& r, dfcg_solve_report* o) {
+  if (!o) return;
+  o->iterations = r.iterations;
+  o->objective = r.objective;
+  o->residual = r.residual;
+  o->rank = r.rank;
+  o->wall_ms = r.wall_ms;
+}
+
+void to_trace(const std::vector<IterTrace>& tr, dfcg_iter_trace* out, int64_t cap, int64_t* len) {
+  if (len) *len = static_cast<int64_t>(tr.size());
+  if (!out) return;
+  for (size_t i = 0; i < tr.size() && static_cast<int64_t>(i) < cap; ++i)
+    out[i] = {tr[i].it, tr[i].rank, tr[i].k_final, tr[i].svd_calls, tr[i].rel, tr[i].mu, tr[i].sigma_sum};
+}
+
+double* dup_array(const std::vector<double>& v) {
+  double* p = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(1, v.size())));
+  if (!p) throw std::bad_alloc();
+  if (!v.empty()) std::memcpy(p, v.data(), sizeof(double) * v.size());
+  return p;
+}
+
+// LowRankEstimate ctor validation (matrix_io.hpp:73-84) on a host estimate.
+HostLowRank from_c(const dfcg_lowrank* e) {
+  if (!e) throw std::invalid_argument("LowRankEstimate: null estimate");
+  HostLowRank h;
+  h.m = e->m;
+  h.n = e->n;
+  h.k = e->k;
+  if (h.m < 1 || h.n < 1) throw std::invalid_argument("LowRankEstimate: dims must be positive");
+  if (h.k < 0 || h.k > std::min(h.m, h.n)) throw std::invalid_argument("LowRankEstimate: k exceeds min(m, n)");
+  h.left.assign(e->left, e->left + h.m * h.k);
+  h.right.assign(e->right, e->right + h.n * h.k);
+  for (double v : h.left)
+    if (!std::isfinite(v)) throw std::invalid_argument("LowRankEstimate: non-finite factor entry");
+  for (double v : h.right)
+    if (!std::isfinite(v)) throw std::invalid_argument("LowRankEstimate: non-finite factor entry");
+  return h;
+}
+
+void to_c(const HostLowRank& h, dfcg_lowrank* out) {
+  out->m = h.m;
+  out->n = h.n;
+  out->k = h.k;
+  out->left = dup_array(h.left);
+  out->right = dup_array(h.right);
+}
+
+void to_c(cudaStream_t s, const DevLowRank& d, dfcg_lowrank* out) {
+  HostLowRank h;
+  download_lowrank(s, d, h);
+  to_c(h, out);
+}
+
+DevLowRank to_dev(cudaStream_t s, const dfcg_lowrank* e) {
+  DevLowRank d;
+  upload_lowrank(s, from_c(e), d);
+  return d;
+}
+
+std::vector<std::vector<i64>> groups_from(int64_t t, const int64_t* offsets, const int64_t* cols, int64_t n) {
+  if (t < 0) throw std::invalid_argument("partition: negative group count");
+  std::vector<std::vector<i64>> g(static_cast<size_t>(t));
+  std::vector<char> seen(static_cast<size_t>(std::max<int64_t>(n, 0)), 0);
+  size_t total = 0, min_sz = static_cast<size_t>(std::max<int64_t>(n, 0)), max_sz = 0;
+  for (int64_t i = 0; i < t; ++i) {
+    g[static_cast<size_t>(i)].assign(cols + offsets[i], cols + offsets[i + 1]);
+    const auto& grp = g[static_cast<size_t>(i)];
+    min_sz = std::min(min_sz, grp.size());
+    max_sz = std::max(max_sz, grp.size());
+    for (size_t p = 0; p < grp.size(); ++p) {  // PartitionPlan ctor checks (sampling.hpp:32-51)
+      const i64 c = grp[p];
+      if (c < 0 || c >= n) throw std::out_of_range("PartitionPlan: column out of range");
+      if (seen[static_cast<size_t>(c)]++) throw std::invalid_argument("PartitionPlan: overlapping groups");
+      if (p > 0 && grp[p - 1] >= c) throw std::invalid_argument("PartitionPlan: group not sorted");
+      ++total;
+    }
+  }
+  if (total != static_cast<size_t>(n)) throw std::invalid_argument("PartitionPlan: groups do not cover all columns");
+  if (t > 0 && max_sz > min_sz + 1) throw std::invalid_argument("PartitionPlan: group sizes differ by more than 1");
+  return g;
+}
+
+}  // namespace
+
+// Shared error channel for the host utilities in hostgen.cpp.
+int dfcg_guard_call(const std::function<void()>& f) { return guard(f); }
+
+extern "C" {
+
+int dfcg_ctx_create(int device, dfcg_ctx** out) {
+  return guard([&] {
+    int n = 0;
+    DFCG_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw std::invalid_argument("dfcg_ctx_create: no such CUDA device");
+    auto* c = new dfcg_ctx{new DeviceContext(device)};
+    *out = c;
+  });
+}
+
+void dfcg_ctx_destroy(dfcg_ctx* ctx) {
+  if (!ctx) return;
+  delete ctx->dev;
+  delete ctx;
+}
+
+const char* dfcg_last_error(void) { return g_err.c_str(); }
+int64_t dfcg_last_error_block(void) { return g_err_block; }
+void dfcg_free(void* p) { std::free(p); }
+
+void dfcg_lowrank_free(dfcg_lowrank* e) {
+  if (!e) return;
+  std::free(e->left);
+  std::free(e->right);
+  e->left = e->right = nullptr;
+}
+
+void dfcg_sparse_free(dfcg_sparse* s) {
+  if (!s) return;
+  std::free(s->row);
+  std::free(s->col);
+  std::free(s->val);
+  s->row = s->col = nullptr;
+  s->val = nullptr;
+}
+
+int dfcg_apg_mc(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_apg_cfg* cfg, dfcg_lowrank* out,
+                dfcg_solve_report* rep, dfcg_iter_trace* trace, int64_t trace_cap, int64_t* trace_len) {
+  return guard([&] {
+    if (!ctx || !in || !out) throw std::invalid_argument("dfcg_apg_mc: null argument");
+    HostObs obs = HostObs::make(in->m, in->n, std::vector<long long>(in->row, in->row + in->nnz),
+                                std::vector<long long>(in->col, in->col + in->nnz),
+                                std::vector<double>(in->val, in->val + in->nnz));
+    CallStream cs(*ctx->dev);
+    DevLowRank L;
+    SolveReport r;
+    std::vector<IterTrace> tr;
+    apg_mc_device(*ctx->dev, cs.s, obs.m, obs.n, obs.count(), obs.row.data(), obs.col.data(), obs.val.data(),
+                  to_cfg(cfg), L, r, &tr);
+    to_c(cs.s, L, out);
+    to_report(r, rep);
+    to_trace(tr, trace, trace_cap, trace_len);
+  });
+}
+
+int dfcg_apg_rmf(dfcg_ctx* ctx, const double* M_colmajor, int64_t m, int64_t n, double lambda,
+                 const dfcg_apg_cfg* cfg, dfcg_lowrank* L, dfcg_sparse* S, dfcg_solve_report* rep,
+                 dfcg_iter_trace* trace, int64_t trace_cap, int64_t* trace_len) {
+  return guard([&] {
+    if (!ctx || !M_colmajor || !L) throw std::invalid_argument("dfcg_apg_rmf: null argument");
+    if (m < 1 || n < 1) throw std::invalid_argument("apg_rmf: dims must be positive");
+    CallStream cs(*ctx->dev);
+    DevLowRank Ld;
+    SolveReport r;
+    std::vector<IterTrace> tr;
+    std::vector<long long> sr, sc;
+    std::vector<double> sv;
+    apg_rmf_device(*ctx->dev, cs.s, M_colmajor, m, n, lambda, to_cfg(cfg), Ld, sr, sc, sv, r, &tr);
+    to_c(cs.s, Ld, L);
+    if (S) {
+      S->m = m;
+      S->n = n;
+      S->count = static_cast<int64_t>(sv.size());
+      S->row = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<size_t>(1, sr.size())));
+      S->col = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<size_t>(1, sc.size())));
+      S->val = dup_array(sv);
+      if (!sr.empty()) {
+        std::memcpy(S->row, sr.data(), sizeof(int64_t) * sr.size());
+        std::memcpy(S->col, sc.data(), sizeof(int64_t) * sc.size());
+      }
+    }
+    to_report(r, rep);
+    to_trace(tr, trace, trace_cap, trace_len);
+  });
+}
+
+int dfcg_column_project(dfcg_ctx* ctx, const dfcg_lowrank* basis, int64_t t, const dfcg_lowrank* blocks,
+                        const int64_t* group_offsets, const int64_t* group_cols, int64_t n, dfcg_lowrank* out) {
+  return guard([&] {
+    if (!ctx || !basis || !out) throw std::invalid_argument("dfcg_column_project: null argument");
+    if (t == 0) throw std::invalid_argument("column_project: no blocks");
+    auto groups = groups_from(t, group_offsets, group_cols, n);
+    CallStream cs(*ctx->dev);
+    DevLowRank b = to_dev(cs.s, basis);
+    std::vector<DevLowRank> bl(static_cast<size_t>(t));
+    std::vector<const DevLowRank*> p;
+    for (int64_t i = 0; i < t; ++i) {
+      bl[static_cast<size_t>(i)] = to_dev(cs.s, &blocks[i]);
+      p.push_back(&bl[static_cast<size_t>(i)]);
+    }
+    DevLowRank o;
+    column_project(cs.s, b, p, groups, n, o);
+    to_c(cs.s, o, out);
+  });
+}
+
+int dfcg_gen_nystrom(dfcg_ctx* ctx, const dfcg_lowrank* C_hat, const dfcg_lowrank* R_hat, int64_t d,
+                     const int64_t* row_idx, int64_t l, const int64_t* col_idx, dfcg_lowrank* out) {
+  return guard([&] {
+    if (!ctx || !C_hat || !R_hat || !out) throw std::invalid_argument("dfcg_gen_nystrom: null argument");
+    CallStream cs(*ctx->dev);
+    DevLowRank C = to_dev(cs.s, C_hat), R = to_dev(cs.s, R_hat), o;
+    gen_nystrom(cs.s, C, R, std::vector<i64>(row_idx, row_idx + d), std::vector<i64>(col_idx, col_idx + l), o);
+    to_c(cs.s, o, out);
+  });
+}
+
+int dfcg_average_estimates(dfcg_ctx* ctx, int64_t count, const dfcg_lowrank* ests, int64_t recompress_to,
+                           dfcg_lowrank* out) {
+  return guard([&] {
+    if (!ctx || !out) throw std::invalid_argument("dfcg_average_estimates: null argument");
+    if (count <= 0) throw std::invalid_argument("average_estimates: empty list");
+    CallStream cs(*ctx->dev);
+    std::vector<DevLowRank> d(static_cast<size_t>(count));
+    std::vector<const DevLowRank*> p;
+    for (int64_t i = 0; i < count; ++i) {
+      d[static_cast<size_t>(i)] = to_dev(cs.s, &ests[i]);
+      p.push_back(&d[static_cast<size_t>(i)]);
+    }
+    DevLowRank o;
+    std::optional<i64> rc;
+    if (recompress_to >= 0) rc = recompress_to;
+    average_estimates(cs.s, p, rc, o);
+    to_c(cs.s, o, out);
+  });
+}
+
+int dfcg_random_project(dfcg_ctx* ctx, int64_t t, const dfcg_lowrank* blocks, const int64_t* group_offsets,
+                        const int64_t* group_cols, int64_t n, int64_t k, int64_t p, int64_t q, uint64_t seed,
+                        uint64_t stream, dfcg_lowrank* out) {
+  return guard([&] {
+    if (!ctx || !out) throw std::invalid_argument("dfcg_random_project: null argument");
+    if (t == 0) throw std::invalid_argument("random_project: no blocks");
+    auto groups = groups_from(t, group_offsets, group_cols, n);
+    CallStream cs(*ctx->dev);
+    std::vector<DevLowRank> d(static_cast<size_t>(t));
+    std::vector<const DevLowRank*> ptr;
+    for (int64_t i = 0; i < t; ++i) {
+      d[static_cast<size_t>(i)] = to_dev(cs.s, &blocks[i]);
+      ptr.push_back(&d[static_cast<size_t>(i)]);
+    }
+    SeededRng rng(seed, stream);
+    DevLowRank o;
+    random_project(cs.s, ptr, groups, n, k, p, q, rng, o);
+    to_c(cs.s, o, out);
+  });
+}
+
+int dfcg_svd_of_product(dfcg_ctx* ctx, const dfcg_lowrank* in, dfcg_lowrank* out, double* s_out, int64_t* rank) {
+  return guard([&] {
+    if (!ctx || !in || !out) throw std::invalid_argument("dfcg_svd_of_product: null argument");
+    CallStream cs(*ctx->dev);
+    // raw factor pair (k may exceed min(m, n) here, as in svd_of_product's callers)
+    HostLowRank h;
+    h.m = in->m;
+    h.n = in->n;
+    h.k = in->k;
+    h.left.assign(in->left, in->left + h.m * h.k);
+    h.right.assign(in->right, in->right + h.n * h.k);
+    DBuf<double> l(std::max<i64>(1, h.m * h.k), cs.s), r(std::max<i64>(1, h.n * h.k), cs.s),
+        tl(std::max<i64>(1, h.m * h.k), cs.s), tr(std::max<i64>(1, h.n * h.k), cs.s);
+    if (h.k > 0) {
+      DFCG_CUDA(cudaMemcpyAsync(tl.get(), h.left.data(), sizeof(double) * h.m * h.k, cudaMemcpyHostToDevice, cs.s));
+      DFCG_CUDA(cudaMemcpyAsync(tr.get(), h.right.data(), sizeof(double) * h.n * h.k, cudaMemcpyHostToDevice, cs.s));
+      transpose(cs.s, h.k, h.m, tl.get(), h.m, l.get(), h.k);
+      transpose(cs.s, h.k, h.n, tr.get(), h.n, r.get(), h.k);
+    }
+    SvdOfProduct f = svd_of_product(cs.s, h.m, h.n, h.k, l.get(), r.get());
+    to_c(cs.s, f.est, out);
+    if (s_out)
+      for (size_t i = 0; i < f.s.size(); ++i) s_out[i] = f.s[i];
+    if (rank) *rank = f.r;
+  });
+}
+
+int dfcg_dfc_run(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_dfc_cfg* c, dfcg_lowrank* out, dfcg_dfc_report* rep) {
+  return guard([&] {
+    if (!ctx || !in || !c || !out) throw std::invalid_argument("dfcg_dfc_run: null argument");
+    HostObs obs = HostObs::make(in->m, in->n, std::vector<long long>(in->row, in->row + in->nnz),
+                                std::vector<long long>(in->col, in->col + in->nnz),
+                                std::vector<double>(in->val, in->val + in->nnz));
+    DfcConfig cfg;
+    if (c->variant < 0 || c->variant > 2) throw std::invalid_argument("dfc_run: unknown variant");
+    cfg.variant = static_cast<DfcVariant>(c->variant);
+    cfg.ensemble = c->ensemble != 0;
+    cfg.t = c->t;
+    cfg.l = c->l;
+    cfg.d = c->d;
+    cfg.rp_p = c->rp_p;
+    cfg.rp_q = c->rp_q;
+    cfg.seed = c->seed;
+    cfg.solver_cfg = to_cfg(&c->solver);
+    cfg.task = c->task == 1 ? Task::RMF : Task::MC;
+    cfg.lambda = c->lambda;
+    cfg.workers = c->workers;
+    auto [est, r] = dfc_run(*ctx->dev, obs, cfg);
+    {
+      CallStream cs(*ctx->dev);
+      to_c(cs.s, est, out);
+    }
+    if (rep) {
+      rep->divide_ms = r.divide_ms;
+      rep->factor_ms = r.factor_ms;
+      rep->combine_ms = r.combine_ms;
+      rep->total_ms = r.total_ms;
+      rep->chosen_k = r.chosen_k;
+      rep->k_clamped = r.k_clamped;
+      rep->rank_deficient = r.rank_deficient;
+      rep->n_sub = static_cast<int64_t>(r.subproblems.size());
+      rep->subproblems = static_cast<dfcg_solve_report*>(
+          std::malloc(sizeof(dfcg_solve_report) * std::max<size_t>(1, r.subproblems.size())));
+      for (size_t i = 0; i < r.subproblems.size(); ++i) to_report(r.subproblems[i], &rep->subproblems[i]);
+    }
+  });
+}
+
+void dfcg_dfc_report_free(dfcg_dfc_report* rep) {
+  if (!rep) return;
+  std::free(rep->subproblems);
+  rep->subproblems = nullptr;
+}
+
+}  // extern "C"

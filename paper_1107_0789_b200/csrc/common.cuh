@@ -1,0 +1,128 @@
+// Shared device utilities for the DFC B200 library (FP64 throughout).
+//
+// Conventions: every dense matrix on the device is ROW-MAJOR ("C order") with an
+// explicit leading dimension, so factor rows are contiguous for the SDDMM gathers
+// and sketch rows are contiguous for the SpMM gathers. The C ABI converts from the
+// reference's column-major Eigen layout (P/include/dfc/matrix_io.hpp:19) at the edge.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace dfcg {
+
+using i64 = std::int64_t;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define DFCG_CUDA(call)                                                                          \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess)                                                                       \
+      throw ::dfcg::CudaError(std::string(#call) + " failed: " + cudaGetErrorString(e_) + " at " + \
+                              __FILE__ + ":" + std::to_string(__LINE__));                        \
+  } while (0)
+
+#define DFCG_LAUNCH_CHECK() DFCG_CUDA(cudaGetLastError())
+
+inline int cdiv(i64 a, i64 b) { return static_cast<int>((a + b - 1) / b); }
+
+// Stream-ordered device buffer (cudaMallocAsync from the device's default pool,
+// whose release threshold is raised at context creation so reuse is cheap).
+template <class T>
+class DBuf {
+ public:
+  DBuf() = default;
+  DBuf(i64 n, cudaStream_t s) { alloc(n, s); }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      s_ = o.s_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  void alloc(i64 n, cudaStream_t s) {
+    release();
+    s_ = s;
+    n_ = n;
+    if (n > 0) DFCG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), sizeof(T) * static_cast<size_t>(n), s));
+  }
+  // Grow-only reallocation (contents not preserved).
+  void ensure(i64 n, cudaStream_t s) {
+    if (n > n_ || p_ == nullptr) alloc(std::max<i64>(n, 1), s);
+  }
+  void release() {
+    if (p_) cudaFreeAsync(p_, s_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  i64 size() const { return n_; }
+  void zero(cudaStream_t s) const {
+    if (n_ > 0) DFCG_CUDA(cudaMemsetAsync(p_, 0, sizeof(T) * static_cast<size_t>(n_), s));
+  }
+
+ private:
+  T* p_ = nullptr;
+  i64 n_ = 0;
+  cudaStream_t s_ = nullptr;
+};
+
+// ---------------------------------------------------------------- dense kernels (dense.cu)
+// C[MxN] = alpha * op(A)[MxK] * op(B)[KxN] + beta * C, all row-major.
+//   !ta: A(i,k) = A[i*lda + k]      ta: A(i,k) = A[k*lda + i]
+//   !tb: B(k,j) = B[k*ldb + j]      tb: B(k,j) = B[j*ldb + k]
+// FP64 DMMA (mma.sync m8n8k4), cp.async multi-stage pipeline, deterministic split-K.
+void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+          const double* B, i64 ldb, double beta, double* C, i64 ldc);
+
+// dst (rows x cols, ldd) = alpha * src (rows x cols, lds)  [alpha may be 1]
+void copy2d(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd, double alpha = 1.0);
+// dst (cols x rows, ldd) = src^T  (src rows x cols, lds)
+void transpose(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd);
+// Set a rows x cols block to the identity pattern (ones on the diagonal).
+void set_identity(cudaStream_t s, i64 rows, i64 cols, double* dst, i64 ldd);
+// out = sum(a .* b) over n elements, deterministic (fixed-shape tree).  out is a device scalar.
+void dot_sum(cudaStream_t s, i64 n, const double* a, const double* b, double* out);
+// Columns gather+scale: dst[:, c] = src[:, idx[c]] * (scale ? scale[c] : 1), rows x ncols, row-major.
+void gather_cols(cudaStream_t s, i64 rows, i64 ncols, const double* src, i64 lds, const int* idx,
+                 const double* scale, double* dst, i64 ldd);
+// Column norms of a row-major rows x cols matrix: out[c] = ||src[:, c]||_2 (deterministic).
+void col_norms(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* out);
+
+// ---------------------------------------------------------------- factorizations (factor.cu)
+struct Workspace;  // forward
+
+// Thin QR of a row-major rows x cols matrix X (rows >= cols): X = Q R, Q overwrites X,
+// R (cols x cols, row-major, upper) written when R != nullptr. CholeskyQR2 fast path
+// with a blocked Householder fallback when the Gram factor is too ill-conditioned.
+// Returns true when the Householder fallback ran.
+bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
+// Householder QR only (tests / fallback).
+void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
+
+// Thin SVD of a row-major rows x cols matrix A (rows >= cols), A is destroyed.
+//   U (rows x cols, ldu), S (cols, device), V (cols x cols, ldv), singular values sorted
+//   nonincreasing (host copy returned in s_host).
+// Method: (rows > 1.25 cols) CholQR2/Householder -> one-sided block Jacobi on R, else
+// one-sided block Jacobi directly on A.
+void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U, i64 ldu, double* V, i64 ldv,
+              std::vector<double>& s_host);
+
+}  // namespace dfcg

@@ -1,0 +1,402 @@
+// Dense FP64 building blocks: DMMA GEMM (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; FP64 has
+// no tcgen05 kind on sm_100a), copies/transposes, deterministic reductions.
+//
+// GEMM tiling: CTA 64x64, BK=16, 4 warps (2x2) of 32x32, 3-stage cp.async pipeline.
+// Shared-memory tiles are stored in the global layout's contiguous order and padded so
+// every DMMA fragment load is a 2-wavefront (conflict-free for 8-byte lanes) access.
+#include "common.cuh"
+
+namespace dfcg {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
+constexpr int PAD_K = BK + 4;   // [rows][k] layout, k contiguous
+constexpr int PAD_MN = BM + 4;  // [k][rows] layout, rows contiguous
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Tile sizes in doubles for one stage.
+template <bool T>  // T == "tile stored [k][rows]" (rows contiguous)
+struct TileShape {
+  static constexpr int elems = T ? BK * PAD_MN : BM * PAD_K;
+};
+
+// Load a 64 (rows) x 16 (k) operand tile into shared memory.
+//   KMajor == false: element (r, k) at g[(r0 + r) * ld + k0 + k]   (k contiguous)
+//   KMajor == true : element (r, k) at g[(k0 + k) * ld + r0 + r]   (rows contiguous)
+template <bool KMajor>
+__device__ __forceinline__ void load_tile(double* sm, const double* g, i64 ld, i64 r0, i64 k0, i64 R, i64 Kend,
+                                          int tid) {
+#pragma unroll
+  for (int it = 0; it < (BM * BK) / THREADS; ++it) {
+    const int e = tid + it * THREADS;
+    if (!KMajor) {
+      const int r = e / BK, k = e % BK;
+      const i64 gr = r0 + r, gk = k0 + k;
+      const bool ok = gr < R && gk < Kend;
+      cp_async8(sm + r * PAD_K + k, ok ? g + gr * ld + gk : g, ok);
+    } else {
+      const int k = e / BM, r = e % BM;
+      const i64 gr = r0 + r, gk = k0 + k;
+      const bool ok = gr < R && gk < Kend;
+      cp_async8(sm + k * PAD_MN + r, ok ? g + gk * ld + gr : g, ok);
+    }
+  }
+}
+
+template <bool KMajor>
+__device__ __forceinline__ double frag(const double* sm, int r, int k) {
+  return KMajor ? sm[k * PAD_MN + r] : sm[r * PAD_K + k];
+}
+
+// A tile: rows = M index. !TA -> A(i,k) at A[i*lda+k] -> [rows][k] layout (KMajor=false).
+//                          TA -> A(i,k) at A[k*lda+i] -> [k][rows] layout (KMajor=true).
+// B tile: rows = N index. !TB -> B(k,j) at B[k*ldb+j] -> rows (j) contiguous -> KMajor=true.
+//                          TB -> B(k,j) at B[j*ldb+k] -> k contiguous -> KMajor=false.
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(THREADS) gemm_kernel(i64 M, i64 N, i64 K, i64 kchunk, double alpha,
+                                                      const double* __restrict__ A, i64 lda,
+                                                      const double* __restrict__ B, i64 ldb, double beta,
+                                                      double* __restrict__ C, i64 ldc, double* __restrict__ ws) {
+  extern __shared__ double smem[];
+  constexpr bool AK = TA, BKm = !TB;
+  constexpr int AE = TileShape<AK>::elems, BE = TileShape<BKm>::elems;
+  double* sA = smem;
+  double* sB = smem + STAGES * AE;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const i64 m0 = static_cast<i64>(blockIdx.y) * BM, n0 = static_cast<i64>(blockIdx.x) * BN;
+  const i64 kbeg = static_cast<i64>(blockIdx.z) * kchunk;
+  const i64 kend = min(K, kbeg + kchunk);
+  const int ntiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < ntiles) {
+      load_tile<AK>(sA + st * AE, A, lda, m0, kbeg + st * BK, M, kend, tid);
+      load_tile<BKm>(sB + st * BE, B, ldb, n0, kbeg + st * BK, N, kend, tid);
+    }
+    cp_async_commit();
+  }
+
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k for A and B (B: col = lane>>2)
+  for (int t = 0; t < ntiles; ++t) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = t + STAGES - 1;
+      if (nt < ntiles) {
+        const int st = nt % STAGES;
+        load_tile<AK>(sA + st * AE, A, lda, m0, kbeg + static_cast<i64>(nt) * BK, M, kend, tid);
+        load_tile<BKm>(sB + st * BE, B, ldb, n0, kbeg + static_cast<i64>(nt) * BK, N, kend, tid);
+      }
+      cp_async_commit();
+    }
+    const double* a = sA + (t % STAGES) * AE;
+    const double* b = sB + (t % STAGES) * BE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = frag<AK>(a, wm + i * 8 + fr, kk + fk);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = frag<BKm>(b, wn + j * 8 + fr, kk + fk);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: lane holds C(row = lane/4, col = 2*(lane%4) + {0,1}) of each 8x8 tile.
+  const int er = lane >> 2, ec = (lane & 3) * 2;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const i64 row = m0 + wm + i * 8 + er;
+      if (row >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const i64 col = n0 + wn + j * 8 + ec + h;
+        if (col >= N) continue;
+        if (ws) {
+          ws[(static_cast<i64>(blockIdx.z) * M + row) * N + col] = acc[i][j][h];
+        } else {
+          double v = alpha * acc[i][j][h];
+          if (beta != 0.0) v += beta * C[row * ldc + col];
+          C[row * ldc + col] = v;
+        }
+      }
+    }
+  }
+}
+
+__global__ void splitk_reduce(i64 M, i64 N, int splits, const double* __restrict__ ws, double alpha, double beta,
+                              double* __restrict__ C, i64 ldc) {
+  const i64 total = M * N;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += ws[z * total + e];
+    const i64 row = e / N, col = e % N;
+    double v = alpha * s;
+    if (beta != 0.0) v += beta * C[row * ldc + col];
+    C[row * ldc + col] = v;
+  }
+}
+
+__global__ void scale_kernel(i64 M, i64 N, double beta, double* C, i64 ldc) {
+  const i64 total = M * N;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 row = e / N, col = e % N;
+    C[row * ldc + col] = beta == 0.0 ? 0.0 : beta * C[row * ldc + col];
+  }
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <bool TA, bool TB>
+void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+                 i64 ldb, double beta, double* C, i64 ldc) {
+  const size_t smem =
+      sizeof(double) * STAGES * (TileShape<TA>::elems + TileShape<!TB>::elems);
+  static unsigned configured = 0;  // one bit per device
+  int dev = 0;
+  DFCG_CUDA(cudaGetDevice(&dev));
+  if (!(configured & (1u << dev))) {
+    DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    configured |= 1u << dev;
+  }
+  const int gx = cdiv(N, BN), gy = cdiv(M, BM);
+  const i64 tiles = static_cast<i64>(gx) * gy;
+  const int target = 2 * num_sms();
+  int splits = 1;
+  if (tiles < target && K > 4 * BK) {
+    splits = static_cast<int>(std::min<i64>((target + tiles - 1) / tiles, (K + 255) / 256));
+    splits = std::max(1, std::min(splits, 64));
+  }
+  i64 kchunk = (K + splits - 1) / splits;
+  kchunk = (kchunk + BK - 1) / BK * BK;
+  splits = static_cast<int>((K + kchunk - 1) / kchunk);
+  if (splits <= 1) {
+    gemm_kernel<TA, TB><<<dim3(gx, gy, 1), THREADS, smem, s>>>(M, N, K, std::max<i64>(K, 1), alpha, A, lda, B, ldb,
+                                                                 beta, C, ldc, nullptr);
+    DFCG_LAUNCH_CHECK();
+    return;
+  }
+  DBuf<double> ws(static_cast<i64>(splits) * M * N, s);
+  gemm_kernel<TA, TB><<<dim3(gx, gy, splits), THREADS, smem, s>>>(M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C,
+                                                                    ldc, ws.get());
+  DFCG_LAUNCH_CHECK();
+  const int rb = static_cast<int>(std::min<i64>((M * N + 255) / 256, 4L * num_sms()));
+  splitk_reduce<<<rb, 256, 0, s>>>(M, N, splits, ws.get(), alpha, beta, C, ldc);
+  DFCG_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- small kernels
+__global__ void copy2d_kernel(i64 rows, i64 cols, const double* __restrict__ src, i64 lds, double* __restrict__ dst,
+                              i64 ldd, double alpha) {
+  const i64 total = rows * cols;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = e / cols, c = e % cols;
+    dst[r * ldd + c] = alpha == 1.0 ? src[r * lds + c] : alpha * src[r * lds + c];
+  }
+}
+
+__global__ void transpose_kernel(i64 rows, i64 cols, const double* __restrict__ src, i64 lds,
+                                 double* __restrict__ dst, i64 ldd) {
+  __shared__ double tile[32][33];
+  const i64 r0 = static_cast<i64>(blockIdx.y) * 32, c0 = static_cast<i64>(blockIdx.x) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const i64 r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[r * lds + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const i64 c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * ldd + r] = tile[threadIdx.x][i];
+  }
+}
+
+__global__ void identity_kernel(i64 rows, i64 cols, double* dst, i64 ldd) {
+  const i64 total = rows * cols;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = e / cols, c = e % cols;
+    dst[r * ldd + c] = r == c ? 1.0 : 0.0;
+  }
+}
+
+// Deterministic two-level reduction: fixed grid of 256 blocks writing partials, then
+// one block summing them in index order.
+constexpr int RED_BLOCKS = 256, RED_THREADS = 256;
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+  if (w == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  }
+  return v;  // valid in thread 0
+}
+
+__global__ void dot_partial(i64 n, const double* __restrict__ a, const double* __restrict__ b, double* part) {
+  double acc = 0.0;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    acc += a[i] * b[i];
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void sum_final(int n, const double* part, double* out) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) *out = acc;
+}
+
+__global__ void gather_cols_kernel(i64 rows, i64 ncols, const double* __restrict__ src, i64 lds,
+                                   const int* __restrict__ idx, const double* __restrict__ scale,
+                                   double* __restrict__ dst, i64 ldd) {
+  const i64 total = rows * ncols;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = e / ncols;
+    const int c = static_cast<int>(e % ncols);
+    const double v = src[r * lds + idx[c]];
+    dst[r * ldd + c] = scale ? v * scale[c] : v;
+  }
+}
+
+// One block per 32-column strip; threads stride rows; fixed-order combination.
+__global__ void col_norms_kernel(i64 rows, i64 cols, const double* __restrict__ src, i64 lds, double* out) {
+  __shared__ double part[8][33];
+  const int c = threadIdx.x & 31, rgrp = threadIdx.x >> 5;  // 8 row groups
+  const i64 col = static_cast<i64>(blockIdx.x) * 32 + c;
+  double acc = 0.0;
+  if (col < cols)
+    for (i64 r = rgrp; r < rows; r += 8) {
+      const double v = src[r * lds + col];
+      acc += v * v;
+    }
+  part[rgrp][c] = acc;
+  __syncthreads();
+  if (rgrp == 0 && col < cols) {
+    double s = 0.0;
+    for (int g = 0; g < 8; ++g) s += part[g][c];
+    out[col] = sqrt(s);
+  }
+}
+
+int grid_for(i64 total, int threads = 256) {
+  return static_cast<int>(std::max<i64>(1, std::min<i64>((total + threads - 1) / threads, 8L * num_sms())));
+}
+
+}  // namespace
+
+void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+          const double* B, i64 ldb, double beta, double* C, i64 ldc) {
+  if (M <= 0 || N <= 0) return;
+  if (K <= 0 || alpha == 0.0) {
+    scale_kernel<<<grid_for(M * N), 256, 0, s>>>(M, N, beta, C, ldc);
+    DFCG_LAUNCH_CHECK();
+    return;
+  }
+  if (!ta && !tb) launch_gemm<false, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (ta && !tb) launch_gemm<true, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (!ta && tb) launch_gemm<false, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else launch_gemm<true, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+void copy2d(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd, double alpha) {
+  if (rows <= 0 || cols <= 0) return;
+  if (alpha == 1.0) {
+    DFCG_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ldd, src, sizeof(double) * lds, sizeof(double) * cols, rows,
+                                cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  copy2d_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, src, lds, dst, ldd, alpha);
+  DFCG_LAUNCH_CHECK();
+}
+
+void transpose(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid(cdiv(cols, 32), cdiv(rows, 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(rows, cols, src, lds, dst, ldd);
+  DFCG_LAUNCH_CHECK();
+}
+
+void set_identity(cudaStream_t s, i64 rows, i64 cols, double* dst, i64 ldd) {
+  if (rows <= 0 || cols <= 0) return;
+  identity_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, dst, ldd);
+  DFCG_LAUNCH_CHECK();
+}
+
+void dot_sum(cudaStream_t s, i64 n, const double* a, const double* b, double* out) {
+  DBuf<double> part(RED_BLOCKS, s);
+  dot_partial<<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, a, b, part.get());
+  DFCG_LAUNCH_CHECK();
+  sum_final<<<1, RED_THREADS, 0, s>>>(RED_BLOCKS, part.get(), out);
+  DFCG_LAUNCH_CHECK();
+}
+
+void gather_cols(cudaStream_t s, i64 rows, i64 ncols, const double* src, i64 lds, const int* idx,
+                 const double* scale, double* dst, i64 ldd) {
+  if (rows <= 0 || ncols <= 0) return;
+  gather_cols_kernel<<<grid_for(rows * ncols), 256, 0, s>>>(rows, ncols, src, lds, idx, scale, dst, ldd);
+  DFCG_LAUNCH_CHECK();
+}
+
+void col_norms(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* out) {
+  if (cols <= 0) return;
+  col_norms_kernel<<<cdiv(cols, 32), 256, 0, s>>>(rows, cols, src, lds, out);
+  DFCG_LAUNCH_CHECK();
+}
+
+}  // namespace dfcg

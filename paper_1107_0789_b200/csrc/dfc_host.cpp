@@ -1,0 +1,411 @@
+// Host DFC orchestrator (see dfc_host.hpp). Restates dfc_proj / dfc_rp / dfc_nys
+// (P/include/dfc/dfc.hpp:166-335) and the D-step (P/include/dfc/sampling.hpp:15-113) with
+// the same RNG stream ids, so partitions and samples are identical to the reference's.
+// Block solves run concurrently on one device (one pooled stream per worker thread).
+#include "dfc_host.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <numeric>
+#include <thread>
+
+namespace dfcg {
+
+HostObs HostObs::make(i64 m, i64 n, std::vector<long long> row, std::vector<long long> col, std::vector<double> val) {
+  if (m < 1 || n < 1) throw std::invalid_argument("ObservedMatrix: dims must be positive");
+  const size_t N = val.size();
+  if (row.size() != N || col.size() != N) throw std::invalid_argument("ObservedMatrix: ragged triplets");
+  std::vector<size_t> ord(N);
+  std::iota(ord.begin(), ord.end(), size_t{0});
+  bool sorted = true;
+  for (size_t i = 1; i < N && sorted; ++i)
+    sorted = col[i - 1] < col[i] || (col[i - 1] == col[i] && row[i - 1] <= row[i]);
+  HostObs o;
+  o.m = m;
+  o.n = n;
+  if (!sorted) {
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](size_t a, size_t b) { return col[a] != col[b] ? col[a] < col[b] : row[a] < row[b]; });
+    o.row.resize(N);
+    o.col.resize(N);
+    o.val.resize(N);
+    for (size_t i = 0; i < N; ++i) {
+      o.row[i] = row[ord[i]];
+      o.col[i] = col[ord[i]];
+      o.val[i] = val[ord[i]];
+    }
+  } else {
+    o.row = std::move(row);
+    o.col = std::move(col);
+    o.val = std::move(val);
+  }
+  for (size_t i = 0; i < N; ++i) {
+    if (o.row[i] < 0 || o.row[i] >= m || o.col[i] < 0 || o.col[i] >= n)
+      throw std::out_of_range("ObservedMatrix: entry (" + std::to_string(o.row[i]) + ", " + std::to_string(o.col[i]) +
+                              ") outside " + std::to_string(m) + "x" + std::to_string(n));
+    if (!std::isfinite(o.val[i])) throw std::invalid_argument("ObservedMatrix: non-finite value");
+    if (i > 0 && o.row[i - 1] == o.row[i] && o.col[i - 1] == o.col[i])
+      throw std::invalid_argument("ObservedMatrix: duplicate entry (" + std::to_string(o.row[i]) + ", " +
+                                  std::to_string(o.col[i]) + ")");
+  }
+  return o;
+}
+
+// sampling.hpp:15-26
+std::vector<i64> sample_without_replacement(i64 n, i64 l, SeededRng& rng) {
+  if (n < 1) throw std::invalid_argument("sample_without_replacement: empty population");
+  if (l < 1 || l > n) throw std::invalid_argument("sample_without_replacement: need 1 <= l <= n");
+  std::vector<i64> perm(static_cast<size_t>(n));
+  std::iota(perm.begin(), perm.end(), i64{0});
+  for (i64 i = 0; i < l; ++i) {
+    const i64 j = i + static_cast<i64>(rng.index(static_cast<std::uint64_t>(n - i)));
+    std::swap(perm[static_cast<size_t>(i)], perm[static_cast<size_t>(j)]);
+  }
+  perm.resize(static_cast<size_t>(l));
+  return perm;
+}
+
+// sampling.hpp:66-79
+std::vector<std::vector<i64>> partition_columns(i64 n, i64 t, SeededRng& rng) {
+  if (t < 1 || t > n) throw std::invalid_argument("partition_columns: need 1 <= t <= n");
+  std::vector<i64> perm = sample_without_replacement(n, n, rng);
+  const i64 base = n / t, rem = n % t;
+  std::vector<std::vector<i64>> groups(static_cast<size_t>(t));
+  size_t at = 0;
+  for (i64 g = 0; g < t; ++g) {
+    const i64 sz = base + (g < rem ? 1 : 0);
+    auto& grp = groups[static_cast<size_t>(g)];
+    grp.assign(perm.begin() + static_cast<std::ptrdiff_t>(at), perm.begin() + static_cast<std::ptrdiff_t>(at + sz));
+    std::sort(grp.begin(), grp.end());
+    at += static_cast<size_t>(sz);
+  }
+  return groups;
+}
+
+// sampling.hpp:83-97 (entries stay column-major sorted: columns are relabelled monotonically)
+HostObs extract_columns(const HostObs& obs, const std::vector<i64>& idx) {
+  std::vector<i64> pos(static_cast<size_t>(obs.n), -1);
+  for (size_t p = 0; p < idx.size(); ++p) {
+    const i64 c = idx[p];
+    if (c < 0 || c >= obs.n) throw std::out_of_range("extract_columns: index out of range");
+    if (pos[static_cast<size_t>(c)] >= 0) throw std::invalid_argument("extract_columns: duplicate index");
+    pos[static_cast<size_t>(c)] = static_cast<i64>(p);
+  }
+  std::vector<long long> r, c;
+  std::vector<double> v;
+  for (i64 e = 0; e < obs.count(); ++e) {
+    const i64 p = pos[static_cast<size_t>(obs.col[e])];
+    if (p >= 0) {
+      r.push_back(obs.row[e]);
+      c.push_back(p);
+      v.push_back(obs.val[e]);
+    }
+  }
+  return HostObs::make(obs.m, static_cast<i64>(idx.size()), std::move(r), std::move(c), std::move(v));
+}
+
+// sampling.hpp:99-113
+HostObs extract_rows(const HostObs& obs, const std::vector<i64>& idx) {
+  std::vector<i64> pos(static_cast<size_t>(obs.m), -1);
+  for (size_t p = 0; p < idx.size(); ++p) {
+    const i64 r = idx[p];
+    if (r < 0 || r >= obs.m) throw std::out_of_range("extract_rows: index out of range");
+    if (pos[static_cast<size_t>(r)] >= 0) throw std::invalid_argument("extract_rows: duplicate index");
+    pos[static_cast<size_t>(r)] = static_cast<i64>(p);
+  }
+  std::vector<long long> r, c;
+  std::vector<double> v;
+  for (i64 e = 0; e < obs.count(); ++e) {
+    const i64 p = pos[static_cast<size_t>(obs.row[e])];
+    if (p >= 0) {
+      r.push_back(p);
+      c.push_back(obs.col[e]);
+      v.push_back(obs.val[e]);
+    }
+  }
+  return HostObs::make(static_cast<i64>(idx.size()), obs.n, std::move(r), std::move(c), std::move(v));
+}
+
+// make_base_solver, dfc.hpp:70-78.
+BaseSolver make_base_solver(DeviceContext& ctx, Task task, const ApgConfig& cfg, double lambda) {
+  if (task == Task::MC)
+    return [&ctx, cfg](const HostObs& b, cudaStream_t s) {
+      DevLowRank L;
+      SolveReport rep;
+      apg_mc_device(ctx, s, b.m, b.n, b.count(), b.row.data(), b.col.data(), b.val.data(), cfg, L, rep, nullptr);
+      return std::pair<DevLowRank, SolveReport>{std::move(L), rep};
+    };
+  return [&ctx, cfg, lambda](const HostObs& b, cudaStream_t s) {
+    const double lam = lambda > 0 ? lambda : 1.0 / std::sqrt(static_cast<double>(std::max(b.m, b.n)));
+    std::vector<double> dense(static_cast<size_t>(b.m * b.n), 0.0);  // densify (matrix_io.hpp:119-123)
+    for (i64 e = 0; e < b.count(); ++e) dense[static_cast<size_t>(b.col[e] * b.m + b.row[e])] = b.val[e];
+    DevLowRank L;
+    SolveReport rep;
+    std::vector<long long> sr, sc;
+    std::vector<double> sv;
+    apg_rmf_device(ctx, s, dense.data(), b.m, b.n, lam, cfg, L, sr, sc, sv, rep, nullptr);
+    return std::pair<DevLowRank, SolveReport>{std::move(L), rep};
+  };
+}
+
+namespace {
+
+// parallel_for, dfc.hpp:84-119 — each worker thread holds its own pooled stream.
+template <class Fn>
+void parallel_for(DeviceContext& ctx, std::size_t count, int workers, Fn&& fn) {
+  if (workers < 1) throw std::invalid_argument("parallel_for: workers must be >= 1");
+  const std::size_t nthreads = std::min<std::size_t>(static_cast<std::size_t>(workers), count);
+  std::vector<std::string> failures(count);
+  std::vector<char> failed(count, 0);
+  if (nthreads <= 1) {
+    CallStream cs(ctx);
+    for (std::size_t i = 0; i < count; ++i) {
+      try {
+        fn(i, cs.s);
+      } catch (const std::exception& e) {
+        throw BlockError(i, e.what());
+      }
+    }
+    return;
+  }
+  std::atomic<std::size_t> next{0};
+  auto worker = [&]() {
+    CallStream cs(ctx);
+    for (;;) {
+      const std::size_t i = next.fetch_add(1);
+      if (i >= count) return;
+      try {
+        fn(i, cs.s);
+      } catch (const std::exception& e) {
+        failures[i] = e.what();
+        failed[i] = 1;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (std::size_t w = 0; w < nthreads; ++w) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  for (std::size_t i = 0; i < count; ++i)
+    if (failed[i]) throw BlockError(i, failures[i]);
+}
+
+struct PhaseClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double lap() {
+    const auto t1 = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t0 = t1;
+    return ms;
+  }
+};
+
+// solve_blocks, dfc.hpp:133-147.
+void solve_blocks(DeviceContext& ctx, const std::vector<HostObs>& blocks, const BaseSolver& solver, int workers,
+                  std::vector<DevLowRank>& ests, std::vector<SolveReport>& reports) {
+  ests.clear();
+  ests.resize(blocks.size());
+  reports.assign(blocks.size(), SolveReport{});
+  parallel_for(ctx, blocks.size(), workers, [&](std::size_t i, cudaStream_t s) {
+    if (blocks[i].empty()) {
+      ests[i].m = blocks[i].m;
+      ests[i].n = blocks[i].n;
+      ests[i].k = 0;
+      return;
+    }
+    auto [est, rep] = solver(blocks[i], s);
+    ests[i] = std::move(est);
+    reports[i] = rep;
+  });
+}
+
+std::vector<i64> block_ranks(const std::vector<DevLowRank>& ests) {
+  std::vector<i64> r;
+  for (const auto& e : ests) r.push_back(e.k);
+  return r;
+}
+
+std::vector<const DevLowRank*> ptrs(const std::vector<DevLowRank>& v) {
+  std::vector<const DevLowRank*> p;
+  for (const auto& e : v) p.push_back(&e);
+  return p;
+}
+
+}  // namespace
+
+// median_rank, dfc.hpp:159-164.
+i64 median_rank(const std::vector<i64>& ranks) {
+  if (ranks.empty()) throw std::invalid_argument("median_rank: empty list");
+  std::vector<i64> sorted = ranks;
+  std::sort(sorted.begin(), sorted.end());
+  return std::max<i64>(1, sorted[(sorted.size() - 1) / 2]);
+}
+
+// dfc_proj, dfc.hpp:166-200.
+std::pair<DevLowRank, DfcReport> dfc_proj(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg,
+                                          const BaseSolver& solver) {
+  if (cfg.variant != DfcVariant::Proj) throw std::invalid_argument("dfc_proj: wrong variant");
+  if (cfg.t < 1 || cfg.t > obs.n) throw std::invalid_argument("dfc_proj: need 1 <= t <= n");
+  DfcReport report;
+  PhaseClock total, phase;
+  SeededRng prng(cfg.seed, streams::partition);
+  auto plan = partition_columns(obs.n, cfg.t, prng);
+  std::vector<HostObs> blocks;
+  for (const auto& g : plan) blocks.push_back(extract_columns(obs, g));
+  report.divide_ms = phase.lap();
+  std::vector<DevLowRank> ests;
+  solve_blocks(ctx, blocks, solver, cfg.workers, ests, report.subproblems);
+  report.factor_ms = phase.lap();
+  DevLowRank out;
+  out.m = obs.m;
+  out.n = obs.n;
+  const auto bl = ptrs(ests);
+  if (!cfg.ensemble) {
+    CallStream cs(ctx);
+    column_project(cs.s, ests[0], bl, plan, obs.n, out);
+  } else {
+    std::vector<DevLowRank> projected(ests.size());
+    parallel_for(ctx, ests.size(), cfg.workers,
+                 [&](std::size_t i, cudaStream_t s) { column_project(s, ests[i], bl, plan, obs.n, projected[i]); });
+    CallStream cs(ctx);
+    average_estimates(cs.s, ptrs(projected), median_rank(block_ranks(ests)), out);
+  }
+  report.combine_ms = phase.lap();
+  report.total_ms = total.lap();
+  return {std::move(out), std::move(report)};
+}
+
+// dfc_rp, dfc.hpp:202-248.
+std::pair<DevLowRank, DfcReport> dfc_rp(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg,
+                                        const BaseSolver& solver) {
+  if (cfg.variant != DfcVariant::Rp) throw std::invalid_argument("dfc_rp: wrong variant");
+  if (cfg.t < 1 || cfg.t > obs.n) throw std::invalid_argument("dfc_rp: need 1 <= t <= n");
+  DfcReport report;
+  PhaseClock total, phase;
+  SeededRng prng(cfg.seed, streams::partition);
+  auto plan = partition_columns(obs.n, cfg.t, prng);
+  std::vector<HostObs> blocks;
+  for (const auto& g : plan) blocks.push_back(extract_columns(obs, g));
+  report.divide_ms = phase.lap();
+  std::vector<DevLowRank> ests;
+  solve_blocks(ctx, blocks, solver, cfg.workers, ests, report.subproblems);
+  report.factor_ms = phase.lap();
+  i64 k = median_rank(block_ranks(ests)), p = cfg.rp_p;
+  const i64 minmn = std::min(obs.m, obs.n);
+  if (k + p > minmn) {
+    report.k_clamped = true;
+    p = std::min(p, minmn - 1);
+    k = minmn - p;
+  }
+  report.chosen_k = k;
+  DevLowRank out;
+  const auto bl = ptrs(ests);
+  if (!cfg.ensemble) {
+    SeededRng rng(cfg.seed, streams::rp_draw);
+    CallStream cs(ctx);
+    random_project(cs.s, bl, plan, obs.n, k, p, cfg.rp_q, rng, out);
+  } else {
+    std::vector<DevLowRank> draws(static_cast<size_t>(cfg.t));
+    parallel_for(ctx, draws.size(), cfg.workers, [&](std::size_t i, cudaStream_t s) {
+      SeededRng rng(cfg.seed, streams::rp_draw + 1 + i);
+      random_project(s, bl, plan, obs.n, k, p, cfg.rp_q, rng, draws[i]);
+    });
+    CallStream cs(ctx);
+    average_estimates(cs.s, ptrs(draws), k, out);
+  }
+  report.combine_ms = phase.lap();
+  report.total_ms = total.lap();
+  return {std::move(out), std::move(report)};
+}
+
+// dfc_nys, dfc.hpp:250-324.
+std::pair<DevLowRank, DfcReport> dfc_nys(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg,
+                                         const BaseSolver& solver) {
+  if (cfg.variant != DfcVariant::Nys) throw std::invalid_argument("dfc_nys: wrong variant");
+  const i64 m = obs.m, n = obs.n;
+  if (cfg.l < 1 || cfg.l > n) throw std::invalid_argument("dfc_nys: need 1 <= l <= n");
+  if (cfg.d < 1 || cfg.d > m) throw std::invalid_argument("dfc_nys: need 1 <= d <= m");
+  DfcReport report;
+  PhaseClock total, phase;
+  SeededRng row_rng(cfg.seed, streams::nys_rows);
+  std::vector<i64> row_idx = sample_without_replacement(m, cfg.d, row_rng);
+  std::sort(row_idx.begin(), row_idx.end());
+  auto pair_deficient = [&](cudaStream_t s, const DevLowRank& C, const DevLowRank& R) {
+    const i64 kmax = std::max(C.k, R.k);
+    if (kmax == 0 || C.k == 0) return kmax > 0;
+    const i64 d = static_cast<i64>(row_idx.size());
+    // Wleft = C.left[row_idx, :]
+    std::vector<double> hl(static_cast<size_t>(C.m * C.k)), hw(static_cast<size_t>(d * C.k));
+    DFCG_CUDA(cudaMemcpyAsync(hl.data(), C.left.get(), sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, s));
+    DFCG_CUDA(cudaStreamSynchronize(s));
+    for (i64 i = 0; i < d; ++i)
+      for (i64 c = 0; c < C.k; ++c) hw[static_cast<size_t>(i * C.k + c)] = hl[static_cast<size_t>(row_idx[i] * C.k + c)];
+    DBuf<double> W(d * C.k, s);
+    DFCG_CUDA(cudaMemcpyAsync(W.get(), hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice, s));
+    SvdOfProduct f = svd_of_product(s, d, C.n, C.k, W.get(), C.right.get());
+    return f.r < kmax;
+  };
+  if (!cfg.ensemble) {
+    SeededRng col_rng(cfg.seed, streams::nys_cols);
+    std::vector<i64> col_idx = sample_without_replacement(n, cfg.l, col_rng);
+    std::sort(col_idx.begin(), col_idx.end());
+    std::vector<HostObs> blocks{extract_columns(obs, col_idx), extract_rows(obs, row_idx)};
+    report.divide_ms = phase.lap();
+    std::vector<DevLowRank> ests;
+    solve_blocks(ctx, blocks, solver, cfg.workers, ests, report.subproblems);
+    report.factor_ms = phase.lap();
+    DevLowRank out;
+    {
+      CallStream cs(ctx);
+      report.rank_deficient = pair_deficient(cs.s, ests[0], ests[1]);
+      gen_nystrom(cs.s, ests[0], ests[1], row_idx, col_idx, out);
+    }
+    report.combine_ms = phase.lap();
+    report.total_ms = total.lap();
+    return {std::move(out), std::move(report)};
+  }
+  const i64 groups =
+      std::clamp<i64>(static_cast<i64>(std::llround(static_cast<double>(n) / static_cast<double>(cfg.l))), 1, n);
+  SeededRng prng(cfg.seed, streams::partition);
+  auto plan = partition_columns(n, groups, prng);
+  std::vector<HostObs> blocks;
+  for (const auto& g : plan) blocks.push_back(extract_columns(obs, g));
+  blocks.push_back(extract_rows(obs, row_idx));
+  report.divide_ms = phase.lap();
+  std::vector<DevLowRank> ests;
+  solve_blocks(ctx, blocks, solver, cfg.workers, ests, report.subproblems);
+  report.factor_ms = phase.lap();
+  const DevLowRank& R_hat = ests.back();
+  const size_t nc = ests.size() - 1;
+  std::vector<DevLowRank> combined(nc);
+  std::vector<char> deficient(nc, 0);
+  parallel_for(ctx, nc, cfg.workers, [&](std::size_t i, cudaStream_t s) {
+    deficient[i] = pair_deficient(s, ests[i], R_hat) ? 1 : 0;
+    gen_nystrom(s, ests[i], R_hat, row_idx, plan[i], combined[i]);
+  });
+  for (char f : deficient) report.rank_deficient = report.rank_deficient || f;
+  std::vector<i64> col_ranks;
+  for (size_t i = 0; i < nc; ++i) col_ranks.push_back(ests[i].k);
+  DevLowRank out;
+  {
+    CallStream cs(ctx);
+    average_estimates(cs.s, ptrs(combined), median_rank(col_ranks), out);
+  }
+  report.combine_ms = phase.lap();
+  report.total_ms = total.lap();
+  return {std::move(out), std::move(report)};
+}
+
+// dfc_run, dfc.hpp:326-335.
+std::pair<DevLowRank, DfcReport> dfc_run(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg) {
+  const BaseSolver solver = make_base_solver(ctx, cfg.task, cfg.solver_cfg, cfg.lambda);
+  switch (cfg.variant) {
+    case DfcVariant::Proj: return dfc_proj(ctx, obs, cfg, solver);
+    case DfcVariant::Rp: return dfc_rp(ctx, obs, cfg, solver);
+    case DfcVariant::Nys: return dfc_nys(ctx, obs, cfg, solver);
+  }
+  throw std::logic_error("dfc_run: unknown variant");
+}
+
+}  // namespace dfcg

@@ -1,0 +1,78 @@
+// Host-side DFC orchestrator (C++), mirroring P/include/dfc/dfc.hpp and the D-step helpers of
+// P/include/dfc/sampling.hpp. The F-step BaseSolver and the C-step combiners run on the
+// device; estimates stay resident in HBM between the steps.
+#pragma once
+
+#include <functional>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "solver.hpp"
+
+namespace dfcg {
+
+// ObservedMatrix (matrix_io.hpp:36-67): triplets sorted column-major, validated.
+struct HostObs {
+  i64 m = 0, n = 0;
+  std::vector<long long> row, col;
+  std::vector<double> val;
+  i64 count() const { return static_cast<i64>(val.size()); }
+  bool empty() const { return val.empty(); }
+  static HostObs make(i64 m, i64 n, std::vector<long long> row, std::vector<long long> col, std::vector<double> val);
+};
+
+enum class Task { MC = 0, RMF = 1 };
+enum class DfcVariant { Proj = 0, Rp = 1, Nys = 2 };
+
+namespace streams {
+inline constexpr std::uint64_t partition = 0xDFC0000000000001ull;
+inline constexpr std::uint64_t nys_rows = 0xDFC0000000000002ull;
+inline constexpr std::uint64_t nys_cols = 0xDFC0000000000003ull;
+inline constexpr std::uint64_t rp_draw = 0xDFC0000000000100ull;
+}  // namespace streams
+
+struct DfcConfig {
+  DfcVariant variant = DfcVariant::Proj;
+  bool ensemble = false;
+  i64 t = 4, l = 0, d = 0;
+  i64 rp_p = 5, rp_q = 2;
+  std::uint64_t seed = 0;
+  ApgConfig solver_cfg;
+  Task task = Task::MC;
+  double lambda = 0.0;
+  int workers = 1;
+};
+
+struct BlockError : std::runtime_error {
+  BlockError(std::size_t block, const std::string& what)
+      : std::runtime_error("block " + std::to_string(block) + ": " + what), block(block) {}
+  std::size_t block;
+};
+
+struct DfcReport {
+  std::vector<SolveReport> subproblems;
+  double divide_ms = 0, factor_ms = 0, combine_ms = 0, total_ms = 0;
+  i64 chosen_k = 0;
+  bool k_clamped = false, rank_deficient = false;
+};
+
+// BaseSolver (dfc.hpp:67-68), returning a device-resident estimate.
+using BaseSolver = std::function<std::pair<DevLowRank, SolveReport>(const HostObs&, cudaStream_t)>;
+BaseSolver make_base_solver(DeviceContext& ctx, Task task, const ApgConfig& cfg, double lambda = 0.0);
+
+std::vector<i64> sample_without_replacement(i64 n, i64 l, SeededRng& rng);
+std::vector<std::vector<i64>> partition_columns(i64 n, i64 t, SeededRng& rng);
+HostObs extract_columns(const HostObs& obs, const std::vector<i64>& idx);
+HostObs extract_rows(const HostObs& obs, const std::vector<i64>& idx);
+i64 median_rank(const std::vector<i64>& ranks);
+
+std::pair<DevLowRank, DfcReport> dfc_run(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg);
+std::pair<DevLowRank, DfcReport> dfc_proj(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg,
+                                          const BaseSolver& solver);
+std::pair<DevLowRank, DfcReport> dfc_rp(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg,
+                                        const BaseSolver& solver);
+std::pair<DevLowRank, DfcReport> dfc_nys(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg,
+                                         const BaseSolver& solver);
+
+}  // namespace dfcg

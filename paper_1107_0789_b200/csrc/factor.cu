@@ -1,0 +1,633 @@
+// Dense FP64 factorizations on the device: thin QR and thin SVD.
+//
+// thin_qr  (stands in for Eigen HouseholderQR in thin_qr, P/include/dfc/sketch.hpp:41-47):
+//   CholeskyQR2 — Gram by DMMA GEMM, blocked Cholesky (64x64 diagonal blocks in shared
+//   memory, TRSM/SYRK as GEMMs), explicit triangular inverse, Q = X R^-1 as one GEMM —
+//   repeated twice. When a Cholesky pivot signals cond(X) > ~3e5 (or rank deficiency), the
+//   call falls back to blocked Householder QR (panel kernel + compact-WY GEMM updates),
+//   which is what the reference computes. Only span(Q) matters downstream: every consumer
+//   (randomized range finder, svd_of_product) is invariant to the choice of basis.
+// thin_svd (stands in for Eigen BDCSVD, sketch.hpp:57-86, solvers.hpp:90-93):
+//   optional QR preconditioning, then one-sided block Jacobi (16-column blocks, round-robin
+//   pair ordering, Gram/update by DMMA, inner 32x32 symmetric Jacobi in shared memory).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "common.cuh"
+
+namespace dfcg {
+
+namespace {
+
+int grid_for(i64 total, int threads = 256) {
+  return static_cast<int>(std::max<i64>(1, std::min<i64>((total + threads - 1) / threads, 4096)));
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// ================================================================ Cholesky (upper, G = R^T R)
+constexpr int CNB = 64;
+
+__global__ void diag_max_kernel(i64 n, const double* G, i64 ldg, double* out) {
+  __shared__ double sh[256];
+  double m = 0.0;
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, G[i * ldg + i]);
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// Factor the kb x kb diagonal block at (k0,k0) in place (upper R), write its inverse into
+// Rinv at (k0,k0). Pivots below rel_tol * maxdiag set *fail and are replaced by 1.
+__global__ void potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr, const double* maxdiag,
+                                  double rel_tol, int* fail) {
+  extern __shared__ double dyn[];
+  double(*a)[CNB + 1] = reinterpret_cast<double(*)[CNB + 1]>(dyn);
+  double(*inv)[CNB + 1] = reinterpret_cast<double(*)[CNB + 1]>(dyn + CNB * (CNB + 1));
+  __shared__ double piv;
+  const int t = threadIdx.x;
+  for (int e = t; e < kb * kb; e += blockDim.x) a[e / kb][e % kb] = G[(e / kb) * ldg + (e % kb)];
+  __syncthreads();
+  const double thr = rel_tol * (*maxdiag);
+  for (int k = 0; k < kb; ++k) {
+    if (t == 0) {
+      double d = a[k][k];
+      if (!(d > thr) || !isfinite(d)) {
+        atomicExch(fail, 1);
+        d = 1.0;
+      }
+      piv = sqrt(d);
+      a[k][k] = piv;
+    }
+    __syncthreads();
+    for (int j = k + 1 + t; j < kb; j += blockDim.x) a[k][j] /= piv;
+    __syncthreads();
+    const int rem = kb - k - 1;
+    for (int e = t; e < rem * rem; e += blockDim.x) {
+      const int i = k + 1 + e / rem, j = k + 1 + e % rem;
+      if (j >= i) a[i][j] -= a[k][i] * a[k][j];
+    }
+    __syncthreads();
+  }
+  // zero strictly-lower part, invert the upper triangle column by column
+  for (int e = t; e < kb * kb; e += blockDim.x) {
+    const int i = e / kb, j = e % kb;
+    if (i > j) a[i][j] = 0.0;
+    inv[i][j] = 0.0;
+  }
+  __syncthreads();
+  for (int j = t; j < kb; j += blockDim.x) {
+    inv[j][j] = 1.0 / a[j][j];
+    for (int i = j - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int l = i + 1; l <= j; ++l) s += a[i][l] * inv[l][j];
+      inv[i][j] = -s / a[i][i];
+    }
+  }
+  __syncthreads();
+  for (int e = t; e < kb * kb; e += blockDim.x) {
+    const int i = e / kb, j = e % kb;
+    G[i * ldg + j] = a[i][j];
+    Rinv[i * ldr + j] = inv[i][j];
+  }
+}
+
+__global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
+  const i64 total = n * n;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = e / n, j = e % n;
+    if (i > j) A[i * lda + j] = 0.0;
+  }
+}
+
+// In-place blocked Cholesky of G (n x n) -> upper R (lower part zeroed); Rinv = R^-1.
+constexpr size_t kPotrfSmem = sizeof(double) * 2 * CNB * (CNB + 1);
+
+void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol, int* fail) {
+  static unsigned configured = 0;
+  int dev = 0;
+  DFCG_CUDA(cudaGetDevice(&dev));
+  if (!(configured & (1u << dev))) {
+    DFCG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kPotrfSmem)));
+    configured |= 1u << dev;
+  }
+  DBuf<double> maxdiag(1, s);
+  diag_max_kernel<<<1, 256, 0, s>>>(n, G, ldg, maxdiag.get());
+  DFCG_LAUNCH_CHECK();
+  DFCG_CUDA(cudaMemset2DAsync(Rinv, sizeof(double) * ldr, 0, sizeof(double) * n, n, s));
+  for (i64 k0 = 0; k0 < n; k0 += CNB) {
+    const int kb = static_cast<int>(std::min<i64>(CNB, n - k0));
+    double* Gkk = G + k0 * ldg + k0;
+    potrf_diag_kernel<<<1, 256, kPotrfSmem, s>>>(kb, Gkk, ldg, Rinv + k0 * ldr + k0, ldr, maxdiag.get(), rel_tol,
+                                                 fail);
+    DFCG_LAUNCH_CHECK();
+    const i64 rem = n - k0 - kb;
+    if (rem > 0) {
+      double* panel = G + k0 * ldg + k0 + kb;  // kb x rem
+      // R[k, J] = Rkk^-T G[k, J]
+      gemm(s, true, false, kb, rem, kb, 1.0, Rinv + k0 * ldr + k0, ldr, panel, ldg, 0.0, panel, ldg);
+      // G[J, J] -= R[k,J]^T R[k,J]
+      double* trail = G + (k0 + kb) * ldg + k0 + kb;
+      gemm(s, true, false, rem, rem, kb, -1.0, panel, ldg, panel, ldg, 1.0, trail, ldg);
+    }
+  }
+  zero_lower_kernel<<<grid_for(n * n), 256, 0, s>>>(n, G, ldg);
+  DFCG_LAUNCH_CHECK();
+  // Off-diagonal blocks of the inverse: Rinv[0:J, J] = -Rinv[0:J,0:J] R[0:J, J] Rinv[J,J].
+  if (n > CNB) {
+    DBuf<double> T(n * CNB, s);
+    for (i64 j0 = CNB; j0 < n; j0 += CNB) {
+      const i64 jb = std::min<i64>(CNB, n - j0);
+      gemm(s, false, false, j0, jb, j0, 1.0, Rinv, ldr, G + j0, ldg, 0.0, T.get(), jb);
+      gemm(s, false, false, j0, jb, jb, -1.0, T.get(), jb, Rinv + j0 * ldr + j0, ldr, 0.0, Rinv + j0, ldr);
+    }
+  }
+}
+
+// ================================================================ Householder QR (fallback)
+constexpr int HNB = 32, HTHREADS = 512;
+
+// LAPACK dgeqr2 on the panel X[p0:, p0:p0+nb] (row-major, ld). Reflector j stored below the
+// diagonal (implicit unit head), beta on the diagonal, tau[j].
+__global__ void __launch_bounds__(HTHREADS) hh_panel_kernel(i64 rows, int nb, double* X, i64 ld, double* tau) {
+  __shared__ double red[HTHREADS / 32][HNB + 1];
+  __shared__ double colsum[HNB + 1];
+  __shared__ double s_beta, s_tau, s_scale;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int j = 0; j < nb; ++j) {
+    // norm^2 of X[j+1:, j]
+    double acc = 0.0;
+    for (i64 r = j + 1 + t; r < rows; r += HTHREADS) {
+      const double v = X[r * ld + j];
+      acc += v * v;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp][0] = acc;
+    __syncthreads();
+    if (t == 0) {
+      double nrm2 = 0.0;
+      for (int w = 0; w < HTHREADS / 32; ++w) nrm2 += red[w][0];
+      const double alpha = X[static_cast<i64>(j) * ld + j];
+      if (nrm2 == 0.0) {
+        s_tau = 0.0;
+        s_beta = alpha;
+        s_scale = 0.0;
+      } else {
+        const double beta = -copysign(sqrt(alpha * alpha + nrm2), alpha);
+        s_tau = (beta - alpha) / beta;
+        s_scale = 1.0 / (alpha - beta);
+        s_beta = beta;
+      }
+      tau[j] = s_tau;
+      X[static_cast<i64>(j) * ld + j] = s_beta;
+    }
+    __syncthreads();
+    const double sc = s_scale, tj = s_tau;
+    for (i64 r = j + 1 + t; r < rows; r += HTHREADS) X[r * ld + j] *= sc;
+    __syncthreads();
+    if (tj == 0.0) continue;
+    // w_c = x_c[j] + sum_r v_r x_c[r] for remaining panel columns c
+    const int nc = nb - j - 1;
+    if (nc <= 0) continue;
+    double part[HNB];
+#pragma unroll
+    for (int c = 0; c < HNB; ++c) part[c] = 0.0;
+    for (i64 r = j + 1 + t; r < rows; r += HTHREADS) {
+      const double v = X[r * ld + j];
+#pragma unroll
+      for (int c = 0; c < HNB; ++c)
+        if (c < nc) part[c] += v * X[r * ld + j + 1 + c];
+    }
+#pragma unroll
+    for (int c = 0; c < HNB; ++c) {
+      double v = part[c];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][c] = v;
+    }
+    __syncthreads();
+    if (t < nc) {
+      double s = X[static_cast<i64>(j) * ld + j + 1 + t];
+      for (int w = 0; w < HTHREADS / 32; ++w) s += red[w][t];
+      colsum[t] = tj * s;
+    }
+    __syncthreads();
+    for (int c = t; c < nc; c += HTHREADS) X[static_cast<i64>(j) * ld + j + 1 + c] -= colsum[c];
+    for (i64 r = j + 1 + t; r < rows; r += HTHREADS) {
+      const double v = X[r * ld + j];
+      for (int c = 0; c < nc; ++c) X[r * ld + j + 1 + c] -= colsum[c] * v;
+    }
+    __syncthreads();
+  }
+}
+
+// Explicit panel V (rows x nb, unit diagonal, zeros above) from the factored panel.
+__global__ void hh_extract_v(i64 rows, int nb, const double* X, i64 ld, double* V) {
+  const i64 total = rows * nb;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = e / nb;
+    const int c = static_cast<int>(e % nb);
+    V[e] = r < c ? 0.0 : (r == c ? 1.0 : X[r * ld + c]);
+  }
+}
+
+// dlarft (forward, columnwise): T upper nb x nb from S = V^T V and tau.
+__global__ void hh_build_t(int nb, const double* S, const double* tau, double* T) {
+  __shared__ double t[HNB][HNB + 1];
+  const int i = threadIdx.x;
+  for (int e = i; e < HNB * (HNB + 1); e += blockDim.x) (&t[0][0])[e] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    // T[0:j, j] = -tau_j * T[0:j, 0:j] * S[0:j, j]
+    double v = 0.0;
+    if (i < j)
+      for (int l = i; l < j; ++l) v += t[i][l] * S[l * nb + j];
+    __syncthreads();
+    if (i < j) t[i][j] = -tau[j] * v;
+    if (i == j) t[j][j] = tau[j];
+    __syncthreads();
+  }
+  for (int e = i; e < nb * nb; e += blockDim.x) T[e] = t[e / nb][e % nb];
+}
+
+__global__ void extract_upper(i64 n, const double* X, i64 ldx, double* R, i64 ldr) {
+  const i64 total = n * n;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = e / n, j = e % n;
+    R[i * ldr + j] = i <= j ? X[i * ldx + j] : 0.0;
+  }
+}
+
+// ================================================================ one-sided block Jacobi SVD
+constexpr int JNB = 16, JW = 2 * JNB, JTHREADS = 256, JCHUNK = 64;
+
+// Round-robin schedule: pairs[(round * npairs + p) * 2 + {0,1}] = block ids.
+std::vector<int> round_robin(int p) {
+  std::vector<int> out;
+  std::vector<int> ring(p);
+  std::iota(ring.begin(), ring.end(), 0);
+  for (int r = 0; r < p - 1; ++r) {
+    for (int k = 0; k < p / 2; ++k) {
+      out.push_back(ring[k]);
+      out.push_back(ring[p - 1 - k]);
+    }
+    // rotate all but the first
+    const int last = ring[p - 1];
+    for (int k = p - 1; k > 1; --k) ring[k] = ring[k - 1];
+    ring[1] = last;
+  }
+  return out;
+}
+
+// One Jacobi round: each CTA orthogonalises the 32 columns of one block pair of W (rows x n)
+// and applies the same rotation to the pair's columns of V (nv x n).
+__global__ void __launch_bounds__(JTHREADS) jacobi_round_kernel(i64 rows, i64 nv, double* W, i64 ldw, double* V,
+                                                                i64 ldv, const int* pairs, double tol,
+                                                                unsigned long long* offmax, int inner_sweeps) {
+  __shared__ double chunk[JCHUNK][JW + 1];
+  __shared__ double g[JW][JW + 1];
+  __shared__ double rot[JW][JW + 1];
+  __shared__ double cs[JW / 2][2];
+  __shared__ int pp[JW / 2][2];
+  __shared__ double s_off;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int bi = pairs[2 * blockIdx.x], bj = pairs[2 * blockIdx.x + 1];
+  // column c of the pair (0..31) -> global column
+  auto gcol = [&](int c) -> i64 { return c < JNB ? static_cast<i64>(bi) * JNB + c : static_cast<i64>(bj) * JNB + c - JNB; };
+
+  // ---- Gram G = P^T P, P = W[:, pair cols]; warp w owns output tiles (w/2, 2*(w%2)+{0,1}) of 4x4 8x8 tiles
+  double acc[2][2] = {{0, 0}, {0, 0}};
+  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
+  for (i64 r0 = 0; r0 < rows; r0 += JCHUNK) {
+    __syncthreads();
+    for (int e = t; e < JCHUNK * JW; e += JTHREADS) {
+      const int r = e / JW, c = e % JW;
+      const i64 gr = r0 + r;
+      chunk[r][c] = gr < rows ? W[gr * ldw + gcol(c)] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < JCHUNK; k += 4) {
+      // A = P^T (32 x K): A(i,k) = chunk[k][i]; B = P: B(k,j) = chunk[k][j]
+      const double a = chunk[k + (lane & 3)][ti * 8 + (lane >> 2)];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double b = chunk[k + (lane & 3)][(tj0 + q) * 8 + (lane >> 2)];
+        dmma(acc[q], a, b);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int r = ti * 8 + (lane >> 2), c = (tj0 + q) * 8 + (lane & 3) * 2;
+    g[r][c] = acc[q][0];
+    g[r][c + 1] = acc[q][1];
+  }
+  for (int e = t; e < JW * JW; e += JTHREADS) rot[e / JW][e % JW] = (e / JW == e % JW) ? 1.0 : 0.0;
+  __syncthreads();
+
+  auto off_measure = [&]() {
+    // max |g_ab| / sqrt(g_aa g_bb) over all a < b of the 32 pair columns
+    double mx = 0.0;
+    for (int e = t; e < JW * JW; e += JTHREADS) {
+      const int a = e / JW, b = e % JW;
+      if (a >= b) continue;
+      const double d = sqrt(g[a][a]) * sqrt(g[b][b]);
+      if (d > 0.0) mx = fmax(mx, fabs(g[a][b]) / d);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __syncthreads();
+    if (t == 0) s_off = 0.0;
+    __syncthreads();
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_off),
+                             static_cast<unsigned long long>(__double_as_longlong(mx)));
+    __syncthreads();
+    return s_off;
+  };
+  const double off0 = off_measure();
+  if (t == 0) atomicMax(offmax, static_cast<unsigned long long>(__double_as_longlong(off0)));
+  if (off0 <= tol) return;  // pair already orthogonal: leave columns untouched
+
+  // ---- inner cyclic Jacobi on g (32x32), parallel ordering (16 rotations per step)
+  for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
+    if (sweep > 0 && off_measure() <= 0.1 * tol) break;
+    for (int step = 0; step < JW - 1; ++step) {
+      if (t < JW / 2) {
+        // round-robin pairing on 32 items: fixed 0, ring of 31
+        int a, b;
+        if (t == 0) {
+          a = 0;
+          b = 1 + (step % (JW - 1));
+        } else {
+          a = 1 + ((step + t) % (JW - 1));
+          b = 1 + ((step + (JW - 1) - t) % (JW - 1));
+        }
+        if (a > b) {
+          const int tmp = a;
+          a = b;
+          b = tmp;
+        }
+        pp[t][0] = a;
+        pp[t][1] = b;
+        const double gpq = g[a][b], gpp = g[a][a], gqq = g[b][b];
+        double c = 1.0, sn = 0.0;
+        if (fabs(gpq) > 1e-300 && fabs(gpq) > 1e-17 * sqrt(gpp * gqq)) {
+          const double theta = (gqq - gpp) / (2.0 * gpq);
+          const double tt = copysign(1.0, theta) / (fabs(theta) + sqrt(1.0 + theta * theta));
+          c = 1.0 / sqrt(1.0 + tt * tt);
+          sn = tt * c;
+        }
+        cs[t][0] = c;
+        cs[t][1] = sn;
+      }
+      __syncthreads();
+      // columns: g <- g J ; rot <- rot J
+      for (int e = t; e < (JW / 2) * JW; e += JTHREADS) {
+        const int k = e / JW, r = e % JW;
+        const int a = pp[k][0], b = pp[k][1];
+        const double c = cs[k][0], sn = cs[k][1];
+        const double ga = g[r][a], gb = g[r][b];
+        g[r][a] = c * ga - sn * gb;
+        g[r][b] = sn * ga + c * gb;
+        const double ra = rot[r][a], rb = rot[r][b];
+        rot[r][a] = c * ra - sn * rb;
+        rot[r][b] = sn * ra + c * rb;
+      }
+      __syncthreads();
+      // rows: g <- J^T g
+      for (int e = t; e < (JW / 2) * JW; e += JTHREADS) {
+        const int k = e / JW, r = e % JW;
+        const int a = pp[k][0], b = pp[k][1];
+        const double c = cs[k][0], sn = cs[k][1];
+        const double ga = g[a][r], gb = g[b][r];
+        g[a][r] = c * ga - sn * gb;
+        g[b][r] = sn * ga + c * gb;
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- apply rot to the pair's columns of W (rows) and V (nv rows): P <- P rot
+  auto apply = [&](double* M, i64 ld, i64 nrows) {
+    for (i64 r0 = 0; r0 < nrows; r0 += JCHUNK) {
+      __syncthreads();
+      for (int e = t; e < JCHUNK * JW; e += JTHREADS) {
+        const int r = e / JW, c = e % JW;
+        const i64 gr = r0 + r;
+        chunk[r][c] = gr < nrows ? M[gr * ld + gcol(c)] : 0.0;
+      }
+      __syncthreads();
+      // output 64 x 32 = 8 x 4 tiles; warp w: tile row w, cols 0..3
+      double o[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+      for (int k = 0; k < JW; k += 4) {
+        const double a = chunk[warp * 8 + (lane >> 2)][k + (lane & 3)];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dmma(o[q], a, rot[k + (lane & 3)][q * 8 + (lane >> 2)]);
+      }
+      const i64 gr = r0 + warp * 8 + (lane >> 2);
+      if (gr < nrows) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = q * 8 + (lane & 3) * 2;
+          M[gr * ld + gcol(c)] = o[q][0];
+          M[gr * ld + gcol(c + 1)] = o[q][1];
+        }
+      }
+    }
+  };
+  apply(W, ldw, rows);
+  apply(V, ldv, nv);
+}
+
+__global__ void scale_cols_kernel(i64 rows, i64 cols, double* A, i64 lda, const double* s, i64 ldo, double* out,
+                                  const int* perm) {
+  const i64 total = rows * cols;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = e / cols, c = e % cols;
+    const int src = perm[c];
+    const double sv = s[c];
+    out[r * ldo + c] = sv > 0.0 ? A[r * lda + src] / sv : 0.0;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- Householder QR
+void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr) {
+  if (rows < cols) throw std::invalid_argument("householder_qr: rows < cols");
+  const i64 np = (cols + HNB - 1) / HNB;
+  DBuf<double> tau(cols, s), Tall(np * HNB * HNB, s), V(rows * HNB, s), S(HNB * HNB, s),
+      W1(HNB * std::max<i64>(cols, 1), s), W2(HNB * std::max<i64>(cols, 1), s);
+  for (i64 p = 0; p < np; ++p) {
+    const i64 p0 = p * HNB;
+    const int nb = static_cast<int>(std::min<i64>(HNB, cols - p0));
+    const i64 pr = rows - p0;
+    double* panel = X + p0 * ldx + p0;
+    hh_panel_kernel<<<1, HTHREADS, 0, s>>>(pr, nb, panel, ldx, tau.get() + p0);
+    DFCG_LAUNCH_CHECK();
+    hh_extract_v<<<grid_for(pr * nb), 256, 0, s>>>(pr, nb, panel, ldx, V.get());
+    DFCG_LAUNCH_CHECK();
+    gemm(s, true, false, nb, nb, pr, 1.0, V.get(), nb, V.get(), nb, 0.0, S.get(), nb);
+    double* T = Tall.get() + p * HNB * HNB;
+    hh_build_t<<<1, HNB, 0, s>>>(nb, S.get(), tau.get() + p0, T);
+    DFCG_LAUNCH_CHECK();
+    const i64 rem = cols - p0 - nb;
+    if (rem > 0) {
+      double* A2 = X + p0 * ldx + p0 + nb;
+      gemm(s, true, false, nb, rem, pr, 1.0, V.get(), nb, A2, ldx, 0.0, W1.get(), rem);        // V^T A2
+      gemm(s, true, false, nb, rem, nb, 1.0, T, nb, W1.get(), rem, 0.0, W2.get(), rem);         // T^T W1
+      gemm(s, false, false, pr, rem, nb, -1.0, V.get(), nb, W2.get(), rem, 1.0, A2, ldx);       // A2 -= V W2
+    }
+  }
+  if (R) {
+    extract_upper<<<grid_for(cols * cols), 256, 0, s>>>(cols, X, ldx, R, ldr);
+    DFCG_LAUNCH_CHECK();
+  }
+  // Q = H_1 ... H_np [I; 0], accumulated backwards into a fresh buffer then copied over X.
+  DBuf<double> Q(rows * cols, s);
+  set_identity(s, rows, cols, Q.get(), cols);
+  for (i64 p = np - 1; p >= 0; --p) {
+    const i64 p0 = p * HNB;
+    const int nb = static_cast<int>(std::min<i64>(HNB, cols - p0));
+    const i64 pr = rows - p0;
+    hh_extract_v<<<grid_for(pr * nb), 256, 0, s>>>(pr, nb, X + p0 * ldx + p0, ldx, V.get());
+    DFCG_LAUNCH_CHECK();
+    const double* T = Tall.get() + p * HNB * HNB;
+    const i64 qc = cols - p0;
+    double* Qs = Q.get() + p0 * cols + p0;
+    gemm(s, true, false, nb, qc, pr, 1.0, V.get(), nb, Qs, cols, 0.0, W1.get(), qc);   // V^T Q
+    gemm(s, false, false, nb, qc, nb, 1.0, T, nb, W1.get(), qc, 0.0, W2.get(), qc);    // T W1
+    gemm(s, false, false, pr, qc, nb, -1.0, V.get(), nb, W2.get(), qc, 1.0, Qs, cols); // Q -= V W2
+  }
+  copy2d(s, rows, cols, Q.get(), cols, X, ldx);
+}
+
+// ---------------------------------------------------------------- CholeskyQR2 + fallback
+bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr) {
+  if (cols <= 0) return false;
+  if (rows < cols) throw std::invalid_argument("thin_qr: rows < cols");
+  DBuf<int> fail(1, s);
+  fail.zero(s);
+  DBuf<double> G(cols * cols, s), Rinv(cols * cols, s), Q1(rows * cols, s), Q2(rows * cols, s), R1;
+  const double rel_tol = 1e-11;
+  // pass 1
+  gemm(s, true, false, cols, cols, rows, 1.0, X, ldx, X, ldx, 0.0, G.get(), cols);
+  cholesky_inverse(s, cols, G.get(), cols, Rinv.get(), cols, rel_tol, fail.get());
+  gemm(s, false, false, rows, cols, cols, 1.0, X, ldx, Rinv.get(), cols, 0.0, Q1.get(), cols);
+  if (R) {
+    R1.alloc(cols * cols, s);
+    DFCG_CUDA(cudaMemcpyAsync(R1.get(), G.get(), sizeof(double) * cols * cols, cudaMemcpyDeviceToDevice, s));
+  }
+  // pass 2
+  gemm(s, true, false, cols, cols, rows, 1.0, Q1.get(), cols, Q1.get(), cols, 0.0, G.get(), cols);
+  cholesky_inverse(s, cols, G.get(), cols, Rinv.get(), cols, rel_tol, fail.get());
+  gemm(s, false, false, rows, cols, cols, 1.0, Q1.get(), cols, Rinv.get(), cols, 0.0, Q2.get(), cols);
+  int h_fail = 0;
+  DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  if (h_fail) {
+    householder_qr(s, rows, cols, X, ldx, R, ldr);
+    return true;
+  }
+  copy2d(s, rows, cols, Q2.get(), cols, X, ldx);
+  if (R) gemm(s, false, false, cols, cols, cols, 1.0, G.get(), cols, R1.get(), cols, 0.0, R, ldr);  // R2 R1
+  return false;
+}
+
+// ---------------------------------------------------------------- thin SVD
+void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U, i64 ldu, double* V, i64 ldv,
+              std::vector<double>& s_host) {
+  s_host.assign(static_cast<size_t>(std::max<i64>(cols, 0)), 0.0);
+  if (cols <= 0) return;
+  if (rows < cols) throw std::invalid_argument("thin_svd: rows < cols");
+  const int p0 = static_cast<int>((cols + JNB - 1) / JNB);
+  const int p = p0 + (p0 & 1);
+  const i64 np = static_cast<i64>(p) * JNB;  // padded column count
+  const bool precond = rows * 4 > cols * 5;
+  DBuf<double> Qbuf;
+  const i64 wrows = precond ? cols : rows;
+  DBuf<double> W(wrows * np, s), J(np * np, s);
+  W.zero(s);
+  if (precond) {
+    Qbuf.alloc(rows * cols, s);
+    copy2d(s, rows, cols, A, lda, Qbuf.get(), cols);
+    DBuf<double> Rt(cols * cols, s);
+    thin_qr(s, rows, cols, Qbuf.get(), cols, Rt.get(), cols);
+    copy2d(s, cols, cols, Rt.get(), cols, W.get(), np);
+  } else {
+    copy2d(s, rows, cols, A, lda, W.get(), np);
+  }
+  set_identity(s, np, np, J.get(), np);
+  const std::vector<int> sched = round_robin(p);
+  DBuf<int> pairs(static_cast<i64>(sched.size()), s);
+  DFCG_CUDA(cudaMemcpyAsync(pairs.get(), sched.data(), sizeof(int) * sched.size(), cudaMemcpyHostToDevice, s));
+  DBuf<unsigned long long> off(1, s);
+  const double tol = 2.2e-16 * std::max(8.0, std::sqrt(static_cast<double>(wrows)));
+  const int npairs = p / 2;
+  for (int sweep = 0; sweep < 60 && p > 1; ++sweep) {
+    off.zero(s);
+    for (int r = 0; r < p - 1; ++r) {
+      jacobi_round_kernel<<<npairs, JTHREADS, 0, s>>>(wrows, np, W.get(), np, J.get(), np,
+                                                      pairs.get() + 2 * static_cast<i64>(r) * npairs, tol, off.get(),
+                                                      6);
+      DFCG_LAUNCH_CHECK();
+    }
+    unsigned long long h_off = 0;
+    DFCG_CUDA(cudaMemcpyAsync(&h_off, off.get(), sizeof(h_off), cudaMemcpyDeviceToHost, s));
+    DFCG_CUDA(cudaStreamSynchronize(s));
+    double offv;
+    std::memcpy(&offv, &h_off, sizeof(double));
+    if (offv <= tol) break;
+  }
+  // singular values = column norms; sort descending (stable by index)
+  DBuf<double> sig(np, s);
+  col_norms(s, wrows, np, W.get(), np, sig.get());
+  std::vector<double> h_sig(np);
+  DFCG_CUDA(cudaMemcpyAsync(h_sig.data(), sig.get(), sizeof(double) * np, cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int> perm(cols);
+  std::iota(perm.begin(), perm.end(), 0);
+  // padded columns (>= cols) are exactly zero; only the first `cols` real columns are candidates
+  std::vector<int> all(np);
+  std::iota(all.begin(), all.end(), 0);
+  std::stable_sort(all.begin(), all.end(), [&](int a, int b) { return h_sig[a] > h_sig[b]; });
+  for (i64 c = 0; c < cols; ++c) {
+    perm[c] = all[c];
+    s_host[c] = h_sig[all[c]];
+  }
+  DBuf<int> dperm(cols, s);
+  DBuf<double> dsig(cols, s);
+  DFCG_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), sizeof(int) * cols, cudaMemcpyHostToDevice, s));
+  DFCG_CUDA(cudaMemcpyAsync(dsig.get(), s_host.data(), sizeof(double) * cols, cudaMemcpyHostToDevice, s));
+  // V = J[:, perm] restricted to the real rows
+  gather_cols(s, cols, cols, J.get(), np, dperm.get(), nullptr, V, ldv);
+  if (precond) {
+    DBuf<double> Wn(cols * cols, s);
+    scale_cols_kernel<<<grid_for(cols * cols), 256, 0, s>>>(cols, cols, W.get(), np, dsig.get(), cols, Wn.get(),
+                                                            dperm.get());
+    DFCG_LAUNCH_CHECK();
+    gemm(s, false, false, rows, cols, cols, 1.0, Qbuf.get(), cols, Wn.get(), cols, 0.0, U, ldu);
+  } else {
+    scale_cols_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, W.get(), np, dsig.get(), ldu, U,
+                                                            dperm.get());
+    DFCG_LAUNCH_CHECK();
+  }
+  DFCG_CUDA(cudaStreamSynchronize(s));  // host vectors (perm, s_host) used by async copies
+}
+
+}  // namespace dfcg

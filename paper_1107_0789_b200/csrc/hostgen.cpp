@@ -1,0 +1,169 @@
+// Host utilities (include/dfcg_host.h): the reference's RNG, sampling and instance
+// generators (P/include/dfc/rng.hpp, sampling.hpp, simgen.hpp), restated so the bench can
+// synthesise the reference's exact inputs on the GPU box.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <string>
+
+#include "../../include/dfcg_host.h"
+#include "dfc_host.hpp"
+
+using namespace dfcg;
+
+namespace {
+
+template <class T>
+T* dup(const std::vector<T>& v) {
+  T* p = static_cast<T*>(std::malloc(sizeof(T) * std::max<size_t>(1, v.size())));
+  if (!p) throw std::bad_alloc();
+  if (!v.empty()) std::memcpy(p, v.data(), sizeof(T) * v.size());
+  return p;
+}
+
+// gen_low_rank, simgen.hpp:30-40 (factor std (1/r)^(1/4), A then B, column-major fill).
+void gen_low_rank(i64 m, i64 n, i64 r, SeededRng& rng, std::vector<double>& A, std::vector<double>& B) {
+  if (r < 1 || r > std::min(m, n)) throw std::invalid_argument("gen_low_rank: need 1 <= r <= min(m,n)");
+  const double sd = std::pow(1.0 / static_cast<double>(r), 0.25);
+  A.assign(static_cast<size_t>(m * r), 0.0);
+  B.assign(static_cast<size_t>(n * r), 0.0);
+  for (i64 j = 0; j < r; ++j)
+    for (i64 i = 0; i < m; ++i) A[static_cast<size_t>(j * m + i)] = rng.normal(0.0, sd);
+  for (i64 j = 0; j < r; ++j)
+    for (i64 i = 0; i < n; ++i) B[static_cast<size_t>(j * n + i)] = rng.normal(0.0, sd);
+}
+
+double row_dot(const std::vector<double>& A, i64 m, i64 i, const std::vector<double>& B, i64 n, i64 j, i64 r) {
+  double acc = 0.0;
+  for (i64 k = 0; k < r; ++k) acc += A[static_cast<size_t>(k * m + i)] * B[static_cast<size_t>(k * n + j)];
+  return acc;
+}
+
+}  // namespace
+
+extern "C" {
+
+void dfcg_rng_u64(uint64_t seed, uint64_t stream, int64_t n, uint64_t* out) {
+  SeededRng r(seed, stream);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.next_u64();
+}
+void dfcg_rng_uniform(uint64_t seed, uint64_t stream, int64_t n, double* out) {
+  SeededRng r(seed, stream);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.uniform();
+}
+void dfcg_rng_normal(uint64_t seed, uint64_t stream, int64_t n, double* out) {
+  SeededRng r(seed, stream);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+
+}  // extern "C"
+
+// The remaining entry points report errors through capi.cpp's thread-local channel.
+extern int dfcg_guard_call(const std::function<void()>& f);
+
+extern "C" {
+
+int dfcg_rng_index(uint64_t seed, uint64_t stream, int64_t count, uint64_t bound, uint64_t* out) {
+  return dfcg_guard_call([&] {
+    SeededRng r(seed, stream);
+    for (int64_t i = 0; i < count; ++i) out[i] = r.index(bound);
+  });
+}
+
+int dfcg_sample_without_replacement(uint64_t seed, uint64_t stream, int64_t n, int64_t l, int64_t* out) {
+  return dfcg_guard_call([&] {
+    SeededRng r(seed, stream);
+    auto v = sample_without_replacement(n, l, r);
+    std::memcpy(out, v.data(), sizeof(int64_t) * v.size());
+  });
+}
+
+int dfcg_partition_columns(uint64_t seed, uint64_t stream, int64_t n, int64_t t, int64_t* cols, int64_t* offsets) {
+  return dfcg_guard_call([&] {
+    SeededRng r(seed, stream);
+    auto plan = partition_columns(n, t, r);
+    int64_t at = 0;
+    offsets[0] = 0;
+    for (size_t g = 0; g < plan.size(); ++g) {
+      for (i64 c : plan[g]) cols[at++] = c;
+      offsets[g + 1] = at;
+    }
+  });
+}
+
+// gen_mc_instance, simgen.hpp:45-59.
+int dfcg_gen_mc_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigma, uint64_t seed, uint64_t stream,
+                         dfcg_lowrank* L0, int64_t** rows, int64_t** cols, double** vals) {
+  return dfcg_guard_call([&] {
+    if (s < 1 || s > m * n) throw std::invalid_argument("gen_mc_instance: need 1 <= s <= m*n");
+    if (sigma < 0) throw std::invalid_argument("gen_mc_instance: sigma must be nonnegative");
+    SeededRng rng(seed, stream);
+    std::vector<double> A, B;
+    gen_low_rank(m, n, r, rng, A, B);
+    std::vector<i64> cells = sample_without_replacement(m * n, s, rng);
+    std::vector<long long> ri(static_cast<size_t>(s)), ci(static_cast<size_t>(s));
+    std::vector<double> v(static_cast<size_t>(s));
+    for (i64 e = 0; e < s; ++e) {
+      const i64 c = cells[static_cast<size_t>(e)];
+      const i64 i = c % m, j = c / m;
+      const double noise = sigma > 0 ? rng.normal(0.0, sigma) : 0.0;
+      ri[static_cast<size_t>(e)] = i;
+      ci[static_cast<size_t>(e)] = j;
+      v[static_cast<size_t>(e)] = row_dot(A, m, i, B, n, j, r) + noise;
+    }
+    std::vector<i64>().swap(cells);
+    HostObs obs = HostObs::make(m, n, std::move(ri), std::move(ci), std::move(v));  // sorts column-major
+    L0->m = m;
+    L0->n = n;
+    L0->k = r;
+    L0->left = dup(A);
+    L0->right = dup(B);
+    *rows = dup(std::vector<int64_t>(obs.row.begin(), obs.row.end()));
+    *cols = dup(std::vector<int64_t>(obs.col.begin(), obs.col.end()));
+    *vals = dup(obs.val);
+  });
+}
+
+// gen_rmf_instance, simgen.hpp:64-82 (outlier range parameterised).
+int dfcg_gen_rmf_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigma, uint64_t seed, uint64_t stream,
+                          double lo, double hi, dfcg_lowrank* L0, dfcg_sparse* S0, double* M) {
+  return dfcg_guard_call([&] {
+    if (s < 0 || s > m * n) throw std::invalid_argument("gen_rmf_instance: need 0 <= s <= m*n");
+    if (sigma < 0) throw std::invalid_argument("gen_rmf_instance: sigma must be nonnegative");
+    SeededRng rng(seed, stream);
+    std::vector<double> A, B;
+    gen_low_rank(m, n, r, rng, A, B);
+    std::vector<long long> sr, sc;
+    std::vector<double> sv;
+    if (s > 0) {
+      std::vector<i64> cells = sample_without_replacement(m * n, s, rng);
+      for (i64 c : cells) {
+        const double u = rng.uniform();
+        sr.push_back(c % m);
+        sc.push_back(c / m);
+        sv.push_back((lo == 0.0 && hi == 1.0) ? u : lo + (hi - lo) * u);
+      }
+    }
+    // M = materialize(L0) + S0 (+ noise, column-major fill)
+    for (i64 j = 0; j < n; ++j)
+      for (i64 i = 0; i < m; ++i) M[j * m + i] = row_dot(A, m, i, B, n, j, r);
+    for (size_t e = 0; e < sv.size(); ++e) M[sc[e] * m + sr[e]] += sv[e];
+    if (sigma > 0)
+      for (i64 j = 0; j < n; ++j)
+        for (i64 i = 0; i < m; ++i) M[j * m + i] += rng.normal(0.0, sigma);
+    L0->m = m;
+    L0->n = n;
+    L0->k = r;
+    L0->left = dup(A);
+    L0->right = dup(B);
+    S0->m = m;
+    S0->n = n;
+    S0->count = static_cast<int64_t>(sv.size());
+    S0->row = dup(std::vector<int64_t>(sr.begin(), sr.end()));
+    S0->col = dup(std::vector<int64_t>(sc.begin(), sc.end()));
+    S0->val = dup(sv);
+  });
+}
+
+}  // extern "C"

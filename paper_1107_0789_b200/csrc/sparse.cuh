@@ -1,0 +1,58 @@
+// Observed-set (Omega) structures and the sparse kernels of the APG-MC iteration:
+//   SDDMM residual  r_e = <Yl[i,:], Yr[j,:]> - M_e     (eval_on_support, P/include/dfc/solvers.hpp:215-225,281-285)
+//   SpMM            out (+)= alpha * R   X             (FactoredSparseOp::apply,         solvers.hpp:121-125)
+//   SpMM^T          out (+)= alpha * R^T X             (FactoredSparseOp::apply_adjoint, solvers.hpp:126-130)
+// R shares the pattern of M; its values live in CSR order (r_csr) and the CSC walk reads
+// them through the csc->csr permutation, so the SDDMM writes one coalesced stream.
+#pragma once
+
+#include "common.cuh"
+
+namespace dfcg {
+
+// One segmented-SpMM work item: a run of entries of one row of the structure.
+struct SegItem {
+  int row;
+  int slot;  // -1: sole segment of its row (write directly); else workspace row
+  long long e0, e1;
+};
+
+struct SegPlan {
+  DBuf<SegItem> items;
+  DBuf<int> red_rowptr;  // rows with >1 segment: [row] -> slots range (size rows+1), or empty
+  i64 n_items = 0, n_slots = 0, rows = 0;
+  std::vector<int> h_multi_rows;  // rows needing a reduction
+  DBuf<int> multi_rows;
+};
+
+struct DevOmega {
+  i64 m = 0, n = 0, nnz = 0;
+  // CSR (row-major walk): entries sorted by (row, col).
+  DBuf<int> csr_rowptr, csr_row, csr_col;
+  DBuf<double> m_csr;
+  // CSC (column walk, the reference's entry order): entries sorted by (col, row).
+  DBuf<int> csc_colptr, csc_row;
+  DBuf<long long> csc2csr;  // CSC position -> CSR position
+  DBuf<double> m_csc;
+  SegPlan plan_csr, plan_csc;
+  std::vector<long long> h_csc2csr;  // host copy (outputs in reference order)
+
+  // rows/cols: CSC-sorted (column-major order, as ObservedMatrix guarantees).
+  void build(cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows, const long long* cols, const double* vals);
+};
+
+// r_csr[t] = <Yl[row_t,:], Yr[col_t,:]> - (sub ? m_csr[t] : 0)   (kY may be 0 -> r = -m)
+void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl, i64 ldl, const double* Yr,
+                    i64 ldr, const double* sub, double* r_csr);
+
+// out[rows x b] = alpha * S X + beta * out, S given by (structure, values).
+//   transpose == false: S = R (m x n) via CSR, X is n x b, out is m x b.
+//   transpose == true : S = R^T (n x m) via CSC, X is m x b, out is n x b.
+// vals are always in CSR order (the CSC walk indexes them through csc2csr).
+void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals_csr, i64 b, double alpha,
+          const double* X, i64 ldx, double beta, double* out, i64 ldo);
+
+// D[i, j] += alpha * vals[(i,j)] for the observed pattern (row-major m x n dense D).
+void scatter_add_dense(cudaStream_t s, const DevOmega& om, const double* vals_csr, double alpha, double* D, i64 ldd);
+
+}  // namespace dfcg

@@ -1,0 +1,125 @@
+"""Host utilities of libdfcg.so (include/dfcg_host.h): the reference's SeededRng, sampling
+and instance generators (P/include/dfc/rng.hpp, sampling.hpp, simgen.hpp), in C++.
+
+These build the exact inputs the reference builds (same seeds, same draw order); they do not
+touch the GPU and are what bench.py uses to synthesise its workloads.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import Estimate, LowRankC, Observed, SparseC, _check, _d, _i, _lowrank_out, i64, i64ptr, lib, u64
+
+dpp = C.POINTER(C.POINTER(C.c_double))
+
+
+class SeededRng:
+    """Stateless view: draws the first n values of SeededRng(seed, stream)."""
+
+    def __init__(self, seed: int, stream: int = 0):
+        self.seed, self.stream = seed, stream
+
+    def u64(self, n):
+        out = np.empty(n, np.uint64)
+        lib().dfcg_rng_u64(u64(self.seed), u64(self.stream), i64(n), out.ctypes.data_as(C.POINTER(C.c_uint64)))
+        return out
+
+    def uniform(self, n):
+        out = np.empty(n, np.float64)
+        lib().dfcg_rng_uniform(u64(self.seed), u64(self.stream), i64(n), _d(out))
+        return out
+
+    def normal(self, n):
+        out = np.empty(n, np.float64)
+        lib().dfcg_rng_normal(u64(self.seed), u64(self.stream), i64(n), _d(out))
+        return out
+
+    def index(self, count, bound):
+        out = np.empty(count, np.uint64)
+        _check(lib().dfcg_rng_index(u64(self.seed), u64(self.stream), i64(count), u64(bound),
+                                    out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out
+
+
+def sample_without_replacement(seed, stream, n, l):
+    out = np.empty(max(l, 0), np.int64)
+    _check(lib().dfcg_sample_without_replacement(u64(seed), u64(stream), i64(n), i64(l), _i(out)))
+    return out
+
+
+def partition_columns(seed, stream, n, t):
+    cols = np.empty(max(n, 0), np.int64)
+    offs = np.empty(max(t, 0) + 1, np.int64)
+    _check(lib().dfcg_partition_columns(u64(seed), u64(stream), i64(n), i64(t), _i(cols), _i(offs)))
+    return [cols[offs[g]:offs[g + 1]].copy() for g in range(t)]
+
+
+def extract_columns(obs: Observed, idx) -> Observed:
+    """extract_columns (P/include/dfc/sampling.hpp:83-97), vectorised."""
+    idx = np.asarray(idx, np.int64)
+    pos = np.full(obs.n, -1, np.int64)
+    if np.any((idx < 0) | (idx >= obs.n)):
+        raise IndexError("extract_columns: index out of range")
+    if len(np.unique(idx)) != len(idx):
+        raise ValueError("extract_columns: duplicate index")
+    pos[idx] = np.arange(len(idx))
+    p = pos[obs.cols]
+    keep = p >= 0
+    r, c, v = obs.rows[keep], p[keep], obs.vals[keep]
+    order = np.lexsort((r, c))
+    return Observed(obs.m, len(idx), r[order], c[order], v[order])
+
+
+def extract_rows(obs: Observed, idx) -> Observed:
+    """extract_rows (sampling.hpp:99-113), vectorised."""
+    idx = np.asarray(idx, np.int64)
+    pos = np.full(obs.m, -1, np.int64)
+    if np.any((idx < 0) | (idx >= obs.m)):
+        raise IndexError("extract_rows: index out of range")
+    if len(np.unique(idx)) != len(idx):
+        raise ValueError("extract_rows: duplicate index")
+    pos[idx] = np.arange(len(idx))
+    p = pos[obs.rows]
+    keep = p >= 0
+    r, c, v = p[keep], obs.cols[keep], obs.vals[keep]
+    order = np.lexsort((r, c))
+    return Observed(len(idx), obs.n, r[order], c[order], v[order])
+
+
+def median_rank(ranks):
+    """median_rank (P/include/dfc/dfc.hpp:159-164): lower median floored at 1."""
+    if len(ranks) == 0:
+        raise ValueError("median_rank: empty list")
+    s = sorted(ranks)
+    return max(1, s[(len(s) - 1) // 2])
+
+
+def gen_mc_instance(m, n, r, s, sigma, seed, stream=0):
+    """gen_mc_instance (P/include/dfc/simgen.hpp:45-59) with SeededRng(seed, stream)."""
+    L0 = LowRankC()
+    rows, cols, vals = i64ptr(), i64ptr(), C.POINTER(C.c_double)()
+    _check(lib().dfcg_gen_mc_instance(i64(m), i64(n), i64(r), i64(s), C.c_double(sigma), u64(seed), u64(stream),
+                                      C.byref(L0), C.byref(rows), C.byref(cols), C.byref(vals)))
+    R = np.ctypeslib.as_array(rows, shape=(s,)).copy()
+    Cc = np.ctypeslib.as_array(cols, shape=(s,)).copy()
+    V = np.ctypeslib.as_array(vals, shape=(s,)).copy()
+    for p in (rows, cols, vals):
+        lib().dfcg_free(C.cast(p, C.c_void_p))
+    return _lowrank_out(L0), Observed(m, n, R, Cc, V)
+
+
+def gen_rmf_instance(m, n, r, s, sigma, seed, stream=0, lo=0.0, hi=1.0):
+    """gen_rmf_instance (simgen.hpp:64-82); outliers U[lo, hi] (reference: U[0,1])."""
+    L0 = LowRankC()
+    S0 = SparseC()
+    M = np.empty((m, n), np.float64, order="F")
+    _check(lib().dfcg_gen_rmf_instance(i64(m), i64(n), i64(r), i64(s), C.c_double(sigma), u64(seed), u64(stream),
+                                       C.c_double(lo), C.c_double(hi), C.byref(L0), C.byref(S0), _d(M)))
+    cnt = S0.count
+    rows = np.ctypeslib.as_array(S0.row, shape=(max(cnt, 1),))[:cnt].copy()
+    cols = np.ctypeslib.as_array(S0.col, shape=(max(cnt, 1),))[:cnt].copy()
+    vals = np.ctypeslib.as_array(S0.val, shape=(max(cnt, 1),))[:cnt].copy()
+    lib().dfcg_sparse_free(C.byref(S0))
+    return _lowrank_out(L0), (rows, cols, vals), M
