@@ -1,0 +1,121 @@
+"""CPU-only checks of the product's host side: the C-ABI library loads and exports every
+symbol include/*.h declares, its host RNG / sampling / generators reproduce the reference's
+golden vectors and the oracle bit for bit, and compute calls refuse to run without a GPU."""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1107_0789_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_pins.json")))
+
+
+def declared_functions():
+    names = []
+    for h in ("dfcg.h", "dfcg_host.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"^\s*(?:int|void|const char\*|int64_t)\s+\**(dfcg_\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    L = P.lib()
+    names = declared_functions()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(L, name), name
+
+
+def test_host_rng_golden():  # P/tests/test_rng.cpp:11-48
+    r = P.SeededRng(42, 0)
+    assert [int(x) for x in r.u64(4)] == [int(v, 16) for v in GOLD["rng_raw_42_0"]["values"]]
+    assert list(r.uniform(3)) == GOLD["rng_uniform_42_0"]["values"]
+    assert list(r.normal(2)) == GOLD["rng_normal_42_0"]["values"]
+    assert [int(x) for x in r.index(5, 10)] == GOLD["rng_index10_42_0"]["values"]
+    assert int(P.SeededRng(42, 1).u64(1)[0]) == int(GOLD["rng_raw_42_1"]["values"][0], 16)
+    with pytest.raises(ValueError):
+        P.SeededRng(5, 0).index(1, 0)
+
+
+def test_host_normal_stream_matches_oracle():  # the SVT draws from SeededRng(0x737674, 0|1)
+    for stream in (0, 1):
+        assert np.array_equal(P.SeededRng(0x737674, stream).normal(5000), O.rng_normal(0x737674, stream, 5000))
+
+
+def test_generators_match_oracle_bitwise():
+    L0p, obp = P.gen_mc_instance(60, 50, 3, 900, 0.1, 5)
+    L0o, obo = O.gen_mc_instance(60, 50, 3, 900, 0.1, 5, 0)
+    assert np.array_equal(L0p.left, L0o.left) and np.array_equal(L0p.right, L0o.right)
+    for a, b in ((obp.rows, obo.rows), (obp.cols, obo.cols), (obp.vals, obo.vals)):
+        assert np.array_equal(a, b)
+    Lp, Sp, Mp = P.gen_rmf_instance(30, 40, 2, 100, 0.05, 3)
+    Lo, So, Mo = O.gen_rmf_instance(30, 40, 2, 100, 0.05, 3, 0)
+    assert np.array_equal(Mp, Mo) and all(np.array_equal(a, b) for a, b in zip(Sp, So))
+    Lp, Sp, Mp = P.gen_rmf_instance(30, 40, 2, 100, 0.01, 4, lo=-10.0, hi=10.0)
+    Lo, So, Mo = O.gen_rmf_instance(30, 40, 2, 100, 0.01, 4, 0, -10.0, 10.0)
+    assert np.array_equal(Mp, Mo)
+
+
+def test_generator_validation():
+    with pytest.raises(ValueError):
+        P.gen_mc_instance(4, 4, 1, 0, 0.1, 1)
+    with pytest.raises(ValueError):
+        P.gen_mc_instance(4, 4, 1, 17, 0.1, 1)
+    with pytest.raises(ValueError):
+        P.gen_mc_instance(4, 4, 5, 4, 0.1, 1)
+
+
+def test_sampling_matches_oracle():
+    for n, t in ((100, 7), (17, 17), (1000, 64)):
+        gp = P.partition_columns(3, 0xDFC0000000000001, n, t)
+        go = O.partition_columns(3, 0xDFC0000000000001, n, t)
+        assert all(np.array_equal(a, b) for a, b in zip(gp, go))
+    assert np.array_equal(P.sample_without_replacement(9, 2, 50, 13), O.sample_without_replacement(9, 2, 50, 13))
+    with pytest.raises(ValueError):
+        P.partition_columns(1, 0, 5, 6)
+
+
+def test_extract_matches_oracle():
+    L0, obs = P.gen_mc_instance(40, 30, 2, 500, 0.1, 2)
+    oo = O.Observed(obs.m, obs.n, obs.rows, obs.cols, obs.vals)
+    idx = np.array([3, 7, 8, 20, 29])
+    a, b = P.extract_columns(obs, idx), O.extract_columns(oo, idx)
+    assert (a.m, a.n) == (b.m, b.n)
+    assert np.array_equal(a.rows, b.rows) and np.array_equal(a.cols, b.cols) and np.array_equal(a.vals, b.vals)
+    a, b = P.extract_rows(obs, idx), O.extract_rows(oo, idx)
+    assert np.array_equal(a.rows, b.rows) and np.array_equal(a.cols, b.cols) and np.array_equal(a.vals, b.vals)
+    with pytest.raises(ValueError):
+        P.extract_columns(obs, [1, 1])
+    with pytest.raises(IndexError):
+        P.extract_rows(obs, [40])
+
+
+def test_median_rank():  # P/tests/test_dfc.cpp:43-49
+    assert P.median_rank([2, 3, 5]) == 3
+    assert P.median_rank([2, 4]) == 2
+    assert P.median_rank([0, 0, 0]) == 1
+    assert P.median_rank([7]) == 7
+    with pytest.raises(ValueError):
+        P.median_rank([])
+
+
+def _has_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-GPU failure mode")
+def test_compute_fails_loudly_without_gpu():
+    L0, obs = P.gen_mc_instance(20, 20, 2, 200, 0.1, 1)
+    with pytest.raises(P.DfcError):
+        P.apg_mc(obs)
