@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""bench.py — DFC-Proj noisy matrix completion at BASELINE config c2 on B200.
+
+Workload (BASELINE.json configs[1]): M = L0 + noise, m = n = 10000, r = 10,
+10% of entries observed (s = 1e7, the reference generator gen_mc_instance,
+P/include/dfc/simgen.hpp:45-59, seed 1), sigma = 0.1; DFC-Proj with t = 8 column blocks of
+10000 x 1250 (partition seed 1, P/include/dfc/dfc.hpp:166-200) and the default ApgConfig
+(P/include/dfc/solvers.hpp:19-26). Data are synthetic, seed-generated with the reference's
+own generator semantics (no dataset is involved).
+
+Metric: base-APG iterations/s ("block-iterations/s": one APG iteration of one 10000 x 1250
+block = one unit). A step = one APG iteration on every block (blocks sharded over the ranks,
+each advancing on its own CUDA stream). Before the W warm-up steps every block runs a fixed
+prologue of --prologue iterations (default 26) so the timed window sits in the steady
+rank ~700 regime that dominates a c2 solve; the reference arm measures the same window.
+Inputs are larger than L2 (the 10k x 10k factors alone exceed 126 MB); no flush needed.
+
+e2e: the full DFC-Proj solve through the public C ABI (host triplets in, host estimate out,
+H2D/D2H inside the timed region): block-iterations/s over the whole solve, plus the solve time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DFC-Proj MC solve time & base-APG iters/s at 10k×10k r=10; roofline frac"
+UNIT = "block-iterations/s"
+PARTITION_STREAM = 0xDFC0000000000001
+FP64_DMMA_PEAK_TFLOPS = 37.1  # measured: tools/fp64_peak.cu on this pool's B200 (profiles/fp64_peak.txt)
+
+WORKLOADS = {
+    "c2": dict(m=10000, n=10000, r=10, s=10_000_000, sigma=0.1, t=8, seed=1),
+    "c1": dict(m=1000, n=1000, r=10, s=200_000, sigma=0.1, t=4, seed=1),
+}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.samples, self._stop = device, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and "Active" in s[4 + i]
+                          and "Not" not in s[4 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_blocks(P, wl):
+    L0, obs = P.gen_mc_instance(wl["m"], wl["n"], wl["r"], wl["s"], wl["sigma"], wl["seed"])
+    groups = P.partition_columns(wl["seed"], PARTITION_STREAM, wl["n"], wl["t"])
+    blocks = [P.extract_columns(obs, g) for g in groups]
+    return L0, obs, groups, blocks
+
+
+def roofline_entry(prof, peaks, peak_kind):
+    ops = {k: v for k, v in prof.items() if v["launches"] > 0}
+    if not ops:
+        return None
+    name, v = max(ops.items(), key=lambda kv: kv[1]["ms"])
+    per_launch_ms = v["ms"] / v["launches"]
+    share = v["ms"] / sum(x["ms"] for x in ops.values())
+    if name in ("gemm", "jacobi", "cholesky", "qr_fallback"):
+        achieved = v["flops"] / (v["ms"] * 1e-3) / 1e12
+        peak = FP64_DMMA_PEAK_TFLOPS
+        entry = dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
+                     peak_source="measured FP64 DMMA (tools/fp64_peak.cu, profiles/fp64_peak.txt)")
+    else:
+        achieved = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        entry = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s",
+                     peak_source=f"{peak_kind} MEASURED_PEAKS.json hbm_gbs")
+    entry.update(frac=entry["achieved"] / entry["peak"], traffic=None, kernel=name, share_of_step=share,
+                 launches=v["launches"], avg_launch_ms=per_launch_ms,
+                 per_op={k: dict(ms=round(x["ms"], 3), launches=x["launches"],
+                                 tflops=round(x["flops"] / max(x["ms"], 1e-9) / 1e9, 3),
+                                 gbs=round(x["bytes"] / max(x["ms"], 1e-9) / 1e6, 1)) for k, x in ops.items()})
+    traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            entry["traffic"] = json.load(open(traffic_file)).get(name)
+        except Exception:
+            pass
+    return entry
+
+
+def cpu_sample(O, block, cfg_kwargs, prologue, steps, threads):
+    """Oracle (restated reference, CPU) on one block: prologue, then `steps` timed iterations."""
+    import ctypes as C
+
+    L = O.lib()
+    L.orc_set_blas_threads(threads)
+    h = O._obs_handle(O.Observed(block.m, block.n, block.rows, block.cols, block.vals))
+    run = C.c_void_p()
+    O._check(L.orc_mc_run_new(h.ptr, C.byref(O.apg_cfg(**cfg_kwargs)), C.byref(run)))
+    done = C.c_longlong()
+    try:
+        O._check(L.orc_mc_run_step(run, C.c_longlong(prologue), C.byref(done)))
+        t0 = time.perf_counter()
+        O._check(L.orc_mc_run_step(run, C.c_longlong(steps), C.byref(done)))
+        dt = time.perf_counter() - t0
+    finally:
+        L.orc_mc_run_free(run)
+        L.orc_set_blas_threads(1)
+    return done.value, dt
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference's CPU path (oracle port; the C++/Eigen reference cannot be
+    built here) on the host cores, same workload / metric / unit, bounded sample: block 0."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    import paper_1107_0789_b200.host as H  # host-side generator only (no GPU)
+    import paper_1107_0789_b200 as P
+
+    threads = os.cpu_count() or 1
+    L0, obs, groups, blocks = make_blocks(P, wl)
+    blk = blocks[0]
+    import ctypes as C
+
+    L = O.lib()
+    L.orc_set_blas_threads(threads)
+    h = O._obs_handle(O.Observed(blk.m, blk.n, blk.rows, blk.cols, blk.vals))
+    run = C.c_void_p()
+    O._check(L.orc_mc_run_new(h.ptr, C.byref(O.apg_cfg()), C.byref(run)))
+    done = C.c_longlong()
+    O._check(L.orc_mc_run_step(run, C.c_longlong(args.prologue + args.warmup), C.byref(done)))
+    t0 = time.perf_counter()
+    O._check(L.orc_mc_run_step(run, C.c_longlong(args.steps), C.byref(done)))
+    dt = time.perf_counter() - t0
+    L.orc_mc_run_free(run)
+    value = done.value / dt
+    line = dict(impl="reference", metric=METRIC, value=value, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * dt / max(args.steps, 1), higher_is_better=True,
+                scaling="strong", vs_baseline=None, dtype="f64", data="synthetic (reference generator, seed 1)",
+                config=dict(workload=f"{args.workload}: DFC-Proj MC {wl['m']}x{wl['n']} r={wl['r']} "
+                                     f"{wl['s']} obs sigma={wl['sigma']} t={wl['t']} default ApgConfig",
+                            window=f"APG iterations {args.prologue + args.warmup + 1}.."
+                                   f"{args.prologue + args.warmup + args.steps} of block 0"),
+                cpu_baseline=dict(value=value, unit=UNIT, cores=threads, kind="port",
+                                  sample=f"block 0 (10000x1250), {done.value} steady-state APG iterations after a "
+                                         f"{args.prologue + args.warmup}-iteration prologue; oracle/ restatement "
+                                         f"(OpenBLAS, {threads} threads)"),
+                e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--prologue", type=int, default=26)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+        return
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1107_0789_b200 as P
+
+    peaks, peak_kind = measured_peaks()
+    L0, obs, groups, blocks = make_blocks(P, wl)
+    mine = [g for g in range(wl["t"]) if g % world == rank]
+    cfg = P.ApgConfig()
+    solvers = {g: P.McSolver(blocks[g], cfg, device=local) for g in mine}
+    pool = ThreadPoolExecutor(max_workers=max(1, len(mine)))
+
+    def advance(n):
+        return sum(pool.map(lambda g: solvers[g].step(n), mine))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    advance(args.prologue)
+    for _ in range(args.warmup):
+        advance(1)
+    barrier()
+    launches0 = P.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record()
+        iters = 0
+        for _ in range(args.steps):
+            iters += advance(1)
+        torch.cuda.synchronize()
+        e1.record()
+        e1.synchronize()
+    launches = P.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    tot = torch.tensor([ms, float(iters)], dtype=torch.float64, device="cuda")
+    if dist:
+        mx = tot.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tot.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms, iters_all = mx[0].item(), sm[1].item()
+    else:
+        iters_all = float(iters)
+    value = iters_all / (ms * 1e-3)
+
+    # kernel accounting on one extra step (outside the timed region)
+    P.prof_enable(True)
+    advance(1)
+    prof = P.prof_collect()
+    P.prof_enable(False)
+    roof = roofline_entry(prof, peaks, peak_kind)
+
+    # combine on the current block estimates (column_project, P/include/dfc/sketch.hpp:170-199)
+    ests = {g: solvers[g].finish()[0] for g in mine}
+    combine_ms = None
+    if dist:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, {g: (e.left, e.right) for g, e in ests.items()})
+        allests = {g: P.Estimate(*lr) for part in gathered for g, lr in part.items()}
+    else:
+        allests = ests
+    if rank == 0:
+        t0 = time.perf_counter()
+        P.column_project(allests[0], [allests[g] for g in range(wl["t"])], groups, device=local)
+        combine_ms = 1e3 * (time.perf_counter() - t0)
+    for sv in solvers.values():
+        sv.close()
+
+    # e2e: full DFC-Proj solve through the public C ABI (host buffers in and out)
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        rep_iters = []
+
+        def solve(g):
+            est, rep = P.apg_mc(blocks[g], cfg, device=local)
+            return g, est, rep
+
+        outs = list(pool.map(solve, mine))
+        for g, est, rep in outs:
+            h2d += blocks[g].count * 24
+            d2h += (est.left.size + est.right.size) * 8
+            rep_iters.append(rep.iterations)
+        local_ests = {g: (est.left, est.right) for g, est, _ in outs}
+        if dist:
+            gathered = [None] * world
+            dist.all_gather_object(gathered, local_ests)
+            allf = {g: P.Estimate(*lr) for part in gathered for g, lr in part.items()}
+            it_t = torch.tensor([float(sum(rep_iters))], dtype=torch.float64, device="cuda")
+            dist.all_reduce(it_t)
+            tot_iters = it_t.item()
+        else:
+            allf = {g: P.Estimate(*lr) for g, lr in local_ests.items()}
+            tot_iters = float(sum(rep_iters))
+        if rank == 0:
+            final = P.column_project(allf[0], [allf[g] for g in range(wl["t"])], groups, device=local)
+            d2h += (final.left.size + final.right.size) * 8
+        barrier()
+        wall = time.perf_counter() - t0
+        wt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        wall = wt.item()
+        e2e = dict(value=tot_iters / wall, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
+                   dfc_proj_solve_s=wall, block_iterations=int(tot_iters),
+                   note="one e2e step = the whole DFC-Proj solve (all blocks to convergence + combine) "
+                        "through the C ABI from host triplets to host factors")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle as O
+
+        threads = os.cpu_count() or 1
+        done, dt = cpu_sample(O, blocks[0], {}, args.prologue + args.warmup, args.cpu_steps, threads)
+        cpu = dict(value=done / dt, unit=UNIT, cores=threads, kind="port",
+                   sample=f"block 0 (10000x1250): APG iterations {args.prologue + args.warmup + 1}.."
+                          f"{args.prologue + args.warmup + done} after the same prologue; oracle/ restatement "
+                          f"(OpenBLAS, {threads} threads)")
+
+    if rank == 0:
+        line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+                    ms_per_step=ms / max(args.steps, 1), higher_is_better=True, scaling="strong", vs_baseline=None,
+                    dtype="f64", data="synthetic (reference generator gen_mc_instance, seed 1)",
+                    config=dict(workload=f"{args.workload}: DFC-Proj MC {wl['m']}x{wl['n']} r={wl['r']} "
+                                         f"{wl['s']} obs sigma={wl['sigma']} t={wl['t']} default ApgConfig",
+                                window=f"APG iterations {args.prologue + args.warmup + 1}.."
+                                       f"{args.prologue + args.warmup + args.steps} of every block",
+                                blocks_per_gpu=len(mine), l2="inputs > L2 (no flush)",
+                                parallelism=f"{wl['t']} blocks over {world} GPU(s), one CUDA stream per block"),
+                    roofline=roof, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
+                    clocks=clocks.summary(), combine_ms=combine_ms)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -97,6 +97,7 @@ typedef struct {
   int64_t k_final;  /* k of the last partial SVD of the iteration; 0 = dense SVD path */
   int32_t svd_calls;
   double rel, mu, sigma_sum;
+  double ms; /* host wall time of the iteration (each iteration ends in a device sync) */
 } dfcg_iter_trace;
 
 /* DfcConfig, P/include/dfc/dfc.hpp:36-48. variant: 0 Proj, 1 Rp, 2 Nys; task: 0 MC, 1 RMF. */
@@ -136,6 +137,18 @@ int dfcg_apg_mc(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_apg_cfg* cfg, dfcg
 int dfcg_apg_rmf(dfcg_ctx* ctx, const double* M_colmajor, int64_t m, int64_t n, double lambda,
                  const dfcg_apg_cfg* cfg, dfcg_lowrank* L, dfcg_sparse* S, dfcg_solve_report* rep,
                  dfcg_iter_trace* trace, int64_t trace_cap, int64_t* trace_len);
+
+/* Resumable apg_mc with the observation set resident on the device: create uploads Omega
+ * and computes mu_init; step advances up to n_iters APG iterations (*done = iterations run,
+ * fewer if the stop test fired); finish reports and returns the current estimate without
+ * ending the run. Each solver owns a CUDA stream, so solvers stepped from different host
+ * threads run concurrently on the GPU. */
+typedef struct dfcg_mc_solver dfcg_mc_solver;
+int dfcg_mc_solver_create(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_apg_cfg* cfg, dfcg_mc_solver** out);
+int dfcg_mc_solver_step(dfcg_mc_solver* sv, int64_t n_iters, int64_t* done, dfcg_iter_trace* trace,
+                        int64_t trace_cap, int64_t* trace_len);
+int dfcg_mc_solver_finish(dfcg_mc_solver* sv, dfcg_lowrank* out, dfcg_solve_report* rep);
+void dfcg_mc_solver_destroy(dfcg_mc_solver* sv);
 
 /* ---- C step: combiners --------------------------------------------------------------- */
 /* Partition plan as CSR: group g owns group_cols[group_offsets[g] : group_offsets[g+1]]. */

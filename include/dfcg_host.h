@@ -38,6 +38,16 @@ int dfcg_gen_mc_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigm
 int dfcg_gen_rmf_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigma, uint64_t seed, uint64_t stream,
                           double lo, double hi, dfcg_lowrank* L0, dfcg_sparse* S0, double* M);
 
+/* ---- kernel accounting (bench / profiling; off by default) ---------------------------
+ * Op classes, in order: 0 gemm, 1 sddmm, 2 spmm, 3 cholesky, 4 qr_fallback, 5 jacobi,
+ * 6 elementwise, 7 reduce, 8 other. dfcg_prof_enable clears previous records. */
+#define DFCG_PROF_NUM_OPS 9
+void dfcg_prof_enable(int on);
+int64_t dfcg_launch_count(void);
+/* Per op class: launches, summed CUDA-event ms, algorithmic FLOPs and bytes. Returns the
+ * number of classes filled (DFCG_PROF_NUM_OPS) or a negative error. */
+int dfcg_prof_collect(int64_t* launches, double* ms, double* flops, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

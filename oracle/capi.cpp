@@ -261,6 +261,26 @@ int orc_apg_mc(const OrcObs* obs, const OrcApgCfg* c, OrcEst** out, OrcReport* r
   });
 }
 
+// Resumable APG-MC run (bench windows): create, step n iterations, finish, free.
+int orc_mc_run_new(const OrcObs* obs, const OrcApgCfg* c, orc::ApgMcRun** out) {
+  return guard([&] { *out = new orc::ApgMcRun(obs->obs, to_cfg(c)); });
+}
+int orc_mc_run_step(orc::ApgMcRun* r, long long n, long long* done) {
+  return guard([&] {
+    long long k = 0;
+    while (k < n && r->step()) ++k;
+    *done = k;
+  });
+}
+int orc_mc_run_finish(orc::ApgMcRun* r, OrcEst** out, OrcReport* rep) {
+  return guard([&] {
+    auto [L, rp] = r->finish();
+    *out = new OrcEst{std::move(L)};
+    to_report(rp, rep);
+  });
+}
+void orc_mc_run_free(orc::ApgMcRun* r) { delete r; }
+
 int orc_apg_rmf(long long m, long long n, const double* M, double lambda, const OrcApgCfg* c, OrcEst** L, OrcTrip** S,
                 OrcReport* rep, OrcTrace* trace, long long cap, long long* len) {
   return guard([&] {

@@ -814,86 +814,91 @@ static double sum_of(const std::vector<double>& v) {
   return s;
 }
 
-// apg_mc, solvers.hpp:241-327.
-std::pair<LowRankEstimate, SolveReport> apg_mc(const ObservedMatrix& obs, const ApgConfig& cfg,
-                                               std::vector<IterTrace>* trace) {
-  const auto start = std::chrono::steady_clock::now();
+// apg_mc, solvers.hpp:241-327, as a resumable run (setup in the ctor, one APG iteration per
+// step(), report in finish()); apg_mc() drives it to completion exactly like the reference loop.
+ApgMcRun::ApgMcRun(const ObservedMatrix& obs_, const ApgConfig& cfg_)
+    : obs(obs_), cfg(cfg_), svd_rng(0x737674u, 0), L_prev(LowRankEstimate::zero(1, 1)),
+      L_curr(LowRankEstimate::zero(1, 1)) {
+  start = std::chrono::steady_clock::now();
   if (obs.empty()) throw std::invalid_argument("apg_mc: empty observation set");
   detail::validate_config(cfg);
   const Index m = obs.rows(), n = obs.cols(), N = obs.count();
-
-  detail::Csc M;
-  M.m = m;
-  M.n = n;
-  M.colptr.assign(static_cast<std::size_t>(n + 1), 0);
-  M.row.resize(static_cast<std::size_t>(N));
-  M.val.resize(static_cast<std::size_t>(N));
+  M = std::make_unique<detail::Csc>();
+  M->m = m;
+  M->n = n;
+  M->colptr.assign(static_cast<std::size_t>(n + 1), 0);
+  M->row.resize(static_cast<std::size_t>(N));
+  M->val.resize(static_cast<std::size_t>(N));
   for (Index e = 0; e < N; ++e) {
     const auto& o = obs.entries()[static_cast<std::size_t>(e)];
-    M.colptr[static_cast<std::size_t>(o.col + 1)]++;
-    M.row[static_cast<std::size_t>(e)] = o.row;
-    M.val[static_cast<std::size_t>(e)] = o.value;
+    M->colptr[static_cast<std::size_t>(o.col + 1)]++;
+    M->row[static_cast<std::size_t>(e)] = o.row;
+    M->val[static_cast<std::size_t>(e)] = o.value;
   }
-  for (Index j = 0; j < n; ++j) M.colptr[static_cast<std::size_t>(j + 1)] += M.colptr[static_cast<std::size_t>(j)];
-  const std::vector<double> m_vals = M.val;
-
-  const double mu_init = cfg.mu_init.value_or(0.99 * detail::spectral_norm(M));
-  const double mu_floor = cfg.mu_floor.value_or(1e-4 * mu_init);
+  for (Index j = 0; j < n; ++j) M->colptr[static_cast<std::size_t>(j + 1)] += M->colptr[static_cast<std::size_t>(j)];
+  m_vals = M->val;
+  mu_init = cfg.mu_init.value_or(0.99 * detail::spectral_norm(*M));
+  mu_floor = cfg.mu_floor.value_or(1e-4 * mu_init);
   if (mu_floor > mu_init) throw std::invalid_argument("apg_mc: mu_floor exceeds mu_init");
+  R = std::make_unique<detail::Csc>(*M);
+  L_prev = LowRankEstimate::zero(m, n);
+  L_curr = L_prev;
+  last = empty_svd(m, n);
+  mu = mu_used = mu_init;
+}
 
-  SeededRng svd_rng(0x737674u, 0);
-  detail::Csc R = M;
-  LowRankEstimate L_prev = LowRankEstimate::zero(m, n), L_curr = L_prev;
-  SvdFactors last = empty_svd(m, n);
-  double tau_prev = 1.0, tau_curr = 1.0, mu = mu_init, mu_used = mu_init;
-  Index rank_hint = 1;
-  int iters = 0;
+ApgMcRun::~ApgMcRun() = default;
 
-  for (int it = 1; it <= cfg.max_iters; ++it) {
-    iters = it;
-    const double beta = (tau_prev - 1.0) / tau_curr;
-    LowRankEstimate Y = detail::extrapolate(L_curr, L_prev, beta);
-    std::vector<double> y_vals = detail::eval_on_support(Y, obs.entries());
-    for (Index i = 0; i < N; ++i) R.val[static_cast<std::size_t>(i)] = y_vals[static_cast<std::size_t>(i)] - m_vals[static_cast<std::size_t>(i)];
+bool ApgMcRun::step(std::vector<IterTrace>* trace) {
+  if (stopped || iters >= cfg.max_iters) return false;
+  const Index m = obs.rows(), n = obs.cols(), N = obs.count();
+  const int it = ++iters;
+  const double beta = (tau_prev - 1.0) / tau_curr;
+  LowRankEstimate Y = detail::extrapolate(L_curr, L_prev, beta);
+  std::vector<double> y_vals = detail::eval_on_support(Y, obs.entries());
+  for (Index i = 0; i < N; ++i)
+    R->val[static_cast<std::size_t>(i)] = y_vals[static_cast<std::size_t>(i)] - m_vals[static_cast<std::size_t>(i)];
 
-    double step = 1.0;
-    SvdFactors f;
-    LowRankEstimate L_next = LowRankEstimate::zero(m, n);
-    detail::SvtStats st;
-    for (;;) {
-      detail::FactoredSparseOp G{Y.left(), Y.right(), R, -step};
-      f = detail::svt_operator(G, step * mu, rank_hint, svd_rng, &st);
-      L_next = f.to_estimate();
-      if (!cfg.line_search || step <= 0.125) break;
-      std::vector<double> nv = detail::eval_on_support(L_next, obs.entries());
-      double f_next = 0, f_y = 0, lin = 0;
-      for (Index i = 0; i < N; ++i) {
-        const std::size_t u = static_cast<std::size_t>(i);
-        f_next += (nv[u] - m_vals[u]) * (nv[u] - m_vals[u]);
-        f_y += (y_vals[u] - m_vals[u]) * (y_vals[u] - m_vals[u]);
-        lin += (y_vals[u] - m_vals[u]) * (nv[u] - y_vals[u]);
-      }
-      f_next *= 0.5;
-      f_y *= 0.5;
-      const double dist2 = factored_diff_norm(L_next, Y);
-      if (f_next <= f_y + lin + dist2 * dist2 / (2.0 * step) + 1e-12) break;
-      step *= 0.5;
+  double step = 1.0;
+  SvdFactors f;
+  LowRankEstimate L_next = LowRankEstimate::zero(m, n);
+  detail::SvtStats st;
+  for (;;) {
+    detail::FactoredSparseOp G{Y.left(), Y.right(), *R, -step};
+    f = detail::svt_operator(G, step * mu, rank_hint, svd_rng, &st);
+    L_next = f.to_estimate();
+    if (!cfg.line_search || step <= 0.125) break;
+    std::vector<double> nv = detail::eval_on_support(L_next, obs.entries());
+    double f_next = 0, f_y = 0, lin = 0;
+    for (Index i = 0; i < N; ++i) {
+      const std::size_t u = static_cast<std::size_t>(i);
+      f_next += (nv[u] - m_vals[u]) * (nv[u] - m_vals[u]);
+      f_y += (y_vals[u] - m_vals[u]) * (y_vals[u] - m_vals[u]);
+      lin += (y_vals[u] - m_vals[u]) * (nv[u] - y_vals[u]);
     }
-
-    const double rel = factored_diff_norm(L_next, L_curr) / std::max(1.0, detail::factored_norm(L_curr));
-    const double tau_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tau_curr * tau_curr));
-    L_prev = std::move(L_curr);
-    L_curr = std::move(L_next);
-    last = std::move(f);
-    tau_prev = tau_curr;
-    tau_curr = tau_next;
-    rank_hint = std::max<Index>(1, L_curr.rank_bound());
-    mu_used = mu;
-    if (trace) trace->push_back({it, L_curr.rank_bound(), st.k_final, st.calls, rel, mu, sum_of(last.s)});
-    mu = std::max(cfg.mu_decay * mu, mu_floor);
-    if (rel < cfg.rel_tol) break;
+    f_next *= 0.5;
+    f_y *= 0.5;
+    const double dist2 = factored_diff_norm(L_next, Y);
+    if (f_next <= f_y + lin + dist2 * dist2 / (2.0 * step) + 1e-12) break;
+    step *= 0.5;
   }
+  const double rel = factored_diff_norm(L_next, L_curr) / std::max(1.0, detail::factored_norm(L_curr));
+  const double tau_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tau_curr * tau_curr));
+  L_prev = std::move(L_curr);
+  L_curr = std::move(L_next);
+  last = std::move(f);
+  tau_prev = tau_curr;
+  tau_curr = tau_next;
+  rank_hint = std::max<Index>(1, L_curr.rank_bound());
+  mu_used = mu;
+  if (trace) trace->push_back({it, L_curr.rank_bound(), st.k_final, st.calls, rel, mu, sum_of(last.s)});
+  mu = std::max(cfg.mu_decay * mu, mu_floor);
+  if (rel < cfg.rel_tol) stopped = true;
+  return true;
+}
 
+std::pair<LowRankEstimate, SolveReport> ApgMcRun::finish() const {
+  const Index N = obs.count();
   SolveReport rep;
   rep.iterations = iters;
   rep.rank = L_curr.rank_bound();
@@ -906,7 +911,15 @@ std::pair<LowRankEstimate, SolveReport> apg_mc(const ObservedMatrix& obs, const 
   rep.residual = std::sqrt(res2);
   rep.objective = mu_used * sum_of(last.s) + 0.5 * rep.residual * rep.residual;
   rep.wall_ms = ms_since(start);
-  return {std::move(L_curr), rep};
+  return {L_curr, rep};
+}
+
+std::pair<LowRankEstimate, SolveReport> apg_mc(const ObservedMatrix& obs, const ApgConfig& cfg,
+                                               std::vector<IterTrace>* trace) {
+  ApgMcRun run(obs, cfg);
+  while (run.step(trace)) {
+  }
+  return run.finish();
 }
 
 // apg_rmf, solvers.hpp:332-414.

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <numeric>
 #include <optional>
 #include <random>
@@ -272,6 +273,31 @@ std::tuple<LowRankEstimate, OutlierEstimate, SolveReport> apg_rmf(const Mat& M, 
                                                                   const ApgConfig& cfg = {},
                                                                   std::vector<IterTrace>* trace = nullptr);
 double factored_inner(const LowRankEstimate& a, const LowRankEstimate& b);
+
+namespace detail {
+struct Csc;
+}
+// Resumable apg_mc (bench sampling of fixed iteration windows; same arithmetic as apg_mc).
+struct ApgMcRun {
+  ApgMcRun(const ObservedMatrix& obs, const ApgConfig& cfg);
+  ~ApgMcRun();
+  bool step(std::vector<IterTrace>* trace = nullptr);  // false once stopped / at max_iters
+  std::pair<LowRankEstimate, SolveReport> finish() const;
+
+  ObservedMatrix obs;
+  ApgConfig cfg;
+  std::unique_ptr<detail::Csc> M, R;
+  std::vector<double> m_vals;
+  double mu_init = 0, mu_floor = 0;
+  SeededRng svd_rng;
+  LowRankEstimate L_prev, L_curr;
+  SvdFactors last;
+  double tau_prev = 1.0, tau_curr = 1.0, mu = 0, mu_used = 0;
+  Index rank_hint = 1;
+  int iters = 0;
+  bool stopped = false;
+  std::chrono::steady_clock::time_point start;
+};
 double factored_diff_norm(const LowRankEstimate& a, const LowRankEstimate& b);
 
 // ---------------------------------------------------------------- orchestrator (P/include/dfc/dfc.hpp:24-335)

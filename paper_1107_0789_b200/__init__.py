@@ -14,6 +14,7 @@ from ._lib import (  # noqa: F401
     BlockError,
     DfcError,
     Estimate,
+    McSolver,
     Observed,
     Report,
     apg_mc,
@@ -34,6 +35,9 @@ from .host import (  # noqa: F401
     extract_columns,
     extract_rows,
     gen_mc_instance,
+    launch_count,
+    prof_collect,
+    prof_enable,
     gen_rmf_instance,
     median_rank,
     partition_columns,

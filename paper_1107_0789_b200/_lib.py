@@ -62,7 +62,7 @@ class SparseC(C.Structure):
 
 class TraceC(C.Structure):
     _fields_ = [("it", C.c_int32), ("rank", i64), ("k_final", i64), ("svd_calls", C.c_int32),
-                ("rel", C.c_double), ("mu", C.c_double), ("sigma_sum", C.c_double)]
+                ("rel", C.c_double), ("mu", C.c_double), ("sigma_sum", C.c_double), ("ms", C.c_double)]
 
 
 class DfcCfgC(C.Structure):
@@ -232,6 +232,9 @@ def _lowrank_in(e: Estimate, keep: _Keep) -> LowRankC:
 
 def _lowrank_out(c: LowRankC) -> Estimate:
     m, n, k = c.m, c.n, c.k
+    if k == 0:
+        lib().dfcg_lowrank_free(C.byref(c))
+        return Estimate(np.zeros((m, 0), order="F"), np.zeros((n, 0), order="F"))
     left = np.ctypeslib.as_array(c.left, shape=(max(k, 1) * m,))[: m * k].copy().reshape((m, k), order="F")
     right = np.ctypeslib.as_array(c.right, shape=(max(k, 1) * n,))[: n * k].copy().reshape((n, k), order="F")
     lib().dfcg_lowrank_free(C.byref(c))
@@ -249,7 +252,7 @@ def _obs_in(obs: Observed, keep: _Keep) -> ObsC:
 
 def _trace_list(tr, n):
     return [dict(it=tr[i].it, rank=tr[i].rank, k_final=tr[i].k_final, svd_calls=tr[i].svd_calls, rel=tr[i].rel,
-                 mu=tr[i].mu, sigma_sum=tr[i].sigma_sum) for i in range(n)]
+                 mu=tr[i].mu, sigma_sum=tr[i].sigma_sum, ms=tr[i].ms) for i in range(n)]
 
 
 # ------------------------------------------------------------------ F step
@@ -288,6 +291,43 @@ def apg_rmf(M: np.ndarray, lam: float, cfg: ApgConfig | None = None, device: int
     lib().dfcg_sparse_free(C.byref(S))
     return _lowrank_out(L), (rows, cols, vals), Report(rep.iterations, rep.objective, rep.residual, rep.rank,
                                                        rep.wall_ms, _trace_list(tr, min(n.value, cap)))
+
+
+class McSolver:
+    """Resumable apg_mc with Omega resident on the GPU (dfcg_mc_solver_*)."""
+
+    def __init__(self, obs: Observed, cfg: ApgConfig | None = None, device: int = 0):
+        self.cfg = cfg or ApgConfig()
+        keep = _Keep()
+        o = _obs_in(obs, keep)
+        self._h = C.c_void_p()
+        _check(lib().dfcg_mc_solver_create(context(device), C.byref(o), C.byref(self.cfg.c()), C.byref(self._h)))
+
+    def step(self, n: int = 1, trace: bool = False):
+        done = i64()
+        cap = max(n, 1) if trace else 0
+        tr = (TraceC * max(cap, 1))()
+        tl = i64()
+        _check(lib().dfcg_mc_solver_step(self._h, i64(n), C.byref(done), tr if trace else None, i64(cap),
+                                         C.byref(tl)))
+        return (done.value, _trace_list(tr, min(tl.value, cap))) if trace else done.value
+
+    def finish(self):
+        out = LowRankC()
+        rep = ReportC()
+        _check(lib().dfcg_mc_solver_finish(self._h, C.byref(out), C.byref(rep)))
+        return _lowrank_out(out), Report(rep.iterations, rep.objective, rep.residual, rep.rank, rep.wall_ms)
+
+    def close(self):
+        if self._h:
+            lib().dfcg_mc_solver_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------ C step

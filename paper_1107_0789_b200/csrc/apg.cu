@@ -146,6 +146,7 @@ __global__ void multi_sum_final(int K, int nb, const double* part, double* out) 
 
 template <int K, class F>
 std::vector<double> multi_sum(cudaStream_t s, i64 n, F f) {
+  prof::Scope scope(prof::kReduce, s, 3.0 * K * n, 8.0 * 4 * n);
   DBuf<double> part(K * RB, s), out(K, s);
   multi_sum_partial<K><<<RB, RT, 0, s>>>(n, f, part.get());
   DFCG_LAUNCH_CHECK();
@@ -290,12 +291,14 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
   cur.pos += w * b;
   transpose(s, b, w, Gt.get(), w, G.get(), b);
   op.apply(s, G.get(), b, X.get());
-  thin_qr(s, m, b, X.get(), b, nullptr, 0);
+  // intermediate bases only need a well-conditioned basis of the same span (one CholQR pass);
+  // the final Q, used as a projector, gets the full CholeskyQR2.
+  thin_qr(s, m, b, X.get(), b, nullptr, 0, q > 0 ? 1 : 2);
   for (i64 it = 0; it < q; ++it) {
     op.apply_adjoint(s, X.get(), b, Z.get());
-    thin_qr(s, w, b, Z.get(), b, nullptr, 0);
+    thin_qr(s, w, b, Z.get(), b, nullptr, 0, 1);
     op.apply(s, Z.get(), b, X.get());
-    thin_qr(s, m, b, X.get(), b, nullptr, 0);
+    thin_qr(s, m, b, X.get(), b, nullptr, 0, it + 1 < q ? 1 : 2);
   }
   op.apply_adjoint(s, X.get(), b, Z.get());  // Z = A^T Q  (w x b)
   DBuf<double> Uz(w * b, s), Vz(b * b, s);
@@ -427,133 +430,176 @@ void validate_config(const ApgConfig& cfg) {
 }
 
 // ---------------------------------------------------------------- apg_mc
+// spectral_norm (solvers.hpp:147-165) of P_Omega(M): alternating power iteration.
+static double spectral_norm_omega(cudaStream_t s, const DevOmega& om) {
+  const i64 m = om.m, n = om.n;
+  DBuf<double> v(n, s), wv(m, s), z(n, s), nrm(1, s);
+  fill_kernel<<<grid_for(n), 256, 0, s>>>(n, 1.0, v.get());
+  DFCG_LAUNCH_CHECK();
+  dot_sum(s, n, v.get(), v.get(), nrm.get());
+  sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+  scale_by_inv_kernel<<<grid_for(n), 256, 0, s>>>(n, v.get(), nrm.get(), v.get());
+  DFCG_LAUNCH_CHECK();
+  double sv = 0.0, prev = 0.0;
+  for (int it = 0; it < 200; ++it) {
+    spmm(s, om, false, om.m_csr.get(), 1, 1.0, v.get(), 1, 0.0, wv.get(), 1);
+    dot_sum(s, m, wv.get(), wv.get(), nrm.get());
+    sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+    const double nw = host_scalar(s, nrm.get());
+    if (nw == 0.0) return 0.0;
+    scale_by_inv_kernel<<<grid_for(m), 256, 0, s>>>(m, wv.get(), nrm.get(), wv.get());
+    spmm(s, om, true, om.m_csr.get(), 1, 1.0, wv.get(), 1, 0.0, z.get(), 1);
+    dot_sum(s, n, z.get(), z.get(), nrm.get());
+    sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
+    sv = host_scalar(s, nrm.get());
+    if (sv == 0.0) return 0.0;
+    scale_by_inv_kernel<<<grid_for(n), 256, 0, s>>>(n, z.get(), nrm.get(), v.get());
+    DFCG_LAUNCH_CHECK();
+    if (std::abs(sv - prev) <= 1e-10 * sv) break;
+    prev = sv;
+  }
+  return sv;
+}
+
+struct McSolver::State {
+  DevOmega om;
+  NormalCursor cur;
+  DBuf<double> r_csr;
+  DevLowRank Lp, Lc;
+  double icc = 0.0;  // factored_inner(L_curr, L_curr)
+  std::vector<double> last_s;
+  double mu_init = 0, mu_floor = 0, tau_prev = 1.0, tau_curr = 1.0, mu = 0, mu_used = 0;
+  i64 rank_hint = 1;
+};
+
+McSolver::McSolver(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows,
+                   const long long* cols, const double* vals, const ApgConfig& cfg)
+    : ctx_(ctx), s_(s), m_(m), n_(n), nnz_(nnz), cfg_(cfg), st_(std::make_unique<State>()) {
+  start_ = std::chrono::steady_clock::now();
+  if (nnz == 0) throw std::invalid_argument("apg_mc: empty observation set");
+  validate_config(cfg);
+  State& st = *st_;
+  st.om.build(s, m, n, nnz, rows, cols, vals);
+  st.mu_init = cfg.mu_init ? *cfg.mu_init : 0.99 * spectral_norm_omega(s, st.om);
+  st.mu_floor = cfg.mu_floor ? *cfg.mu_floor : 1e-4 * st.mu_init;
+  if (st.mu_floor > st.mu_init) throw std::invalid_argument("apg_mc: mu_floor exceeds mu_init");
+  st.cur = NormalCursor{&ctx.normals(0), 0};
+  st.r_csr.alloc(nnz, s);
+  st.Lp.m = st.Lc.m = m;
+  st.Lp.n = st.Lc.n = n;
+  st.mu = st.mu_used = st.mu_init;
+}
+
+McSolver::~McSolver() = default;
+
+// One iteration of the apg_mc loop (solvers.hpp:275-317).
+bool McSolver::step(std::vector<IterTrace>* trace) {
+  if (stopped_ || iters_ >= cfg_.max_iters) return false;
+  const auto it_start = std::chrono::steady_clock::now();
+  State& st = *st_;
+  cudaStream_t s = s_;
+  const i64 m = m_, n = n_, nnz = nnz_;
+  const int it = ++iters_;
+  const double beta = (st.tau_prev - 1.0) / st.tau_curr;
+  // Y = extrapolate(L_curr, L_prev, beta) as concatenated factors (no compaction).
+  DevLowRank& Lc = st.Lc;
+  DevLowRank& Lp = st.Lp;
+  const bool concat = !(beta == 0.0 || Lp.k == 0);
+  const i64 kY = concat ? Lc.k + Lp.k : Lc.k;
+  DBuf<double> Yl, Yr;
+  if (kY > 0) {
+    Yl.alloc(m * kY, s);
+    Yr.alloc(n * kY, s);
+    if (Lc.k > 0) {
+      copy2d(s, m, Lc.k, Lc.left.get(), Lc.k, Yl.get(), kY);
+      copy2d(s, n, Lc.k, Lc.right.get(), Lc.k, Yr.get(), kY, 1.0 + beta);
+    }
+    if (concat) {
+      copy2d(s, m, Lp.k, Lp.left.get(), Lp.k, Yl.get() + Lc.k, kY);
+      copy2d(s, n, Lp.k, Lp.right.get(), Lp.k, Yr.get() + Lc.k, kY, -beta);
+    }
+  }
+  // R = P_Omega(Y) - P_Omega(M)
+  sddmm_residual(s, st.om, kY, Yl.get(), kY, Yr.get(), kY, st.om.m_csr.get(), st.r_csr.get());
+
+  double step = 1.0;
+  SvtResult f;
+  for (;;) {
+    OpMC G{&st.om, st.r_csr.get(), -step, m, n, kY, Yl.get(), Yr.get()};
+    f = SvtResult{};
+    svt_operator(s, G, step * st.mu, st.rank_hint, st.cur, f);
+    if (!cfg_.line_search || step <= 0.125) break;
+    // backtracking majorization test (solvers.hpp:294-302)
+    DBuf<double> nd(nnz, s);
+    sddmm_residual(s, st.om, f.r, f.left.get(), f.r, f.right.get(), f.r, st.om.m_csr.get(), nd.get());  // next - m
+    const double f_next = 0.5 * dev_dot(s, nnz, nd.get(), nd.get());
+    const double rr = dev_dot(s, nnz, st.r_csr.get(), st.r_csr.get());
+    const double f_y = 0.5 * rr;
+    const double lin = dev_dot(s, nnz, st.r_csr.get(), nd.get()) - rr;  // sum (y-m)(next-y)
+    const double d2 = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get()) -
+                      2.0 * factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), kY, Yl.get(), Yr.get()) +
+                      factored_inner(s, m, n, kY, Yl.get(), Yr.get(), kY, Yl.get(), Yr.get());
+    const double dist2 = std::sqrt(std::max(0.0, d2));
+    if (f_next <= f_y + lin + dist2 * dist2 / (2.0 * step) + 1e-12) break;
+    step *= 0.5;
+  }
+  // rel = ||L_next - L_curr|| / max(1, ||L_curr||) via factored inner products (:305-306)
+  const double inn = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get());
+  const double inc = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), Lc.k, Lc.left.get(), Lc.right.get());
+  const double d2 = inn - 2.0 * inc + st.icc;
+  const double rel = std::sqrt(std::max(0.0, d2)) / std::max(1.0, std::sqrt(std::max(0.0, st.icc)));
+  const double tau_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * st.tau_curr * st.tau_curr));
+  Lp = std::move(Lc);
+  Lc = DevLowRank{};
+  Lc.m = m;
+  Lc.n = n;
+  Lc.k = f.r;
+  Lc.left = std::move(f.left);
+  Lc.right = std::move(f.right);
+  st.icc = inn;
+  st.last_s = f.s;
+  st.tau_prev = st.tau_curr;
+  st.tau_curr = tau_next;
+  st.rank_hint = std::max<i64>(1, Lc.k);
+  st.mu_used = st.mu;
+  if (trace) trace->push_back({it, Lc.k, f.k_final, f.calls, rel, st.mu, sum_of(st.last_s), ms_since(it_start)});
+  st.mu = std::max(cfg_.mu_decay * st.mu, st.mu_floor);
+  if (rel < cfg_.rel_tol) stopped_ = true;
+  return true;
+}
+
+// Report (solvers.hpp:319-326); the estimate is copied so the solver can keep stepping.
+void McSolver::finish(DevLowRank& out, SolveReport& rep) {
+  State& st = *st_;
+  cudaStream_t s = s_;
+  const DevLowRank& Lc = st.Lc;
+  rep.iterations = iters_;
+  rep.rank = Lc.k;
+  DBuf<double> fin(nnz_, s);
+  sddmm_residual(s, st.om, Lc.k, Lc.left.get(), Lc.k, Lc.right.get(), Lc.k, st.om.m_csr.get(), fin.get());
+  rep.residual = std::sqrt(dev_dot(s, nnz_, fin.get(), fin.get()));
+  rep.objective = st.mu_used * sum_of(st.last_s) + 0.5 * rep.residual * rep.residual;
+  out = DevLowRank{};
+  out.m = m_;
+  out.n = n_;
+  out.k = Lc.k;
+  if (Lc.k > 0) {
+    out.left.alloc(m_ * Lc.k, s);
+    out.right.alloc(n_ * Lc.k, s);
+    copy2d(s, m_, Lc.k, Lc.left.get(), Lc.k, out.left.get(), Lc.k);
+    copy2d(s, n_, Lc.k, Lc.right.get(), Lc.k, out.right.get(), Lc.k);
+  }
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  rep.wall_ms = ms_since(start_);
+}
+
 void apg_mc_device(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows,
                    const long long* cols, const double* vals, const ApgConfig& cfg, DevLowRank& out, SolveReport& rep,
                    std::vector<IterTrace>* trace) {
-  const auto start = std::chrono::steady_clock::now();
-  if (nnz == 0) throw std::invalid_argument("apg_mc: empty observation set");
-  validate_config(cfg);
-  DevOmega om;
-  om.build(s, m, n, nnz, rows, cols, vals);
-
-  // spectral_norm (solvers.hpp:147-165) of P_Omega(M): alternating power iteration.
-  auto spectral = [&]() {
-    DBuf<double> v(n, s), wv(m, s), z(n, s), nrm(1, s);
-    fill_kernel<<<grid_for(n), 256, 0, s>>>(n, 1.0, v.get());
-    DFCG_LAUNCH_CHECK();
-    dot_sum(s, n, v.get(), v.get(), nrm.get());
-    sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
-    scale_by_inv_kernel<<<grid_for(n), 256, 0, s>>>(n, v.get(), nrm.get(), v.get());
-    DFCG_LAUNCH_CHECK();
-    double sv = 0.0, prev = 0.0;
-    for (int it = 0; it < 200; ++it) {
-      spmm(s, om, false, om.m_csr.get(), 1, 1.0, v.get(), 1, 0.0, wv.get(), 1);
-      dot_sum(s, m, wv.get(), wv.get(), nrm.get());
-      sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
-      const double nw = host_scalar(s, nrm.get());
-      if (nw == 0.0) return 0.0;
-      scale_by_inv_kernel<<<grid_for(m), 256, 0, s>>>(m, wv.get(), nrm.get(), wv.get());
-      spmm(s, om, true, om.m_csr.get(), 1, 1.0, wv.get(), 1, 0.0, z.get(), 1);
-      dot_sum(s, n, z.get(), z.get(), nrm.get());
-      sqrt_kernel<<<1, 1, 0, s>>>(nrm.get());
-      sv = host_scalar(s, nrm.get());
-      if (sv == 0.0) return 0.0;
-      scale_by_inv_kernel<<<grid_for(n), 256, 0, s>>>(n, z.get(), nrm.get(), v.get());
-      DFCG_LAUNCH_CHECK();
-      if (std::abs(sv - prev) <= 1e-10 * sv) break;
-      prev = sv;
-    }
-    return sv;
-  };
-  const double mu_init = cfg.mu_init ? *cfg.mu_init : 0.99 * spectral();
-  const double mu_floor = cfg.mu_floor ? *cfg.mu_floor : 1e-4 * mu_init;
-  if (mu_floor > mu_init) throw std::invalid_argument("apg_mc: mu_floor exceeds mu_init");
-
-  NormalCursor cur{&ctx.normals(0), 0};
-  DBuf<double> r_csr(nnz, s);
-  DevLowRank Lp, Lc;  // k = 0
-  Lp.m = Lc.m = m;
-  Lp.n = Lc.n = n;
-  double icc = 0.0;  // factored_inner(L_curr, L_curr)
-  std::vector<double> last_s;
-  double tau_prev = 1.0, tau_curr = 1.0, mu = mu_init, mu_used = mu_init;
-  i64 rank_hint = 1;
-  int iters = 0;
-  for (int it = 1; it <= cfg.max_iters; ++it) {
-    iters = it;
-    const double beta = (tau_prev - 1.0) / tau_curr;
-    // Y = extrapolate(L_curr, L_prev, beta) as concatenated factors (no compaction).
-    const bool concat = !(beta == 0.0 || Lp.k == 0);
-    const i64 kY = concat ? Lc.k + Lp.k : Lc.k;
-    DBuf<double> Yl, Yr;
-    if (kY > 0) {
-      Yl.alloc(m * kY, s);
-      Yr.alloc(n * kY, s);
-      if (Lc.k > 0) {
-        copy2d(s, m, Lc.k, Lc.left.get(), Lc.k, Yl.get(), kY);
-        copy2d(s, n, Lc.k, Lc.right.get(), Lc.k, Yr.get(), kY, 1.0 + beta);
-      }
-      if (concat) {
-        copy2d(s, m, Lp.k, Lp.left.get(), Lp.k, Yl.get() + Lc.k, kY);
-        copy2d(s, n, Lp.k, Lp.right.get(), Lp.k, Yr.get() + Lc.k, kY, -beta);
-      }
-    }
-    // R = P_Omega(Y) - P_Omega(M)
-    sddmm_residual(s, om, kY, Yl.get(), kY, Yr.get(), kY, om.m_csr.get(), r_csr.get());
-
-    double step = 1.0;
-    SvtResult f;
-    for (;;) {
-      OpMC G{&om, r_csr.get(), -step, m, n, kY, Yl.get(), Yr.get()};
-      f = SvtResult{};
-      svt_operator(s, G, step * mu, rank_hint, cur, f);
-      if (!cfg.line_search || step <= 0.125) break;
-      // backtracking majorization test (solvers.hpp:294-302)
-      DBuf<double> nd(nnz, s);
-      sddmm_residual(s, om, f.r, f.left.get(), f.r, f.right.get(), f.r, om.m_csr.get(), nd.get());  // next - m
-      const double f_next = 0.5 * dev_dot(s, nnz, nd.get(), nd.get());
-      const double rr = dev_dot(s, nnz, r_csr.get(), r_csr.get());
-      const double f_y = 0.5 * rr;
-      const double lin = dev_dot(s, nnz, r_csr.get(), nd.get()) - rr;  // sum (y-m)(next-y)
-      const double d2 = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get()) -
-                        2.0 * factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), kY, Yl.get(), Yr.get()) +
-                        factored_inner(s, m, n, kY, Yl.get(), Yr.get(), kY, Yl.get(), Yr.get());
-      const double dist2 = std::sqrt(std::max(0.0, d2));
-      if (f_next <= f_y + lin + dist2 * dist2 / (2.0 * step) + 1e-12) break;
-      step *= 0.5;
-    }
-    // rel = ||L_next - L_curr|| / max(1, ||L_curr||) via factored inner products (:305-306)
-    const double inn = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get());
-    const double inc = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), Lc.k, Lc.left.get(), Lc.right.get());
-    const double d2 = inn - 2.0 * inc + icc;
-    const double rel = std::sqrt(std::max(0.0, d2)) / std::max(1.0, std::sqrt(std::max(0.0, icc)));
-    const double tau_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tau_curr * tau_curr));
-    Lp = std::move(Lc);
-    Lc = DevLowRank{};
-    Lc.m = m;
-    Lc.n = n;
-    Lc.k = f.r;
-    Lc.left = std::move(f.left);
-    Lc.right = std::move(f.right);
-    icc = inn;
-    last_s = f.s;
-    tau_prev = tau_curr;
-    tau_curr = tau_next;
-    rank_hint = std::max<i64>(1, Lc.k);
-    mu_used = mu;
-    if (trace) trace->push_back({it, Lc.k, f.k_final, f.calls, rel, mu, sum_of(last_s)});
-    mu = std::max(cfg.mu_decay * mu, mu_floor);
-    if (rel < cfg.rel_tol) break;
+  McSolver solver(ctx, s, m, n, nnz, rows, cols, vals, cfg);
+  while (solver.step(trace)) {
   }
-  rep.iterations = iters;
-  rep.rank = Lc.k;
-  DBuf<double> fin(nnz, s);
-  sddmm_residual(s, om, Lc.k, Lc.left.get(), Lc.k, Lc.right.get(), Lc.k, om.m_csr.get(), fin.get());
-  rep.residual = std::sqrt(dev_dot(s, nnz, fin.get(), fin.get()));
-  rep.objective = mu_used * sum_of(last_s) + 0.5 * rep.residual * rep.residual;
-  out = std::move(Lc);
-  DFCG_CUDA(cudaStreamSynchronize(s));
-  rep.wall_ms = ms_since(start);
+  solver.finish(out, rep);
 }
 
 // ---------------------------------------------------------------- apg_rmf
@@ -617,6 +663,7 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
     YS.alloc(mn, s);
     Gd.alloc(mn, s);
   }
+  auto it_start = std::chrono::steady_clock::now();
   for (int it = 1; it <= cfg.max_iters; ++it) {
     iters = it;
     const double beta = (tau_prev - 1.0) / tau_curr;
@@ -628,6 +675,7 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
       DFCG_LAUNCH_CHECK();
     }
     for (;;) {
+      prof::Scope scope(prof::kElementwise, s, 10.0 * mn, (cfg.line_search ? 5.0 : 7.0) * 8.0 * mn);
       if (cfg.line_search) {
         rmf_step_kernel<<<gb, 256, 0, s>>>(mn, step, step * lambda * mu, YL.get(), YS.get(), Gd.get(), GL.get(),
                                            Sn.get());
@@ -687,7 +735,8 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
     tau_curr = tau_next;
     rank_hint = std::max<i64>(1, last.r);
     mu_used = mu;
-    if (trace) trace->push_back({it, last.r, last.k_final, last.calls, rel, mu, sum_of(last.s)});
+    if (trace) trace->push_back({it, last.r, last.k_final, last.calls, rel, mu, sum_of(last.s), ms_since(it_start)});
+    it_start = std::chrono::steady_clock::now();
     mu = std::max(cfg.mu_decay * mu, mu_floor);
     if (rel < cfg.rel_tol) break;
   }

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <new>
 #include <string>
 
@@ -14,6 +15,12 @@ using namespace dfcg;
 
 struct dfcg_ctx {
   DeviceContext* dev;
+};
+
+struct dfcg_mc_solver {
+  DeviceContext* dev;
+  cudaStream_t s;
+  std::unique_ptr<McSolver> solver;
 };
 
 namespace {
@@ -75,7 +82,7 @@ void to_trace(const std::vector<IterTrace>& tr, dfcg_iter_trace* out, int64_t ca
   if (len) *len = static_cast<int64_t>(tr.size());
   if (!out) return;
   for (size_t i = 0; i < tr.size() && static_cast<int64_t>(i) < cap; ++i)
-    out[i] = {tr[i].it, tr[i].rank, tr[i].k_final, tr[i].svd_calls, tr[i].rel, tr[i].mu, tr[i].sigma_sum};
+    out[i] = {tr[i].it, tr[i].rank, tr[i].k_final, tr[i].svd_calls, tr[i].rel, tr[i].mu, tr[i].sigma_sum, tr[i].ms};
 }
 
 double* dup_array(const std::vector<double>& v) {
@@ -206,6 +213,62 @@ int dfcg_apg_mc(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_apg_cfg* cfg, dfcg
     to_report(r, rep);
     to_trace(tr, trace, trace_cap, trace_len);
   });
+}
+
+int dfcg_mc_solver_create(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_apg_cfg* cfg, dfcg_mc_solver** out) {
+  return guard([&] {
+    if (!ctx || !in || !out) throw std::invalid_argument("dfcg_mc_solver_create: null argument");
+    HostObs obs = HostObs::make(in->m, in->n, std::vector<long long>(in->row, in->row + in->nnz),
+                                std::vector<long long>(in->col, in->col + in->nnz),
+                                std::vector<double>(in->val, in->val + in->nnz));
+    DFCG_CUDA(cudaSetDevice(ctx->dev->device));
+    auto* h = new dfcg_mc_solver{ctx->dev, ctx->dev->acquire(), nullptr};
+    try {
+      h->solver = std::make_unique<McSolver>(*ctx->dev, h->s, obs.m, obs.n, obs.count(), obs.row.data(),
+                                             obs.col.data(), obs.val.data(), to_cfg(cfg));
+      DFCG_CUDA(cudaStreamSynchronize(h->s));
+    } catch (...) {
+      ctx->dev->release(h->s);
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int dfcg_mc_solver_step(dfcg_mc_solver* sv, int64_t n_iters, int64_t* done, dfcg_iter_trace* trace,
+                        int64_t trace_cap, int64_t* trace_len) {
+  return guard([&] {
+    if (!sv) throw std::invalid_argument("dfcg_mc_solver_step: null solver");
+    DFCG_CUDA(cudaSetDevice(sv->dev->device));
+    std::vector<IterTrace> tr;
+    int64_t k = 0;
+    while (k < n_iters && sv->solver->step(&tr)) ++k;
+    DFCG_CUDA(cudaStreamSynchronize(sv->s));
+    if (done) *done = k;
+    to_trace(tr, trace, trace_cap, trace_len);
+  });
+}
+
+int dfcg_mc_solver_finish(dfcg_mc_solver* sv, dfcg_lowrank* out, dfcg_solve_report* rep) {
+  return guard([&] {
+    if (!sv || !out) throw std::invalid_argument("dfcg_mc_solver_finish: null argument");
+    DFCG_CUDA(cudaSetDevice(sv->dev->device));
+    DevLowRank L;
+    SolveReport r;
+    sv->solver->finish(L, r);
+    to_c(sv->s, L, out);
+    to_report(r, rep);
+  });
+}
+
+void dfcg_mc_solver_destroy(dfcg_mc_solver* sv) {
+  if (!sv) return;
+  cudaSetDevice(sv->dev->device);
+  sv->solver.reset();
+  cudaStreamSynchronize(sv->s);
+  sv->dev->release(sv->s);
+  delete sv;
 }
 
 int dfcg_apg_rmf(dfcg_ctx* ctx, const double* M_colmajor, int64_t m, int64_t n, double lambda,

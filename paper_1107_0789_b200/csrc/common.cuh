@@ -15,6 +15,8 @@
 #include <utility>
 #include <vector>
 
+#include "prof.hpp"
+
 namespace dfcg {
 
 using i64 = std::int64_t;
@@ -31,7 +33,11 @@ struct CudaError : std::runtime_error {
                               __FILE__ + ":" + std::to_string(__LINE__));                        \
   } while (0)
 
-#define DFCG_LAUNCH_CHECK() DFCG_CUDA(cudaGetLastError())
+#define DFCG_LAUNCH_CHECK()             \
+  do {                                  \
+    ::dfcg::prof::count_launch();       \
+    DFCG_CUDA(cudaGetLastError());      \
+  } while (0)
 
 inline int cdiv(i64 a, i64 b) { return static_cast<int>((a + b - 1) / b); }
 
@@ -113,15 +119,17 @@ struct Workspace;  // forward
 // R (cols x cols, row-major, upper) written when R != nullptr. CholeskyQR2 fast path
 // with a blocked Householder fallback when the Gram factor is too ill-conditioned.
 // Returns true when the Householder fallback ran.
-bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
+// passes = 1 gives a well-conditioned basis of span(X) (orthogonality ~ eps cond(X)^2),
+// enough for the intermediate bases of the range finder; passes = 2 is CholeskyQR2.
+bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr, int passes = 2);
 // Householder QR only (tests / fallback).
 void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
 
 // Thin SVD of a row-major rows x cols matrix A (rows >= cols), A is destroyed.
 //   U (rows x cols, ldu), S (cols, device), V (cols x cols, ldv), singular values sorted
 //   nonincreasing (host copy returned in s_host).
-// Method: (rows > 1.25 cols) CholQR2/Householder -> one-sided block Jacobi on R, else
-// one-sided block Jacobi directly on A.
+// Method: columns sorted by norm, thin QR (CholQR2 / Householder fallback), one-sided block
+// Jacobi on R^T (QR-preconditioned Jacobi; few sweeps since R^T is graded).
 void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U, i64 ldu, double* V, i64 ldv,
               std::vector<double>& s_host);
 

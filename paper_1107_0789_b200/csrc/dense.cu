@@ -343,6 +343,8 @@ int grid_for(i64 total, int threads = 256) {
 void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc) {
   if (M <= 0 || N <= 0) return;
+  prof::Scope scope(prof::kGemm, s, 2.0 * M * N * K,
+                    8.0 * (M * K + K * N + M * N * (beta != 0.0 ? 2.0 : 1.0)));
   if (K <= 0 || alpha == 0.0) {
     scale_kernel<<<grid_for(M * N), 256, 0, s>>>(M, N, beta, C, ldc);
     DFCG_LAUNCH_CHECK();
@@ -361,12 +363,14 @@ void copy2d(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, doub
                                 cudaMemcpyDeviceToDevice, s));
     return;
   }
+  prof::Scope scope(prof::kElementwise, s, 0.0, 16.0 * rows * cols);
   copy2d_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, src, lds, dst, ldd, alpha);
   DFCG_LAUNCH_CHECK();
 }
 
 void transpose(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd) {
   if (rows <= 0 || cols <= 0) return;
+  prof::Scope scope(prof::kElementwise, s, 0.0, 16.0 * rows * cols);
   dim3 grid(cdiv(cols, 32), cdiv(rows, 32));
   transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(rows, cols, src, lds, dst, ldd);
   DFCG_LAUNCH_CHECK();
@@ -379,6 +383,7 @@ void set_identity(cudaStream_t s, i64 rows, i64 cols, double* dst, i64 ldd) {
 }
 
 void dot_sum(cudaStream_t s, i64 n, const double* a, const double* b, double* out) {
+  prof::Scope scope(prof::kReduce, s, 2.0 * n, 16.0 * n);
   DBuf<double> part(RED_BLOCKS, s);
   dot_partial<<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, a, b, part.get());
   DFCG_LAUNCH_CHECK();
@@ -389,12 +394,14 @@ void dot_sum(cudaStream_t s, i64 n, const double* a, const double* b, double* ou
 void gather_cols(cudaStream_t s, i64 rows, i64 ncols, const double* src, i64 lds, const int* idx,
                  const double* scale, double* dst, i64 ldd) {
   if (rows <= 0 || ncols <= 0) return;
+  prof::Scope scope(prof::kElementwise, s, 0.0, 16.0 * rows * ncols);
   gather_cols_kernel<<<grid_for(rows * ncols), 256, 0, s>>>(rows, ncols, src, lds, idx, scale, dst, ldd);
   DFCG_LAUNCH_CHECK();
 }
 
 void col_norms(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* out) {
   if (cols <= 0) return;
+  prof::Scope scope(prof::kReduce, s, 2.0 * rows * cols, 8.0 * rows * cols);
   col_norms_kernel<<<cdiv(cols, 32), 256, 0, s>>>(rows, cols, src, lds, out);
   DFCG_LAUNCH_CHECK();
 }

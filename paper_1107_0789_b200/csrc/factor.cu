@@ -12,6 +12,8 @@
 //   pair ordering, Gram/update by DMMA, inner 32x32 symmetric Jacobi in shared memory).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -54,28 +56,27 @@ __global__ void potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 
   extern __shared__ double dyn[];
   double(*a)[CNB + 1] = reinterpret_cast<double(*)[CNB + 1]>(dyn);
   double(*inv)[CNB + 1] = reinterpret_cast<double(*)[CNB + 1]>(dyn + CNB * (CNB + 1));
-  __shared__ double piv;
   const int t = threadIdx.x;
   for (int e = t; e < kb * kb; e += blockDim.x) a[e / kb][e % kb] = G[(e / kb) * ldg + (e % kb)];
   __syncthreads();
   const double thr = rel_tol * (*maxdiag);
+  const int ty = t >> 4, tx = t & 15;  // 16 x 16 thread grid for the trailing update
   for (int k = 0; k < kb; ++k) {
+    // every thread derives the pivot itself (a[k][k] is final after the previous sync)
+    double d = a[k][k];
+    const bool bad = !(d > thr) || !isfinite(d);
+    if (bad) d = 1.0;
+    const double pv = sqrt(d), ipv = 1.0 / pv;
+    __syncthreads();  // all reads of a[k][k] done before row k is rewritten
     if (t == 0) {
-      double d = a[k][k];
-      if (!(d > thr) || !isfinite(d)) {
-        atomicExch(fail, 1);
-        d = 1.0;
-      }
-      piv = sqrt(d);
-      a[k][k] = piv;
+      if (bad) atomicExch(fail, 1);
+      a[k][k] = pv;
     }
+    for (int j = k + 1 + t; j < kb; j += blockDim.x) a[k][j] *= ipv;
     __syncthreads();
-    for (int j = k + 1 + t; j < kb; j += blockDim.x) a[k][j] /= piv;
-    __syncthreads();
-    const int rem = kb - k - 1;
-    for (int e = t; e < rem * rem; e += blockDim.x) {
-      const int i = k + 1 + e / rem, j = k + 1 + e % rem;
-      if (j >= i) a[i][j] -= a[k][i] * a[k][j];
+    for (int i = k + 1 + ty; i < kb; i += 16) {
+      const double aki = a[k][i];
+      for (int j = i + tx; j < kb; j += 16) a[i][j] -= aki * a[k][j];
     }
     __syncthreads();
   }
@@ -86,15 +87,20 @@ __global__ void potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 
     inv[i][j] = 0.0;
   }
   __syncthreads();
-  for (int j = t; j < kb; j += blockDim.x) {
-    inv[j][j] = 1.0 / a[j][j];
-    for (int i = j - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int l = i + 1; l <= j; ++l) s += a[i][l] * inv[l][j];
-      inv[i][j] = -s / a[i][i];
+  // inverse of the upper triangle, one row at a time from the bottom; 4 lanes per column
+  // share the inner product (blockDim.x == 256 -> 64 columns x 4 lanes).
+  {
+    const int j = t >> 2, part = t & 3;
+    for (int i = kb - 1; i >= 0; --i) {
+      double acc = 0.0;
+      if (j < kb && j > i)
+        for (int l = i + 1 + part; l <= j; l += 4) acc += a[i][l] * inv[l][j];
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (j < kb && j >= i && part == 0) inv[i][j] = ((i == j ? 1.0 : 0.0) - acc) / a[i][i];
+      __syncthreads();
     }
   }
-  __syncthreads();
   for (int e = t; e < kb * kb; e += blockDim.x) {
     const int i = e / kb, j = e % kb;
     G[i * ldg + j] = a[i][j];
@@ -130,6 +136,7 @@ void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i
   for (i64 k0 = 0; k0 < n; k0 += CNB) {
     const int kb = static_cast<int>(std::min<i64>(CNB, n - k0));
     double* Gkk = G + k0 * ldg + k0;
+    prof::Scope scope(prof::kCholesky, s, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
     potrf_diag_kernel<<<1, 256, kPotrfSmem, s>>>(kb, Gkk, ldg, Rinv + k0 * ldr + k0, ldr, maxdiag.get(), rel_tol,
                                                  fail);
     DFCG_LAUNCH_CHECK();
@@ -272,7 +279,7 @@ __global__ void extract_upper(i64 n, const double* X, i64 ldx, double* R, i64 ld
 }
 
 // ================================================================ one-sided block Jacobi SVD
-constexpr int JNB = 16, JW = 2 * JNB, JTHREADS = 256, JCHUNK = 64;
+constexpr int JCHUNK = 64;
 
 // Round-robin schedule: pairs[(round * npairs + p) * 2 + {0,1}] = block ids.
 std::vector<int> round_robin(int p) {
@@ -284,19 +291,23 @@ std::vector<int> round_robin(int p) {
       out.push_back(ring[k]);
       out.push_back(ring[p - 1 - k]);
     }
-    // rotate all but the first
-    const int last = ring[p - 1];
+    const int last = ring[p - 1];  // rotate all but the first
     for (int k = p - 1; k > 1; --k) ring[k] = ring[k - 1];
     ring[1] = last;
   }
   return out;
 }
 
-// One Jacobi round: each CTA orthogonalises the 32 columns of one block pair of W (rows x n)
-// and applies the same rotation to the pair's columns of V (nv x n).
-__global__ void __launch_bounds__(JTHREADS) jacobi_round_kernel(i64 rows, i64 nv, double* W, i64 ldw, double* V,
-                                                                i64 ldv, const int* pairs, double tol,
-                                                                unsigned long long* offmax, int inner_sweeps) {
+// One Jacobi round: each CTA orthogonalises the JW = 2*NB columns of one block pair of W
+// (rows x n) and applies the same rotation to the pair's columns of V (nv x n).
+//   Gram by DMMA over 64-row chunks -> inner cyclic Jacobi EVD of the JW x JW Gram in shared
+//   memory (parallel ordering, JW/2 rotations per step) -> [W_I W_J] <- [W_I W_J] R, same for V.
+// Pairs whose columns are already orthogonal to `tol` are left untouched.
+template <int NB>
+__global__ void __launch_bounds__(16 * NB) jacobi_round_kernel(i64 rows, i64 nv, double* W, i64 ldw, double* V,
+                                                               i64 ldv, const int* pairs, double tol,
+                                                               unsigned long long* offmax, int inner_sweeps) {
+  constexpr int JW = 2 * NB, T = 16 * NB, NT = JW / 8;  // NT = 8x8 tiles per side
   __shared__ double chunk[JCHUNK][JW + 1];
   __shared__ double g[JW][JW + 1];
   __shared__ double rot[JW][JW + 1];
@@ -305,15 +316,16 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_round_kernel(i64 rows, i64 nv
   __shared__ double s_off;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int bi = pairs[2 * blockIdx.x], bj = pairs[2 * blockIdx.x + 1];
-  // column c of the pair (0..31) -> global column
-  auto gcol = [&](int c) -> i64 { return c < JNB ? static_cast<i64>(bi) * JNB + c : static_cast<i64>(bj) * JNB + c - JNB; };
+  auto gcol = [&](int c) -> i64 { return c < NB ? static_cast<i64>(bi) * NB + c : static_cast<i64>(bj) * NB + c - NB; };
 
-  // ---- Gram G = P^T P, P = W[:, pair cols]; warp w owns output tiles (w/2, 2*(w%2)+{0,1}) of 4x4 8x8 tiles
-  double acc[2][2] = {{0, 0}, {0, 0}};
-  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
+  // ---- Gram G = P^T P over the rows; warp w owns tiles w*TPW .. w*TPW+TPW-1 of the NT x NT grid
+  constexpr int TPW = (NT * NT) / (T / 32);
+  double acc[TPW][2];
+#pragma unroll
+  for (int q = 0; q < TPW; ++q) acc[q][0] = acc[q][1] = 0.0;
   for (i64 r0 = 0; r0 < rows; r0 += JCHUNK) {
     __syncthreads();
-    for (int e = t; e < JCHUNK * JW; e += JTHREADS) {
+    for (int e = t; e < JCHUNK * JW; e += T) {
       const int r = e / JW, c = e % JW;
       const i64 gr = r0 + r;
       chunk[r][c] = gr < rows ? W[gr * ldw + gcol(c)] : 0.0;
@@ -321,28 +333,28 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_round_kernel(i64 rows, i64 nv
     __syncthreads();
 #pragma unroll 4
     for (int k = 0; k < JCHUNK; k += 4) {
-      // A = P^T (32 x K): A(i,k) = chunk[k][i]; B = P: B(k,j) = chunk[k][j]
-      const double a = chunk[k + (lane & 3)][ti * 8 + (lane >> 2)];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const double b = chunk[k + (lane & 3)][(tj0 + q) * 8 + (lane >> 2)];
+      for (int q = 0; q < TPW; ++q) {
+        const int tile = warp * TPW + q, ti = tile / NT, tj = tile % NT;
+        const double a = chunk[k + (lane & 3)][ti * 8 + (lane >> 2)];  // A = P^T
+        const double b = chunk[k + (lane & 3)][tj * 8 + (lane >> 2)];  // B = P
         dmma(acc[q], a, b);
       }
     }
   }
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int r = ti * 8 + (lane >> 2), c = (tj0 + q) * 8 + (lane & 3) * 2;
+  for (int q = 0; q < TPW; ++q) {
+    const int tile = warp * TPW + q, ti = tile / NT, tj = tile % NT;
+    const int r = ti * 8 + (lane >> 2), c = tj * 8 + (lane & 3) * 2;
     g[r][c] = acc[q][0];
     g[r][c + 1] = acc[q][1];
   }
-  for (int e = t; e < JW * JW; e += JTHREADS) rot[e / JW][e % JW] = (e / JW == e % JW) ? 1.0 : 0.0;
+  for (int e = t; e < JW * JW; e += T) rot[e / JW][e % JW] = (e / JW == e % JW) ? 1.0 : 0.0;
   __syncthreads();
 
-  auto off_measure = [&]() {
-    // max |g_ab| / sqrt(g_aa g_bb) over all a < b of the 32 pair columns
+  auto off_measure = [&]() {  // max |g_ab| / sqrt(g_aa g_bb), a < b
     double mx = 0.0;
-    for (int e = t; e < JW * JW; e += JTHREADS) {
+    for (int e = t; e < JW * JW; e += T) {
       const int a = e / JW, b = e % JW;
       if (a >= b) continue;
       const double d = sqrt(g[a][a]) * sqrt(g[b][b]);
@@ -352,21 +364,190 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_round_kernel(i64 rows, i64 nv
     __syncthreads();
     if (t == 0) s_off = 0.0;
     __syncthreads();
-    if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_off),
-                             static_cast<unsigned long long>(__double_as_longlong(mx)));
+    if (lane == 0)
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_off), static_cast<unsigned long long>(__double_as_longlong(mx)));
     __syncthreads();
     return s_off;
   };
   const double off0 = off_measure();
   if (t == 0) atomicMax(offmax, static_cast<unsigned long long>(__double_as_longlong(off0)));
-  if (off0 <= tol) return;  // pair already orthogonal: leave columns untouched
+  if (off0 <= tol) return;
 
-  // ---- inner cyclic Jacobi on g (32x32), parallel ordering (16 rotations per step)
+  // ---- inner cyclic Jacobi EVD of g (JW x JW)
   for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
     if (sweep > 0 && off_measure() <= 0.1 * tol) break;
     for (int step = 0; step < JW - 1; ++step) {
       if (t < JW / 2) {
-        // round-robin pairing on 32 items: fixed 0, ring of 31
+        int a, b;  // round-robin on JW items: 0 fixed, ring of JW-1
+        if (t == 0) {
+          a = 0;
+          b = 1 + (step % (JW - 1));
+        } else {
+          a = 1 + ((step + t) % (JW - 1));
+          b = 1 + ((step + (JW - 1) - t) % (JW - 1));
+        }
+        if (a > b) {
+          const int tmp = a;
+          a = b;
+          b = tmp;
+        }
+        pp[t][0] = a;
+        pp[t][1] = b;
+        const double gpq = g[a][b], gpp = g[a][a], gqq = g[b][b];
+        double c = 1.0, sn = 0.0;
+        if (fabs(gpq) > 1e-300 && fabs(gpq) > 1e-17 * sqrt(gpp * gqq)) {
+          const double theta = (gqq - gpp) / (2.0 * gpq);
+          const double tt = copysign(1.0, theta) / (fabs(theta) + sqrt(1.0 + theta * theta));
+          c = 1.0 / sqrt(1.0 + tt * tt);
+          sn = tt * c;
+        }
+        cs[t][0] = c;
+        cs[t][1] = sn;
+      }
+      __syncthreads();
+      for (int e = t; e < (JW / 2) * JW; e += T) {  // columns: g <- g J ; rot <- rot J
+        const int k = e / JW, r = e % JW;
+        const int a = pp[k][0], b = pp[k][1];
+        const double c = cs[k][0], sn = cs[k][1];
+        const double ga = g[r][a], gb = g[r][b];
+        g[r][a] = c * ga - sn * gb;
+        g[r][b] = sn * ga + c * gb;
+        const double ra = rot[r][a], rb = rot[r][b];
+        rot[r][a] = c * ra - sn * rb;
+        rot[r][b] = sn * ra + c * rb;
+      }
+      __syncthreads();
+      for (int e = t; e < (JW / 2) * JW; e += T) {  // rows: g <- J^T g
+        const int k = e / JW, r = e % JW;
+        const int a = pp[k][0], b = pp[k][1];
+        const double c = cs[k][0], sn = cs[k][1];
+        const double ga = g[a][r], gb = g[b][r];
+        g[a][r] = c * ga - sn * gb;
+        g[b][r] = sn * ga + c * gb;
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- P <- P rot on W (rows) and V (nv rows); 64-row chunks, 8 x NT tiles, 4 per warp
+  auto apply = [&](double* M, i64 ld, i64 nrows) {
+    for (i64 r0 = 0; r0 < nrows; r0 += JCHUNK) {
+      __syncthreads();
+      for (int e = t; e < JCHUNK * JW; e += T) {
+        const int r = e / JW, c = e % JW;
+        const i64 gr = r0 + r;
+        chunk[r][c] = gr < nrows ? M[gr * ld + gcol(c)] : 0.0;
+      }
+      __syncthreads();
+      double o[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+      for (int k = 0; k < JW; k += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int tile = warp * 4 + q, rt = tile / NT, ct = tile % NT;
+          dmma(o[q], chunk[rt * 8 + (lane >> 2)][k + (lane & 3)], rot[k + (lane & 3)][ct * 8 + (lane >> 2)]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int tile = warp * 4 + q, rt = tile / NT, ct = tile % NT;
+        const i64 gr = r0 + rt * 8 + (lane >> 2);
+        if (gr < nrows) {
+          const int c = ct * 8 + (lane & 3) * 2;
+          M[gr * ld + gcol(c)] = o[q][0];
+          M[gr * ld + gcol(c + 1)] = o[q][1];
+        }
+      }
+    }
+  };
+  apply(W, ldw, rows);
+  apply(V, ldv, nv);
+}
+
+// Shared-memory-resident variant of the round (rows <= kResidentRows): the pair's columns
+// of W are loaded once, the Gram is split over the 8 warps (fixed-order partial sums), and
+// the rotation is applied from shared memory straight back to global W; V is streamed
+// through registers (each warp owns whole 8-row tiles, so the in-place update is safe).
+constexpr int kResidentRows = 1408;
+
+template <int NB>
+__global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i64 nv, double* W, i64 ldw, double* V,
+                                                                    i64 ldv, const int* pairs, double tol,
+                                                                    unsigned long long* offmax, int inner_sweeps) {
+  constexpr int JW = 2 * NB, T = 256, NT = JW / 8, LD = JW + 1;
+  extern __shared__ double dyn[];
+  const i64 rows4 = (rows + 3) / 4 * 4;
+  double* Wp = dyn;                  // rows4 x LD
+  double* red = Wp + rows4 * LD;     // 8 warps x JW*JW partial Grams
+  __shared__ double g[JW][JW + 1];
+  __shared__ double rot[JW][JW + 1];
+  __shared__ double cs[JW / 2][2];
+  __shared__ int pp[JW / 2][2];
+  __shared__ double s_off;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int bi = pairs[2 * blockIdx.x], bj = pairs[2 * blockIdx.x + 1];
+  auto gcol = [&](int c) -> i64 { return c < NB ? static_cast<i64>(bi) * NB + c : static_cast<i64>(bj) * NB + c - NB; };
+
+  for (i64 e = t; e < rows4 * JW; e += T) {
+    const i64 r = e / JW;
+    const int c = static_cast<int>(e % JW);
+    Wp[r * LD + c] = r < rows ? W[r * ldw + gcol(c)] : 0.0;
+  }
+  __syncthreads();
+  {
+    double acc[NT * NT][2];
+#pragma unroll
+    for (int q = 0; q < NT * NT; ++q) acc[q][0] = acc[q][1] = 0.0;
+    for (i64 k = 4 * warp; k < rows4; k += 32) {
+      const double* row = Wp + (k + (lane & 3)) * LD + (lane >> 2);
+#pragma unroll
+      for (int ti = 0; ti < NT; ++ti)
+#pragma unroll
+        for (int tj = 0; tj < NT; ++tj) dmma(acc[ti * NT + tj], row[ti * 8], row[tj * 8]);
+    }
+#pragma unroll
+    for (int ti = 0; ti < NT; ++ti)
+#pragma unroll
+      for (int tj = 0; tj < NT; ++tj) {
+        const int r = ti * 8 + (lane >> 2), c = tj * 8 + (lane & 3) * 2;
+        red[warp * JW * JW + r * JW + c] = acc[ti * NT + tj][0];
+        red[warp * JW * JW + r * JW + c + 1] = acc[ti * NT + tj][1];
+      }
+  }
+  __syncthreads();
+  for (int e = t; e < JW * JW; e += T) {
+    double v = 0.0;
+    for (int w = 0; w < T / 32; ++w) v += red[w * JW * JW + e];
+    g[e / JW][e % JW] = v;
+    rot[e / JW][e % JW] = (e / JW == e % JW) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+
+  auto off_measure = [&]() {
+    double mx = 0.0;
+    for (int e = t; e < JW * JW; e += T) {
+      const int a = e / JW, b = e % JW;
+      if (a >= b) continue;
+      const double d = sqrt(g[a][a]) * sqrt(g[b][b]);
+      if (d > 0.0) mx = fmax(mx, fabs(g[a][b]) / d);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __syncthreads();
+    if (t == 0) s_off = 0.0;
+    __syncthreads();
+    if (lane == 0)
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_off), static_cast<unsigned long long>(__double_as_longlong(mx)));
+    __syncthreads();
+    return s_off;
+  };
+  const double off0 = off_measure();
+  if (t == 0) atomicMax(offmax, static_cast<unsigned long long>(__double_as_longlong(off0)));
+  if (off0 <= tol) return;
+
+  for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
+    if (sweep > 0 && off_measure() <= 0.1 * tol) break;
+    for (int step = 0; step < JW - 1; ++step) {
+      if (t < JW / 2) {
         int a, b;
         if (t == 0) {
           a = 0;
@@ -394,8 +575,7 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_round_kernel(i64 rows, i64 nv
         cs[t][1] = sn;
       }
       __syncthreads();
-      // columns: g <- g J ; rot <- rot J
-      for (int e = t; e < (JW / 2) * JW; e += JTHREADS) {
+      for (int e = t; e < (JW / 2) * JW; e += T) {
         const int k = e / JW, r = e % JW;
         const int a = pp[k][0], b = pp[k][1];
         const double c = cs[k][0], sn = cs[k][1];
@@ -407,8 +587,7 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_round_kernel(i64 rows, i64 nv
         rot[r][b] = sn * ra + c * rb;
       }
       __syncthreads();
-      // rows: g <- J^T g
-      for (int e = t; e < (JW / 2) * JW; e += JTHREADS) {
+      for (int e = t; e < (JW / 2) * JW; e += T) {
         const int k = e / JW, r = e % JW;
         const int a = pp[k][0], b = pp[k][1];
         const double c = cs[k][0], sn = cs[k][1];
@@ -420,37 +599,63 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_round_kernel(i64 rows, i64 nv
     }
   }
 
-  // ---- apply rot to the pair's columns of W (rows) and V (nv rows): P <- P rot
-  auto apply = [&](double* M, i64 ld, i64 nrows) {
-    for (i64 r0 = 0; r0 < nrows; r0 += JCHUNK) {
-      __syncthreads();
-      for (int e = t; e < JCHUNK * JW; e += JTHREADS) {
-        const int r = e / JW, c = e % JW;
-        const i64 gr = r0 + r;
-        chunk[r][c] = gr < nrows ? M[gr * ld + gcol(c)] : 0.0;
-      }
-      __syncthreads();
-      // output 64 x 32 = 8 x 4 tiles; warp w: tile row w, cols 0..3
-      double o[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  // W[:, pair] <- Wp rot (from shared memory)
+  const i64 rtiles = (rows + 7) / 8;
+  for (i64 rt = warp; rt < rtiles; rt += T / 32) {
+    double o[NT][2];
 #pragma unroll
-      for (int k = 0; k < JW; k += 4) {
-        const double a = chunk[warp * 8 + (lane >> 2)][k + (lane & 3)];
+    for (int ct = 0; ct < NT; ++ct) o[ct][0] = o[ct][1] = 0.0;
+    const i64 r = rt * 8 + (lane >> 2);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dmma(o[q], a, rot[k + (lane & 3)][q * 8 + (lane >> 2)]);
-      }
-      const i64 gr = r0 + warp * 8 + (lane >> 2);
-      if (gr < nrows) {
+    for (int k = 0; k < JW; k += 4) {
+      const double a = r < rows4 ? Wp[r * LD + k + (lane & 3)] : 0.0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c = q * 8 + (lane & 3) * 2;
-          M[gr * ld + gcol(c)] = o[q][0];
-          M[gr * ld + gcol(c + 1)] = o[q][1];
-        }
+      for (int ct = 0; ct < NT; ++ct) dmma(o[ct], a, rot[k + (lane & 3)][ct * 8 + (lane >> 2)]);
+    }
+    if (r < rows) {
+#pragma unroll
+      for (int ct = 0; ct < NT; ++ct) {
+        const int c = ct * 8 + (lane & 3) * 2;
+        W[r * ldw + gcol(c)] = o[ct][0];
+        W[r * ldw + gcol(c + 1)] = o[ct][1];
       }
     }
-  };
-  apply(W, ldw, rows);
-  apply(V, ldv, nv);
+  }
+  // V[:, pair] <- V[:, pair] rot (streamed; each warp reads its whole tile before writing it)
+  const i64 vtiles = (nv + 7) / 8;
+  for (i64 rt = warp; rt < vtiles; rt += T / 32) {
+    const i64 r = rt * 8 + (lane >> 2);
+    double a[JW / 4];
+#pragma unroll
+    for (int kk = 0; kk < JW / 4; ++kk) a[kk] = r < nv ? V[r * ldv + gcol(kk * 4 + (lane & 3))] : 0.0;
+    double o[NT][2];
+#pragma unroll
+    for (int ct = 0; ct < NT; ++ct) o[ct][0] = o[ct][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < JW / 4; ++kk)
+#pragma unroll
+      for (int ct = 0; ct < NT; ++ct) dmma(o[ct], a[kk], rot[kk * 4 + (lane & 3)][ct * 8 + (lane >> 2)]);
+    __syncwarp();
+    if (r < nv) {
+#pragma unroll
+      for (int ct = 0; ct < NT; ++ct) {
+        const int c = ct * 8 + (lane & 3) * 2;
+        V[r * ldv + gcol(c)] = o[ct][0];
+        V[r * ldv + gcol(c + 1)] = o[ct][1];
+      }
+    }
+  }
+}
+
+// dst[idx[p], :] = src[p, :]
+__global__ void scatter_rows_int_kernel(i64 l, i64 c, const double* __restrict__ src, i64 lds,
+                                        const int* __restrict__ idx, double* __restrict__ dst, i64 ldd) {
+  const i64 total = l * c;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 p = e / c, j = e % c;
+    dst[static_cast<i64>(idx[p]) * ldd + j] = src[p * lds + j];
+  }
 }
 
 __global__ void scale_cols_kernel(i64 rows, i64 cols, double* A, i64 lda, const double* s, i64 ldo, double* out,
@@ -478,6 +683,7 @@ void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, doub
     const int nb = static_cast<int>(std::min<i64>(HNB, cols - p0));
     const i64 pr = rows - p0;
     double* panel = X + p0 * ldx + p0;
+    prof::Scope scope(prof::kQrFallback, s, 4.0 * pr * nb * nb, 16.0 * pr * nb);
     hh_panel_kernel<<<1, HTHREADS, 0, s>>>(pr, nb, panel, ldx, tau.get() + p0);
     DFCG_LAUNCH_CHECK();
     hh_extract_v<<<grid_for(pr * nb), 256, 0, s>>>(pr, nb, panel, ldx, V.get());
@@ -518,12 +724,13 @@ void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, doub
 }
 
 // ---------------------------------------------------------------- CholeskyQR2 + fallback
-bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr) {
+bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr, int passes) {
   if (cols <= 0) return false;
   if (rows < cols) throw std::invalid_argument("thin_qr: rows < cols");
+  if (R) passes = 2;
   DBuf<int> fail(1, s);
   fail.zero(s);
-  DBuf<double> G(cols * cols, s), Rinv(cols * cols, s), Q1(rows * cols, s), Q2(rows * cols, s), R1;
+  DBuf<double> G(cols * cols, s), Rinv(cols * cols, s), Q1(rows * cols, s), Q2, R1;
   const double rel_tol = 1e-11;
   // pass 1
   gemm(s, true, false, cols, cols, rows, 1.0, X, ldx, X, ldx, 0.0, G.get(), cols);
@@ -533,10 +740,14 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
     R1.alloc(cols * cols, s);
     DFCG_CUDA(cudaMemcpyAsync(R1.get(), G.get(), sizeof(double) * cols * cols, cudaMemcpyDeviceToDevice, s));
   }
-  // pass 2
-  gemm(s, true, false, cols, cols, rows, 1.0, Q1.get(), cols, Q1.get(), cols, 0.0, G.get(), cols);
-  cholesky_inverse(s, cols, G.get(), cols, Rinv.get(), cols, rel_tol, fail.get());
-  gemm(s, false, false, rows, cols, cols, 1.0, Q1.get(), cols, Rinv.get(), cols, 0.0, Q2.get(), cols);
+  const double* Qfinal = Q1.get();
+  if (passes >= 2) {
+    Q2.alloc(rows * cols, s);
+    gemm(s, true, false, cols, cols, rows, 1.0, Q1.get(), cols, Q1.get(), cols, 0.0, G.get(), cols);
+    cholesky_inverse(s, cols, G.get(), cols, Rinv.get(), cols, rel_tol, fail.get());
+    gemm(s, false, false, rows, cols, cols, 1.0, Q1.get(), cols, Rinv.get(), cols, 0.0, Q2.get(), cols);
+    Qfinal = Q2.get();
+  }
   int h_fail = 0;
   DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
   DFCG_CUDA(cudaStreamSynchronize(s));
@@ -544,7 +755,7 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
     householder_qr(s, rows, cols, X, ldx, R, ldr);
     return true;
   }
-  copy2d(s, rows, cols, Q2.get(), cols, X, ldx);
+  copy2d(s, rows, cols, Qfinal, cols, X, ldx);
   if (R) gemm(s, false, false, cols, cols, cols, 1.0, G.get(), cols, R1.get(), cols, 0.0, R, ldr);  // R2 R1
   return false;
 }
@@ -555,57 +766,87 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   s_host.assign(static_cast<size_t>(std::max<i64>(cols, 0)), 0.0);
   if (cols <= 0) return;
   if (rows < cols) throw std::invalid_argument("thin_svd: rows < cols");
-  const int p0 = static_cast<int>((cols + JNB - 1) / JNB);
-  const int p = p0 + (p0 & 1);
-  const i64 np = static_cast<i64>(p) * JNB;  // padded column count
-  const bool precond = rows * 4 > cols * 5;
-  DBuf<double> Qbuf;
-  const i64 wrows = precond ? cols : rows;
+  // Preconditioning (Drmac-Veselic style): columns sorted by norm, thin QR  A P = Q R, then
+  // one-sided Jacobi on R^T (graded, near-orthogonal columns -> few sweeps):
+  //   R^T J = W (orthogonal columns, norms sigma)  =>  A = (Q J) Sigma (P W Sigma^-1)^T.
+  DBuf<double> nrm(cols, s);
+  col_norms(s, rows, cols, A, lda, nrm.get());
+  std::vector<double> h_nrm(cols);
+  DFCG_CUDA(cudaMemcpyAsync(h_nrm.data(), nrm.get(), sizeof(double) * cols, cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int> cperm(cols);
+  std::iota(cperm.begin(), cperm.end(), 0);
+  std::stable_sort(cperm.begin(), cperm.end(), [&](int a, int b) { return h_nrm[a] > h_nrm[b]; });
+  DBuf<int> dcperm(cols, s);
+  DFCG_CUDA(cudaMemcpyAsync(dcperm.get(), cperm.data(), sizeof(int) * cols, cudaMemcpyHostToDevice, s));
+  DBuf<double> Qx(rows * cols, s), R(cols * cols, s);
+  gather_cols(s, rows, cols, A, lda, dcperm.get(), nullptr, Qx.get(), cols);
+  thin_qr(s, rows, cols, Qx.get(), cols, R.get(), cols);
+
+  constexpr int NB = 8, JW = 2 * NB;
+  const int p0 = static_cast<int>((cols + NB - 1) / NB);
+  const int p = std::max(2, p0 + (p0 & 1));
+  const i64 np = static_cast<i64>(p) * NB;  // padded column count
+  const i64 wrows = cols;
   DBuf<double> W(wrows * np, s), J(np * np, s);
   W.zero(s);
-  if (precond) {
-    Qbuf.alloc(rows * cols, s);
-    copy2d(s, rows, cols, A, lda, Qbuf.get(), cols);
-    DBuf<double> Rt(cols * cols, s);
-    thin_qr(s, rows, cols, Qbuf.get(), cols, Rt.get(), cols);
-    copy2d(s, cols, cols, Rt.get(), cols, W.get(), np);
-  } else {
-    copy2d(s, rows, cols, A, lda, W.get(), np);
-  }
+  transpose(s, cols, cols, R.get(), cols, W.get(), np);  // W = R^T
   set_identity(s, np, np, J.get(), np);
   const std::vector<int> sched = round_robin(p);
   DBuf<int> pairs(static_cast<i64>(sched.size()), s);
   DFCG_CUDA(cudaMemcpyAsync(pairs.get(), sched.data(), sizeof(int) * sched.size(), cudaMemcpyHostToDevice, s));
   DBuf<unsigned long long> off(1, s);
-  const double tol = 2.2e-16 * std::max(8.0, std::sqrt(static_cast<double>(wrows)));
+  const double tol = 1e-13;
   const int npairs = p / 2;
-  for (int sweep = 0; sweep < 60 && p > 1; ++sweep) {
+  const bool resident = wrows <= kResidentRows;
+  const size_t smem = sizeof(double) * (((wrows + 3) / 4 * 4) * (JW + 1) + 8 * JW * JW);
+  if (resident) {
+    static unsigned configured = 0;
+    int dev = 0;
+    DFCG_CUDA(cudaGetDevice(&dev));
+    if (!(configured & (1u << dev))) {
+      const size_t max_smem = sizeof(double) * (kResidentRows * (JW + 1) + 8 * JW * JW);
+      DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(max_smem)));
+      configured |= 1u << dev;
+    }
+  }
+  static const bool trace_svd = std::getenv("DFCG_TRACE_SVD") != nullptr;
+  for (int sweep = 0; sweep < 60; ++sweep) {
     off.zero(s);
-    for (int r = 0; r < p - 1; ++r) {
-      jacobi_round_kernel<<<npairs, JTHREADS, 0, s>>>(wrows, np, W.get(), np, J.get(), np,
-                                                      pairs.get() + 2 * static_cast<i64>(r) * npairs, tol, off.get(),
-                                                      6);
-      DFCG_LAUNCH_CHECK();
+    {
+      prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 4.0 * (wrows + np)) * JW * JW,
+                        (p - 1.0) * npairs * 16.0 * (wrows + np) * JW);
+      for (int r = 0; r < p - 1; ++r) {
+        const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
+        if (resident)
+          jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, np, W.get(), np, J.get(), np, pr, tol,
+                                                                     off.get(), 2);
+        else
+          jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, np, W.get(), np, J.get(), np, pr, tol, off.get(),
+                                                              2);
+        DFCG_LAUNCH_CHECK();
+      }
     }
     unsigned long long h_off = 0;
     DFCG_CUDA(cudaMemcpyAsync(&h_off, off.get(), sizeof(h_off), cudaMemcpyDeviceToHost, s));
     DFCG_CUDA(cudaStreamSynchronize(s));
     double offv;
     std::memcpy(&offv, &h_off, sizeof(double));
+    if (trace_svd)
+      std::fprintf(stderr, "[svd] %lldx%lld sweep %d off %.3e\n", (long long)rows, (long long)cols, sweep, offv);
     if (offv <= tol) break;
   }
-  // singular values = column norms; sort descending (stable by index)
+  // singular values = column norms of W; sort descending (stable by index)
   DBuf<double> sig(np, s);
   col_norms(s, wrows, np, W.get(), np, sig.get());
   std::vector<double> h_sig(np);
   DFCG_CUDA(cudaMemcpyAsync(h_sig.data(), sig.get(), sizeof(double) * np, cudaMemcpyDeviceToHost, s));
   DFCG_CUDA(cudaStreamSynchronize(s));
-  std::vector<int> perm(cols);
-  std::iota(perm.begin(), perm.end(), 0);
-  // padded columns (>= cols) are exactly zero; only the first `cols` real columns are candidates
   std::vector<int> all(np);
   std::iota(all.begin(), all.end(), 0);
   std::stable_sort(all.begin(), all.end(), [&](int a, int b) { return h_sig[a] > h_sig[b]; });
+  std::vector<int> perm(cols);
   for (i64 c = 0; c < cols; ++c) {
     perm[c] = all[c];
     s_host[c] = h_sig[all[c]];
@@ -614,20 +855,18 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   DBuf<double> dsig(cols, s);
   DFCG_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), sizeof(int) * cols, cudaMemcpyHostToDevice, s));
   DFCG_CUDA(cudaMemcpyAsync(dsig.get(), s_host.data(), sizeof(double) * cols, cudaMemcpyHostToDevice, s));
-  // V = J[:, perm] restricted to the real rows
-  gather_cols(s, cols, cols, J.get(), np, dperm.get(), nullptr, V, ldv);
-  if (precond) {
-    DBuf<double> Wn(cols * cols, s);
-    scale_cols_kernel<<<grid_for(cols * cols), 256, 0, s>>>(cols, cols, W.get(), np, dsig.get(), cols, Wn.get(),
-                                                            dperm.get());
-    DFCG_LAUNCH_CHECK();
-    gemm(s, false, false, rows, cols, cols, 1.0, Qbuf.get(), cols, Wn.get(), cols, 0.0, U, ldu);
-  } else {
-    scale_cols_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, W.get(), np, dsig.get(), ldu, U,
-                                                            dperm.get());
-    DFCG_LAUNCH_CHECK();
-  }
-  DFCG_CUDA(cudaStreamSynchronize(s));  // host vectors (perm, s_host) used by async copies
+  // U = Q J[:, perm]
+  DBuf<double> Js(cols * cols, s);
+  gather_cols(s, cols, cols, J.get(), np, dperm.get(), nullptr, Js.get(), cols);
+  gemm(s, false, false, rows, cols, cols, 1.0, Qx.get(), cols, Js.get(), cols, 0.0, U, ldu);
+  // V = P (W[:, perm] / sigma): row j of the normalised W goes to row cperm[j]
+  DBuf<double> Wn(cols * cols, s);
+  scale_cols_kernel<<<grid_for(cols * cols), 256, 0, s>>>(cols, cols, W.get(), np, dsig.get(), cols, Wn.get(),
+                                                          dperm.get());
+  DFCG_LAUNCH_CHECK();
+  scatter_rows_int_kernel<<<grid_for(cols * cols), 256, 0, s>>>(cols, cols, Wn.get(), cols, dcperm.get(), V, ldv);
+  DFCG_LAUNCH_CHECK();
+  DFCG_CUDA(cudaStreamSynchronize(s));  // host vectors (perm, s_host, cperm) used by async copies
 }
 
 }  // namespace dfcg

@@ -1,0 +1,78 @@
+// Kernel accounting (see prof.hpp) and its C ABI (dfcg_prof_*, declared in include/dfcg_host.h).
+#include "prof.hpp"
+
+#include <mutex>
+#include <vector>
+
+#include "../../include/dfcg_host.h"
+
+namespace dfcg {
+namespace prof {
+
+std::atomic<bool> g_enabled{false};
+std::atomic<long long> g_launches{0};
+
+namespace {
+struct Rec {
+  Op op;
+  double flops, bytes;
+  cudaEvent_t e0, e1;
+};
+std::mutex g_mu;
+std::vector<Rec> g_recs;
+}  // namespace
+
+Scope::Scope(Op op, cudaStream_t s, double flops, double bytes)
+    : op_(op), s_(s), flops_(flops), bytes_(bytes) {
+  if (!g_enabled.load(std::memory_order_relaxed)) return;
+  on_ = true;
+  cudaEventCreate(&e0_);
+  cudaEventCreate(&e1_);
+  cudaEventRecord(e0_, s_);
+}
+
+Scope::~Scope() {
+  if (!on_) return;
+  cudaEventRecord(e1_, s_);
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_recs.push_back({op_, flops_, bytes_, e0_, e1_});
+}
+
+}  // namespace prof
+}  // namespace dfcg
+
+using namespace dfcg::prof;
+
+extern "C" {
+
+void dfcg_prof_enable(int on) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (auto& r : g_recs) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  g_recs.clear();
+  g_enabled.store(on != 0);
+}
+
+int64_t dfcg_launch_count(void) { return g_launches.load(); }
+
+int dfcg_prof_collect(int64_t* launches, double* ms, double* flops, double* bytes) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (int i = 0; i < kNumOps; ++i) {
+    launches[i] = 0;
+    ms[i] = flops[i] = bytes[i] = 0.0;
+  }
+  for (auto& r : g_recs) {
+    if (cudaEventSynchronize(r.e1) != cudaSuccess) return -4;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.e0, r.e1);
+    launches[r.op] += 1;
+    ms[r.op] += t;
+    flops[r.op] += r.flops;
+    bytes[r.op] += r.bytes;
+  }
+  return kNumOps;
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// Opt-in kernel accounting: CUDA-event timing per op class on the launching stream, plus the
+// algorithmic FLOPs / bytes of each launch, so bench.py can report achieved GB/s or TFLOP/s of
+// the dominant kernel measured live (roofline). Off by default; when off a scope costs one
+// relaxed atomic load. A global launch counter backs bench.py's gpu_launches claim.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+namespace dfcg {
+namespace prof {
+
+enum Op : int {
+  kGemm = 0,
+  kSddmm,
+  kSpmm,
+  kCholesky,
+  kQrFallback,
+  kJacobi,
+  kElementwise,
+  kReduce,
+  kOther,
+  kNumOps
+};
+
+extern std::atomic<bool> g_enabled;
+extern std::atomic<long long> g_launches;
+
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// RAII scope: records start/stop events on `s` when profiling is enabled.
+class Scope {
+ public:
+  Scope(Op op, cudaStream_t s, double flops, double bytes);
+  ~Scope();
+  Scope(const Scope&) = delete;
+  Scope& operator=(const Scope&) = delete;
+
+ private:
+  bool on_ = false;
+  Op op_;
+  cudaStream_t s_;
+  double flops_, bytes_;
+  cudaEvent_t e0_ = nullptr, e1_ = nullptr;
+};
+
+}  // namespace prof
+}  // namespace dfcg

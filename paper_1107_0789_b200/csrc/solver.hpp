@@ -1,6 +1,7 @@
 // Internal C++ API of the device solvers (below the C ABI in capi.cpp).
 #pragma once
 
+#include <chrono>
 #include <memory>
 #include <mutex>
 #include <optional>
@@ -34,6 +35,7 @@ struct IterTrace {
   i64 rank, k_final;
   int svd_calls;
   double rel, mu, sigma_sum;
+  double ms = 0.0;
 };
 
 // Factored estimate on the device: L = left (m x k) * right (n x k)^T, both ROW-major.
@@ -72,6 +74,31 @@ struct CallStream {
 };
 
 void validate_config(const ApgConfig& cfg);
+
+// Resumable apg_mc (solvers.hpp:241-327): the ctor uploads Omega and computes mu_init,
+// step() runs one APG iteration, finish() reports (and copies out the current estimate).
+// Same arithmetic as running the reference loop to completion.
+class McSolver {
+ public:
+  McSolver(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows, const long long* cols,
+           const double* vals, const ApgConfig& cfg);
+  ~McSolver();
+  bool step(std::vector<IterTrace>* trace = nullptr);
+  void finish(DevLowRank& out, SolveReport& rep);
+  int iterations() const { return iters_; }
+  bool stopped() const { return stopped_ || iters_ >= cfg_.max_iters; }
+
+ private:
+  struct State;
+  DeviceContext& ctx_;
+  cudaStream_t s_;
+  i64 m_, n_, nnz_;
+  ApgConfig cfg_;
+  std::unique_ptr<State> st_;
+  int iters_ = 0;
+  bool stopped_ = false;
+  std::chrono::steady_clock::time_point start_;
+};
 
 // apg_mc on an ObservedMatrix given as CSC-sorted triplets. Result stays on the device.
 void apg_mc_device(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows,

@@ -196,6 +196,8 @@ void DevOmega::build(cudaStream_t s, i64 m_, i64 n_, i64 nnz_, const long long* 
 void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl, i64 ldl, const double* Yr, i64 ldr,
                     const double* sub, double* r_csr) {
   if (om.nnz == 0) return;
+  // algorithmic bytes: row+col index, M_e, r_e per entry + both factors once
+  prof::Scope scope(prof::kSddmm, s, 2.0 * kY * om.nnz, 24.0 * om.nnz + 8.0 * (om.m + om.n) * kY);
   const int G = pow2_at_least((kY + 3) / 4);
   const i64 warps = (om.nnz + (32 / G) - 1) / (32 / G);
   const int blocks = static_cast<int>(std::min<i64>((warps + 7) / 8, 65535L * 4));
@@ -222,6 +224,10 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   const i64 out_rows = transpose ? om.n : om.m;
   if (b <= 0 || out_rows <= 0) return;
   const int* ptr = transpose ? om.csc_colptr.get() : om.csr_rowptr.get();
+  // algorithmic bytes: idx + value (+ permutation) per entry, X read once, out written (read if beta)
+  const i64 in_rows = transpose ? om.m : om.n;
+  prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,
+                    (transpose ? 20.0 : 12.0) * om.nnz + 8.0 * b * (in_rows + out_rows * (beta != 0.0 ? 2 : 1)));
   empty_rows_kernel<<<grid_for(out_rows * b), 256, 0, s>>>(out_rows, ptr, b, beta, out, ldo);
   DFCG_LAUNCH_CHECK();
   if (p.n_items == 0) return;

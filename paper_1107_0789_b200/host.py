@@ -123,3 +123,30 @@ def gen_rmf_instance(m, n, r, s, sigma, seed, stream=0, lo=0.0, hi=1.0):
     vals = np.ctypeslib.as_array(S0.val, shape=(max(cnt, 1),))[:cnt].copy()
     lib().dfcg_sparse_free(C.byref(S0))
     return _lowrank_out(L0), (rows, cols, vals), M
+
+
+# ------------------------------------------------------------------ kernel accounting
+PROF_OPS = ("gemm", "sddmm", "spmm", "cholesky", "qr_fallback", "jacobi", "elementwise", "reduce", "other")
+
+
+def prof_enable(on: bool = True):
+    """Start (and clear) / stop CUDA-event accounting of every library op (bench only)."""
+    lib().dfcg_prof_enable(C.c_int(1 if on else 0))
+
+
+def prof_collect() -> dict:
+    """{op: dict(launches, ms, flops, bytes)} since the last prof_enable(True)."""
+    n = len(PROF_OPS)
+    launches = np.zeros(n, np.int64)
+    ms, fl, by = np.zeros(n), np.zeros(n), np.zeros(n)
+    rc = lib().dfcg_prof_collect(_i(launches), _d(ms), _d(fl), _d(by))
+    if rc < 0:
+        _check(rc)
+    return {op: dict(launches=int(launches[i]), ms=float(ms[i]), flops=float(fl[i]), bytes=float(by[i]))
+            for i, op in enumerate(PROF_OPS)}
+
+
+def launch_count() -> int:
+    """Total kernels launched by libdfcg in this process."""
+    lib().dfcg_launch_count.restype = i64
+    return int(lib().dfcg_launch_count())
