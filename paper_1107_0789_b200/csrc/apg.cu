@@ -12,7 +12,10 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+
+#include <cuda_profiler_api.h>
 
 #include "solver.hpp"
 
@@ -495,6 +498,17 @@ McSolver::~McSolver() = default;
 // One iteration of the apg_mc loop (solvers.hpp:275-317).
 bool McSolver::step(std::vector<IterTrace>* trace) {
   if (stopped_ || iters_ >= cfg_.max_iters) return false;
+  // ncu --profile-from-start off: DFCG_PROFILE_ITER=k brackets iteration k of every solve.
+  static const int profile_iter = std::getenv("DFCG_PROFILE_ITER") ? std::atoi(std::getenv("DFCG_PROFILE_ITER")) : -1;
+  struct ProfRange {
+    bool on;
+    explicit ProfRange(bool o) : on(o) {
+      if (on) cudaProfilerStart();
+    }
+    ~ProfRange() {
+      if (on) cudaProfilerStop();
+    }
+  } prof_range(iters_ + 1 == profile_iter);
   const auto it_start = std::chrono::steady_clock::now();
   State& st = *st_;
   cudaStream_t s = s_;

@@ -10,9 +10,7 @@ namespace dfcg {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
-constexpr int PAD_K = BK + 4;   // [rows][k] layout, k contiguous
-constexpr int PAD_MN = BM + 4;  // [k][rows] layout, rows contiguous
+constexpr int BK = 16, STAGES = 3;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -31,78 +29,77 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// Tile sizes in doubles for one stage.
-template <bool T>  // T == "tile stored [k][rows]" (rows contiguous)
-struct TileShape {
-  static constexpr int elems = T ? BK * PAD_MN : BM * PAD_K;
-};
-
-// Load a 64 (rows) x 16 (k) operand tile into shared memory.
-//   KMajor == false: element (r, k) at g[(r0 + r) * ld + k0 + k]   (k contiguous)
-//   KMajor == true : element (r, k) at g[(k0 + k) * ld + r0 + r]   (rows contiguous)
-template <bool KMajor>
-__device__ __forceinline__ void load_tile(double* sm, const double* g, i64 ld, i64 r0, i64 k0, i64 R, i64 Kend,
-                                          int tid) {
+// Shared-memory operand tile of ROWS (M or N index) x BK (k).
+//   KMajor == false: [rows][k] with k contiguous, row stride BK + 4
+//   KMajor == true : [k][rows] with rows contiguous, k stride ROWS + 4
+// Both paddings make every DMMA fragment load a 2-wavefront (conflict-free) access.
+template <bool KMajor, int ROWS>
+struct Tile {
+  static constexpr int PAD_K = BK + 4, PAD_R = ROWS + 4;
+  static constexpr int elems = KMajor ? BK * PAD_R : ROWS * PAD_K;
+  template <int THREADS>
+  __device__ __forceinline__ static void load(double* sm, const double* g, i64 ld, i64 r0, i64 k0, i64 R, i64 Kend,
+                                              int tid) {
 #pragma unroll
-  for (int it = 0; it < (BM * BK) / THREADS; ++it) {
-    const int e = tid + it * THREADS;
-    if (!KMajor) {
-      const int r = e / BK, k = e % BK;
-      const i64 gr = r0 + r, gk = k0 + k;
-      const bool ok = gr < R && gk < Kend;
-      cp_async8(sm + r * PAD_K + k, ok ? g + gr * ld + gk : g, ok);
-    } else {
-      const int k = e / BM, r = e % BM;
-      const i64 gr = r0 + r, gk = k0 + k;
-      const bool ok = gr < R && gk < Kend;
-      cp_async8(sm + k * PAD_MN + r, ok ? g + gk * ld + gr : g, ok);
+    for (int it = 0; it < (ROWS * BK) / THREADS; ++it) {
+      const int e = tid + it * THREADS;
+      if (!KMajor) {
+        const int r = e / BK, k = e % BK;
+        const i64 gr = r0 + r, gk = k0 + k;
+        const bool ok = gr < R && gk < Kend;
+        cp_async8(sm + r * PAD_K + k, ok ? g + gr * ld + gk : g, ok);
+      } else {
+        const int k = e / ROWS, r = e % ROWS;
+        const i64 gr = r0 + r, gk = k0 + k;
+        const bool ok = gr < R && gk < Kend;
+        cp_async8(sm + k * PAD_R + r, ok ? g + gk * ld + gr : g, ok);
+      }
     }
   }
-}
+  __device__ __forceinline__ static double frag(const double* sm, int r, int k) {
+    return KMajor ? sm[k * PAD_R + r] : sm[r * PAD_K + k];
+  }
+};
 
-template <bool KMajor>
-__device__ __forceinline__ double frag(const double* sm, int r, int k) {
-  return KMajor ? sm[k * PAD_MN + r] : sm[r * PAD_K + k];
-}
-
-// A tile: rows = M index. !TA -> A(i,k) at A[i*lda+k] -> [rows][k] layout (KMajor=false).
-//                          TA -> A(i,k) at A[k*lda+i] -> [k][rows] layout (KMajor=true).
-// B tile: rows = N index. !TB -> B(k,j) at B[k*ldb+j] -> rows (j) contiguous -> KMajor=true.
-//                          TB -> B(k,j) at B[j*ldb+k] -> k contiguous -> KMajor=false.
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(THREADS) gemm_kernel(i64 M, i64 N, i64 K, i64 kchunk, double alpha,
-                                                      const double* __restrict__ A, i64 lda,
-                                                      const double* __restrict__ B, i64 ldb, double beta,
-                                                      double* __restrict__ C, i64 ldc, double* __restrict__ ws) {
+// C tile BM x BN per CTA; warps in a (BM/WM) x (BN/WN) grid, each computing WM x WN with
+// (WM/8) x (WN/8) DMMA 8x8 accumulators.
+// A tile: !TA -> A(i,k) at A[i*lda+k] -> [rows][k]; TA -> A(i,k) at A[k*lda+i] -> [k][rows].
+// B tile: !TB -> B(k,j) at B[k*ldb+j] -> [k][rows]; TB -> B(k,j) at B[j*ldb+k] -> [rows][k].
+template <bool TA, bool TB, int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+    gemm_kernel(i64 M, i64 N, i64 K, i64 kchunk, double alpha, const double* __restrict__ A, i64 lda,
+                const double* __restrict__ B, i64 ldb, double beta, double* __restrict__ C, i64 ldc,
+                double* __restrict__ ws) {
+  constexpr int THREADS = (BM / WM) * (BN / WN) * 32, FM = WM / 8, FN = WN / 8;
+  using TileA = Tile<TA, BM>;
+  using TileB = Tile<!TB, BN>;
   extern __shared__ double smem[];
-  constexpr bool AK = TA, BKm = !TB;
-  constexpr int AE = TileShape<AK>::elems, BE = TileShape<BKm>::elems;
   double* sA = smem;
-  double* sB = smem + STAGES * AE;
+  double* sB = smem + STAGES * TileA::elems;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp / (BN / WN)) * WM, wn = (warp % (BN / WN)) * WN;
   const i64 m0 = static_cast<i64>(blockIdx.y) * BM, n0 = static_cast<i64>(blockIdx.x) * BN;
   const i64 kbeg = static_cast<i64>(blockIdx.z) * kchunk;
   const i64 kend = min(K, kbeg + kchunk);
   const int ntiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
 
-  double acc[4][4][2];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
     if (st < ntiles) {
-      load_tile<AK>(sA + st * AE, A, lda, m0, kbeg + st * BK, M, kend, tid);
-      load_tile<BKm>(sB + st * BE, B, ldb, n0, kbeg + st * BK, N, kend, tid);
+      TileA::template load<THREADS>(sA + st * TileA::elems, A, lda, m0, kbeg + st * BK, M, kend, tid);
+      TileB::template load<THREADS>(sB + st * TileB::elems, B, ldb, n0, kbeg + st * BK, N, kend, tid);
     }
     cp_async_commit();
   }
 
-  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k for A and B (B: col = lane>>2)
+  const int fr = lane >> 2, fk = lane & 3;
   for (int t = 0; t < ntiles; ++t) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -110,24 +107,26 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(i64 M, i64 N, i64 K, i64 
       const int nt = t + STAGES - 1;
       if (nt < ntiles) {
         const int st = nt % STAGES;
-        load_tile<AK>(sA + st * AE, A, lda, m0, kbeg + static_cast<i64>(nt) * BK, M, kend, tid);
-        load_tile<BKm>(sB + st * BE, B, ldb, n0, kbeg + static_cast<i64>(nt) * BK, N, kend, tid);
+        TileA::template load<THREADS>(sA + st * TileA::elems, A, lda, m0, kbeg + static_cast<i64>(nt) * BK, M,
+                                      kend, tid);
+        TileB::template load<THREADS>(sB + st * TileB::elems, B, ldb, n0, kbeg + static_cast<i64>(nt) * BK, N,
+                                      kend, tid);
       }
       cp_async_commit();
     }
-    const double* a = sA + (t % STAGES) * AE;
-    const double* b = sB + (t % STAGES) * BE;
+    const double* a = sA + (t % STAGES) * TileA::elems;
+    const double* b = sB + (t % STAGES) * TileB::elems;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
+      double af[FM], bf[FN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = frag<AK>(a, wm + i * 8 + fr, kk + fk);
+      for (int i = 0; i < FM; ++i) af[i] = TileA::frag(a, wm + i * 8 + fr, kk + fk);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = frag<BKm>(b, wn + j * 8 + fr, kk + fk);
+      for (int j = 0; j < FN; ++j) bf[j] = TileB::frag(b, wn + j * 8 + fr, kk + fk);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
@@ -135,9 +134,9 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(i64 M, i64 N, i64 K, i64 
   // Epilogue: lane holds C(row = lane/4, col = 2*(lane%4) + {0,1}) of each 8x8 tile.
   const int er = lane >> 2, ec = (lane & 3) * 2;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < FM; ++i) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < FN; ++j) {
       const i64 row = m0 + wm + i * 8 + er;
       if (row >= M) continue;
 #pragma unroll
@@ -190,16 +189,16 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <bool TA, bool TB>
-void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
-                 i64 ldb, double beta, double* C, i64 ldc) {
-  const size_t smem =
-      sizeof(double) * STAGES * (TileShape<TA>::elems + TileShape<!TB>::elems);
+template <bool TA, bool TB, int BM, int BN, int WM, int WN>
+void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+                     i64 ldb, double beta, double* C, i64 ldc) {
+  constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
+  const size_t smem = sizeof(double) * STAGES * (Tile<TA, BM>::elems + Tile<!TB, BN>::elems);
   static unsigned configured = 0;  // one bit per device
   int dev = 0;
   DFCG_CUDA(cudaGetDevice(&dev));
   if (!(configured & (1u << dev))) {
-    DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, BM, BN, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
     configured |= 1u << dev;
   }
@@ -215,18 +214,30 @@ void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double
   kchunk = (kchunk + BK - 1) / BK * BK;
   splits = static_cast<int>((K + kchunk - 1) / kchunk);
   if (splits <= 1) {
-    gemm_kernel<TA, TB><<<dim3(gx, gy, 1), THREADS, smem, s>>>(M, N, K, std::max<i64>(K, 1), alpha, A, lda, B, ldb,
-                                                                 beta, C, ldc, nullptr);
+    gemm_kernel<TA, TB, BM, BN, WM, WN><<<dim3(gx, gy, 1), THREADS, smem, s>>>(M, N, K, std::max<i64>(K, 1), alpha, A,
+                                                                               lda, B, ldb, beta, C, ldc, nullptr);
     DFCG_LAUNCH_CHECK();
     return;
   }
   DBuf<double> ws(static_cast<i64>(splits) * M * N, s);
-  gemm_kernel<TA, TB><<<dim3(gx, gy, splits), THREADS, smem, s>>>(M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C,
-                                                                    ldc, ws.get());
+  gemm_kernel<TA, TB, BM, BN, WM, WN><<<dim3(gx, gy, splits), THREADS, smem, s>>>(M, N, K, kchunk, alpha, A, lda, B,
+                                                                                  ldb, beta, C, ldc, ws.get());
   DFCG_LAUNCH_CHECK();
   const int rb = static_cast<int>(std::min<i64>((M * N + 255) / 256, 4L * num_sms()));
   splitk_reduce<<<rb, 256, 0, s>>>(M, N, splits, ws.get(), alpha, beta, C, ldc);
   DFCG_LAUNCH_CHECK();
+}
+
+// Large outputs get 128 x 128 CTA tiles (8 warps of 64 x 32: half the L2 traffic per FLOP);
+// small or skinny ones keep 64 x 64 tiles so enough CTAs exist to fill the 148 SMs.
+template <bool TA, bool TB>
+void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+                 i64 ldb, double beta, double* C, i64 ldc) {
+  const i64 big_tiles = static_cast<i64>(cdiv(M, 128)) * cdiv(N, 128);
+  if (M >= 128 && N >= 128 && big_tiles >= num_sms())
+    launch_gemm_cfg<TA, TB, 128, 128, 64, 32>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else
+    launch_gemm_cfg<TA, TB, 64, 64, 32, 32>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 // ---------------------------------------------------------------- small kernels

@@ -49,63 +49,132 @@ __global__ void diag_max_kernel(i64 n, const double* G, i64 ldg, double* out) {
   if (threadIdx.x == 0) *out = sh[0];
 }
 
-// Factor the kb x kb diagonal block at (k0,k0) in place (upper R), write its inverse into
-// Rinv at (k0,k0). Pivots below rel_tol * maxdiag set *fail and are replaced by 1.
-__global__ void potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr, const double* maxdiag,
-                                  double rel_tol, int* fail) {
-  extern __shared__ double dyn[];
-  double(*a)[CNB + 1] = reinterpret_cast<double(*)[CNB + 1]>(dyn);
-  double(*inv)[CNB + 1] = reinterpret_cast<double(*)[CNB + 1]>(dyn + CNB * (CNB + 1));
-  const int t = threadIdx.x;
-  for (int e = t; e < kb * kb; e += blockDim.x) a[e / kb][e % kb] = G[(e / kb) * ldg + (e % kb)];
-  __syncthreads();
+// Factor the kb x kb (kb <= 64) diagonal block at (k0,k0) in place (upper R, lower part zeroed)
+// and write R^-1 into Rinv. Register-blocked: 256 threads as a 16 x 16 grid, each owning a
+// 4 x 4 tile; each pivot step broadcasts one row (Cholesky) or one row + one column (inverse)
+// through double-buffered shared memory, so every step costs a single barrier.
+// Pivots below rel_tol * maxdiag set *fail (the caller falls back to Householder QR).
+__global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr,
+                                                         const double* maxdiag, double rel_tol, int* fail) {
+  __shared__ double rowb[2][CNB];
+  __shared__ double colb[2][CNB];
+  __shared__ double dinv[CNB];  // 1 / r_kk, reused by the inverse phase
+  const int t = threadIdx.x, ty = t >> 4, tx = t & 15, r0 = 4 * ty, c0 = 4 * tx;
+  double a[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = r0 + i, c = c0 + j;
+      a[i][j] = (r < kb && c < kb) ? G[r * ldg + c] : (r == c ? 1.0 : 0.0);
+    }
   const double thr = rel_tol * (*maxdiag);
-  const int ty = t >> 4, tx = t & 15;  // 16 x 16 thread grid for the trailing update
+  // ---- Cholesky, right-looking: r_kk = sqrt(a_kk), r_kj = a_kj / r_kk, a_ij -= r_ki r_kj
   for (int k = 0; k < kb; ++k) {
-    // every thread derives the pivot itself (a[k][k] is final after the previous sync)
-    double d = a[k][k];
+    const int p = k & 1;
+    if (ty == (k >> 2)) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (r0 + i == k) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) rowb[p][c0 + j] = a[i][j];
+        }
+    }
+    __syncthreads();
+    double d = rowb[p][k];
     const bool bad = !(d > thr) || !isfinite(d);
     if (bad) d = 1.0;
-    const double pv = sqrt(d), ipv = 1.0 / pv;
-    __syncthreads();  // all reads of a[k][k] done before row k is rewritten
+    const double ipv = rsqrt(d), pv = d * ipv;
     if (t == 0) {
       if (bad) atomicExch(fail, 1);
-      a[k][k] = pv;
+      dinv[k] = ipv;
     }
-    for (int j = k + 1 + t; j < kb; j += blockDim.x) a[k][j] *= ipv;
-    __syncthreads();
-    for (int i = k + 1 + ty; i < kb; i += 16) {
-      const double aki = a[k][i];
-      for (int j = i + tx; j < kb; j += 16) a[i][j] -= aki * a[k][j];
+    double rr[4], rc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rr[i] = rowb[p][r0 + i] * ipv;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) rc[j] = rowb[p][c0 + j] * ipv;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (r0 + i > k && c0 + j > k) a[i][j] -= rr[i] * rc[j];
+    if (ty == (k >> 2)) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (r0 + i == k) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int c = c0 + j;
+            if (c > k) a[i][j] = rc[j];
+            else if (c == k) a[i][j] = pv;
+          }
+        }
     }
-    __syncthreads();
   }
-  // zero strictly-lower part, invert the upper triangle column by column
-  for (int e = t; e < kb * kb; e += blockDim.x) {
-    const int i = e / kb, j = e % kb;
-    if (i > j) a[i][j] = 0.0;
-    inv[i][j] = 0.0;
-  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (r0 + i > c0 + j) a[i][j] = 0.0;
+  // ---- inverse X = R^-1 (upper), right-looking from the bottom:
+  //      X[k,:] /= r_kk ; X[i,:] -= r_ik X[k,:] for i < k
+  double x[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[i][j] = (r0 + i == c0 + j) ? 1.0 : 0.0;
   __syncthreads();
-  // inverse of the upper triangle, one row at a time from the bottom; 4 lanes per column
-  // share the inner product (blockDim.x == 256 -> 64 columns x 4 lanes).
-  {
-    const int j = t >> 2, part = t & 3;
-    for (int i = kb - 1; i >= 0; --i) {
-      double acc = 0.0;
-      if (j < kb && j > i)
-        for (int l = i + 1 + part; l <= j; l += 4) acc += a[i][l] * inv[l][j];
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (j < kb && j >= i && part == 0) inv[i][j] = ((i == j ? 1.0 : 0.0) - acc) / a[i][i];
-      __syncthreads();
+  for (int k = kb - 1; k >= 0; --k) {
+    const int p = k & 1;
+    if (ty == (k >> 2)) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (r0 + i == k) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) rowb[p][c0 + j] = x[i][j];
+        }
+    }
+    if (tx == (k >> 2)) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (c0 + j == k) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) colb[p][r0 + i] = a[i][j];
+        }
+    }
+    __syncthreads();
+    const double ip = dinv[k];
+    double xk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xk[j] = rowb[p][c0 + j] * ip;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (r0 + i < k) {
+        const double rik = colb[p][r0 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[i][j] -= rik * xk[j];
+      }
+    }
+    if (ty == (k >> 2)) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (r0 + i == k) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) x[i][j] = xk[j];
+        }
     }
   }
-  for (int e = t; e < kb * kb; e += blockDim.x) {
-    const int i = e / kb, j = e % kb;
-    G[i * ldg + j] = a[i][j];
-    Rinv[i * ldr + j] = inv[i][j];
-  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = r0 + i, c = c0 + j;
+      if (r < kb && c < kb) {
+        G[r * ldg + c] = a[i][j];
+        Rinv[r * ldr + c] = x[i][j];
+      }
+    }
 }
 
 __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
@@ -118,17 +187,7 @@ __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
 }
 
 // In-place blocked Cholesky of G (n x n) -> upper R (lower part zeroed); Rinv = R^-1.
-constexpr size_t kPotrfSmem = sizeof(double) * 2 * CNB * (CNB + 1);
-
 void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol, int* fail) {
-  static unsigned configured = 0;
-  int dev = 0;
-  DFCG_CUDA(cudaGetDevice(&dev));
-  if (!(configured & (1u << dev))) {
-    DFCG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(kPotrfSmem)));
-    configured |= 1u << dev;
-  }
   DBuf<double> maxdiag(1, s);
   diag_max_kernel<<<1, 256, 0, s>>>(n, G, ldg, maxdiag.get());
   DFCG_LAUNCH_CHECK();
@@ -137,7 +196,7 @@ void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i
     const int kb = static_cast<int>(std::min<i64>(CNB, n - k0));
     double* Gkk = G + k0 * ldg + k0;
     prof::Scope scope(prof::kCholesky, s, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
-    potrf_diag_kernel<<<1, 256, kPotrfSmem, s>>>(kb, Gkk, ldg, Rinv + k0 * ldr + k0, ldr, maxdiag.get(), rel_tol,
+    potrf_diag_kernel<<<1, 256, 0, s>>>(kb, Gkk, ldg, Rinv + k0 * ldr + k0, ldr, maxdiag.get(), rel_tol,
                                                  fail);
     DFCG_LAUNCH_CHECK();
     const i64 rem = n - k0 - kb;
@@ -477,8 +536,9 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i6
   constexpr int JW = 2 * NB, T = 256, NT = JW / 8, LD = JW + 1;
   extern __shared__ double dyn[];
   const i64 rows4 = (rows + 3) / 4 * 4;
-  double* Wp = dyn;                  // rows4 x LD
-  double* red = Wp + rows4 * LD;     // 8 warps x JW*JW partial Grams
+  const i64 cap = rows4 > (nv + 3) / 4 * 4 ? rows4 : (nv + 3) / 4 * 4;
+  double* Wp = dyn;                  // cap x LD (W pair, later V pair)
+  double* red = Wp + cap * LD;       // 8 warps x JW*JW partial Grams
   __shared__ double g[JW][JW + 1];
   __shared__ double rot[JW][JW + 1];
   __shared__ double cs[JW / 2][2];
@@ -523,81 +583,84 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i6
   }
   __syncthreads();
 
-  auto off_measure = [&]() {
-    double mx = 0.0;
-    for (int e = t; e < JW * JW; e += T) {
-      const int a = e / JW, b = e % JW;
-      if (a >= b) continue;
-      const double d = sqrt(g[a][a]) * sqrt(g[b][b]);
-      if (d > 0.0) mx = fmax(mx, fabs(g[a][b]) / d);
+  // ---- off-diagonal measure and inner cyclic Jacobi EVD, both by warp 0 alone (the JW x JW
+  // Gram is tiny): __syncwarp instead of CTA barriers on the sequential rotation steps.
+  if (warp == 0) {
+    auto off_measure = [&]() {  // max |g_ab| / sqrt(g_aa g_bb), a < b (warp-uniform result)
+      double mx = 0.0;
+      for (int e = lane; e < JW * JW; e += 32) {
+        const int a = e / JW, b = e % JW;
+        if (a >= b) continue;
+        const double d = sqrt(g[a][a]) * sqrt(g[b][b]);
+        if (d > 0.0) mx = fmax(mx, fabs(g[a][b]) / d);
+      }
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      return mx;
+    };
+    const double off0 = off_measure();
+    if (lane == 0) {
+      atomicMax(offmax, static_cast<unsigned long long>(__double_as_longlong(off0)));
+      s_off = off0;
     }
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    __syncthreads();
-    if (t == 0) s_off = 0.0;
-    __syncthreads();
-    if (lane == 0)
-      atomicMax(reinterpret_cast<unsigned long long*>(&s_off), static_cast<unsigned long long>(__double_as_longlong(mx)));
-    __syncthreads();
-    return s_off;
-  };
-  const double off0 = off_measure();
-  if (t == 0) atomicMax(offmax, static_cast<unsigned long long>(__double_as_longlong(off0)));
-  if (off0 <= tol) return;
-
-  for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
-    if (sweep > 0 && off_measure() <= 0.1 * tol) break;
-    for (int step = 0; step < JW - 1; ++step) {
-      if (t < JW / 2) {
-        int a, b;
-        if (t == 0) {
-          a = 0;
-          b = 1 + (step % (JW - 1));
-        } else {
-          a = 1 + ((step + t) % (JW - 1));
-          b = 1 + ((step + (JW - 1) - t) % (JW - 1));
+    if (off0 > tol) {
+      for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
+        if (sweep > 0 && off_measure() <= 0.1 * tol) break;
+        for (int step = 0; step < JW - 1; ++step) {
+          if (lane < JW / 2) {
+            int a, b;
+            if (lane == 0) {
+              a = 0;
+              b = 1 + (step % (JW - 1));
+            } else {
+              a = 1 + ((step + lane) % (JW - 1));
+              b = 1 + ((step + (JW - 1) - lane) % (JW - 1));
+            }
+            if (a > b) {
+              const int tmp = a;
+              a = b;
+              b = tmp;
+            }
+            pp[lane][0] = a;
+            pp[lane][1] = b;
+            const double gpq = g[a][b], gpp = g[a][a], gqq = g[b][b];
+            double c = 1.0, sn = 0.0;
+            if (fabs(gpq) > 1e-300 && fabs(gpq) > 1e-17 * sqrt(gpp * gqq)) {
+              const double theta = (gqq - gpp) / (2.0 * gpq);
+              const double tt = copysign(1.0, theta) / (fabs(theta) + sqrt(1.0 + theta * theta));
+              c = 1.0 / sqrt(1.0 + tt * tt);
+              sn = tt * c;
+            }
+            cs[lane][0] = c;
+            cs[lane][1] = sn;
+          }
+          __syncwarp();
+          for (int e = lane; e < (JW / 2) * JW; e += 32) {  // columns: g <- g J ; rot <- rot J
+            const int k = e / JW, r = e % JW;
+            const int a = pp[k][0], b = pp[k][1];
+            const double c = cs[k][0], sn = cs[k][1];
+            const double ga = g[r][a], gb = g[r][b];
+            g[r][a] = c * ga - sn * gb;
+            g[r][b] = sn * ga + c * gb;
+            const double ra = rot[r][a], rb = rot[r][b];
+            rot[r][a] = c * ra - sn * rb;
+            rot[r][b] = sn * ra + c * rb;
+          }
+          __syncwarp();
+          for (int e = lane; e < (JW / 2) * JW; e += 32) {  // rows: g <- J^T g
+            const int k = e / JW, r = e % JW;
+            const int a = pp[k][0], b = pp[k][1];
+            const double c = cs[k][0], sn = cs[k][1];
+            const double ga = g[a][r], gb = g[b][r];
+            g[a][r] = c * ga - sn * gb;
+            g[b][r] = sn * ga + c * gb;
+          }
+          __syncwarp();
         }
-        if (a > b) {
-          const int tmp = a;
-          a = b;
-          b = tmp;
-        }
-        pp[t][0] = a;
-        pp[t][1] = b;
-        const double gpq = g[a][b], gpp = g[a][a], gqq = g[b][b];
-        double c = 1.0, sn = 0.0;
-        if (fabs(gpq) > 1e-300 && fabs(gpq) > 1e-17 * sqrt(gpp * gqq)) {
-          const double theta = (gqq - gpp) / (2.0 * gpq);
-          const double tt = copysign(1.0, theta) / (fabs(theta) + sqrt(1.0 + theta * theta));
-          c = 1.0 / sqrt(1.0 + tt * tt);
-          sn = tt * c;
-        }
-        cs[t][0] = c;
-        cs[t][1] = sn;
       }
-      __syncthreads();
-      for (int e = t; e < (JW / 2) * JW; e += T) {
-        const int k = e / JW, r = e % JW;
-        const int a = pp[k][0], b = pp[k][1];
-        const double c = cs[k][0], sn = cs[k][1];
-        const double ga = g[r][a], gb = g[r][b];
-        g[r][a] = c * ga - sn * gb;
-        g[r][b] = sn * ga + c * gb;
-        const double ra = rot[r][a], rb = rot[r][b];
-        rot[r][a] = c * ra - sn * rb;
-        rot[r][b] = sn * ra + c * rb;
-      }
-      __syncthreads();
-      for (int e = t; e < (JW / 2) * JW; e += T) {
-        const int k = e / JW, r = e % JW;
-        const int a = pp[k][0], b = pp[k][1];
-        const double c = cs[k][0], sn = cs[k][1];
-        const double ga = g[a][r], gb = g[b][r];
-        g[a][r] = c * ga - sn * gb;
-        g[b][r] = sn * ga + c * gb;
-      }
-      __syncthreads();
     }
   }
+  __syncthreads();
+  if (s_off <= tol) return;
 
   // W[:, pair] <- Wp rot (from shared memory)
   const i64 rtiles = (rows + 7) / 8;
@@ -621,21 +684,28 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i6
       }
     }
   }
-  // V[:, pair] <- V[:, pair] rot (streamed; each warp reads its whole tile before writing it)
+  // V[:, pair] <- V[:, pair] rot: stage the pair's columns of V in the (now free) Wp buffer
+  // with one coalesced burst, then the same shared-memory tile product as for W.
+  __syncthreads();
+  const i64 nv4 = (nv + 3) / 4 * 4;
+  for (i64 e = t; e < nv4 * JW; e += T) {
+    const i64 r = e / JW;
+    const int c = static_cast<int>(e % JW);
+    Wp[r * LD + c] = r < nv ? V[r * ldv + gcol(c)] : 0.0;
+  }
+  __syncthreads();
   const i64 vtiles = (nv + 7) / 8;
   for (i64 rt = warp; rt < vtiles; rt += T / 32) {
-    const i64 r = rt * 8 + (lane >> 2);
-    double a[JW / 4];
-#pragma unroll
-    for (int kk = 0; kk < JW / 4; ++kk) a[kk] = r < nv ? V[r * ldv + gcol(kk * 4 + (lane & 3))] : 0.0;
     double o[NT][2];
 #pragma unroll
     for (int ct = 0; ct < NT; ++ct) o[ct][0] = o[ct][1] = 0.0;
+    const i64 r = rt * 8 + (lane >> 2);
 #pragma unroll
-    for (int kk = 0; kk < JW / 4; ++kk)
+    for (int k = 0; k < JW; k += 4) {
+      const double a = r < nv4 ? Wp[r * LD + k + (lane & 3)] : 0.0;
 #pragma unroll
-      for (int ct = 0; ct < NT; ++ct) dmma(o[ct], a[kk], rot[kk * 4 + (lane & 3)][ct * 8 + (lane >> 2)]);
-    __syncwarp();
+      for (int ct = 0; ct < NT; ++ct) dmma(o[ct], a, rot[k + (lane & 3)][ct * 8 + (lane >> 2)]);
+    }
     if (r < nv) {
 #pragma unroll
       for (int ct = 0; ct < NT; ++ct) {
@@ -798,8 +868,9 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   DBuf<unsigned long long> off(1, s);
   const double tol = 1e-13;
   const int npairs = p / 2;
-  const bool resident = wrows <= kResidentRows;
-  const size_t smem = sizeof(double) * (((wrows + 3) / 4 * 4) * (JW + 1) + 8 * JW * JW);
+  const i64 cap_rows = std::max((wrows + 3) / 4 * 4, (np + 3) / 4 * 4);
+  const bool resident = cap_rows <= kResidentRows;
+  const size_t smem = sizeof(double) * (cap_rows * (JW + 1) + 8 * JW * JW);
   if (resident) {
     static unsigned configured = 0;
     int dev = 0;
@@ -821,7 +892,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
         const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
         if (resident)
           jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, np, W.get(), np, J.get(), np, pr, tol,
-                                                                     off.get(), 2);
+                                                                     off.get(), 4);
         else
           jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, np, W.get(), np, J.get(), np, pr, tol, off.get(),
                                                               2);
