@@ -102,6 +102,20 @@ def make_blocks(P, wl):
     return L0, obs, groups, blocks
 
 
+def combine(P, dist, groups, ests, wl, device):
+    """DFC-Proj combine of the block estimates; returns (U_b, right) on rank 0 (else None)."""
+    if dist is None:
+        est = P.column_project(ests[0], [ests[g] for g in range(wl["t"])], groups, device=device)
+        return est.left, est.right
+    from paper_1107_0789_b200.distributed import column_project_distributed
+
+    return column_project_distributed(
+        dist, groups, ests, wl["m"],
+        basis_fn=lambda e: P.svd_of_product(e.left, e.right, device=device)[0].left,
+        project_fn=lambda Ub, e: P.project_block(Ub, e, device=device),
+        device=f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu")
+
+
 def roofline_entry(prof, peaks, peak_kind):
     ops = {k: v for k, v in prof.items() if v["launches"] > 0}
     if not ops:
@@ -225,13 +239,19 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DFCG_DIST_BACKEND=gloo exercises the multi-rank code path with several ranks sharing one
+    # GPU (collectives on the CPU, no cross-rank kernel waits); the real runs use NCCL.
+    backend = os.environ.get("DFCG_DIST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_1107_0789_b200 as P
 
     peaks, peak_kind = measured_peaks()
@@ -265,7 +285,8 @@ def main():
         e1.synchronize()
     launches = P.launch_count() - launches0
     ms = e0.elapsed_time(e1)
-    tot = torch.tensor([ms, float(iters)], dtype=torch.float64, device="cuda")
+    cdev = "cuda" if (dist is None or dist.get_backend() == "nccl") else "cpu"
+    tot = torch.tensor([ms, float(iters)], dtype=torch.float64, device=cdev)
     if dist:
         mx = tot.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -285,19 +306,14 @@ def main():
     P.prof_enable(False)
     roof = roofline_entry(prof, peaks, peak_kind)
 
-    # combine on the current block estimates (column_project, P/include/dfc/sketch.hpp:170-199)
+    # combine on the current block estimates (column_project, P/include/dfc/sketch.hpp:170-199):
+    # basis broadcast + per-rank projection + row gather over NCCL when N > 1
     ests = {g: solvers[g].finish()[0] for g in mine}
-    combine_ms = None
-    if dist:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, {g: (e.left, e.right) for g, e in ests.items()})
-        allests = {g: P.Estimate(*lr) for part in gathered for g, lr in part.items()}
-    else:
-        allests = ests
-    if rank == 0:
-        t0 = time.perf_counter()
-        P.column_project(allests[0], [allests[g] for g in range(wl["t"])], groups, device=local)
-        combine_ms = 1e3 * (time.perf_counter() - t0)
+    barrier()
+    t0 = time.perf_counter()
+    combine(P, dist, groups, ests, wl, local)
+    barrier()
+    combine_ms = 1e3 * (time.perf_counter() - t0)
     for sv in solvers.values():
         sv.close()
 
@@ -318,23 +334,17 @@ def main():
             h2d += blocks[g].count * 24
             d2h += (est.left.size + est.right.size) * 8
             rep_iters.append(rep.iterations)
-        local_ests = {g: (est.left, est.right) for g, est, _ in outs}
+        local_ests = {g: est for g, est, _ in outs}
+        final = combine(P, dist, groups, local_ests, wl, local)
+        if final is not None:
+            d2h += (final[0].size + final[1].size) * 8
+        it_t = torch.tensor([float(sum(rep_iters))], dtype=torch.float64, device=cdev)
         if dist:
-            gathered = [None] * world
-            dist.all_gather_object(gathered, local_ests)
-            allf = {g: P.Estimate(*lr) for part in gathered for g, lr in part.items()}
-            it_t = torch.tensor([float(sum(rep_iters))], dtype=torch.float64, device="cuda")
             dist.all_reduce(it_t)
-            tot_iters = it_t.item()
-        else:
-            allf = {g: P.Estimate(*lr) for g, lr in local_ests.items()}
-            tot_iters = float(sum(rep_iters))
-        if rank == 0:
-            final = P.column_project(allf[0], [allf[g] for g in range(wl["t"])], groups, device=local)
-            d2h += (final.left.size + final.right.size) * 8
+        tot_iters = it_t.item()
         barrier()
         wall = time.perf_counter() - t0
-        wt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        wt = torch.tensor([wall], dtype=torch.float64, device=cdev)
         if dist:
             dist.all_reduce(wt, op=dist.ReduceOp.MAX)
         wall = wt.item()

@@ -170,6 +170,12 @@ int dfcg_random_project(dfcg_ctx* ctx, int64_t t, const dfcg_lowrank* blocks, co
  * (caller buffer of size >= min(m, n, k)) when non-null, rank in *rank. */
 int dfcg_svd_of_product(dfcg_ctx* ctx, const dfcg_lowrank* in, dfcg_lowrank* out, double* s_out, int64_t* rank);
 
+/* One block of the DFC-Proj combine, for the multi-GPU split of column_project
+ * (sketch.hpp:194-196): Rg = block.right (Ub^T block.left)^T, Ub m x kb column-major, Rg
+ * (block.n x kb, column-major) written to a caller buffer. */
+int dfcg_project_block(dfcg_ctx* ctx, const double* Ub, int64_t m, int64_t kb, const dfcg_lowrank* block,
+                       double* Rg);
+
 /* ---- whole D-F-C pipeline (replaces dfc_run) --------------------------------------------- */
 int dfcg_dfc_run(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_dfc_cfg* cfg, dfcg_lowrank* out,
                  dfcg_dfc_report* rep);

@@ -28,6 +28,7 @@ from ._lib import (  # noqa: F401
     high_accuracy,
     lib,
     lib_path,
+    project_block,
     random_project,
     svd_of_product,
 )

@@ -398,6 +398,16 @@ def svd_of_product(left: np.ndarray, right: np.ndarray, device: int = 0):
     return _lowrank_out(out), s[: r.value].copy()
 
 
+def project_block(Ub: np.ndarray, block: Estimate, device: int = 0) -> np.ndarray:
+    """One block of column_project (P/include/dfc/sketch.hpp:194-196): right_g (Ub^T left_g)^T."""
+    keep = _Keep()
+    U = keep.f(Ub)
+    b = _lowrank_in(block, keep)
+    out = np.empty((block.right.shape[0], U.shape[1]), np.float64, order="F")
+    _check(lib().dfcg_project_block(context(device), _d(U), i64(U.shape[0]), i64(U.shape[1]), C.byref(b), _d(out)))
+    return out
+
+
 VARIANTS = {"proj": 0, "rp": 1, "nys": 2}
 TASKS = {"mc": 0, "rmf": 1}
 

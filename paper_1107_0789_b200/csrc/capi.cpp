@@ -2,6 +2,7 @@
 // error-code mapping. Everything below this file is C++/CUDA; nothing here computes.
 #include "../../include/dfcg.h"
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -398,6 +399,31 @@ int dfcg_svd_of_product(dfcg_ctx* ctx, const dfcg_lowrank* in, dfcg_lowrank* out
     if (s_out)
       for (size_t i = 0; i < f.s.size(); ++i) s_out[i] = f.s[i];
     if (rank) *rank = f.r;
+  });
+}
+
+int dfcg_project_block(dfcg_ctx* ctx, const double* Ub, int64_t m, int64_t kb, const dfcg_lowrank* block,
+                       double* Rg) {
+  return guard([&] {
+    if (!ctx || !Ub || !block || !Rg) throw std::invalid_argument("dfcg_project_block: null argument");
+    if (block->m != m) throw std::invalid_argument("column_project: row count mismatch");
+    CallStream cs(*ctx->dev);
+    const i64 w = block->n;
+    if (kb == 0) return;
+    if (block->k == 0) {
+      std::fill(Rg, Rg + w * kb, 0.0);
+      return;
+    }
+    DevLowRank B = to_dev(cs.s, block);
+    // Ub col-major m x kb == row-major kb x m -> transpose to row-major m x kb
+    DBuf<double> ut(m * kb, cs.s), U(m * kb, cs.s), proj(kb * B.k, cs.s), R(w * kb, cs.s), Rt(w * kb, cs.s);
+    DFCG_CUDA(cudaMemcpyAsync(ut.get(), Ub, sizeof(double) * m * kb, cudaMemcpyHostToDevice, cs.s));
+    transpose(cs.s, kb, m, ut.get(), m, U.get(), kb);
+    gemm(cs.s, true, false, kb, B.k, m, 1.0, U.get(), kb, B.left.get(), B.k, 0.0, proj.get(), B.k);
+    gemm(cs.s, false, true, w, kb, B.k, 1.0, B.right.get(), B.k, proj.get(), B.k, 0.0, R.get(), kb);
+    transpose(cs.s, w, kb, R.get(), kb, Rt.get(), w);
+    DFCG_CUDA(cudaMemcpyAsync(Rg, Rt.get(), sizeof(double) * w * kb, cudaMemcpyDeviceToHost, cs.s));
+    DFCG_CUDA(cudaStreamSynchronize(cs.s));
   });
 }
 

@@ -109,6 +109,82 @@ __global__ void scatter_dense_kernel(i64 N, const int* __restrict__ row, const i
     D[static_cast<i64>(row[t]) * ldd + col[t]] += alpha * vals[t];
 }
 
+// Shared-memory-chunked SpMM for wide sketches: CTA (chunk c, slab q, row split) stages
+// X[q*H : (q+1)*H, 16c : 16c+16] in shared memory once and streams its structure rows'
+// entries against it (half-warp per output row, lane = column), so each X element is read
+// from L2 once per CTA instead of once per nonzero. Partial sums per slab when ns > 1.
+constexpr int CW = 16, SLAB_THREADS = 512;
+template <bool T>
+__global__ void __launch_bounds__(SLAB_THREADS) spmm_slab_kernel(i64 rows, int ns, int rsplit,
+                                                                 const int* __restrict__ slab,
+                                                                 const int* __restrict__ idx,
+                                                                 const long long* __restrict__ perm,
+                                                                 const double* __restrict__ vals, i64 in_rows, i64 b,
+                                                                 double alpha, const double* __restrict__ X, i64 ldx,
+                                                                 double beta, double* __restrict__ out, i64 ldo,
+                                                                 double* __restrict__ ws) {
+  extern __shared__ double xs[];  // H x CW
+  constexpr int H = DevOmega::kSlabRows, NW = SLAB_THREADS / 32;
+  const int c = blockIdx.x, q = blockIdx.y, split = blockIdx.z;
+  const i64 c0 = static_cast<i64>(c) * CW, s0 = static_cast<i64>(q) * H;
+  const i64 h = min(static_cast<i64>(H), in_rows - s0);
+  const int w = static_cast<int>(min(static_cast<i64>(CW), b - c0));
+  for (i64 e = threadIdx.x; e < h * CW; e += blockDim.x) {
+    const i64 r = e / CW;
+    const int cc = static_cast<int>(e % CW);
+    xs[e] = cc < w ? X[(s0 + r) * ldx + c0 + cc] : 0.0;
+  }
+  __syncthreads();
+  // warp per structure row: the row's entries are fetched 32 at a time (coalesced, one per
+  // lane) and broadcast by shuffles; half-warp hh takes entries j + 16 hh of each batch, lane
+  // column = lane & 15; the two halves are combined at the end (fixed order).
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, col = lane & 15, hh = lane >> 4;
+  const i64 per = (rows + rsplit - 1) / rsplit;
+  const i64 rb = static_cast<i64>(split) * per, re = min(rows, rb + per);
+  for (i64 r = rb + warp; r < re; r += NW) {
+    const int e0 = slab[r * (ns + 1) + q], e1 = slab[r * (ns + 1) + q + 1];
+    double acc = 0.0;
+    for (int base = e0; base < e1; base += 32) {
+      const int e = base + lane;
+      int myidx = static_cast<int>(s0);
+      double myv = 0.0;
+      if (e < e1) {
+        myidx = idx[e];
+        myv = T ? vals[perm[e]] : vals[e];
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int src = j + 16 * hh;
+        const int ii = __shfl_sync(0xffffffffu, myidx, src);
+        const double v = __shfl_sync(0xffffffffu, myv, src);
+        acc = fma(v, xs[static_cast<i64>(ii - s0) * CW + col], acc);
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+    if (hh == 0 && col < w) {
+      if (ns == 1) {
+        double* o = out + r * ldo + c0 + col;
+        *o = beta == 0.0 ? alpha * acc : alpha * acc + beta * *o;
+      } else {
+        ws[(static_cast<i64>(q) * rows + r) * b + c0 + col] = acc;
+      }
+    }
+  }
+}
+
+__global__ void slab_reduce_kernel(i64 rows, int ns, i64 b, const double* __restrict__ ws, double alpha,
+                                   double beta, double* __restrict__ out, i64 ldo) {
+  const i64 total = rows * b;
+  for (i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = t / b, c = t % b;
+    double s = 0.0;
+    for (int q = 0; q < ns; ++q) s += ws[(static_cast<i64>(q) * rows + r) * b + c];
+    double* o = out + r * ldo + c;
+    *o = beta == 0.0 ? alpha * s : alpha * s + beta * *o;
+  }
+}
+
 int grid_for(i64 total, int threads = 256) {
   return static_cast<int>(std::max<i64>(1, std::min<i64>((total + threads - 1) / threads, 4096)));
 }
@@ -190,6 +266,24 @@ void DevOmega::build(cudaStream_t s, i64 m_, i64 n_, i64 nnz_, const long long* 
   upload(s, csc2csr, c2r);
   build_plan(s, plan_csr, m, rowptr);
   build_plan(s, plan_csc, n, colptr);
+  // slab offsets (input index = column for CSR rows, row for CSC columns; both sorted)
+  auto slabs = [&](i64 rows, const std::vector<int>& ptr, const std::vector<int>& idx, i64 in_rows, int& ns,
+                   DBuf<int>& out) {
+    ns = static_cast<int>((in_rows + kSlabRows - 1) / kSlabRows);
+    std::vector<int> h(static_cast<size_t>(rows * (ns + 1)));
+    for (i64 r = 0; r < rows; ++r) {
+      int e = ptr[r];
+      for (int q = 0; q <= ns; ++q) {
+        const long long lim = static_cast<long long>(q) * kSlabRows;
+        while (e < ptr[r + 1] && idx[e] < lim) ++e;
+        h[static_cast<size_t>(r * (ns + 1) + q)] = q == ns ? ptr[r + 1] : e;
+      }
+    }
+    upload(s, out, h);
+    DFCG_CUDA(cudaStreamSynchronize(s));
+  };
+  slabs(m, rowptr, rcol, n, nslab_csr, slab_csr);
+  slabs(n, colptr, crow, m, nslab_csc, slab_csc);
   h_csc2csr = std::move(c2r);
 }
 
@@ -224,6 +318,43 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   const i64 out_rows = transpose ? om.n : om.m;
   if (b <= 0 || out_rows <= 0) return;
   const int* ptr = transpose ? om.csc_colptr.get() : om.csr_rowptr.get();
+  if (b >= 48) {  // wide sketch: shared-memory-chunked path
+    const i64 in_rows = transpose ? om.m : om.n;
+    prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,
+                      (transpose ? 20.0 : 12.0) * om.nnz + 8.0 * b * (in_rows + out_rows * (beta != 0.0 ? 2 : 1)));
+    const int ns = transpose ? om.nslab_csc : om.nslab_csr;
+    const int chunks = cdiv(b, CW);
+    const int rsplit = std::max(1, std::min<int>(static_cast<int>((out_rows + 15) / 16),
+                                                 (148 + chunks * ns - 1) / (chunks * ns)));
+    const size_t smem = sizeof(double) * DevOmega::kSlabRows * CW;
+    static unsigned configured = 0;
+    int dev = 0;
+    DFCG_CUDA(cudaGetDevice(&dev));
+    if (!(configured & (1u << dev))) {
+      DFCG_CUDA(cudaFuncSetAttribute(spmm_slab_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      DFCG_CUDA(cudaFuncSetAttribute(spmm_slab_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      configured |= 1u << dev;
+    }
+    DBuf<double> ws;
+    if (ns > 1) ws.alloc(static_cast<i64>(ns) * out_rows * b, s);
+    const dim3 grid(chunks, ns, rsplit);
+    if (transpose)
+      spmm_slab_kernel<true><<<grid, SLAB_THREADS, smem, s>>>(out_rows, ns, rsplit, om.slab_csc.get(), om.csc_row.get(),
+                                                     om.csc2csr.get(), vals_csr, in_rows, b, alpha, X, ldx, beta, out,
+                                                     ldo, ws.get());
+    else
+      spmm_slab_kernel<false><<<grid, SLAB_THREADS, smem, s>>>(out_rows, ns, rsplit, om.slab_csr.get(), om.csr_col.get(),
+                                                      om.csc2csr.get(), vals_csr, in_rows, b, alpha, X, ldx, beta,
+                                                      out, ldo, ws.get());
+    DFCG_LAUNCH_CHECK();
+    if (ns > 1) {
+      slab_reduce_kernel<<<grid_for(out_rows * b), 256, 0, s>>>(out_rows, ns, b, ws.get(), alpha, beta, out, ldo);
+      DFCG_LAUNCH_CHECK();
+    }
+    return;
+  }
   // algorithmic bytes: idx + value (+ permutation) per entry, X read once, out written (read if beta)
   const i64 in_rows = transpose ? om.m : om.n;
   prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,
