@@ -689,15 +689,17 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
       DFCG_LAUNCH_CHECK();
     }
     for (;;) {
-      prof::Scope scope(prof::kElementwise, s, 10.0 * mn, (cfg.line_search ? 5.0 : 7.0) * 8.0 * mn);
-      if (cfg.line_search) {
-        rmf_step_kernel<<<gb, 256, 0, s>>>(mn, step, step * lambda * mu, YL.get(), YS.get(), Gd.get(), GL.get(),
-                                           Sn.get());
-      } else {
-        rmf_fused_kernel<<<gb, 256, 0, s>>>(mn, beta, step, step * lambda * mu, Ld.get(), Ldp.get(), Sc.get(),
-                                            Sp.get(), M.get(), GL.get(), Sn.get());
+      {
+        prof::Scope scope(prof::kElementwise, s, 10.0 * mn, (cfg.line_search ? 5.0 : 7.0) * 8.0 * mn);
+        if (cfg.line_search) {
+          rmf_step_kernel<<<gb, 256, 0, s>>>(mn, step, step * lambda * mu, YL.get(), YS.get(), Gd.get(), GL.get(),
+                                             Sn.get());
+        } else {
+          rmf_fused_kernel<<<gb, 256, 0, s>>>(mn, beta, step, step * lambda * mu, Ld.get(), Ldp.get(), Sc.get(),
+                                              Sp.get(), M.get(), GL.get(), Sn.get());
+        }
+        DFCG_LAUNCH_CHECK();
       }
-      DFCG_LAUNCH_CHECK();
       OpDense op{GL.get(), m, n};
       f = SvtResult{};
       svt_operator(s, op, step * mu, rank_hint, cur, f);

@@ -98,6 +98,10 @@ class DBuf {
 void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc);
 
+// Upper triangle (tiles on or above the diagonal) of G = X^T X, X rows x cols row-major; the
+// strictly-lower tiles of G are not written (SYRK: half the Gram FLOPs).
+void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* G, i64 ldg);
+
 // dst (rows x cols, ldd) = alpha * src (rows x cols, lds)  [alpha may be 1]
 void copy2d(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd, double alpha = 1.0);
 // dst (cols x rows, ldd) = src^T  (src rows x cols, lds)

@@ -69,7 +69,7 @@ template <bool TA, bool TB, int BM, int BN, int WM, int WN>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     gemm_kernel(i64 M, i64 N, i64 K, i64 kchunk, double alpha, const double* __restrict__ A, i64 lda,
                 const double* __restrict__ B, i64 ldb, double beta, double* __restrict__ C, i64 ldc,
-                double* __restrict__ ws) {
+                double* __restrict__ ws, int upper_only) {
   constexpr int THREADS = (BM / WM) * (BN / WN) * 32, FM = WM / 8, FN = WN / 8;
   using TileA = Tile<TA, BM>;
   using TileB = Tile<!TB, BN>;
@@ -80,6 +80,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp / (BN / WN)) * WM, wn = (warp % (BN / WN)) * WN;
   const i64 m0 = static_cast<i64>(blockIdx.y) * BM, n0 = static_cast<i64>(blockIdx.x) * BN;
+  // SYRK-style: tiles strictly below the diagonal are skipped (their C entries are left as is)
+  if (upper_only && m0 >= n0 + BN) return;
   const i64 kbeg = static_cast<i64>(blockIdx.z) * kchunk;
   const i64 kend = min(K, kbeg + kchunk);
   const int ntiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
@@ -191,7 +193,7 @@ int num_sms() {
 
 template <bool TA, bool TB, int BM, int BN, int WM, int WN>
 void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
-                     i64 ldb, double beta, double* C, i64 ldc) {
+                     i64 ldb, double beta, double* C, i64 ldc, int upper_only) {
   constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
   const size_t smem = sizeof(double) * STAGES * (Tile<TA, BM>::elems + Tile<!TB, BN>::elems);
   static unsigned configured = 0;  // one bit per device
@@ -203,7 +205,7 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
     configured |= 1u << dev;
   }
   const int gx = cdiv(N, BN), gy = cdiv(M, BM);
-  const i64 tiles = static_cast<i64>(gx) * gy;
+  const i64 tiles = upper_only ? static_cast<i64>(gx) * (gx + 1) / 2 : static_cast<i64>(gx) * gy;
   const int target = 2 * num_sms();
   int splits = 1;
   if (tiles < target && K > 4 * BK) {
@@ -215,13 +217,16 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
   splits = static_cast<int>((K + kchunk - 1) / kchunk);
   if (splits <= 1) {
     gemm_kernel<TA, TB, BM, BN, WM, WN><<<dim3(gx, gy, 1), THREADS, smem, s>>>(M, N, K, std::max<i64>(K, 1), alpha, A,
-                                                                               lda, B, ldb, beta, C, ldc, nullptr);
+                                                                               lda, B, ldb, beta, C, ldc, nullptr,
+                                                                               upper_only);
     DFCG_LAUNCH_CHECK();
     return;
   }
   DBuf<double> ws(static_cast<i64>(splits) * M * N, s);
+  if (upper_only) ws.zero(s);  // skipped tiles leave their partials unwritten
   gemm_kernel<TA, TB, BM, BN, WM, WN><<<dim3(gx, gy, splits), THREADS, smem, s>>>(M, N, K, kchunk, alpha, A, lda, B,
-                                                                                  ldb, beta, C, ldc, ws.get());
+                                                                                  ldb, beta, C, ldc, ws.get(),
+                                                                                  upper_only);
   DFCG_LAUNCH_CHECK();
   const int rb = static_cast<int>(std::min<i64>((M * N + 255) / 256, 4L * num_sms()));
   splitk_reduce<<<rb, 256, 0, s>>>(M, N, splits, ws.get(), alpha, beta, C, ldc);
@@ -232,12 +237,14 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
 // small or skinny ones keep 64 x 64 tiles so enough CTAs exist to fill the 148 SMs.
 template <bool TA, bool TB>
 void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
-                 i64 ldb, double beta, double* C, i64 ldc) {
+                 i64 ldb, double beta, double* C, i64 ldc, int upper_only) {
   const i64 big_tiles = static_cast<i64>(cdiv(M, 128)) * cdiv(N, 128);
-  if (M >= 128 && N >= 128 && big_tiles >= num_sms())
-    launch_gemm_cfg<TA, TB, 128, 128, 64, 32>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  // 128x128 tiles when the output alone fills the GPU, or when a long K lets split-K fill it
+  const bool big = M >= 128 && N >= 128 && (big_tiles >= num_sms() || (M >= 256 && N >= 256 && K >= 2048));
+  if (big)
+    launch_gemm_cfg<TA, TB, 128, 128, 64, 32>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, upper_only);
   else
-    launch_gemm_cfg<TA, TB, 64, 64, 32, 32>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    launch_gemm_cfg<TA, TB, 64, 64, 32, 32>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, upper_only);
 }
 
 // ---------------------------------------------------------------- small kernels
@@ -361,10 +368,16 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
     DFCG_LAUNCH_CHECK();
     return;
   }
-  if (!ta && !tb) launch_gemm<false, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else if (ta && !tb) launch_gemm<true, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else if (!ta && tb) launch_gemm<false, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else launch_gemm<true, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (!ta && !tb) launch_gemm<false, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+  else if (ta && !tb) launch_gemm<true, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+  else if (!ta && tb) launch_gemm<false, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+  else launch_gemm<true, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+}
+
+void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* G, i64 ldg) {
+  if (rows <= 0 || cols <= 0) return;
+  prof::Scope scope(prof::kGemm, s, 1.0 * cols * (cols + 1) * rows, 8.0 * (rows * cols + cols * cols));
+  launch_gemm<true, false>(s, cols, cols, rows, 1.0, X, ldx, X, ldx, 0.0, G, ldg, 1);
 }
 
 void copy2d(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd, double alpha) {

@@ -33,6 +33,11 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(pred ? 8 : 0));
+}
+
 // ================================================================ Cholesky (upper, G = R^T R)
 constexpr int CNB = 64;
 
@@ -530,13 +535,16 @@ constexpr int kResidentRows = 1408;
 template <int NB>
 __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i64 nv, double* W, i64 ldw, double* V,
                                                                     i64 ldv, const int* pairs, double tol,
-                                                                    unsigned long long* offmax, int inner_sweeps) {
+                                                                    unsigned long long* offmax, int inner_sweeps,
+                                                                    int prefetch_v) {
   constexpr int JW = 2 * NB, T = 256, NT = JW / 8, LD = JW + 1;
   extern __shared__ double dyn[];
   const i64 rows4 = (rows + 3) / 4 * 4;
-  const i64 cap = rows4 > (nv + 3) / 4 * 4 ? rows4 : (nv + 3) / 4 * 4;
-  double* Wp = dyn;                  // cap x LD (W pair, later V pair)
-  double* red = Wp + cap * LD;       // 8 warps x JW*JW partial Grams
+  const i64 nv4 = (nv + 3) / 4 * 4;
+  const i64 cap = rows4 > nv4 ? rows4 : nv4;
+  double* Wp = dyn;                                 // cap x LD (W pair; V pair too unless prefetched)
+  double* Vp = prefetch_v ? Wp + cap * LD : Wp;     // V pair staged at kernel start when it fits
+  double* red = Wp + (prefetch_v ? 2 : 1) * cap * LD;  // 8 warps x JW*JW partial Grams
   __shared__ double g[JW][JW + 1];
   __shared__ double rot[JW][JW + 1];
   __shared__ double cs[JW / 2][2];
@@ -546,10 +554,24 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i6
   const int bi = pairs[2 * blockIdx.x], bj = pairs[2 * blockIdx.x + 1];
   auto gcol = [&](int c) -> i64 { return c < NB ? static_cast<i64>(bi) * NB + c : static_cast<i64>(bj) * NB + c - NB; };
 
+  // stage the pair's columns with cp.async: every load in flight at once (a plain load->store
+  // loop serialises on global latency — ncu showed it as the round's dominant stall)
   for (i64 e = t; e < rows4 * JW; e += T) {
     const i64 r = e / JW;
     const int c = static_cast<int>(e % JW);
-    Wp[r * LD + c] = r < rows ? W[r * ldw + gcol(c)] : 0.0;
+    cp_async8(Wp + r * LD + c, r < rows ? W + r * ldw + gcol(c) : W, r < rows);
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (prefetch_v) {  // second group: the V pair, consumed only after the rotation is known
+    for (i64 e = t; e < nv4 * JW; e += T) {
+      const i64 r = e / JW;
+      const int c = static_cast<int>(e % JW);
+      cp_async8(Vp + r * LD + c, r < nv ? V + r * ldv + gcol(c) : V, r < nv);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+  } else {
+    asm volatile("cp.async.wait_group 0;\n" ::);
   }
   __syncthreads();
   {
@@ -681,15 +703,18 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i6
       }
     }
   }
-  // V[:, pair] <- V[:, pair] rot: stage the pair's columns of V in the (now free) Wp buffer
-  // with one coalesced burst, then the same shared-memory tile product as for W.
+  // V[:, pair] <- V[:, pair] rot: the V pair is either already prefetched into Vp or staged
+  // now in the (free) Wp buffer, then the same shared-memory tile product as for W.
   __syncthreads();
-  const i64 nv4 = (nv + 3) / 4 * 4;
-  for (i64 e = t; e < nv4 * JW; e += T) {
-    const i64 r = e / JW;
-    const int c = static_cast<int>(e % JW);
-    Wp[r * LD + c] = r < nv ? V[r * ldv + gcol(c)] : 0.0;
+  if (!prefetch_v) {
+    for (i64 e = t; e < nv4 * JW; e += T) {
+      const i64 r = e / JW;
+      const int c = static_cast<int>(e % JW);
+      cp_async8(Vp + r * LD + c, r < nv ? V + r * ldv + gcol(c) : V, r < nv);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
   }
+  asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
   const i64 vtiles = (nv + 7) / 8;
   for (i64 rt = warp; rt < vtiles; rt += T / 32) {
@@ -699,7 +724,7 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i6
     const i64 r = rt * 8 + (lane >> 2);
 #pragma unroll
     for (int k = 0; k < JW; k += 4) {
-      const double a = r < nv4 ? Wp[r * LD + k + (lane & 3)] : 0.0;
+      const double a = r < nv4 ? Vp[r * LD + k + (lane & 3)] : 0.0;
 #pragma unroll
       for (int ct = 0; ct < NT; ++ct) dmma(o[ct], a, rot[k + (lane & 3)][ct * 8 + (lane >> 2)]);
     }
@@ -799,8 +824,8 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
   fail.zero(s);
   DBuf<double> G(cols * cols, s), Rinv(cols * cols, s), Q1(rows * cols, s), Q2, R1;
   const double rel_tol = 1e-11;
-  // pass 1
-  gemm(s, true, false, cols, cols, rows, 1.0, X, ldx, X, ldx, 0.0, G.get(), cols);
+  // pass 1 (the Cholesky reads only the upper triangle of the Gram)
+  gram_upper(s, rows, cols, X, ldx, G.get(), cols);
   cholesky_inverse(s, cols, G.get(), cols, Rinv.get(), cols, rel_tol, fail.get());
   gemm(s, false, false, rows, cols, cols, 1.0, X, ldx, Rinv.get(), cols, 0.0, Q1.get(), cols);
   if (R) {
@@ -810,7 +835,7 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
   const double* Qfinal = Q1.get();
   if (passes >= 2) {
     Q2.alloc(rows * cols, s);
-    gemm(s, true, false, cols, cols, rows, 1.0, Q1.get(), cols, Q1.get(), cols, 0.0, G.get(), cols);
+    gram_upper(s, rows, cols, Q1.get(), cols, G.get(), cols);
     cholesky_inverse(s, cols, G.get(), cols, Rinv.get(), cols, rel_tol, fail.get());
     gemm(s, false, false, rows, cols, cols, 1.0, Q1.get(), cols, Rinv.get(), cols, 0.0, Q2.get(), cols);
     Qfinal = Q2.get();
@@ -869,7 +894,8 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   const int npairs = p / 2;
   const i64 cap_rows = std::max((wrows + 3) / 4 * 4, (np + 3) / 4 * 4);
   const bool resident = cap_rows <= kResidentRows;
-  const size_t smem = sizeof(double) * (cap_rows * (JW + 1) + 8 * JW * JW);
+  const int prefetch_v = 2 * cap_rows <= kResidentRows ? 1 : 0;  // W and V pairs both fit
+  const size_t smem = sizeof(double) * ((prefetch_v ? 2 : 1) * cap_rows * (JW + 1) + 8 * JW * JW);
   if (resident) {
     static unsigned configured = 0;
     int dev = 0;
@@ -891,7 +917,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
         const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
         if (resident)
           jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, np, W.get(), np, J.get(), np, pr, tol,
-                                                                     off.get(), 1);
+                                                                     off.get(), 1, prefetch_v);
         else
           jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, np, W.get(), np, J.get(), np, pr, tol, off.get(),
                                                               2);

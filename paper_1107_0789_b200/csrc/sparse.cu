@@ -13,6 +13,9 @@ namespace dfcg {
 namespace {
 
 constexpr int SEG = 64;
+// The chunked path re-walks every nonzero once per 16-column chunk; measured 2x slower than
+// the segmented kernel at b ~ 700 (ncu: instruction-bound), so it is disabled for now.
+constexpr i64 kSlabMinB = i64{1} << 40;
 
 int pow2_at_least(i64 v) {
   int g = 1;
@@ -54,17 +57,38 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
   const i64 gid = ((static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * PER_WARP + lane / G;
   if (gid >= n_items) return;
   const SegItem it = items[gid];
-  for (i64 c0 = 0; c0 < b; c0 += 4 * G) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (long long e = it.e0; e < it.e1; ++e) {
+  constexpr int CPL = 8;  // columns per lane per pass: one walk of the segment covers 8 G columns
+  for (i64 c0 = 0; c0 < b; c0 += CPL * G) {
+    double acc[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) acc[q] = 0.0;
+    // entries in batches of 4: all index/value loads issued before the dependent X gathers
+    long long e = it.e0;
+    for (; e + 4 <= it.e1; e += 4) {
+      int ix[4];
+      double vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ix[u] = idx[e + u];
+        vv[u] = T ? vals[perm[e + u]] : vals[e + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* x = X + static_cast<i64>(ix[u]) * ldx + c0 + lig;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          if (c0 + lig + q * G < b) acc[q] = fma(vv[u], x[q * G], acc[q]);
+      }
+    }
+    for (; e < it.e1; ++e) {
       const double v = T ? vals[perm[e]] : vals[e];
       const double* x = X + static_cast<i64>(idx[e]) * ldx + c0 + lig;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < CPL; ++q)
         if (c0 + lig + q * G < b) acc[q] = fma(v, x[q * G], acc[q]);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < CPL; ++q) {
       const i64 c = c0 + lig + q * G;
       if (c >= b) continue;
       if (it.slot < 0) {
@@ -318,7 +342,7 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   const i64 out_rows = transpose ? om.n : om.m;
   if (b <= 0 || out_rows <= 0) return;
   const int* ptr = transpose ? om.csc_colptr.get() : om.csr_rowptr.get();
-  if (b >= 48) {  // wide sketch: shared-memory-chunked path
+  if (b >= kSlabMinB) {  // wide sketch: shared-memory-chunked path (off: slower than the segmented kernel)
     const i64 in_rows = transpose ? om.m : om.n;
     prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,
                       (transpose ? 20.0 : 12.0) * om.nnz + 8.0 * b * (in_rows + out_rows * (beta != 0.0 ? 2 : 1)));
