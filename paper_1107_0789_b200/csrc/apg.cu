@@ -38,6 +38,28 @@ __global__ void scale_cols_kernel(i64 rows, i64 cols, const double* __restrict__
   }
 }
 
+// r = a pc + b pp - m (a term is skipped, not multiplied, when its coefficient is 0: the
+// buffer may hold stale values then)
+__global__ void residual_combine_kernel(i64 n, double a, const double* __restrict__ pc, double b,
+                                        const double* __restrict__ pp, const double* __restrict__ mv,
+                                        double* __restrict__ r) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    double v = 0.0;
+    if (a != 0.0) v = a * pc[i];
+    if (b != 0.0) v = fma(b, pp[i], v);
+    r[i] = v - mv[i];
+  }
+}
+
+void residual_combine(cudaStream_t s, i64 n, double a, const double* pc, double b, const double* pp,
+                      const double* mv, double* r) {
+  if (n <= 0) return;
+  prof::Scope scope(prof::kElementwise, s, 3.0 * n, 8.0 * n * ((a != 0.0) + (b != 0.0) + 2.0));
+  residual_combine_kernel<<<grid_for(n), 256, 0, s>>>(n, a, pc, b, pp, mv, r);
+  DFCG_LAUNCH_CHECK();
+}
+
 __global__ void fill_kernel(i64 n, double v, double* x) {
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x)
@@ -184,6 +206,7 @@ struct OpMC {
   i64 m, w, kY;
   const double* left;   // m x kY row-major (ld kY)
   const double* right;  // w x kY row-major
+  i64 kc;               // the first kc columns of `left` are L_curr's left factor
   i64 rows() const { return m; }
   i64 cols() const { return w; }
   void apply(cudaStream_t s, const double* X, i64 b, double* out) const {  // X w x b -> out m x b
@@ -196,16 +219,19 @@ struct OpMC {
       spmm(s, *om, false, r_csr, b, coeff, X, b, 0.0, out, b);
     }
   }
-  void apply_adjoint(cudaStream_t s, const double* X, i64 b, double* out) const {  // X m x b -> out w x b
+  // keep (optional): receives T = left^T X (kY x b), whose first kc rows are L_curr.left^T X.
+  void apply_adjoint(cudaStream_t s, const double* X, i64 b, double* out, DBuf<double>* keep = nullptr) const {
     if (kY > 0) {
       DBuf<double> T(kY * b, s);
       gemm(s, true, false, kY, b, m, 1.0, left, kY, X, b, 0.0, T.get(), b);
       gemm(s, false, false, w, b, kY, 1.0, right, kY, T.get(), b, 0.0, out, b);
       spmm(s, *om, true, r_csr, b, coeff, X, b, 1.0, out, b);
+      if (keep) *keep = std::move(T);
     } else {
       spmm(s, *om, true, r_csr, b, coeff, X, b, 0.0, out, b);
     }
   }
+  i64 keep_rows() const { return kc; }
   void to_dense(cudaStream_t s, double* D) const {  // m x w row-major
     if (kY > 0) gemm(s, false, true, m, w, kY, 1.0, left, kY, right, kY, 0.0, D, w);
     else DFCG_CUDA(cudaMemsetAsync(D, 0, sizeof(double) * m * w, s));
@@ -222,9 +248,10 @@ struct OpDense {
   void apply(cudaStream_t s, const double* X, i64 b, double* out) const {
     gemm(s, true, false, m, b, w, 1.0, At, m, X, b, 0.0, out, b);
   }
-  void apply_adjoint(cudaStream_t s, const double* X, i64 b, double* out) const {
+  void apply_adjoint(cudaStream_t s, const double* X, i64 b, double* out, DBuf<double>* = nullptr) const {
     gemm(s, false, false, w, b, m, 1.0, At, m, X, b, 0.0, out, b);
   }
+  i64 keep_rows() const { return -1; }  // no factor Grams for a dense operator
   void to_dense(cudaStream_t s, double* D) const { transpose(s, w, m, At, m, D, w); }
 };
 
@@ -235,6 +262,11 @@ struct SvtResult {
   std::vector<double> s;
   i64 k_final = 0;
   int calls = 0;
+  // Left-factor Grams from the randomized path (left = Q Vz with Q^T Q = I): ll = left^T left
+  // = Vz^T Vz (r x r) and lc = Lc.left^T left (kc x r) read off the last adjoint product, so
+  // the factored inner products of the stop test need no m-side GEMM.
+  bool grams = false;
+  DBuf<double> ll, lc;
 };
 
 // shrink_factors (solvers.hpp:83-88) applied to device factors U (m x ncand, ldu) and
@@ -266,12 +298,12 @@ void svt_dense(cudaStream_t s, const Op& op, double tau, SvtResult& res) {
   std::vector<double> sv;
   if (m >= w) {
     DBuf<double> U(m * w, s), V(w * w, s);
-    thin_svd(s, m, w, D.get(), w, U.get(), w, V.get(), w, sv);
+    thin_svd(s, m, w, D.get(), w, U.get(), w, V.get(), w, sv, tau);
     shrink_into(s, m, w, U.get(), w, V.get(), w, sv, tau, res);
   } else {
     DBuf<double> Dt(w * m, s), U(w * m, s), V(m * m, s);
     transpose(s, m, w, D.get(), w, Dt.get(), m);
-    thin_svd(s, w, m, Dt.get(), m, U.get(), m, V.get(), m, sv);  // D^T = U S V^T -> D = V S U^T
+    thin_svd(s, w, m, Dt.get(), m, U.get(), m, V.get(), m, sv, tau);  // D^T = U S V^T -> D = V S U^T
     shrink_into(s, m, w, V.get(), m, U.get(), m, sv, tau, res);
   }
 }
@@ -303,10 +335,11 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
     op.apply(s, Z.get(), b, X.get());
     thin_qr(s, m, b, X.get(), b, nullptr, 0, it + 1 < q ? 1 : 2);
   }
-  op.apply_adjoint(s, X.get(), b, Z.get());  // Z = A^T Q  (w x b)
+  DBuf<double> T;
+  op.apply_adjoint(s, X.get(), b, Z.get(), &T);  // Z = A^T Q  (w x b)
   DBuf<double> Uz(w * b, s), Vz(b * b, s);
   std::vector<double> sv;
-  thin_svd(s, w, b, Z.get(), b, Uz.get(), b, Vz.get(), b, sv);
+  thin_svd(s, w, b, Z.get(), b, Uz.get(), b, Vz.get(), b, sv, tau);
   const i64 kk = std::min<i64>(k, static_cast<i64>(sv.size()));
   sv.resize(static_cast<size_t>(kk));
   if (!(kk < k || sv[static_cast<size_t>(kk - 1)] <= tau)) return false;
@@ -320,6 +353,16 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
   res.left.alloc(m * r, s);
   res.right.alloc(w * r, s);
   gemm(s, false, false, m, r, b, 1.0, X.get(), b, Vz.get(), b, 0.0, res.left.get(), r);
+  const i64 kc = op.keep_rows();
+  if (kc >= 0 && T.size() >= kc * b) {  // left = Q Vz_r: left^T left = Vz_r^T Vz_r, Lc.left^T left = T[:kc] Vz_r
+    res.grams = true;
+    res.ll.alloc(r * r, s);
+    gemm(s, true, false, r, r, b, 1.0, Vz.get(), b, Vz.get(), b, 0.0, res.ll.get(), r);
+    if (kc > 0) {
+      res.lc.alloc(kc * r, s);
+      gemm(s, false, false, kc, r, b, 1.0, T.get(), b, Vz.get(), b, 0.0, res.lc.get(), r);
+    }
+  }
   DBuf<double> sc(r, s);
   DFCG_CUDA(cudaMemcpyAsync(sc.get(), res.s.data(), sizeof(double) * r, cudaMemcpyHostToDevice, s));
   scale_cols_kernel<<<grid_for(w * r), 256, 0, s>>>(w, r, Uz.get(), b, sc.get(), res.right.get(), r);
@@ -468,6 +511,10 @@ struct McSolver::State {
   DevOmega om;
   NormalCursor cur;
   DBuf<double> r_csr;
+  // P_Omega of the current / previous iterate (CSR order): by linearity P_Omega(Y) =
+  // (1+beta) P_Omega(L_curr) - beta P_Omega(L_prev), so each iteration runs one SDDMM at rank
+  // r (the new iterate) instead of one at the concatenated rank of Y.
+  DBuf<double> pc, pp;
   DevLowRank Lp, Lc;
   double icc = 0.0;  // factored_inner(L_curr, L_curr)
   std::vector<double> last_s;
@@ -488,6 +535,8 @@ McSolver::McSolver(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, co
   if (st.mu_floor > st.mu_init) throw std::invalid_argument("apg_mc: mu_floor exceeds mu_init");
   st.cur = NormalCursor{&ctx.normals(0), 0};
   st.r_csr.alloc(nnz, s);
+  st.pc.alloc(nnz, s);
+  st.pp.alloc(nnz, s);
   st.Lp.m = st.Lc.m = m;
   st.Lp.n = st.Lc.n = n;
   st.mu = st.mu_used = st.mu_init;
@@ -533,13 +582,14 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
       copy2d(s, n, Lp.k, Lp.right.get(), Lp.k, Yr.get() + Lc.k, kY, -beta);
     }
   }
-  // R = P_Omega(Y) - P_Omega(M)
-  sddmm_residual(s, st.om, kY, Yl.get(), kY, Yr.get(), kY, st.om.m_csr.get(), st.r_csr.get());
+  // R = P_Omega(Y) - P_Omega(M) = (1+beta) P_Omega(L_curr) - beta P_Omega(L_prev) - P_Omega(M)
+  residual_combine(s, nnz, Lc.k > 0 ? 1.0 + beta : 0.0, st.pc.get(), concat ? -beta : 0.0, st.pp.get(),
+                   st.om.m_csr.get(), st.r_csr.get());
 
   double step = 1.0;
   SvtResult f;
   for (;;) {
-    OpMC G{&st.om, st.r_csr.get(), -step, m, n, kY, Yl.get(), Yr.get()};
+    OpMC G{&st.om, st.r_csr.get(), -step, m, n, kY, Yl.get(), Yr.get(), Lc.k};
     f = SvtResult{};
     svt_operator(s, G, step * st.mu, st.rank_hint, st.cur, f);
     if (!cfg_.line_search || step <= 0.125) break;
@@ -558,8 +608,24 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
     step *= 0.5;
   }
   // rel = ||L_next - L_curr|| / max(1, ||L_curr||) via factored inner products (:305-306)
-  const double inn = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get());
-  const double inc = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), Lc.k, Lc.left.get(), Lc.right.get());
+  double inn, inc;
+  if (f.grams && f.r > 0) {  // m-side Grams come with the SVT result; only the n-side GEMMs remain
+    DBuf<double> rr(f.r * f.r, s);
+    gemm(s, true, false, f.r, f.r, n, 1.0, f.right.get(), f.r, f.right.get(), f.r, 0.0, rr.get(), f.r);
+    inn = dev_dot(s, f.r * f.r, f.ll.get(), rr.get());
+    inc = 0.0;
+    if (Lc.k > 0) {
+      DBuf<double> rc(Lc.k * f.r, s);
+      gemm(s, true, false, Lc.k, f.r, n, 1.0, Lc.right.get(), Lc.k, f.right.get(), f.r, 0.0, rc.get(), f.r);
+      inc = dev_dot(s, Lc.k * f.r, f.lc.get(), rc.get());
+    }
+  } else {
+    inn = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get());
+    inc = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), Lc.k, Lc.left.get(), Lc.right.get());
+  }
+  // P_Omega(L_next) for the next residual (pp <- pc <- new)
+  std::swap(st.pc, st.pp);
+  if (f.r > 0) sddmm_residual(s, st.om, f.r, f.left.get(), f.r, f.right.get(), f.r, nullptr, st.pc.get());
   const double d2 = inn - 2.0 * inc + st.icc;
   const double rel = std::sqrt(std::max(0.0, d2)) / std::max(1.0, std::sqrt(std::max(0.0, st.icc)));
   const double tau_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * st.tau_curr * st.tau_curr));
@@ -590,7 +656,7 @@ void McSolver::finish(DevLowRank& out, SolveReport& rep) {
   rep.iterations = iters_;
   rep.rank = Lc.k;
   DBuf<double> fin(nnz_, s);
-  sddmm_residual(s, st.om, Lc.k, Lc.left.get(), Lc.k, Lc.right.get(), Lc.k, st.om.m_csr.get(), fin.get());
+  residual_combine(s, nnz_, Lc.k > 0 ? 1.0 : 0.0, st.pc.get(), 0.0, st.pp.get(), st.om.m_csr.get(), fin.get());
   rep.residual = std::sqrt(dev_dot(s, nnz_, fin.get(), fin.get()));
   rep.objective = st.mu_used * sum_of(st.last_s) + 0.5 * rep.residual * rep.residual;
   out = DevLowRank{};

@@ -100,6 +100,11 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
 
 // Upper triangle (tiles on or above the diagonal) of G = X^T X, X rows x cols row-major; the
 // strictly-lower tiles of G are not written (SYRK: half the Gram FLOPs).
+// C = alpha A B + beta C with B (N x N) upper triangular, its lower part stored as zeros (the
+// diagonal tiles read it): the K loop of each column tile stops at the diagonal — half the
+// FLOPs of gemm.
+void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
+                  double beta, double* C, i64 ldc);
 void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* G, i64 ldg);
 
 // dst (rows x cols, ldd) = alpha * src (rows x cols, lds)  [alpha may be 1]
@@ -129,12 +134,15 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
 // Householder QR only (tests / fallback).
 void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
 
-// Thin SVD of a row-major rows x cols matrix A (rows >= cols), A is destroyed.
-//   U (rows x cols, ldu), S (cols, device), V (cols x cols, ldv), singular values sorted
-//   nonincreasing (host copy returned in s_host).
+// Thin SVD of a row-major rows x cols matrix A (rows >= cols; A is left intact).
+//   U (rows x cols, ldu), V (cols x cols, ldv), singular values sorted nonincreasing (host
+//   copy returned in s_host).
 // Method: columns sorted by norm, thin QR (CholQR2 / Householder fallback), one-sided block
 // Jacobi on R^T (QR-preconditioned Jacobi; few sweeps since R^T is graded).
+// u_tau > 0 promises that only the triplets with sigma > u_tau are used: U may then be
+// recovered as A V Sigma^-1 instead of accumulating the rotations (columns with sigma <= u_tau
+// are not accurate in that mode).
 void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U, i64 ldu, double* V, i64 ldv,
-              std::vector<double>& s_host);
+              std::vector<double>& s_host, double u_tau = 0.0);
 
 }  // namespace dfcg

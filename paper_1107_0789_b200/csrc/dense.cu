@@ -80,10 +80,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp / (BN / WN)) * WM, wn = (warp % (BN / WN)) * WN;
   const i64 m0 = static_cast<i64>(blockIdx.y) * BM, n0 = static_cast<i64>(blockIdx.x) * BN;
-  // SYRK-style: tiles strictly below the diagonal are skipped (their C entries are left as is)
-  if (upper_only && m0 >= n0 + BN) return;
+  // flags & 1 (SYRK-style): tiles strictly below the diagonal are skipped (C left as is).
+  // flags & 2 (B upper triangular, TRMM-style): B(k, j) = 0 for k > j, so the K loop of this
+  // column tile stops at n0 + BN.
+  if ((upper_only & 1) && m0 >= n0 + BN) return;
   const i64 kbeg = static_cast<i64>(blockIdx.z) * kchunk;
-  const i64 kend = min(K, kbeg + kchunk);
+  i64 kend = min(K, kbeg + kchunk);
+  if (upper_only & 2) kend = min(kend, n0 + BN);
   const int ntiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
 
   double acc[FM][FN][2];
@@ -205,7 +208,7 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
     configured |= 1u << dev;
   }
   const int gx = cdiv(N, BN), gy = cdiv(M, BM);
-  const i64 tiles = upper_only ? static_cast<i64>(gx) * (gx + 1) / 2 : static_cast<i64>(gx) * gy;
+  const i64 tiles = (upper_only & 1) ? static_cast<i64>(gx) * (gx + 1) / 2 : static_cast<i64>(gx) * gy;
   const int target = 2 * num_sms();
   int splits = 1;
   if (tiles < target && K > 4 * BK) {
@@ -223,7 +226,7 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
     return;
   }
   DBuf<double> ws(static_cast<i64>(splits) * M * N, s);
-  if (upper_only) ws.zero(s);  // skipped tiles leave their partials unwritten
+  if (upper_only & 1) ws.zero(s);  // skipped tiles leave their partials unwritten
   gemm_kernel<TA, TB, BM, BN, WM, WN><<<dim3(gx, gy, splits), THREADS, smem, s>>>(M, N, K, kchunk, alpha, A, lda, B,
                                                                                   ldb, beta, C, ldc, ws.get(),
                                                                                   upper_only);
@@ -372,6 +375,13 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
   else if (ta && !tb) launch_gemm<true, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else if (!ta && tb) launch_gemm<false, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else launch_gemm<true, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+}
+
+void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
+                  double beta, double* C, i64 ldc) {
+  if (M <= 0 || N <= 0) return;
+  prof::Scope scope(prof::kGemm, s, 1.0 * M * N * (N + 1), 8.0 * (M * N + N * N / 2 + M * N * (beta != 0.0 ? 2.0 : 1.0)));
+  launch_gemm<false, false>(s, M, N, N, alpha, A, lda, B, ldb, beta, C, ldc, 2);
 }
 
 void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* G, i64 ldg) {

@@ -33,11 +33,6 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(pred ? 8 : 0));
-}
-
 // ================================================================ Cholesky (upper, G = R^T R)
 constexpr int CNB = 64;
 
@@ -526,91 +521,176 @@ __global__ void __launch_bounds__(16 * NB) jacobi_round_kernel(i64 rows, i64 nv,
   apply(V, ldv, nv);
 }
 
-// Shared-memory-resident variant of the round (rows <= kResidentRows): the pair's columns
-// of W are loaded once, the Gram is split over the 8 warps (fixed-order partial sums), and
-// the rotation is applied from shared memory straight back to global W; V is streamed
-// through registers (each warp owns whole 8-row tiles, so the in-place update is safe).
-constexpr int kResidentRows = 1408;
+// Shared-memory-resident variant of the round (rows <= kResidentRows). One CTA per block pair:
+//   stage   the pair's 16 columns of W (and of V when both fit) with 16-byte cp.async into a
+//           swizzled 128-byte-row layout (chunk q of row r at q ^ 2(r & 3): conflict-free for
+//           both DMMA fragment patterns below, no padding, 16-byte aligned);
+//   Gram    by DMMA over the 8 warps, fixed-order reduction through 4 shared slots;
+//   EVD     one cyclic sweep of the 16x16 Gram, one barrier per step: each of 64 threads owns a
+//           2x2 block (P, Q) of the pairing and applies J_P^T G J_Q into the other buffer of a
+//           double-buffered Gram, 128 threads rotate the accumulated rotation; every thread
+//           recomputes the rotations it needs from the pre-step Gram;
+//   apply   W_pair <- W_pair rot by DMMA with the rotation fragments held in registers,
+//           16-byte stores; then the same for the V pair.
+// 1688 rows of 128 B + 4 partial Grams + ~7.4 KB static fit the 227 KB opt-in; a W pair alone
+// of <= ~800 rows leaves room for two CTAs per SM.
+constexpr int kResidentRows = 1688;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(pred ? 16 : 0));
+}
+
+// swizzled position of column c (0..15) in row r of a staged pair
+__device__ __forceinline__ int jswz(int r, int c) { return ((((c >> 1) ^ ((r & 3) << 1))) << 1) | (c & 1); }
+
+// pair k (0..7) of step `step` (0..14) of the 16-column round-robin ordering, a < b
+__device__ __forceinline__ void jpair(int step, int k, int& a, int& b) {
+  if (k == 0) {
+    a = 0;
+    b = 1 + step;
+  } else {
+    int x = step + k, y = step + 15 - k;
+    x = x >= 15 ? x - 15 : x;
+    y = y >= 15 ? y - 15 : y;
+    a = 1 + x;
+    b = 1 + y;
+    if (a > b) {
+      const int tmp = a;
+      a = b;
+      b = tmp;
+    }
+  }
+}
+
+// Reciprocal and reciprocal square root from the MUFU seed plus two Newton steps (seed ~2^-22
+// relative -> full double precision): ~half the dependent instructions of the IEEE-rounded
+// division / sqrt sequences, which dominated the latency of an inner Jacobi step.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);  // y <- y (1.5 - x y^2 / 2)
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+
+// symmetric 2x2 Schur rotation of (a, b): t = 2 g_ab sign(d) / (|d| + sqrt(d^2 + 4 g_ab^2)),
+// d = g_bb - g_aa, c = 1 / sqrt(1 + t^2), s = t c; identity when g_ab is negligible.
+__device__ __forceinline__ void jrot(const double (*g)[17], int a, int b, double& c, double& sn) {
+  const double gpq = g[a][b], gpp = g[a][a], gqq = g[b][b];
+  c = 1.0;
+  sn = 0.0;
+  if (fabs(gpq) > 1e-300 && gpq * gpq > 1e-34 * (gpp * gqq)) {
+    const double dd = gqq - gpp, two = 2.0 * gpq;
+    const double D = fma(dd, dd, two * two);
+    const double h = D * rsqrt_nr(D);  // sqrt(D)
+    const double tt = (dd >= 0.0 ? two : -two) * rcp_nr(fabs(dd) + h);
+    c = rsqrt_nr(fma(tt, tt, 1.0));
+    sn = tt * c;
+  }
+}
 
 template <int NB>
-__global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i64 nv, double* W, i64 ldw, double* V,
+__global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i64 nv_, double* W, i64 ldw, double* V,
                                                                     i64 ldv, const int* pairs, double tol,
                                                                     unsigned long long* offmax, int inner_sweeps,
                                                                     int prefetch_v) {
-  constexpr int JW = 2 * NB, T = 256, NT = JW / 8, LD = JW + 1;
-  extern __shared__ double dyn[];
-  const i64 rows4 = (rows + 3) / 4 * 4;
-  const i64 nv4 = (nv + 3) / 4 * 4;
-  const i64 cap = rows4 > nv4 ? rows4 : nv4;
-  double* Wp = dyn;                                 // cap x LD (W pair; V pair too unless prefetched)
-  double* Vp = prefetch_v ? Wp + cap * LD : Wp;     // V pair staged at kernel start when it fits
-  double* red = Wp + (prefetch_v ? 2 : 1) * cap * LD;  // 8 warps x JW*JW partial Grams
-  __shared__ double g[JW][JW + 1];
+  static_assert(NB == 8, "the swizzle and the step tables assume 16-column pairs");
+  constexpr int JW = 16, T = 256;
+  extern __shared__ __align__(16) double dyn[];
+  const int rows = static_cast<int>(rows_), nv = static_cast<int>(nv_);
+  const int rows4 = (rows + 3) & ~3, nv4 = (nv + 3) & ~3;
+  const int cap = rows4 > nv4 ? rows4 : nv4;
+  double* Wp = dyn;
+  double* Vp = prefetch_v ? Wp + cap * JW : Wp;
+  double* red = Wp + (prefetch_v ? 2 : 1) * cap * JW;  // 4 x JW*JW partial Grams
+  __shared__ double g[2][JW][JW + 1];
   __shared__ double rot[JW][JW + 1];
-  __shared__ double cs[JW / 2][2];
-  __shared__ int pp[JW / 2][2];
   __shared__ double s_off;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int bi = pairs[2 * blockIdx.x], bj = pairs[2 * blockIdx.x + 1];
   auto gcol = [&](int c) -> i64 { return c < NB ? static_cast<i64>(bi) * NB + c : static_cast<i64>(bj) * NB + c - NB; };
 
-  // stage the pair's columns with cp.async: every load in flight at once (a plain load->store
-  // loop serialises on global latency — ncu showed it as the round's dominant stall)
-  for (i64 e = t; e < rows4 * JW; e += T) {
-    const i64 r = e / JW;
-    const int c = static_cast<int>(e % JW);
-    cp_async8(Wp + r * LD + c, r < rows ? W + r * ldw + gcol(c) : W, r < rows);
-  }
+  // staging: thread t moves 16-byte chunk q = t & 7 (pair columns 2q, 2q+1) of rows t/8, t/8+32, ...
+  const int q = t & 7;
+  const i64 gq = gcol(2 * q);
+  auto stage = [&](double* dst, const double* src, i64 ld, int n, int n4) {
+    for (int r = t >> 3; r < n4; r += T / 8) {
+      const bool ok = r < n;
+      cp_async16(dst + r * JW + ((q ^ ((r & 3) << 1)) << 1), ok ? src + r * ld + gq : src, ok);
+    }
+  };
+  stage(Wp, W, ldw, rows, rows4);
   asm volatile("cp.async.commit_group;\n" ::);
   if (prefetch_v) {  // second group: the V pair, consumed only after the rotation is known
-    for (i64 e = t; e < nv4 * JW; e += T) {
-      const i64 r = e / JW;
-      const int c = static_cast<int>(e % JW);
-      cp_async8(Vp + r * LD + c, r < nv ? V + r * ldv + gcol(c) : V, r < nv);
-    }
+    stage(Vp, V, ldv, nv, nv4);
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 1;\n" ::);
   } else {
     asm volatile("cp.async.wait_group 0;\n" ::);
   }
   __syncthreads();
+
+  // ---- Gram (DMMA): lane reads column ti*8 + lane/4 of row k + lane%4 for both operands
   {
-    double acc[NT * NT][2];
+    const int o0 = jswz(lane & 3, lane >> 2), o1 = jswz(lane & 3, 8 + (lane >> 2));
+    double acc[4][2];
 #pragma unroll
-    for (int q = 0; q < NT * NT; ++q) acc[q][0] = acc[q][1] = 0.0;
-    for (i64 k = 4 * warp; k < rows4; k += 32) {
-      const double* row = Wp + (k + (lane & 3)) * LD + (lane >> 2);
-#pragma unroll
-      for (int ti = 0; ti < NT; ++ti)
-#pragma unroll
-        for (int tj = 0; tj < NT; ++tj) dmma(acc[ti * NT + tj], row[ti * 8], row[tj * 8]);
+    for (int e = 0; e < 4; ++e) acc[e][0] = acc[e][1] = 0.0;
+    for (int k = 4 * warp; k < rows4; k += 32) {
+      const double* row = Wp + (k + (lane & 3)) * JW;
+      const double x0 = row[o0], x1 = row[o1];
+      dmma(acc[0], x0, x0);
+      dmma(acc[1], x0, x1);
+      dmma(acc[2], x1, x0);
+      dmma(acc[3], x1, x1);
     }
+    auto publish = [&](int slot) {
 #pragma unroll
-    for (int ti = 0; ti < NT; ++ti)
-#pragma unroll
-      for (int tj = 0; tj < NT; ++tj) {
-        const int r = ti * 8 + (lane >> 2), c = tj * 8 + (lane & 3) * 2;
-        red[warp * JW * JW + r * JW + c] = acc[ti * NT + tj][0];
-        red[warp * JW * JW + r * JW + c + 1] = acc[ti * NT + tj][1];
+      for (int e = 0; e < 4; ++e) {
+        const int r = (e >> 1) * 8 + (lane >> 2), c = (e & 1) * 8 + (lane & 3) * 2;
+        red[slot * JW * JW + r * JW + c] = acc[e][0];
+        red[slot * JW * JW + r * JW + c + 1] = acc[e][1];
       }
+    };
+    if (warp >= 4) publish(warp - 4);
+    __syncthreads();
+    if (warp < 4) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = (e >> 1) * 8 + (lane >> 2), c = (e & 1) * 8 + (lane & 3) * 2;
+        acc[e][0] += red[warp * JW * JW + r * JW + c];
+        acc[e][1] += red[warp * JW * JW + r * JW + c + 1];
+      }
+    }
+    __syncthreads();
+    if (warp < 4) publish(warp);
   }
   __syncthreads();
-  for (int e = t; e < JW * JW; e += T) {
-    double v = 0.0;
-    for (int w = 0; w < T / 32; ++w) v += red[w * JW * JW + e];
-    g[e / JW][e % JW] = v;
-    rot[e / JW][e % JW] = (e / JW == e % JW) ? 1.0 : 0.0;
+  {
+    const int e = t, r = e >> 4, c = e & 15;  // T == JW * JW
+    g[0][r][c] = (red[e] + red[JW * JW + e]) + (red[2 * JW * JW + e] + red[3 * JW * JW + e]);
+    rot[r][c] = r == c ? 1.0 : 0.0;
   }
   __syncthreads();
 
   // ---- off-diagonal measure (all pairs of the JW columns)
   {
+    const int a = t >> 4, b = t & 15;
     double mx = 0.0;
-    for (int e = t; e < JW * JW; e += T) {
-      const int a = e / JW, b = e % JW;
-      if (a >= b) continue;
-      const double d = sqrt(g[a][a]) * sqrt(g[b][b]);
-      if (d > 0.0) mx = fmax(mx, fabs(g[a][b]) / d);
+    if (a < b) {
+      const double d = sqrt(g[0][a][a]) * sqrt(g[0][b][b]);
+      if (d > 0.0) mx = fabs(g[0][a][b]) / d;
     }
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (t == 0) s_off = 0.0;
@@ -621,121 +701,98 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows, i6
   }
   const double off0 = s_off;
   if (t == 0) atomicMax(offmax, static_cast<unsigned long long>(__double_as_longlong(off0)));
-  if (off0 <= tol) return;
+  if (off0 <= tol) {
+    asm volatile("cp.async.wait_group 0;\n" ::);  // no copy may land after the CTA retires
+    return;
+  }
 
-  // ---- inner cyclic Jacobi on the JW x JW Gram: `inner_sweeps` round-robin passes (JW - 1
-  // steps of JW/2 disjoint rotations). Exact convergence of the subproblem is not needed —
-  // the outer sweeps re-check every pair.
+  // ---- inner cyclic Jacobi on the Gram, one barrier per step
+  int cur = 0;
   for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
     for (int step = 0; step < JW - 1; ++step) {
-      if (t < JW / 2) {
+      if (t < 64) {
+        const int P = t >> 3, Q = t & 7;
+        int aP, bP, aQ, bQ;
+        jpair(step, P, aP, bP);
+        jpair(step, Q, aQ, bQ);
+        double cP, sP, cQ, sQ;
+        jrot(g[cur], aP, bP, cP, sP);
+        jrot(g[cur], aQ, bQ, cQ, sQ);
+        const double x00 = g[cur][aP][aQ], x01 = g[cur][aP][bQ], x10 = g[cur][bP][aQ], x11 = g[cur][bP][bQ];
+        const double y00 = cQ * x00 - sQ * x01, y01 = sQ * x00 + cQ * x01;  // columns: G J_Q
+        const double y10 = cQ * x10 - sQ * x11, y11 = sQ * x10 + cQ * x11;
+        const int nx = cur ^ 1;  // rows: J_P^T (G J_Q)
+        g[nx][aP][aQ] = cP * y00 - sP * y10;
+        g[nx][bP][aQ] = sP * y00 + cP * y10;
+        g[nx][aP][bQ] = cP * y01 - sP * y11;
+        g[nx][bP][bQ] = sP * y01 + cP * y11;
+      } else if (t < 64 + 128) {
+        const int u = t - 64, k = u >> 4, r = u & 15;
         int a, b;
-        if (t == 0) {
-          a = 0;
-          b = 1 + (step % (JW - 1));
-        } else {
-          a = 1 + ((step + t) % (JW - 1));
-          b = 1 + ((step + (JW - 1) - t) % (JW - 1));
-        }
-        if (a > b) {
-          const int tmp = a;
-          a = b;
-          b = tmp;
-        }
-        pp[t][0] = a;
-        pp[t][1] = b;
-        const double gpq = g[a][b], gpp = g[a][a], gqq = g[b][b];
-        double c = 1.0, sn = 0.0;
-        if (fabs(gpq) > 1e-300 && fabs(gpq) > 1e-17 * sqrt(gpp * gqq)) {
-          // symmetric 2x2 Schur rotation: t = 2 g_pq sign(d) / (|d| + sqrt(d^2 + 4 g_pq^2)), d = g_qq - g_pp
-          const double dd = gqq - gpp, two = 2.0 * gpq;
-          const double tt = (dd >= 0.0 ? two : -two) / (fabs(dd) + sqrt(dd * dd + two * two));
-          c = rsqrt(1.0 + tt * tt);
-          sn = tt * c;
-        }
-        cs[t][0] = c;
-        cs[t][1] = sn;
-      }
-      __syncthreads();
-      for (int e = t; e < (JW / 2) * JW; e += T) {  // columns: g <- g J ; rot <- rot J
-        const int k = e / JW, r = e % JW;
-        const int a = pp[k][0], b = pp[k][1];
-        const double c = cs[k][0], sn = cs[k][1];
-        const double ga = g[r][a], gb = g[r][b];
-        g[r][a] = c * ga - sn * gb;
-        g[r][b] = sn * ga + c * gb;
+        jpair(step, k, a, b);
+        double c, sn;
+        jrot(g[cur], a, b, c, sn);
         const double ra = rot[r][a], rb = rot[r][b];
         rot[r][a] = c * ra - sn * rb;
         rot[r][b] = sn * ra + c * rb;
       }
       __syncthreads();
-      for (int e = t; e < (JW / 2) * JW; e += T) {  // rows: g <- J^T g
-        const int k = e / JW, r = e % JW;
-        const int a = pp[k][0], b = pp[k][1];
-        const double c = cs[k][0], sn = cs[k][1];
-        const double ga = g[a][r], gb = g[b][r];
-        g[a][r] = c * ga - sn * gb;
-        g[b][r] = sn * ga + c * gb;
-      }
-      __syncthreads();
+      cur ^= 1;
     }
   }
 
-  // W[:, pair] <- Wp rot (from shared memory)
-  const i64 rtiles = (rows + 7) / 8;
-  for (i64 rt = warp; rt < rtiles; rt += T / 32) {
-    double o[NT][2];
+  // ---- apply: M_pair <- M_pair rot from the staged copy; B fragments (rot) live in registers
+  double bf[4][2];
 #pragma unroll
-    for (int ct = 0; ct < NT; ++ct) o[ct][0] = o[ct][1] = 0.0;
-    const i64 r = rt * 8 + (lane >> 2);
+  for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-    for (int k = 0; k < JW; k += 4) {
-      const double a = r < rows4 ? Wp[r * LD + k + (lane & 3)] : 0.0;
+    for (int ct = 0; ct < 2; ++ct) bf[kk][ct] = rot[kk * 4 + (lane & 3)][ct * 8 + (lane >> 2)];
+  int ao[4];  // swizzled A-fragment offsets: row rt*8 + lane/4 (r & 3 == (lane/4) & 3), column kk*4 + lane%4
 #pragma unroll
-      for (int ct = 0; ct < NT; ++ct) dmma(o[ct], a, rot[k + (lane & 3)][ct * 8 + (lane >> 2)]);
-    }
-    if (r < rows) {
+  for (int kk = 0; kk < 4; ++kk) ao[kk] = jswz((lane >> 2) & 3, kk * 4 + (lane & 3));
+  const i64 c0 = gcol((lane & 3) * 2), c1 = gcol(8 + (lane & 3) * 2);
+  auto apply = [&](const double* Sp, double* M, i64 ld, int n, int n4) {
+    const int tiles = (n + 7) >> 3;
+    for (int rt = warp; rt < tiles; rt += T / 32) {
+      const int r = rt * 8 + (lane >> 2);
+      double o0[2] = {0.0, 0.0}, o1[2] = {0.0, 0.0};
+      const double* row = Sp + r * JW;
+      const bool in = r < n4;  // rows past the staged block read as 0 (no divergence around the DMMA)
+      double a[4];
 #pragma unroll
-      for (int ct = 0; ct < NT; ++ct) {
-        const int c = ct * 8 + (lane & 3) * 2;
-        W[r * ldw + gcol(c)] = o[ct][0];
-        W[r * ldw + gcol(c + 1)] = o[ct][1];
+      for (int kk = 0; kk < 4; ++kk) a[kk] = in ? row[ao[kk]] : 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        dmma(o0, a[kk], bf[kk][0]);
+        dmma(o1, a[kk], bf[kk][1]);
+      }
+      if (r < n) {
+        *reinterpret_cast<double2*>(M + r * ld + c0) = make_double2(o0[0], o0[1]);
+        *reinterpret_cast<double2*>(M + r * ld + c1) = make_double2(o1[0], o1[1]);
       }
     }
-  }
-  // V[:, pair] <- V[:, pair] rot: the V pair is either already prefetched into Vp or staged
-  // now in the (free) Wp buffer, then the same shared-memory tile product as for W.
+  };
+  apply(Wp, W, ldw, rows, rows4);
+  if (nv == 0) return;
+  // V pair: prefetched into Vp, or staged now into the (free) Wp buffer
   __syncthreads();
   if (!prefetch_v) {
-    for (i64 e = t; e < nv4 * JW; e += T) {
-      const i64 r = e / JW;
-      const int c = static_cast<int>(e % JW);
-      cp_async8(Vp + r * LD + c, r < nv ? V + r * ldv + gcol(c) : V, r < nv);
-    }
+    stage(Vp, V, ldv, nv, nv4);
     asm volatile("cp.async.commit_group;\n" ::);
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
-  const i64 vtiles = (nv + 7) / 8;
-  for (i64 rt = warp; rt < vtiles; rt += T / 32) {
-    double o[NT][2];
-#pragma unroll
-    for (int ct = 0; ct < NT; ++ct) o[ct][0] = o[ct][1] = 0.0;
-    const i64 r = rt * 8 + (lane >> 2);
-#pragma unroll
-    for (int k = 0; k < JW; k += 4) {
-      const double a = r < nv4 ? Vp[r * LD + k + (lane & 3)] : 0.0;
-#pragma unroll
-      for (int ct = 0; ct < NT; ++ct) dmma(o[ct], a, rot[k + (lane & 3)][ct * 8 + (lane >> 2)]);
-    }
-    if (r < nv) {
-#pragma unroll
-      for (int ct = 0; ct < NT; ++ct) {
-        const int c = ct * 8 + (lane & 3) * 2;
-        V[r * ldv + gcol(c)] = o[ct][0];
-        V[r * ldv + gcol(c + 1)] = o[ct][1];
-      }
-    }
+  apply(Vp, V, ldv, nv, nv4);
+}
+
+// A[:, c] /= s[c] (columns with s[c] == 0 are zeroed)
+__global__ void div_cols_kernel(i64 rows, i64 cols, double* A, i64 lda, const double* s) {
+  const i64 total = rows * cols;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = e / cols, c = e % cols;
+    const double sv = s[c];
+    A[r * lda + c] = sv > 0.0 ? A[r * lda + c] / sv : 0.0;
   }
 }
 
@@ -827,7 +884,7 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
   // pass 1 (the Cholesky reads only the upper triangle of the Gram)
   gram_upper(s, rows, cols, X, ldx, G.get(), cols);
   cholesky_inverse(s, cols, G.get(), cols, Rinv.get(), cols, rel_tol, fail.get());
-  gemm(s, false, false, rows, cols, cols, 1.0, X, ldx, Rinv.get(), cols, 0.0, Q1.get(), cols);
+  gemm_upper_b(s, rows, cols, 1.0, X, ldx, Rinv.get(), cols, 0.0, Q1.get(), cols);
   if (R) {
     R1.alloc(cols * cols, s);
     DFCG_CUDA(cudaMemcpyAsync(R1.get(), G.get(), sizeof(double) * cols * cols, cudaMemcpyDeviceToDevice, s));
@@ -837,7 +894,7 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
     Q2.alloc(rows * cols, s);
     gram_upper(s, rows, cols, Q1.get(), cols, G.get(), cols);
     cholesky_inverse(s, cols, G.get(), cols, Rinv.get(), cols, rel_tol, fail.get());
-    gemm(s, false, false, rows, cols, cols, 1.0, Q1.get(), cols, Rinv.get(), cols, 0.0, Q2.get(), cols);
+    gemm_upper_b(s, rows, cols, 1.0, Q1.get(), cols, Rinv.get(), cols, 0.0, Q2.get(), cols);
     Qfinal = Q2.get();
   }
   int h_fail = 0;
@@ -854,7 +911,7 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
 
 // ---------------------------------------------------------------- thin SVD
 void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U, i64 ldu, double* V, i64 ldv,
-              std::vector<double>& s_host) {
+              std::vector<double>& s_host, double u_tau) {
   s_host.assign(static_cast<size_t>(std::max<i64>(cols, 0)), 0.0);
   if (cols <= 0) return;
   if (rows < cols) throw std::invalid_argument("thin_svd: rows < cols");
@@ -869,6 +926,13 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   std::vector<int> cperm(cols);
   std::iota(cperm.begin(), cperm.end(), 0);
   std::stable_sort(cperm.begin(), cperm.end(), [&](int a, int b) { return h_nrm[a] > h_nrm[b]; });
+  // Callers that keep only the triplets with sigma > u_tau may skip accumulating the rotations:
+  // U is then recovered as A V Sigma^-1. Column c carries an error ~ eps (||A|| / sigma_c)^2 +
+  // off * ||A|| / sigma_c, so its contribution sigma_c u_c v_c^T is off by < 1e-9 ||A|| when
+  // ||A||_F <= 1e7 u_tau. This halves the data every Jacobi round moves (the W pair only).
+  double frob2 = 0.0;
+  for (double x : h_nrm) frob2 += x * x;
+  const bool derive_u = u_tau > 0.0 && std::sqrt(frob2) <= 1e7 * u_tau;
   DBuf<int> dcperm(cols, s);
   DFCG_CUDA(cudaMemcpyAsync(dcperm.get(), cperm.data(), sizeof(int) * cols, cudaMemcpyHostToDevice, s));
   DBuf<double> Qx(rows * cols, s), R(cols * cols, s);
@@ -880,10 +944,11 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   const int p = std::max(2, p0 + (p0 & 1));
   const i64 np = static_cast<i64>(p) * NB;  // padded column count
   const i64 wrows = cols;
-  DBuf<double> W(wrows * np, s), J(np * np, s);
+  const i64 nj = derive_u ? 0 : np;  // rows of the accumulated rotation J (0: not accumulated)
+  DBuf<double> W(wrows * np, s), J(std::max<i64>(nj, 1) * np, s);
   W.zero(s);
   transpose(s, cols, cols, R.get(), cols, W.get(), np);  // W = R^T
-  set_identity(s, np, np, J.get(), np);
+  if (nj) set_identity(s, np, np, J.get(), np);
   const std::vector<int> sched = round_robin(p);
   DBuf<int> pairs(static_cast<i64>(sched.size()), s);
   DFCG_CUDA(cudaMemcpyAsync(pairs.get(), sched.data(), sizeof(int) * sched.size(), cudaMemcpyHostToDevice, s));
@@ -892,16 +957,16 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   // singular values converge quadratically, ~tol^2).
   const double tol = 1e-11;
   const int npairs = p / 2;
-  const i64 cap_rows = std::max((wrows + 3) / 4 * 4, (np + 3) / 4 * 4);
+  const i64 cap_rows = std::max((wrows + 3) / 4 * 4, (nj + 3) / 4 * 4);
   const bool resident = cap_rows <= kResidentRows;
-  const int prefetch_v = 2 * cap_rows <= kResidentRows ? 1 : 0;  // W and V pairs both fit
-  const size_t smem = sizeof(double) * ((prefetch_v ? 2 : 1) * cap_rows * (JW + 1) + 8 * JW * JW);
+  const int prefetch_v = nj > 0 && 2 * cap_rows <= kResidentRows ? 1 : 0;  // W and V pairs both fit
+  const size_t smem = sizeof(double) * ((prefetch_v ? 2 : 1) * cap_rows * JW + 4 * JW * JW);
   if (resident) {
     static unsigned configured = 0;
     int dev = 0;
     DFCG_CUDA(cudaGetDevice(&dev));
     if (!(configured & (1u << dev))) {
-      const size_t max_smem = sizeof(double) * (kResidentRows * (JW + 1) + 8 * JW * JW);
+      const size_t max_smem = sizeof(double) * (kResidentRows * JW + 4 * JW * JW);
       DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(max_smem)));
       configured |= 1u << dev;
@@ -911,15 +976,15 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   for (int sweep = 0; sweep < 60; ++sweep) {
     off.zero(s);
     {
-      prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 4.0 * (wrows + np)) * JW * JW,
-                        (p - 1.0) * npairs * 16.0 * (wrows + np) * JW);
+      prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
+                        (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW);
       for (int r = 0; r < p - 1; ++r) {
         const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
         if (resident)
-          jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, np, W.get(), np, J.get(), np, pr, tol,
+          jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol,
                                                                      off.get(), 1, prefetch_v);
         else
-          jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, np, W.get(), np, J.get(), np, pr, tol, off.get(),
+          jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol, off.get(),
                                                               2);
         DFCG_LAUNCH_CHECK();
       }
@@ -951,10 +1016,11 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   DBuf<double> dsig(cols, s);
   DFCG_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), sizeof(int) * cols, cudaMemcpyHostToDevice, s));
   DFCG_CUDA(cudaMemcpyAsync(dsig.get(), s_host.data(), sizeof(double) * cols, cudaMemcpyHostToDevice, s));
-  // U = Q J[:, perm]
-  DBuf<double> Js(cols * cols, s);
-  gather_cols(s, cols, cols, J.get(), np, dperm.get(), nullptr, Js.get(), cols);
-  gemm(s, false, false, rows, cols, cols, 1.0, Qx.get(), cols, Js.get(), cols, 0.0, U, ldu);
+  if (!derive_u) {  // U = Q J[:, perm]
+    DBuf<double> Js(cols * cols, s);
+    gather_cols(s, cols, cols, J.get(), np, dperm.get(), nullptr, Js.get(), cols);
+    gemm(s, false, false, rows, cols, cols, 1.0, Qx.get(), cols, Js.get(), cols, 0.0, U, ldu);
+  }
   // V = P (W[:, perm] / sigma): row j of the normalised W goes to row cperm[j]
   DBuf<double> Wn(cols * cols, s);
   scale_cols_kernel<<<grid_for(cols * cols), 256, 0, s>>>(cols, cols, W.get(), np, dsig.get(), cols, Wn.get(),
@@ -962,6 +1028,11 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   DFCG_LAUNCH_CHECK();
   scatter_rows_int_kernel<<<grid_for(cols * cols), 256, 0, s>>>(cols, cols, Wn.get(), cols, dcperm.get(), V, ldv);
   DFCG_LAUNCH_CHECK();
+  if (derive_u) {  // U = A V Sigma^-1 (A is intact: the QR ran on a permuted copy)
+    gemm(s, false, false, rows, cols, cols, 1.0, A, lda, V, ldv, 0.0, U, ldu);
+    div_cols_kernel<<<grid_for(rows * cols), 256, 0, s>>>(rows, cols, U, ldu, dsig.get());
+    DFCG_LAUNCH_CHECK();
+  }
   DFCG_CUDA(cudaStreamSynchronize(s));  // host vectors (perm, s_host, cperm) used by async copies
 }
 

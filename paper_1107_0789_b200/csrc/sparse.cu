@@ -57,7 +57,7 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
   const i64 gid = ((static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * PER_WARP + lane / G;
   if (gid >= n_items) return;
   const SegItem it = items[gid];
-  constexpr int CPL = 8;  // columns per lane per pass: one walk of the segment covers 8 G columns
+  constexpr int CPL = 4;  // columns per lane per pass: one walk of the segment covers 4 G columns
   for (i64 c0 = 0; c0 < b; c0 += CPL * G) {
     double acc[CPL];
 #pragma unroll
