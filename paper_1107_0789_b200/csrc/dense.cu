@@ -1,10 +1,13 @@
 // Dense FP64 building blocks: DMMA GEMM (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4; FP64 has
 // no tcgen05 kind on sm_100a), copies/transposes, deterministic reductions.
 //
-// GEMM tiling: CTA 64x64, BK=16, 4 warps (2x2) of 32x32, 3-stage cp.async pipeline.
+// GEMM tiling: CTA 64x64, BK=16, 4 warps (2x2) of 32x32, 3-stage cp.async pipeline (see the
+// tile policy above launch_gemm).
 // Shared-memory tiles are stored in the global layout's contiguous order and padded so
 // every DMMA fragment load is a 2-wavefront (conflict-free for 8-byte lanes) access.
 #include "common.cuh"
+
+#include <cstdlib>
 
 namespace dfcg {
 
@@ -207,9 +210,17 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
                                    static_cast<int>(smem)));
     configured |= 1u << dev;
   }
+  static int resident = 0;  // CTAs of this configuration resident per SM
+  if (!resident) {
+    int r = 0;
+    DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, gemm_kernel<TA, TB, BM, BN, WM, WN>, THREADS, smem));
+    resident = std::max(1, r);
+  }
   const int gx = cdiv(N, BN), gy = cdiv(M, BM);
   const i64 tiles = (upper_only & 1) ? static_cast<i64>(gx) * (gx + 1) / 2 : static_cast<i64>(gx) * gy;
-  const int target = 2 * num_sms();
+  // split K until the CTAs fill every resident slot of the GPU about `waves` times
+  static const int waves = std::getenv("DFCG_GEMM_WAVES") ? std::atoi(std::getenv("DFCG_GEMM_WAVES")) : 2;
+  const int target = waves * resident * num_sms();
   int splits = 1;
   if (tiles < target && K > 4 * BK) {
     splits = static_cast<int>(std::min<i64>((target + tiles - 1) / tiles, (K + 255) / 256));
@@ -236,18 +247,28 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
   DFCG_LAUNCH_CHECK();
 }
 
-// Large outputs get 128 x 128 CTA tiles (8 warps of 64 x 32: half the L2 traffic per FLOP);
-// small or skinny ones keep 64 x 64 tiles so enough CTAs exist to fill the 148 SMs.
+// Tile policy (measured on B200 with tools/gemm_bench against cuBLAS, profiles/r01_gemm_*):
+// DMMA throughput needs many resident warps more than large warp tiles — 64x64 CTAs of four
+// 32x32 warps (127 registers, 4 CTAs / 16 warps per SM) beat 128x128 CTAs of 64x32 warps
+// (225 registers, one CTA per SM) by ~25% on the APG shapes, and split-K fills two waves of
+// resident CTAs. DFCG_GEMM_VARIANT / DFCG_GEMM_WAVES select alternatives for experiments.
 template <bool TA, bool TB>
 void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
                  i64 ldb, double beta, double* C, i64 ldc, int upper_only) {
-  const i64 big_tiles = static_cast<i64>(cdiv(M, 128)) * cdiv(N, 128);
-  // 128x128 tiles when the output alone fills the GPU, or when a long K lets split-K fill it
-  const bool big = M >= 128 && N >= 128 && (big_tiles >= num_sms() || (M >= 256 && N >= 256 && K >= 2048));
-  if (big)
-    launch_gemm_cfg<TA, TB, 128, 128, 64, 32>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, upper_only);
-  else
-    launch_gemm_cfg<TA, TB, 64, 64, 32, 32>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, upper_only);
+  static const int variant = std::getenv("DFCG_GEMM_VARIANT") ? std::atoi(std::getenv("DFCG_GEMM_VARIANT")) : 0;
+#define DFCG_GEMM_CFG(bm, bn, wm, wn) \
+  launch_gemm_cfg<TA, TB, bm, bn, wm, wn>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, upper_only)
+  switch (variant) {
+    case 1: DFCG_GEMM_CFG(128, 128, 64, 32); return;
+    case 2: DFCG_GEMM_CFG(128, 128, 32, 32); return;
+    case 3: DFCG_GEMM_CFG(64, 128, 32, 32); return;
+    case 4: DFCG_GEMM_CFG(64, 64, 32, 32); return;
+    case 5: DFCG_GEMM_CFG(32, 64, 16, 32); return;
+    case 6: DFCG_GEMM_CFG(64, 32, 32, 16); return;
+    default: break;
+  }
+  DFCG_GEMM_CFG(64, 64, 32, 32);
+#undef DFCG_GEMM_CFG
 }
 
 // ---------------------------------------------------------------- small kernels

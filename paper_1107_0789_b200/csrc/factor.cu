@@ -33,6 +33,27 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Reciprocal and reciprocal square root from the MUFU seed plus two Newton steps (seed ~2^-22
+// relative -> full double precision): ~half the dependent instructions of the IEEE-rounded
+// division / sqrt sequences, which dominated the latency of an inner Jacobi step.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);  // y <- y (1.5 - x y^2 / 2)
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+
 // ================================================================ Cholesky (upper, G = R^T R)
 constexpr int CNB = 64;
 
@@ -49,130 +70,167 @@ __global__ void diag_max_kernel(i64 n, const double* G, i64 ldg, double* out) {
   if (threadIdx.x == 0) *out = sh[0];
 }
 
-// Factor the kb x kb (kb <= 64) diagonal block at (k0,k0) in place (upper R, lower part zeroed)
-// and write R^-1 into Rinv. 256 threads as a 16 x 16 grid, each owning a 4 x 4 register tile.
-// Every pivot step publishes one row (and for the inverse one column) through double-buffered
-// shared memory with the entries that must not change zeroed, so the rank-1 update of the
-// tile is 16 unconditional FMAs and each step costs one barrier.
+// Factor the kb x kb (kb <= CNB = 64) diagonal block at (k0,k0) in place (upper R, lower part
+// zeroed) and write R^-1 into Rinv. One CTA of 8 warps, the block resident in shared memory,
+// processed in 8-column micro-panels:
+//   factor  warp 0 factors the 8x8 diagonal micro-block warp-synchronously (lane j owns
+//           column j in registers, pivots and row k of R broadcast by shuffles, no barriers);
+//   trsm    one thread per column right of the micro-panel solves R_D^T x = a (8 steps);
+//   update  4x4 register tiles apply the rank-8 update to the trailing upper triangle.
+// The inverse: warp w inverts diagonal micro-block w, then block back-substitution from the
+// bottom block row up, X[I][J] = -X_II sum_{L>I} R[I][L] X[L][J] (two barriers per block row).
+// 3 barriers per micro-panel + 14 for the inverse instead of one per pivot and inverse step
+// (128) in the previous single-level version; the pivot chain is shuffle latency only.
 // Pivots below rel_tol * maxdiag set *fail (the caller falls back to Householder QR).
+constexpr int PB = 8;  // micro-panel width
+constexpr int PLD = CNB + 1;
+constexpr size_t kPotrfSmem = sizeof(double) * (2 * CNB * PLD + PB * PLD + CNB);
+
 __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr,
                                                          const double* maxdiag, double rel_tol, int* fail) {
-  __shared__ double rowb[2][CNB];
-  __shared__ double colb[2][CNB];
-  __shared__ double dinv[CNB];
-  const int t = threadIdx.x, ty = t >> 4, tx = t & 15, r0 = 4 * ty, c0 = 4 * tx;
-  double a[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = r0 + i, c = c0 + j;
-      a[i][j] = (r < kb && c < kb) ? G[r * ldg + c] : (r == c ? 1.0 : 0.0);
-    }
+  extern __shared__ double psm[];
+  double(*A)[PLD] = reinterpret_cast<double(*)[PLD]>(psm);                // R (upper)
+  double(*X)[PLD] = reinterpret_cast<double(*)[PLD]>(psm + CNB * PLD);    // R^-1 (upper)
+  double(*S)[PLD] = reinterpret_cast<double(*)[PLD]>(psm + 2 * CNB * PLD);  // block-row scratch
+  double* dinv = psm + 2 * CNB * PLD + PB * PLD;                           // 1 / r_kk
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const unsigned full = 0xffffffffu;
+  for (int e = t; e < CNB * CNB; e += 256) {
+    const int r = e / CNB, c = e % CNB;
+    A[r][c] = (r < kb && c < kb) ? (r <= c ? G[r * ldg + c] : 0.0) : (r == c ? 1.0 : 0.0);
+    X[r][c] = 0.0;
+  }
   const double thr = rel_tol * (*maxdiag);
-  // ---- Cholesky (upper), right-looking. Step k: the owners of row k publish it with
-  // columns < k zeroed; r_ki = row[i]/sqrt(row[k]) for i > k, 0 otherwise (the pivot column
-  // itself is excluded from the update by zeroing entry k in the scaled copies).
-  for (int k = 0; k < kb; ++k) {
-    const int p = k & 1;
-    const int ok = k - r0;  // owner row within the tile when 0 <= ok < 4
-    if (ok >= 0 && ok < 4) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i == ok) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) rowb[p][c0 + j] = (c0 + j >= k) ? a[i][j] : 0.0;
-        }
-    }
-    __syncthreads();
-    double d = rowb[p][k];
-    const bool bad = !(d > thr) || !isfinite(d);
-    if (bad) d = 1.0;
-    const double ipv = rsqrt(d);
-    if (t == 0) {
-      if (bad) atomicExch(fail, 1);
-      dinv[k] = ipv;
-    }
-    double rr[4], rc[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) rr[i] = (r0 + i == k) ? 0.0 : rowb[p][r0 + i] * ipv;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) rc[j] = (c0 + j == k) ? 0.0 : rowb[p][c0 + j] * ipv;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) a[i][j] -= rr[i] * rc[j];
-    if (ok >= 0 && ok < 4) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i == ok) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) a[i][j] = (c0 + j == k) ? d * ipv : rc[j];
-        }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (r0 + i > c0 + j) a[i][j] = 0.0;
-  // ---- X = R^-1 (upper), right-looking from the bottom: X[k,:] *= 1/r_kk, then
-  // X[i,:] -= r_ik X[k,:] for i < k. The column of R is published with entries >= k zeroed.
-  double x[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) x[i][j] = (r0 + i == c0 + j) ? 1.0 : 0.0;
   __syncthreads();
-  for (int k = kb - 1; k >= 0; --k) {
-    const int p = k & 1;
-    const int ok = k - r0, okc = k - c0;
-    if (ok >= 0 && ok < 4) {
+  for (int c0 = 0; c0 < CNB; c0 += PB) {
+    if (warp == 0) {  // ---- factor the 8x8 diagonal micro-block
+      const int j = lane & (PB - 1);
+      double d[PB];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i == ok) {
+      for (int i = 0; i < PB; ++i) d[i] = i <= j ? A[c0 + i][c0 + j] : 0.0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) rowb[p][c0 + j] = x[i][j];
+      for (int k = 0; k < PB; ++k) {
+        const double piv = __shfl_sync(full, d[k], k);
+        const bool bad = c0 + k < kb && (!(piv > thr) || !isfinite(piv));
+        const double pv = bad ? 1.0 : piv;
+        const double ip = rsqrt_nr(pv);
+        if (lane == 0) {
+          dinv[c0 + k] = ip;
+          if (bad) atomicExch(fail, 1);
         }
-    }
-    if (okc >= 0 && okc < 4) {
+        d[k] = j == k ? pv * ip : (j > k ? d[k] * ip : 0.0);  // row k of R
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j == okc) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) colb[p][r0 + i] = (r0 + i < k) ? a[i][j] : 0.0;
+        for (int i = k + 1; i < PB; ++i) {
+          const double rki = __shfl_sync(full, d[k], i);
+          if (j >= i) d[i] = fma(-rki, d[k], d[i]);
         }
-    }
-    __syncthreads();
-    const double ip = dinv[k];
-    double xk[4], cr[4];
+      }
+      if (lane < PB) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) xk[j] = rowb[p][c0 + j] * ip;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) cr[i] = colb[p][r0 + i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) x[i][j] -= cr[i] * xk[j];
-    if (ok >= 0 && ok < 4) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i == ok) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) x[i][j] = xk[j];
-        }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = r0 + i, c = c0 + j;
-      if (r < kb && c < kb) {
-        G[r * ldg + c] = a[i][j];
-        Rinv[r * ldr + c] = x[i][j];
+        for (int i = 0; i < PB; ++i) A[c0 + i][c0 + j] = d[i];
       }
     }
+    __syncthreads();
+    const int c1 = c0 + PB, n2 = CNB - c1;
+    if (n2 == 0) break;
+    if (t < n2) {  // ---- panel: R[c0:c1, c] = R_D^-T A[c0:c1, c]
+      const int c = c1 + t;
+      double x[PB];
+#pragma unroll
+      for (int i = 0; i < PB; ++i) {
+        double acc = A[c0 + i][c];
+#pragma unroll
+        for (int l = 0; l < i; ++l) acc = fma(-A[c0 + l][c0 + i], x[l], acc);
+        x[i] = acc * dinv[c0 + i];
+        A[c0 + i][c] = x[i];
+      }
+    }
+    __syncthreads();
+    {  // ---- trailing update of the upper triangle (4x4 tiles, tile row <= tile column)
+      const int nt = n2 / 4;
+      for (int e = t; e < nt * nt; e += 256) {
+        const int ti = e / nt, tj = e % nt;
+        if (ti > tj) continue;
+        const int r = c1 + 4 * ti, c = c1 + 4 * tj;
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = A[r + a][c + b];
+#pragma unroll
+        for (int l = 0; l < PB; ++l) {
+          double ri[4], cj[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) ri[a] = A[c0 + l][r + a];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) cj[b] = A[c0 + l][c + b];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(-ri[a], cj[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) A[r + a][c + b] = acc[a][b];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- inverse: diagonal micro-blocks (warp w -> block w; lane j -> column j)
+  {
+    const int w0 = PB * warp, j = lane & (PB - 1);
+    double x[PB];
+#pragma unroll
+    for (int i = PB - 1; i >= 0; --i) {
+      double v = 0.0;
+      if (i == j) {
+        v = dinv[w0 + i];
+      } else if (i < j) {
+        double s = 0.0;
+#pragma unroll
+        for (int l = i + 1; l < PB; ++l)
+          if (l <= j) s = fma(A[w0 + i][w0 + l], x[l], s);
+        v = -dinv[w0 + i] * s;
+      }
+      x[i] = v;
+    }
+    if (lane < PB) {
+#pragma unroll
+      for (int i = 0; i < PB; ++i) X[w0 + i][w0 + j] = x[i];
+    }
+  }
+  __syncthreads();
+  // ---- block back-substitution, bottom block row first
+  for (int I = CNB / PB - 2; I >= 0; --I) {
+    const int r0 = PB * I, cb = r0 + PB, nc = CNB - cb;
+    for (int e = t; e < PB * nc; e += 256) {  // S = R[I, I+1:] X[I+1:, c]  (X upper: rows <= c)
+      const int i = e / nc, c = cb + e % nc;
+      double s0 = 0.0, s1 = 0.0;
+      int l = cb;
+      for (; l + 1 <= c; l += 2) {
+        s0 = fma(A[r0 + i][l], X[l][c], s0);
+        s1 = fma(A[r0 + i][l + 1], X[l + 1][c], s1);
+      }
+      if (l <= c) s0 = fma(A[r0 + i][l], X[l][c], s0);
+      S[i][c] = s0 + s1;
+    }
+    __syncthreads();
+    for (int e = t; e < PB * nc; e += 256) {  // X[I, c] = -X_II S
+      const int i = e / nc, c = cb + e % nc;
+      double v = 0.0;
+#pragma unroll
+      for (int k = 0; k < PB; ++k)
+        if (k >= i) v = fma(X[r0 + i][r0 + k], S[k][c], v);
+      X[r0 + i][c] = -v;
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < kb * kb; e += 256) {
+    const int r = e / kb, c = e % kb;
+    G[r * ldg + c] = r <= c ? A[r][c] : 0.0;
+    Rinv[r * ldr + c] = r <= c ? X[r][c] : 0.0;
+  }
 }
 
 __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
@@ -185,7 +243,17 @@ __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
 }
 
 // In-place blocked Cholesky of G (n x n) -> upper R (lower part zeroed); Rinv = R^-1.
-void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol, int* fail) {
+// want_inverse == false: only R is produced (Rinv then holds just the diagonal-block inverses).
+void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol, int* fail,
+                      bool want_inverse = true) {
+  static unsigned configured = 0;  // one bit per device: opt in to > 48 KB dynamic shared memory
+  int dev = 0;
+  DFCG_CUDA(cudaGetDevice(&dev));
+  if (!(configured & (1u << dev))) {
+    DFCG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kPotrfSmem)));
+    configured |= 1u << dev;
+  }
   DBuf<double> maxdiag(1, s);
   diag_max_kernel<<<1, 256, 0, s>>>(n, G, ldg, maxdiag.get());
   DFCG_LAUNCH_CHECK();
@@ -194,7 +262,7 @@ void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i
     const int kb = static_cast<int>(std::min<i64>(CNB, n - k0));
     double* Gkk = G + k0 * ldg + k0;
     prof::Scope scope(prof::kCholesky, s, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
-    potrf_diag_kernel<<<1, 256, 0, s>>>(kb, Gkk, ldg, Rinv + k0 * ldr + k0, ldr, maxdiag.get(), rel_tol,
+    potrf_diag_kernel<<<1, 256, kPotrfSmem, s>>>(kb, Gkk, ldg, Rinv + k0 * ldr + k0, ldr, maxdiag.get(), rel_tol,
                                                  fail);
     DFCG_LAUNCH_CHECK();
     const i64 rem = n - k0 - kb;
@@ -210,7 +278,7 @@ void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i
   zero_lower_kernel<<<grid_for(n * n), 256, 0, s>>>(n, G, ldg);
   DFCG_LAUNCH_CHECK();
   // Off-diagonal blocks of the inverse: Rinv[0:J, J] = -Rinv[0:J,0:J] R[0:J, J] Rinv[J,J].
-  if (n > CNB) {
+  if (want_inverse && n > CNB) {
     DBuf<double> T(n * CNB, s);
     for (i64 j0 = CNB; j0 < n; j0 += CNB) {
       const i64 jb = std::min<i64>(CNB, n - j0);
@@ -563,27 +631,6 @@ __device__ __forceinline__ void jpair(int step, int k, int& a, int& b) {
   }
 }
 
-// Reciprocal and reciprocal square root from the MUFU seed plus two Newton steps (seed ~2^-22
-// relative -> full double precision): ~half the dependent instructions of the IEEE-rounded
-// division / sqrt sequences, which dominated the latency of an inner Jacobi step.
-__device__ __forceinline__ double rcp_nr(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-}
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-  double e = fma(-h * y, y, 0.5);  // y <- y (1.5 - x y^2 / 2)
-  y = fma(y, e, y);
-  e = fma(-h * y, y, 0.5);
-  return fma(y, e, y);
-}
-
 // symmetric 2x2 Schur rotation of (a, b): t = 2 g_ab sign(d) / (|d| + sqrt(d^2 + 4 g_ab^2)),
 // d = g_bb - g_aa, c = 1 / sqrt(1 + t^2), s = t c; identity when g_ab is negligible.
 __device__ __forceinline__ void jrot(const double (*g)[17], int a, int b, double& c, double& sn) {
@@ -706,15 +753,31 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
     return;
   }
 
-  // ---- inner cyclic Jacobi on the Gram, one barrier per step
+  // ---- inner Jacobi on the Gram, one barrier per step. inner_sweeps > 0: that many cyclic
+  // sweeps over all 120 column pairs (15 steps); inner_sweeps == 0: the 64 cross pairs only
+  // (8 steps, column i of block I with column (i + step) % 8 of block J). The host uses the
+  // full sweep in the first round of every outer sweep (each block appears once there, so its
+  // internal pairs are rotated once per sweep) and cross steps elsewhere: every column pair is
+  // then rotated exactly once per outer sweep, a cyclic Jacobi ordering.
   int cur = 0;
-  for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
-    for (int step = 0; step < JW - 1; ++step) {
+  const bool cross = inner_sweeps == 0;
+  const int nsteps = cross ? NB : (JW - 1) * inner_sweeps;
+  for (int it = 0; it < nsteps; ++it) {
+    const int step = cross ? it : it % (JW - 1);
+    {
+      auto pair_of = [&](int k, int& a, int& b) {
+        if (cross) {
+          a = k;
+          b = NB + ((k + step) & (NB - 1));
+        } else {
+          jpair(step, k, a, b);
+        }
+      };
       if (t < 64) {
         const int P = t >> 3, Q = t & 7;
         int aP, bP, aQ, bQ;
-        jpair(step, P, aP, bP);
-        jpair(step, Q, aQ, bQ);
+        pair_of(P, aP, bP);
+        pair_of(Q, aQ, bQ);
         double cP, sP, cQ, sQ;
         jrot(g[cur], aP, bP, cP, sP);
         jrot(g[cur], aQ, bQ, cQ, sQ);
@@ -729,7 +792,7 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
       } else if (t < 64 + 128) {
         const int u = t - 64, k = u >> 4, r = u & 15;
         int a, b;
-        jpair(step, k, a, b);
+        pair_of(k, a, b);
         double c, sn;
         jrot(g[cur], a, b, c, sn);
         const double ra = rot[r][a], rb = rot[r][b];
@@ -937,7 +1000,23 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   DFCG_CUDA(cudaMemcpyAsync(dcperm.get(), cperm.data(), sizeof(int) * cols, cudaMemcpyHostToDevice, s));
   DBuf<double> Qx(rows * cols, s), R(cols * cols, s);
   gather_cols(s, rows, cols, A, lda, dcperm.get(), nullptr, Qx.get(), cols);
-  thin_qr(s, rows, cols, Qx.get(), cols, R.get(), cols);
+  // With U derived from V only R is needed, and one Cholesky of the Gram gives it: no Q, no
+  // second CholQR pass. The Cholesky succeeds only for kappa(A) < ~3e5, which bounds the
+  // Gram's effect on a kept singular value by eps ||A||^2 / sigma_c < 1e-10 ||A||; otherwise
+  // (or when every triplet is needed) the backward-stable CholQR2 / Householder R is used.
+  bool have_r = false;
+  if (derive_u) {
+    DBuf<int> fail(1, s);
+    DBuf<double> Rinv(cols * cols, s);
+    fail.zero(s);
+    gram_upper(s, rows, cols, Qx.get(), cols, R.get(), cols);
+    cholesky_inverse(s, cols, R.get(), cols, Rinv.get(), cols, 1e-11, fail.get(), false);
+    int h_fail = 0;
+    DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    DFCG_CUDA(cudaStreamSynchronize(s));
+    have_r = h_fail == 0;
+  }
+  if (!have_r) thin_qr(s, rows, cols, Qx.get(), cols, R.get(), cols);
 
   constexpr int NB = 8, JW = 2 * NB;
   const int p0 = static_cast<int>((cols + NB - 1) / NB);
@@ -982,7 +1061,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
         const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
         if (resident)
           jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol,
-                                                                     off.get(), 1, prefetch_v);
+                                                                     off.get(), r == 0 ? 1 : 0, prefetch_v);
         else
           jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol, off.get(),
                                                               2);
