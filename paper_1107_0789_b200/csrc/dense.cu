@@ -7,6 +7,7 @@
 // every DMMA fragment load is a 2-wavefront (conflict-free for 8-byte lanes) access.
 #include "common.cuh"
 
+#include <cmath>
 #include <cstdlib>
 
 namespace dfcg {
@@ -197,34 +198,51 @@ int num_sms() {
   return g_num_sms;
 }
 
+// CTAs of one GEMM configuration resident per SM (configures the shared-memory opt-in once).
 template <bool TA, bool TB, int BM, int BN, int WM, int WN>
-void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
-                     i64 ldb, double beta, double* C, i64 ldc, int upper_only) {
+int gemm_resident() {
   constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
   const size_t smem = sizeof(double) * STAGES * (Tile<TA, BM>::elems + Tile<!TB, BN>::elems);
   static unsigned configured = 0;  // one bit per device
+  static int resident = 0;
   int dev = 0;
   DFCG_CUDA(cudaGetDevice(&dev));
   if (!(configured & (1u << dev))) {
     DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, BM, BN, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-    configured |= 1u << dev;
-  }
-  static int resident = 0;  // CTAs of this configuration resident per SM
-  if (!resident) {
     int r = 0;
     DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, gemm_kernel<TA, TB, BM, BN, WM, WN>, THREADS, smem));
     resident = std::max(1, r);
+    configured |= 1u << dev;
   }
+  return resident;
+}
+
+template <bool TA, bool TB, int BM, int BN, int WM, int WN>
+void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+                     i64 ldb, double beta, double* C, i64 ldc, int upper_only) {
+  constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
+  const size_t smem = sizeof(double) * STAGES * (Tile<TA, BM>::elems + Tile<!TB, BN>::elems);
+  const int resident = gemm_resident<TA, TB, BM, BN, WM, WN>();
   const int gx = cdiv(N, BN), gy = cdiv(M, BM);
   const i64 tiles = (upper_only & 1) ? static_cast<i64>(gx) * (gx + 1) / 2 : static_cast<i64>(gx) * gy;
-  // split K until the CTAs fill every resident slot of the GPU about `waves` times
-  static const int waves = std::getenv("DFCG_GEMM_WAVES") ? std::atoi(std::getenv("DFCG_GEMM_WAVES")) : 2;
-  const int target = waves * resident * num_sms();
+  // Split K when the tiles alone do not fill the resident slots: among the split counts that
+  // keep >= 256 k per CTA, take the one whose CTA count best fills whole waves (ties and a 1%
+  // per-split workspace cost favour fewer splits).
+  const i64 slots = static_cast<i64>(resident) * num_sms();
   int splits = 1;
-  if (tiles < target && K > 4 * BK) {
-    splits = static_cast<int>(std::min<i64>((target + tiles - 1) / tiles, (K + 255) / 256));
-    splits = std::max(1, std::min(splits, 64));
+  if (tiles < slots && K > 4 * BK) {
+    const int smax = static_cast<int>(std::max<i64>(1, std::min<i64>(16, K / 256)));
+    double best = -1.0;
+    for (int sp = 1; sp <= smax; ++sp) {
+      const double w = static_cast<double>(tiles) * sp / slots;
+      const double fill = w >= 1.0 ? w / std::ceil(w) : w;
+      const double sc = fill * (1.0 - 0.01 * (sp - 1));
+      if (sc > best + 1e-9) {
+        best = sc;
+        splits = sp;
+      }
+    }
   }
   i64 kchunk = (K + splits - 1) / splits;
   kchunk = (kchunk + BK - 1) / BK * BK;
@@ -250,8 +268,8 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
 // Tile policy (measured on B200 with tools/gemm_bench against cuBLAS, profiles/r01_gemm_*):
 // DMMA throughput needs many resident warps more than large warp tiles — 64x64 CTAs of four
 // 32x32 warps (127 registers, 4 CTAs / 16 warps per SM) beat 128x128 CTAs of 64x32 warps
-// (225 registers, one CTA per SM) by ~25% on the APG shapes, and split-K fills two waves of
-// resident CTAs. DFCG_GEMM_VARIANT / DFCG_GEMM_WAVES select alternatives for experiments.
+// (225 registers, one CTA per SM) by ~25% on the APG shapes; tile width and split-K count are
+// chosen to fill whole waves of resident CTAs. DFCG_GEMM_VARIANT forces a configuration.
 template <bool TA, bool TB>
 void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
                  i64 ldb, double beta, double* C, i64 ldc, int upper_only) {
@@ -260,14 +278,25 @@ void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double
   launch_gemm_cfg<TA, TB, bm, bn, wm, wn>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, upper_only)
   switch (variant) {
     case 1: DFCG_GEMM_CFG(128, 128, 64, 32); return;
-    case 2: DFCG_GEMM_CFG(128, 128, 32, 32); return;
-    case 3: DFCG_GEMM_CFG(64, 128, 32, 32); return;
     case 4: DFCG_GEMM_CFG(64, 64, 32, 32); return;
     case 5: DFCG_GEMM_CFG(32, 64, 16, 32); return;
-    case 6: DFCG_GEMM_CFG(64, 32, 32, 16); return;
+    case 7: DFCG_GEMM_CFG(64, 48, 32, 24); return;
     default: break;
   }
-  DFCG_GEMM_CFG(64, 64, 32, 32);
+  // 64x64 or 64x48 tiles, whichever wastes less of the last wave and of the ragged last tile
+  // column (N = 720 = 15 x 48: 64-wide tiles leave the 12th column 75% empty).
+  auto score = [&](int bm, int bn, int resident) {
+    const double tm = cdiv(M, bm), tn = cdiv(N, bn);
+    const double area = static_cast<double>(M) * N / (tm * bm * tn * bn);
+    const double tiles = (upper_only & 1) ? tn * (tn + 1) / 2 : tm * tn;
+    const double slots = static_cast<double>(resident) * num_sms();
+    const double waves = tiles / slots;
+    return area * (waves >= 1.0 ? waves / std::ceil(waves) : 1.0);
+  };
+  const double s64 = score(64, 64, gemm_resident<TA, TB, 64, 64, 32, 32>());
+  const double s48 = score(64, 48, gemm_resident<TA, TB, 64, 48, 32, 24>());
+  if (!(upper_only & 1) && s48 > 1.02 * s64) DFCG_GEMM_CFG(64, 48, 32, 24);
+  else DFCG_GEMM_CFG(64, 64, 32, 32);
 #undef DFCG_GEMM_CFG
 }
 

@@ -33,17 +33,8 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// Reciprocal and reciprocal square root from the MUFU seed plus two Newton steps (seed ~2^-22
-// relative -> full double precision): ~half the dependent instructions of the IEEE-rounded
-// division / sqrt sequences, which dominated the latency of an inner Jacobi step.
-__device__ __forceinline__ double rcp_nr(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-}
+// Reciprocal square root from the MUFU seed plus two Newton steps (seed ~2^-22 relative -> full
+// double precision): ~half the dependent instructions of the IEEE-rounded sequence.
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -631,25 +622,37 @@ __device__ __forceinline__ void jpair(int step, int k, int& a, int& b) {
   }
 }
 
-// symmetric 2x2 Schur rotation of (a, b): t = 2 g_ab sign(d) / (|d| + sqrt(d^2 + 4 g_ab^2)),
-// d = g_bb - g_aa, c = 1 / sqrt(1 + t^2), s = t c; identity when g_ab is negligible.
+// Symmetric 2x2 Schur rotation of (a, b): t = 2 g_ab sign(d) / (|d| + sqrt(d^2 + 4 g_ab^2)),
+// d = g_bb - g_aa; identity when g_ab is negligible. The angle is evaluated in single precision
+// on (d, 2 g_ab) scaled by a power of two, then (c, s) is renormalised in double so that
+// c^2 + s^2 = 1 to double rounding: the rotation stays exactly orthogonal and only its angle
+// carries a ~1e-7 relative error, which leaves g_ab at ~1e-7 of its value per visit — still
+// ahead of the quadratic rate. Half the dependent FP64 latency of the all-double formula,
+// which bounded every inner step.
 __device__ __forceinline__ void jrot(const double (*g)[17], int a, int b, double& c, double& sn) {
   const double gpq = g[a][b], gpp = g[a][a], gqq = g[b][b];
   c = 1.0;
   sn = 0.0;
   if (fabs(gpq) > 1e-300 && gpq * gpq > 1e-34 * (gpp * gqq)) {
     const double dd = gqq - gpp, two = 2.0 * gpq;
-    const double D = fma(dd, dd, two * two);
-    const double h = D * rsqrt_nr(D);  // sqrt(D)
-    const double tt = (dd >= 0.0 ? two : -two) * rcp_nr(fabs(dd) + h);
-    c = rsqrt_nr(fma(tt, tt, 1.0));
-    sn = tt * c;
+    const double m = fmax(fabs(dd), fabs(two));
+    const int ex = (__double2hiint(m) >> 20) & 0x7ff;         // biased exponent of m
+    const double sc = __hiloint2double((2046 - ex) << 20, 0);  // 2^-(ex - 1023): m * sc in [1, 2)
+    const float x = static_cast<float>(dd * sc), y = static_cast<float>(two * sc);
+    const float hh = fmaf(x, x, y * y);
+    const float tf = __fdividef(x >= 0.0f ? y : -y, fabsf(x) + hh * rsqrtf(hh));
+    const float cf = rsqrtf(fmaf(tf, tf, 1.0f));
+    const double cd = cf, sd = tf * cf;
+    const double del = fma(cd, cd, sd * sd) - 1.0;        // |del| ~ 1e-7
+    const double nrm = fma(del, fma(del, 0.375, -0.5), 1.0);  // (1 + del)^-1/2 to O(del^3)
+    c = cd * nrm;
+    sn = sd * nrm;
   }
 }
 
 template <int NB>
 __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i64 nv_, double* W, i64 ldw, double* V,
-                                                                    i64 ldv, const int* pairs, double tol,
+                                                                    i64 ldv, int p, int round, double tol,
                                                                     unsigned long long* offmax, int inner_sweeps,
                                                                     int prefetch_v) {
   static_assert(NB == 8, "the swizzle and the step tables assume 16-column pairs");
@@ -665,17 +668,20 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
   __shared__ double rot[JW][JW + 1];
   __shared__ double s_off;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int bi = pairs[2 * blockIdx.x], bj = pairs[2 * blockIdx.x + 1];
+  // round-robin pairing (round_robin() on the host): ring[0] = 0, ring[i] = 1 + (i - 1 - round)
+  // mod (p - 1); CTA k takes (ring[k], ring[p - 1 - k]). No global load before the staging.
+  auto ring = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 - round) % (p - 1) + (p - 1)) % (p - 1); };
+  const int bi = ring(blockIdx.x), bj = ring(p - 1 - blockIdx.x);
   auto gcol = [&](int c) -> i64 { return c < NB ? static_cast<i64>(bi) * NB + c : static_cast<i64>(bj) * NB + c - NB; };
 
   // staging: thread t moves 16-byte chunk q = t & 7 (pair columns 2q, 2q+1) of rows t/8, t/8+32, ...
   const int q = t & 7;
   const i64 gq = gcol(2 * q);
+  const int soff = (q ^ (((t >> 3) & 3) << 1)) << 1;  // swizzled chunk: r & 3 is fixed per thread
   auto stage = [&](double* dst, const double* src, i64 ld, int n, int n4) {
-    for (int r = t >> 3; r < n4; r += T / 8) {
-      const bool ok = r < n;
-      cp_async16(dst + r * JW + ((q ^ ((r & 3) << 1)) << 1), ok ? src + r * ld + gq : src, ok);
-    }
+    const double* sp = src + (t >> 3) * ld + gq;
+    double* dp = dst + (t >> 3) * JW + soff;
+    for (int r = t >> 3; r < n4; r += T / 8, sp += (T / 8) * ld, dp += (T / 8) * JW) cp_async16(dp, r < n ? sp : src, r < n);
   };
   stage(Wp, W, ldw, rows, rows4);
   asm volatile("cp.async.commit_group;\n" ::);
@@ -814,24 +820,35 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) ao[kk] = jswz((lane >> 2) & 3, kk * 4 + (lane & 3));
   const i64 c0 = gcol((lane & 3) * 2), c1 = gcol(8 + (lane & 3) * 2);
+  // two row tiles per iteration: four independent DMMA chains hide the DMMA latency
   auto apply = [&](const double* Sp, double* M, i64 ld, int n, int n4) {
     const int tiles = (n + 7) >> 3;
-    for (int rt = warp; rt < tiles; rt += T / 32) {
-      const int r = rt * 8 + (lane >> 2);
-      double o0[2] = {0.0, 0.0}, o1[2] = {0.0, 0.0};
-      const double* row = Sp + r * JW;
-      const bool in = r < n4;  // rows past the staged block read as 0 (no divergence around the DMMA)
-      double a[4];
+    for (int rt = warp; rt < tiles; rt += 2 * (T / 32)) {
+      const bool two_tiles = rt + T / 32 < tiles;  // warp-uniform
+      const int r = rt * 8 + (lane >> 2), r2 = r + 8 * (T / 32);
+      double o0[2] = {0.0, 0.0}, o1[2] = {0.0, 0.0}, p0[2] = {0.0, 0.0}, p1[2] = {0.0, 0.0};
+      double a[4], b[4];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) a[kk] = in ? row[ao[kk]] : 0.0;
+      for (int kk = 0; kk < 4; ++kk) {  // rows past the staged block read as 0 (no divergence)
+        a[kk] = r < n4 ? Sp[r * JW + ao[kk]] : 0.0;
+        b[kk] = two_tiles && r2 < n4 ? Sp[r2 * JW + ao[kk]] : 0.0;
+      }
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         dmma(o0, a[kk], bf[kk][0]);
         dmma(o1, a[kk], bf[kk][1]);
+        if (two_tiles) {
+          dmma(p0, b[kk], bf[kk][0]);
+          dmma(p1, b[kk], bf[kk][1]);
+        }
       }
       if (r < n) {
         *reinterpret_cast<double2*>(M + r * ld + c0) = make_double2(o0[0], o0[1]);
         *reinterpret_cast<double2*>(M + r * ld + c1) = make_double2(o1[0], o1[1]);
+      }
+      if (two_tiles && r2 < n) {
+        *reinterpret_cast<double2*>(M + r2 * ld + c0) = make_double2(p0[0], p0[1]);
+        *reinterpret_cast<double2*>(M + r2 * ld + c1) = make_double2(p1[0], p1[1]);
       }
     }
   };
@@ -1032,9 +1049,11 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   DBuf<int> pairs(static_cast<i64>(sched.size()), s);
   DFCG_CUDA(cudaMemcpyAsync(pairs.get(), sched.data(), sizeof(int) * sched.size(), cudaMemcpyHostToDevice, s));
   DBuf<unsigned long long> off(1, s);
-  // Off-orthogonality target: singular vectors to ~1e-11 (far below the 1e-6 parity bar; the
-  // singular values converge quadratically, ~tol^2).
-  const double tol = 1e-11;
+  // Pairs whose cosine exceeds tol = 1e-11 are rotated; the sweeps stop once a whole sweep
+  // started with every cosine <= stop_tol = 1e-6. Cyclic Jacobi converges quadratically there,
+  // so that last sweep leaves the columns orthogonal to ~stop_tol^2 (or the rounding floor,
+  // measured ~1e-11 on the c2 shapes — too close to tol to serve as the stopping test too).
+  const double tol = 1e-11, stop_tol = 1e-6;
   const int npairs = p / 2;
   const i64 cap_rows = std::max((wrows + 3) / 4 * 4, (nj + 3) / 4 * 4);
   const bool resident = cap_rows <= kResidentRows;
@@ -1060,7 +1079,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       for (int r = 0; r < p - 1; ++r) {
         const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
         if (resident)
-          jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol,
+          jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, nj, W.get(), np, J.get(), np, p, r, tol,
                                                                      off.get(), r == 0 ? 1 : 0, prefetch_v);
         else
           jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol, off.get(),
@@ -1075,7 +1094,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     std::memcpy(&offv, &h_off, sizeof(double));
     if (trace_svd)
       std::fprintf(stderr, "[svd] %lldx%lld sweep %d off %.3e\n", (long long)rows, (long long)cols, sweep, offv);
-    if (offv <= tol) break;
+    if (offv <= stop_tol) break;
   }
   // singular values = column norms of W; sort descending (stable by index)
   DBuf<double> sig(np, s);
