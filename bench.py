@@ -275,11 +275,12 @@ def main():
     barrier()
     launches0 = P.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # The K steps run back to back per block: every block's thread advances it K iterations on
+    # its own stream, as the F step runs (blocks are independent, P/include/dfc/dfc.hpp:133-147);
+    # a host barrier per iteration would only line the blocks' phases up against each other.
     with ClockSampler(local) as clocks:
         e0.record()
-        iters = 0
-        for _ in range(args.steps):
-            iters += advance(1)
+        iters = advance(args.steps)
         torch.cuda.synchronize()
         e1.record()
         e1.synchronize()

@@ -326,24 +326,54 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
   cur.pos += w * b;
   transpose(s, b, w, Gt.get(), w, G.get(), b);
   op.apply(s, G.get(), b, X.get());
-  // intermediate bases only need a well-conditioned basis of the same span (one CholQR pass);
-  // the final Q, used as a projector, gets the full CholeskyQR2.
-  thin_qr(s, m, b, X.get(), b, nullptr, 0, q > 0 ? 1 : 2);
+  // m-side bases are kept lazily: the orthonormal basis is Q = X M (M = R^-1 of a CholQR
+  // factor of X), and M is applied on the n side after the next product, A^T Q = (A^T X) M,
+  // so the m x b x b triangular products of the intermediate bases (and of the second
+  // CholQR pass of the final one) are never formed. Intermediate bases need one CholQR pass
+  // (same span, well conditioned); the final projector gets two. Any Cholesky breakdown
+  // falls back to the explicit thin_qr (Householder), with M = I.
+  DBuf<double> M(b * b, s), Xt;
+  bool lazy = false;
+  auto orth_m = [&](bool final_basis) {
+    lazy = false;
+    if (!cholqr_factor(s, m, b, X.get(), b, M.get(), b)) {
+      thin_qr(s, m, b, X.get(), b, nullptr, 0, final_basis ? 2 : 1);
+      return;
+    }
+    if (!final_basis) {
+      lazy = true;
+      return;
+    }
+    Xt.alloc(m * b, s);  // pass 1 explicit: X <- X R1^-1; pass 2 lazy
+    gemm_upper_b(s, m, b, 1.0, X.get(), b, M.get(), b, 0.0, Xt.get(), b);
+    std::swap(X, Xt);
+    if (cholqr_factor(s, m, b, X.get(), b, M.get(), b)) lazy = true;
+    else thin_qr(s, m, b, X.get(), b, nullptr, 0, 1);
+  };
+  auto adjoint = [&](DBuf<double>* keep) {  // Z = A^T Q
+    op.apply_adjoint(s, X.get(), b, Z.get(), keep);
+    if (lazy) {
+      DBuf<double> Zm(w * b, s);
+      gemm_upper_b(s, w, b, 1.0, Z.get(), b, M.get(), b, 0.0, Zm.get(), b);
+      std::swap(Z, Zm);
+    }
+  };
+  orth_m(q == 0);
   for (i64 it = 0; it < q; ++it) {
-    op.apply_adjoint(s, X.get(), b, Z.get());
+    adjoint(nullptr);
     thin_qr(s, w, b, Z.get(), b, nullptr, 0, 1);
     op.apply(s, Z.get(), b, X.get());
-    thin_qr(s, m, b, X.get(), b, nullptr, 0, it + 1 < q ? 1 : 2);
+    orth_m(it + 1 == q);
   }
   DBuf<double> T;
-  op.apply_adjoint(s, X.get(), b, Z.get(), &T);  // Z = A^T Q  (w x b)
+  adjoint(&T);  // Z = A^T Q (w x b); T = Yl^T X (before M) for the factor Grams
   DBuf<double> Uz(w * b, s), Vz(b * b, s);
   std::vector<double> sv;
   thin_svd(s, w, b, Z.get(), b, Uz.get(), b, Vz.get(), b, sv, tau);
   const i64 kk = std::min<i64>(k, static_cast<i64>(sv.size()));
   sv.resize(static_cast<size_t>(kk));
   if (!(kk < k || sv[static_cast<size_t>(kk - 1)] <= tau)) return false;
-  // accepted: U = Q Vz[:, :kk], V = Uz[:, :kk]; shrink keeps the first r <= kk columns
+  // accepted: U = Q Vz[:, :kk] = X (M Vz[:, :kk]), V = Uz[:, :kk]; shrink keeps the first r <= kk
   i64 r = 0;
   while (r < kk && sv[static_cast<size_t>(r)] > tau) ++r;
   res.r = r;
@@ -352,15 +382,24 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
   if (r == 0) return true;
   res.left.alloc(m * r, s);
   res.right.alloc(w * r, s);
-  gemm(s, false, false, m, r, b, 1.0, X.get(), b, Vz.get(), b, 0.0, res.left.get(), r);
+  DBuf<double> MV;
+  const double* coef = Vz.get();  // b x r block (ld b) mapping X to the left factor
+  i64 ldcoef = b;
+  if (lazy) {
+    MV.alloc(b * r, s);
+    gemm(s, false, false, b, r, b, 1.0, M.get(), b, Vz.get(), b, 0.0, MV.get(), r);
+    coef = MV.get();
+    ldcoef = r;
+  }
+  gemm(s, false, false, m, r, b, 1.0, X.get(), b, coef, ldcoef, 0.0, res.left.get(), r);
   const i64 kc = op.keep_rows();
-  if (kc >= 0 && T.size() >= kc * b) {  // left = Q Vz_r: left^T left = Vz_r^T Vz_r, Lc.left^T left = T[:kc] Vz_r
+  if (kc >= 0 && T.size() >= kc * b) {  // left = Q Vz_r: left^T left = Vz_r^T Vz_r, Lc.left^T left = T[:kc] coef
     res.grams = true;
     res.ll.alloc(r * r, s);
     gemm(s, true, false, r, r, b, 1.0, Vz.get(), b, Vz.get(), b, 0.0, res.ll.get(), r);
     if (kc > 0) {
       res.lc.alloc(kc * r, s);
-      gemm(s, false, false, kc, r, b, 1.0, T.get(), b, Vz.get(), b, 0.0, res.lc.get(), r);
+      gemm(s, false, false, kc, r, b, 1.0, T.get(), b, coef, ldcoef, 0.0, res.lc.get(), r);
     }
   }
   DBuf<double> sc(r, s);

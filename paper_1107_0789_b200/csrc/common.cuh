@@ -131,6 +131,10 @@ struct Workspace;  // forward
 // passes = 1 gives a well-conditioned basis of span(X) (orthogonality ~ eps cond(X)^2),
 // enough for the intermediate bases of the range finder; passes = 2 is CholeskyQR2.
 bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr, int passes = 2);
+// One CholQR factor without forming Q: Rinv = R^-1 (upper, lower part zero) with
+// R^T R = X^T X, so X Rinv has orthonormal columns to ~eps cond(X)^2. Returns false (Rinv
+// unusable) when a Cholesky pivot signals cond(X) >~ 3e5.
+bool cholqr_factor(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* Rinv, i64 ldr);
 // Householder QR only (tests / fallback).
 void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
 

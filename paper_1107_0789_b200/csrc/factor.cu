@@ -953,6 +953,19 @@ void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, doub
 }
 
 // ---------------------------------------------------------------- CholeskyQR2 + fallback
+bool cholqr_factor(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* Rinv, i64 ldr) {
+  if (cols <= 0) return true;
+  DBuf<int> fail(1, s);
+  fail.zero(s);
+  DBuf<double> G(cols * cols, s);
+  gram_upper(s, rows, cols, X, ldx, G.get(), cols);
+  cholesky_inverse(s, cols, G.get(), cols, Rinv, ldr, 1e-11, fail.get());
+  int h_fail = 0;
+  DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  return h_fail == 0;
+}
+
 bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr, int passes) {
   if (cols <= 0) return false;
   if (rows < cols) throw std::invalid_argument("thin_qr: rows < cols");
