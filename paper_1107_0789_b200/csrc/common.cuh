@@ -121,6 +121,24 @@ void gather_cols(cudaStream_t s, i64 rows, i64 ncols, const double* src, i64 lds
 // Column norms of a row-major rows x cols matrix: out[c] = ||src[:, c]||_2 (deterministic).
 void col_norms(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* out);
 
+// ---------------------------------------------------------------- cp.async helpers (device)
+// 8-byte copies go through L1 (.ca), 16-byte ones bypass it (.cg); pred == false zero-fills.
+#ifdef __CUDACC__
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+#endif
+
 // ---------------------------------------------------------------- factorizations (factor.cu)
 struct Workspace;  // forward
 

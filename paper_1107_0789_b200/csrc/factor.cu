@@ -595,10 +595,6 @@ __global__ void __launch_bounds__(16 * NB) jacobi_round_kernel(i64 rows, i64 nv,
 // of <= ~800 rows leaves room for two CTAs per SM.
 constexpr int kResidentRows = 1688;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
-  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(pred ? 16 : 0));
-}
 
 // swizzled position of column c (0..15) in row r of a staged pair
 __device__ __forceinline__ int jswz(int r, int c) { return ((((c >> 1) ^ ((r & 3) << 1))) << 1) | (c & 1); }

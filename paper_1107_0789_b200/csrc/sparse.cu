@@ -5,6 +5,7 @@
 // SpMM: segmented work list (<= SEG entries per item) so long CSC columns split across
 // warps; multi-segment rows reduce their partials in a fixed order (deterministic).
 #include <algorithm>
+#include <cstdint>
 
 #include "sparse.cuh"
 
@@ -13,9 +14,6 @@ namespace dfcg {
 namespace {
 
 constexpr int SEG = 64;
-// The chunked path re-walks every nonzero once per 16-column chunk; measured 2x slower than
-// the segmented kernel at b ~ 700 (ncu: instruction-bound), so it is disabled for now.
-constexpr i64 kSlabMinB = i64{1} << 40;
 
 int pow2_at_least(i64 v) {
   int g = 1;
@@ -133,79 +131,124 @@ __global__ void scatter_dense_kernel(i64 N, const int* __restrict__ row, const i
     D[static_cast<i64>(row[t]) * ldd + col[t]] += alpha * vals[t];
 }
 
-// Shared-memory-chunked SpMM for wide sketches: CTA (chunk c, slab q, row split) stages
-// X[q*H : (q+1)*H, 16c : 16c+16] in shared memory once and streams its structure rows'
-// entries against it (half-warp per output row, lane = column), so each X element is read
-// from L2 once per CTA instead of once per nonzero. Partial sums per slab when ns > 1.
-constexpr int CW = 16, SLAB_THREADS = 512;
-template <bool T>
-__global__ void __launch_bounds__(SLAB_THREADS) spmm_slab_kernel(i64 rows, int ns, int rsplit,
-                                                                 const int* __restrict__ slab,
-                                                                 const int* __restrict__ idx,
-                                                                 const long long* __restrict__ perm,
-                                                                 const double* __restrict__ vals, i64 in_rows, i64 b,
-                                                                 double alpha, const double* __restrict__ X, i64 ldx,
-                                                                 double beta, double* __restrict__ out, i64 ldo,
-                                                                 double* __restrict__ ws) {
-  extern __shared__ double xs[];  // H x CW
-  constexpr int H = DevOmega::kSlabRows, NW = SLAB_THREADS / 32;
-  const int c = blockIdx.x, q = blockIdx.y, split = blockIdx.z;
-  const i64 c0 = static_cast<i64>(c) * CW, s0 = static_cast<i64>(q) * H;
-  const i64 h = min(static_cast<i64>(H), in_rows - s0);
-  const int w = static_cast<int>(min(static_cast<i64>(CW), b - c0));
-  for (i64 e = threadIdx.x; e < h * CW; e += blockDim.x) {
-    const i64 r = e / CW;
-    const int cc = static_cast<int>(e % CW);
-    xs[e] = cc < w ? X[(s0 + r) * ldx + c0 + cc] : 0.0;
+// Tiled SDDMM: one CTA per 64 x 64 tile of the observed matrix. The tile's factor rows
+// Yl[i0:i0+64, :] and Yr[j0:j0+64, :] stream through shared memory in 32-wide k chunks (double
+// buffered, cp.async) and every thread accumulates the dot products of up to SEPT of the tile's
+// entries from there: each factor row is read from L2 once per tile instead of once per entry
+// (~6x less L2 traffic at 10% density). Each lane walks a chunk starting at k = lane, so the
+// 16 lanes of a shared-memory phase hit 16 distinct banks whatever rows they read.
+constexpr int STR = 64, STC = 64, SKC = 32, SDD_T = 256, SEPT = 4;
+constexpr size_t kSddmmSmem = sizeof(double) * 2 * (STR + STC) * SKC;
+static_assert(STC == DevOmega::kTileCols, "tile width must match the CSR column-tile table");
+
+__global__ void __launch_bounds__(SDD_T) sddmm_tile_kernel(i64 m, i64 n, i64 kY, int ntc, const int* __restrict__ tptr,
+                                                           const int* __restrict__ col, const double* __restrict__ Yl,
+                                                           i64 ldl, const double* __restrict__ Yr, i64 ldr,
+                                                           const double* __restrict__ sub, double* __restrict__ out) {
+  extern __shared__ double sm[];  // [2][STR][SKC] then [2][STC][SKC]
+  double* sl = sm;
+  double* sr = sm + 2 * STR * SKC;
+  __shared__ int pre[STR + 1];
+  __shared__ int base_pos[STR];
+  const int t = threadIdx.x, lane = t & 31;
+  const i64 i0 = static_cast<i64>(blockIdx.y) * STR, j0 = static_cast<i64>(blockIdx.x) * STC;
+  if (t < STR) {
+    const i64 i = i0 + t;
+    int b0 = 0, c = 0;
+    if (i < m) {
+      b0 = tptr[i * (ntc + 1) + blockIdx.x];
+      c = tptr[i * (ntc + 1) + blockIdx.x + 1] - b0;
+    }
+    base_pos[t] = b0;
+    pre[t + 1] = c;
   }
   __syncthreads();
-  // warp per structure row: the row's entries are fetched 32 at a time (coalesced, one per
-  // lane) and broadcast by shuffles; half-warp hh takes entries j + 16 hh of each batch, lane
-  // column = lane & 15; the two halves are combined at the end (fixed order).
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, col = lane & 15, hh = lane >> 4;
-  const i64 per = (rows + rsplit - 1) / rsplit;
-  const i64 rb = static_cast<i64>(split) * per, re = min(rows, rb + per);
-  for (i64 r = rb + warp; r < re; r += NW) {
-    const int e0 = slab[r * (ns + 1) + q], e1 = slab[r * (ns + 1) + q + 1];
-    double acc = 0.0;
-    for (int base = e0; base < e1; base += 32) {
-      const int e = base + lane;
-      int myidx = static_cast<int>(s0);
-      double myv = 0.0;
-      if (e < e1) {
-        myidx = idx[e];
-        myv = T ? vals[perm[e]] : vals[e];
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int src = j + 16 * hh;
-        const int ii = __shfl_sync(0xffffffffu, myidx, src);
-        const double v = __shfl_sync(0xffffffffu, myv, src);
-        acc = fma(v, xs[static_cast<i64>(ii - s0) * CW + col], acc);
-      }
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-    if (hh == 0 && col < w) {
-      if (ns == 1) {
-        double* o = out + r * ldo + c0 + col;
-        *o = beta == 0.0 ? alpha * acc : alpha * acc + beta * *o;
-      } else {
-        ws[(static_cast<i64>(q) * rows + r) * b + c0 + col] = acc;
-      }
-    }
+  if (t == 0) {
+    pre[0] = 0;
+    for (int r = 0; r < STR; ++r) pre[r + 1] += pre[r];
   }
-}
-
-__global__ void slab_reduce_kernel(i64 rows, int ns, i64 b, const double* __restrict__ ws, double alpha,
-                                   double beta, double* __restrict__ out, i64 ldo) {
-  const i64 total = rows * b;
-  for (i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 r = t / b, c = t % b;
-    double s = 0.0;
-    for (int q = 0; q < ns; ++q) s += ws[(static_cast<i64>(q) * rows + r) * b + c];
-    double* o = out + r * ldo + c;
-    *o = beta == 0.0 ? alpha * s : alpha * s + beta * *o;
+  __syncthreads();
+  const int total = pre[STR];
+  if (total == 0) return;
+  const i64 rows_in = min(static_cast<i64>(STR), m - i0), cols_in = min(static_cast<i64>(STC), n - j0);
+  // staging (16-byte cp.async; ldl, ldr even and the bases 16-byte aligned, see the host side):
+  // thread t copies the column pair 2 (t % 16) of rows t / 16, t / 16 + 16, ... of both tiles.
+  // kY is rounded up to even by the host (the padding column holds zeros), so a pair is either
+  // entirely inside k < kY or entirely outside.
+  constexpr int PR = SKC / 2, RS = SDD_T / PR;  // pairs per row, rows per pass
+  const int skk = 2 * (t % PR), sr0 = t / PR;
+  auto stage = [&](int buf, i64 k0) {
+    double* dl = sl + buf * STR * SKC + sr0 * SKC + skk;
+    double* dr = sr + buf * STC * SKC + sr0 * SKC + skk;
+    const bool kin = k0 + skk < kY;
+    const double* gl = Yl + (i0 + sr0) * ldl + k0 + skk;
+    const double* gr = Yr + (j0 + sr0) * ldr + k0 + skk;
+#pragma unroll
+    for (int q = 0; q < STR / RS; ++q) {
+      const bool ok = kin && sr0 + q * RS < rows_in;
+      cp_async16(dl + q * RS * SKC, ok ? gl + q * RS * ldl : Yl, ok);
+    }
+#pragma unroll
+    for (int q = 0; q < STC / RS; ++q) {
+      const bool ok = kin && sr0 + q * RS < cols_in;
+      cp_async16(dr + q * RS * SKC, ok ? gr + q * RS * ldr : Yr, ok);
+    }
+    cp_async_commit();
+  };
+  for (int first = 0; first < total; first += SDD_T * SEPT) {
+    int li[SEPT], lj[SEPT], pos[SEPT];
+    double acc[SEPT];
+#pragma unroll
+    for (int q = 0; q < SEPT; ++q) {
+      const int e = first + t + q * SDD_T;
+      acc[q] = 0.0;
+      li[q] = -1;
+      if (e < total) {
+        int lo = 0, hi = STR;  // largest r with pre[r] <= e
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (pre[mid] <= e) lo = mid;
+          else hi = mid;
+        }
+        li[q] = lo;
+        pos[q] = base_pos[lo] + (e - pre[lo]);
+        lj[q] = static_cast<int>(col[pos[q]] - j0);
+      }
+    }
+    const int nk = static_cast<int>((kY + SKC - 1) / SKC);
+    if (nk > 0) stage(0, 0);
+    for (int kc = 0; kc < nk; ++kc) {
+      if (kc + 1 < nk) {
+        stage((kc + 1) & 1, static_cast<i64>(kc + 1) * SKC);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* dl = sl + (kc & 1) * STR * SKC;
+      const double* dr = sr + (kc & 1) * STC * SKC;
+#pragma unroll
+      for (int q = 0; q < SEPT; ++q) {
+        if (!__any_sync(0xffffffffu, li[q] >= 0)) break;  // later slots are empty for the whole warp
+        if (li[q] < 0) continue;
+        // 16-byte loads, the pair index rotated by lane: 8 lanes of a phase hit 8 distinct slots
+        const double2* a = reinterpret_cast<const double2*>(dl + li[q] * SKC);
+        const double2* b = reinterpret_cast<const double2*>(dr + lj[q] * SKC);
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < SKC / 2; ++kk) {
+          const int k = (kk + lane) & (SKC / 2 - 1);
+          const double2 x = a[k], y = b[k];
+          s0 = fma(x.x, y.x, s0);
+          s1 = fma(x.y, y.y, s1);
+        }
+        acc[q] += s0 + s1;
+      }
+      __syncthreads();  // the buffer just read is refilled by the next iteration's stage
+    }
+#pragma unroll
+    for (int q = 0; q < SEPT; ++q)
+      if (li[q] >= 0) out[pos[q]] = sub ? acc[q] - sub[pos[q]] : acc[q];
   }
 }
 
@@ -290,24 +333,22 @@ void DevOmega::build(cudaStream_t s, i64 m_, i64 n_, i64 nnz_, const long long* 
   upload(s, csc2csr, c2r);
   build_plan(s, plan_csr, m, rowptr);
   build_plan(s, plan_csc, n, colptr);
-  // slab offsets (input index = column for CSR rows, row for CSC columns; both sorted)
-  auto slabs = [&](i64 rows, const std::vector<int>& ptr, const std::vector<int>& idx, i64 in_rows, int& ns,
-                   DBuf<int>& out) {
-    ns = static_cast<int>((in_rows + kSlabRows - 1) / kSlabRows);
-    std::vector<int> h(static_cast<size_t>(rows * (ns + 1)));
-    for (i64 r = 0; r < rows; ++r) {
-      int e = ptr[r];
-      for (int q = 0; q <= ns; ++q) {
-        const long long lim = static_cast<long long>(q) * kSlabRows;
-        while (e < ptr[r + 1] && idx[e] < lim) ++e;
-        h[static_cast<size_t>(r * (ns + 1) + q)] = q == ns ? ptr[r + 1] : e;
+  // column-tile offsets of every CSR row (tiled SDDMM), when the table stays small
+  const i64 tiles = (n + kTileCols - 1) / kTileCols;
+  if (m * (tiles + 1) <= (i64{1} << 26)) {
+    ntc = static_cast<int>(tiles);
+    std::vector<int> h(static_cast<size_t>(m * (tiles + 1)));
+    for (i64 r = 0; r < m; ++r) {
+      int e = rowptr[r];
+      for (i64 q = 0; q <= tiles; ++q) {
+        const long long lim = q * kTileCols;
+        while (e < rowptr[r + 1] && rcol[e] < lim) ++e;
+        h[static_cast<size_t>(r * (tiles + 1) + q)] = q == tiles ? rowptr[r + 1] : e;
       }
     }
-    upload(s, out, h);
+    upload(s, tile_csr, h);
     DFCG_CUDA(cudaStreamSynchronize(s));
-  };
-  slabs(m, rowptr, rcol, n, nslab_csr, slab_csr);
-  slabs(n, colptr, crow, m, nslab_csc, slab_csc);
+  }
   h_csc2csr = std::move(c2r);
 }
 
@@ -316,6 +357,41 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
   if (om.nnz == 0) return;
   // algorithmic bytes: row+col index, M_e, r_e per entry + both factors once
   prof::Scope scope(prof::kSddmm, s, 2.0 * kY * om.nnz, 24.0 * om.nnz + 8.0 * (om.m + om.n) * kY);
+  if (om.ntc > 0 && kY >= SKC) {
+    static unsigned configured = 0;  // one bit per device
+    int dev = 0;
+    DFCG_CUDA(cudaGetDevice(&dev));
+    if (!(configured & (1u << dev))) {
+      DFCG_CUDA(cudaFuncSetAttribute(sddmm_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kSddmmSmem)));
+      configured |= 1u << dev;
+    }
+    // 16-byte staging needs even leading dimensions and an even k extent: repack the factors
+    // (a few tens of microseconds) unless they already qualify; the padding column is zero.
+    const i64 k2 = (kY + 1) & ~i64{1};
+    DBuf<double> pl, pr;
+    const bool aligned = (ldl % 2 == 0) && (ldr % 2 == 0) && k2 == kY &&
+                         (reinterpret_cast<std::uintptr_t>(Yl) % 16 == 0) &&
+                         (reinterpret_cast<std::uintptr_t>(Yr) % 16 == 0);
+    if (!aligned) {
+      pl.alloc(om.m * k2, s);
+      pr.alloc(om.n * k2, s);
+      if (k2 != kY) {
+        pl.zero(s);
+        pr.zero(s);
+      }
+      copy2d(s, om.m, kY, Yl, ldl, pl.get(), k2);
+      copy2d(s, om.n, kY, Yr, ldr, pr.get(), k2);
+      Yl = pl.get();
+      Yr = pr.get();
+      ldl = ldr = k2;
+    }
+    const dim3 grid(om.ntc, static_cast<unsigned>((om.m + STR - 1) / STR));
+    sddmm_tile_kernel<<<grid, SDD_T, kSddmmSmem, s>>>(om.m, om.n, k2, om.ntc, om.tile_csr.get(), om.csr_col.get(), Yl,
+                                                      ldl, Yr, ldr, sub, r_csr);
+    DFCG_LAUNCH_CHECK();
+    return;
+  }
   const int G = pow2_at_least((kY + 3) / 4);
   const i64 warps = (om.nnz + (32 / G) - 1) / (32 / G);
   const int blocks = static_cast<int>(std::min<i64>((warps + 7) / 8, 65535L * 4));
@@ -342,43 +418,6 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   const i64 out_rows = transpose ? om.n : om.m;
   if (b <= 0 || out_rows <= 0) return;
   const int* ptr = transpose ? om.csc_colptr.get() : om.csr_rowptr.get();
-  if (b >= kSlabMinB) {  // wide sketch: shared-memory-chunked path (off: slower than the segmented kernel)
-    const i64 in_rows = transpose ? om.m : om.n;
-    prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,
-                      (transpose ? 20.0 : 12.0) * om.nnz + 8.0 * b * (in_rows + out_rows * (beta != 0.0 ? 2 : 1)));
-    const int ns = transpose ? om.nslab_csc : om.nslab_csr;
-    const int chunks = cdiv(b, CW);
-    const int rsplit = std::max(1, std::min<int>(static_cast<int>((out_rows + 15) / 16),
-                                                 (148 + chunks * ns - 1) / (chunks * ns)));
-    const size_t smem = sizeof(double) * DevOmega::kSlabRows * CW;
-    static unsigned configured = 0;
-    int dev = 0;
-    DFCG_CUDA(cudaGetDevice(&dev));
-    if (!(configured & (1u << dev))) {
-      DFCG_CUDA(cudaFuncSetAttribute(spmm_slab_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-      DFCG_CUDA(cudaFuncSetAttribute(spmm_slab_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-      configured |= 1u << dev;
-    }
-    DBuf<double> ws;
-    if (ns > 1) ws.alloc(static_cast<i64>(ns) * out_rows * b, s);
-    const dim3 grid(chunks, ns, rsplit);
-    if (transpose)
-      spmm_slab_kernel<true><<<grid, SLAB_THREADS, smem, s>>>(out_rows, ns, rsplit, om.slab_csc.get(), om.csc_row.get(),
-                                                     om.csc2csr.get(), vals_csr, in_rows, b, alpha, X, ldx, beta, out,
-                                                     ldo, ws.get());
-    else
-      spmm_slab_kernel<false><<<grid, SLAB_THREADS, smem, s>>>(out_rows, ns, rsplit, om.slab_csr.get(), om.csr_col.get(),
-                                                      om.csc2csr.get(), vals_csr, in_rows, b, alpha, X, ldx, beta,
-                                                      out, ldo, ws.get());
-    DFCG_LAUNCH_CHECK();
-    if (ns > 1) {
-      slab_reduce_kernel<<<grid_for(out_rows * b), 256, 0, s>>>(out_rows, ns, b, ws.get(), alpha, beta, out, ldo);
-      DFCG_LAUNCH_CHECK();
-    }
-    return;
-  }
   // algorithmic bytes: idx + value (+ permutation) per entry, X read once, out written (read if beta)
   const i64 in_rows = transpose ? om.m : om.n;
   prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,

@@ -36,11 +36,12 @@ struct DevOmega {
   DBuf<double> m_csc;
   SegPlan plan_csr, plan_csc;
   std::vector<long long> h_csc2csr;  // host copy (outputs in reference order)
-  // Slab offsets for the shared-memory-chunked SpMM: entries of structure row r whose input
-  // index falls in slab q = [q*kSlabRows, (q+1)*kSlabRows) are [ptr[r*(ns+1)+q], ptr[r*(ns+1)+q+1]).
-  static constexpr int kSlabRows = 1280;
-  int nslab_csr = 1, nslab_csc = 1;  // slabs over the input rows (n for R X, m for R^T X)
-  DBuf<int> slab_csr, slab_csc;
+  // Column-tile offsets of the CSR rows for the tiled SDDMM: the entries of row r in column
+  // tile q = [64q, 64q + 64) are CSR positions [tile_csr[r*(ntc+1)+q], tile_csr[r*(ntc+1)+q+1]).
+  // ntc = 0 when the table would be too large (the entry-parallel kernel is used then).
+  static constexpr int kTileCols = 64;
+  int ntc = 0;
+  DBuf<int> tile_csr;
 
   // rows/cols: CSC-sorted (column-major order, as ObservedMatrix guarantees).
   void build(cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows, const long long* cols, const double* vals);
