@@ -202,6 +202,7 @@ double dev_dot(cudaStream_t s, i64 n, const double* a, const double* b) {
 struct OpMC {
   const DevOmega* om;
   const double* r_csr;
+  const double* r_csc;  // the same residual in CSC order (transposed products)
   double coeff;
   i64 m, w, kY;
   const double* left;   // m x kY row-major (ld kY)
@@ -225,10 +226,10 @@ struct OpMC {
       DBuf<double> T(kY * b, s);
       gemm(s, true, false, kY, b, m, 1.0, left, kY, X, b, 0.0, T.get(), b);
       gemm(s, false, false, w, b, kY, 1.0, right, kY, T.get(), b, 0.0, out, b);
-      spmm(s, *om, true, r_csr, b, coeff, X, b, 1.0, out, b);
+      spmm(s, *om, true, r_csr, b, coeff, X, b, 1.0, out, b, r_csc);
       if (keep) *keep = std::move(T);
     } else {
-      spmm(s, *om, true, r_csr, b, coeff, X, b, 0.0, out, b);
+      spmm(s, *om, true, r_csr, b, coeff, X, b, 0.0, out, b, r_csc);
     }
   }
   i64 keep_rows() const { return kc; }
@@ -549,7 +550,7 @@ static double spectral_norm_omega(cudaStream_t s, const DevOmega& om) {
 struct McSolver::State {
   DevOmega om;
   NormalCursor cur;
-  DBuf<double> r_csr;
+  DBuf<double> r_csr, r_csc;
   // P_Omega of the current / previous iterate (CSR order): by linearity P_Omega(Y) =
   // (1+beta) P_Omega(L_curr) - beta P_Omega(L_prev), so each iteration runs one SDDMM at rank
   // r (the new iterate) instead of one at the concatenated rank of Y.
@@ -574,6 +575,7 @@ McSolver::McSolver(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, co
   if (st.mu_floor > st.mu_init) throw std::invalid_argument("apg_mc: mu_floor exceeds mu_init");
   st.cur = NormalCursor{&ctx.normals(0), 0};
   st.r_csr.alloc(nnz, s);
+  st.r_csc.alloc(nnz, s);
   st.pc.alloc(nnz, s);
   st.pp.alloc(nnz, s);
   st.Lp.m = st.Lc.m = m;
@@ -624,11 +626,12 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   // R = P_Omega(Y) - P_Omega(M) = (1+beta) P_Omega(L_curr) - beta P_Omega(L_prev) - P_Omega(M)
   residual_combine(s, nnz, Lc.k > 0 ? 1.0 + beta : 0.0, st.pc.get(), concat ? -beta : 0.0, st.pp.get(),
                    st.om.m_csr.get(), st.r_csr.get());
+  csr_to_csc(s, st.om, st.r_csr.get(), st.r_csc.get());
 
   double step = 1.0;
   SvtResult f;
   for (;;) {
-    OpMC G{&st.om, st.r_csr.get(), -step, m, n, kY, Yl.get(), Yr.get(), Lc.k};
+    OpMC G{&st.om, st.r_csr.get(), st.r_csc.get(), -step, m, n, kY, Yl.get(), Yr.get(), Lc.k};
     f = SvtResult{};
     svt_operator(s, G, step * st.mu, st.rank_hint, st.cur, f);
     if (!cfg_.line_search || step <= 0.125) break;

@@ -215,13 +215,14 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
   const int resident = gemm_resident<TA, TB, BM, BN, WM, WN>();
   const int gx = cdiv(N, BN), gy = cdiv(M, BM);
   const i64 tiles = (upper_only & 1) ? static_cast<i64>(gx) * (gx + 1) / 2 : static_cast<i64>(gx) * gy;
-  // Split K when the tiles alone do not fill the resident slots: among the split counts that
-  // keep >= 256 k per CTA, take the one whose CTA count best fills whole waves (ties and a 1%
+  // Split K when the tiles alone do not fill the resident slots: among the admissible split
+  // counts, take the one whose CTA count best fills whole waves (ties and a 1%
   // per-split workspace cost favour fewer splits).
   const i64 slots = static_cast<i64>(resident) * num_sms();
   int splits = 1;
   if (tiles < slots && K > 4 * BK) {
-    const int smax = static_cast<int>(std::max<i64>(1, std::min<i64>(16, K / 256)));
+    // >= 128 k per CTA, <= 128 splits, workspace <= 16 Mi doubles
+    const int smax = static_cast<int>(std::max<i64>(1, std::min<i64>({128, K / 128, (i64{1} << 24) / (M * N)})));
     double best = -1.0;
     for (int sp = 1; sp <= smax; ++sp) {
       const double w = static_cast<double>(tiles) * sp / slots;
@@ -374,22 +375,34 @@ __global__ void gather_cols_kernel(i64 rows, i64 ncols, const double* __restrict
   }
 }
 
-// One block per 32-column strip; threads stride rows; fixed-order combination.
-__global__ void col_norms_kernel(i64 rows, i64 cols, const double* __restrict__ src, i64 lds, double* out) {
-  __shared__ double part[8][33];
-  const int c = threadIdx.x & 31, rgrp = threadIdx.x >> 5;  // 8 row groups
+// One block per 32-column strip; 32 row groups with four independent accumulators each (the
+// loads of one thread stay in flight together); fixed-order combination.
+__global__ void __launch_bounds__(1024) col_norms_kernel(i64 rows, i64 cols, const double* __restrict__ src, i64 lds,
+                                                         double* out) {
+  __shared__ double part[32][33];
+  const int c = threadIdx.x & 31, rgrp = threadIdx.x >> 5;  // 32 row groups
   const i64 col = static_cast<i64>(blockIdx.x) * 32 + c;
-  double acc = 0.0;
-  if (col < cols)
-    for (i64 r = rgrp; r < rows; r += 8) {
-      const double v = src[r * lds + col];
-      acc += v * v;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (col < cols) {
+    i64 r = rgrp;
+    for (; r + 96 < rows; r += 128) {
+      const double v0 = src[r * lds + col], v1 = src[(r + 32) * lds + col], v2 = src[(r + 64) * lds + col],
+                   v3 = src[(r + 96) * lds + col];
+      a0 = fma(v0, v0, a0);
+      a1 = fma(v1, v1, a1);
+      a2 = fma(v2, v2, a2);
+      a3 = fma(v3, v3, a3);
     }
-  part[rgrp][c] = acc;
+    for (; r < rows; r += 32) {
+      const double v = src[r * lds + col];
+      a0 = fma(v, v, a0);
+    }
+  }
+  part[rgrp][c] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (rgrp == 0 && col < cols) {
     double s = 0.0;
-    for (int g = 0; g < 8; ++g) s += part[g][c];
+    for (int g = 0; g < 32; ++g) s += part[g][c];
     out[col] = sqrt(s);
   }
 }
@@ -475,7 +488,7 @@ void gather_cols(cudaStream_t s, i64 rows, i64 ncols, const double* src, i64 lds
 void col_norms(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* out) {
   if (cols <= 0) return;
   prof::Scope scope(prof::kReduce, s, 2.0 * rows * cols, 8.0 * rows * cols);
-  col_norms_kernel<<<cdiv(cols, 32), 256, 0, s>>>(rows, cols, src, lds, out);
+  col_norms_kernel<<<cdiv(cols, 32), 1024, 0, s>>>(rows, cols, src, lds, out);
   DFCG_LAUNCH_CHECK();
 }
 

@@ -86,14 +86,15 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
   double* dinv = psm + 2 * CNB * PLD + PB * PLD;                           // 1 / r_kk
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const unsigned full = 0xffffffffu;
-  for (int e = t; e < CNB * CNB; e += 256) {
-    const int r = e / CNB, c = e % CNB;
+  const int kbp = (kb + PB - 1) / PB * PB;  // micro-panels that hold real columns
+  for (int e = t; e < kbp * kbp; e += 256) {
+    const int r = e / kbp, c = e % kbp;
     A[r][c] = (r < kb && c < kb) ? (r <= c ? G[r * ldg + c] : 0.0) : (r == c ? 1.0 : 0.0);
     X[r][c] = 0.0;
   }
   const double thr = rel_tol * (*maxdiag);
   __syncthreads();
-  for (int c0 = 0; c0 < CNB; c0 += PB) {
+  for (int c0 = 0; c0 < kbp; c0 += PB) {
     if (warp == 0) {  // ---- factor the 8x8 diagonal micro-block
       const int j = lane & (PB - 1);
       double d[PB];
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
       }
     }
     __syncthreads();
-    const int c1 = c0 + PB, n2 = CNB - c1;
+    const int c1 = c0 + PB, n2 = kbp - c1;
     if (n2 == 0) break;
     if (t < n2) {  // ---- panel: R[c0:c1, c] = R_D^-T A[c0:c1, c]
       const int c = c1 + t;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
     __syncthreads();
   }
   // ---- inverse: diagonal micro-blocks (warp w -> block w; lane j -> column j)
-  {
+  if (PB * warp < kbp) {
     const int w0 = PB * warp, j = lane & (PB - 1);
     double x[PB];
 #pragma unroll
@@ -193,8 +194,8 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
   }
   __syncthreads();
   // ---- block back-substitution, bottom block row first
-  for (int I = CNB / PB - 2; I >= 0; --I) {
-    const int r0 = PB * I, cb = r0 + PB, nc = CNB - cb;
+  for (int I = kbp / PB - 2; I >= 0; --I) {
+    const int r0 = PB * I, cb = r0 + PB, nc = kbp - cb;
     for (int e = t; e < PB * nc; e += 256) {  // S = R[I, I+1:] X[I+1:, c]  (X upper: rows <= c)
       const int i = e / nc, c = cb + e % nc;
       double s0 = 0.0, s1 = 0.0;

@@ -14,6 +14,7 @@ namespace dfcg {
 namespace {
 
 constexpr int SEG = 64;
+constexpr int kSpmmCpl = 4;
 
 int pow2_at_least(i64 v) {
   int g = 1;
@@ -55,7 +56,7 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
   const i64 gid = ((static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * PER_WARP + lane / G;
   if (gid >= n_items) return;
   const SegItem it = items[gid];
-  constexpr int CPL = 4;  // columns per lane per pass: one walk of the segment covers 4 G columns
+  constexpr int CPL = kSpmmCpl;  // columns per lane per pass: one walk of the segment covers CPL G columns
   for (i64 c0 = 0; c0 < b; c0 += CPL * G) {
     double acc[CPL];
 #pragma unroll
@@ -68,7 +69,7 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         ix[u] = idx[e + u];
-        vv[u] = T ? vals[perm[e + u]] : vals[e + u];
+        vv[u] = perm ? vals[perm[e + u]] : vals[e + u];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -79,7 +80,7 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
       }
     }
     for (; e < it.e1; ++e) {
-      const double v = T ? vals[perm[e]] : vals[e];
+      const double v = perm ? vals[perm[e]] : vals[e];
       const double* x = X + static_cast<i64>(idx[e]) * ldx + c0 + lig;
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
@@ -357,7 +358,7 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
   if (om.nnz == 0) return;
   // algorithmic bytes: row+col index, M_e, r_e per entry + both factors once
   prof::Scope scope(prof::kSddmm, s, 2.0 * kY * om.nnz, 24.0 * om.nnz + 8.0 * (om.m + om.n) * kY);
-  if (om.ntc > 0 && kY >= SKC) {
+  if (om.ntc > 0) {
     static unsigned configured = 0;  // one bit per device
     int dev = 0;
     DFCG_CUDA(cudaGetDevice(&dev));
@@ -413,7 +414,7 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
 }
 
 void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals_csr, i64 b, double alpha,
-          const double* X, i64 ldx, double beta, double* out, i64 ldo) {
+          const double* X, i64 ldx, double beta, double* out, i64 ldo, const double* vals_csc) {
   const SegPlan& p = transpose ? om.plan_csc : om.plan_csr;
   const i64 out_rows = transpose ? om.n : om.m;
   if (b <= 0 || out_rows <= 0) return;
@@ -427,18 +428,22 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   if (p.n_items == 0) return;
   DBuf<double> ws;
   if (p.n_slots) ws.alloc(p.n_slots * b, s);
-  const int G = pow2_at_least(b);
+  // lanes per item: enough for one pass over the b columns at kSpmmCpl columns per lane
+  const int G = pow2_at_least((b + kSpmmCpl - 1) / kSpmmCpl);
   const i64 warps = (p.n_items + (32 / G) - 1) / (32 / G);
   const int blocks = static_cast<int>((warps + 7) / 8);
   const int* idx = transpose ? om.csc_row.get() : om.csr_col.get();
-  const long long* perm = om.csc2csr.get();
+  // the transposed walk streams CSC-ordered values when the caller has them, else it gathers
+  // the CSR values through the permutation (random 8-byte reads)
+  const double* vals = transpose && vals_csc ? vals_csc : vals_csr;
+  const long long* perm = transpose && !vals_csc ? om.csc2csr.get() : nullptr;
 #define SPMM_CASE(g)                                                                                               \
   case g:                                                                                                          \
     if (transpose)                                                                                                 \
-      spmm_kernel<g, true><<<blocks, 256, 0, s>>>(p.n_items, p.items.get(), idx, perm, vals_csr, b, alpha, X, ldx, \
+      spmm_kernel<g, true><<<blocks, 256, 0, s>>>(p.n_items, p.items.get(), idx, perm, vals, b, alpha, X, ldx,     \
                                                    beta, out, ldo, ws.get());                                      \
     else                                                                                                           \
-      spmm_kernel<g, false><<<blocks, 256, 0, s>>>(p.n_items, p.items.get(), idx, perm, vals_csr, b, alpha, X,     \
+      spmm_kernel<g, false><<<blocks, 256, 0, s>>>(p.n_items, p.items.get(), idx, perm, vals, b, alpha, X,         \
                                                     ldx, beta, out, ldo, ws.get());                                \
     break;
   switch (G) {
@@ -457,6 +462,20 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
                                                        beta, out, ldo);
     DFCG_LAUNCH_CHECK();
   }
+}
+
+__global__ void csr_to_csc_kernel(i64 N, const long long* __restrict__ csc2csr, const double* __restrict__ src,
+                                  double* __restrict__ dst) {
+  for (i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; t < N;
+       t += static_cast<i64>(gridDim.x) * blockDim.x)
+    dst[t] = src[csc2csr[t]];
+}
+
+void csr_to_csc(cudaStream_t s, const DevOmega& om, const double* vals_csr, double* vals_csc) {
+  if (om.nnz == 0) return;
+  prof::Scope scope(prof::kElementwise, s, 0.0, 24.0 * om.nnz);
+  csr_to_csc_kernel<<<grid_for(om.nnz), 256, 0, s>>>(om.nnz, om.csc2csr.get(), vals_csr, vals_csc);
+  DFCG_LAUNCH_CHECK();
 }
 
 void scatter_add_dense(cudaStream_t s, const DevOmega& om, const double* vals_csr, double alpha, double* D, i64 ldd) {

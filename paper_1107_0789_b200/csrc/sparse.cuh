@@ -55,8 +55,13 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
 //   transpose == false: S = R (m x n) via CSR, X is n x b, out is m x b.
 //   transpose == true : S = R^T (n x m) via CSC, X is m x b, out is n x b.
 // vals are always in CSR order (the CSC walk indexes them through csc2csr).
+// vals_csc (optional): the same values in CSC order; the transposed walk then streams them
+// instead of gathering vals_csr through the permutation.
 void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals_csr, i64 b, double alpha,
-          const double* X, i64 ldx, double beta, double* out, i64 ldo);
+          const double* X, i64 ldx, double beta, double* out, i64 ldo, const double* vals_csc = nullptr);
+
+// vals_csc[p] = vals_csr[csc2csr[p]]
+void csr_to_csc(cudaStream_t s, const DevOmega& om, const double* vals_csr, double* vals_csc);
 
 // D[i, j] += alpha * vals[(i,j)] for the observed pattern (row-major m x n dense D).
 void scatter_add_dense(cudaStream_t s, const DevOmega& om, const double* vals_csr, double alpha, double* D, i64 ldd);
