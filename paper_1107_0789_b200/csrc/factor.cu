@@ -68,61 +68,92 @@ __global__ void diag_max_kernel(i64 n, const double* G, i64 ldg, double* out) {
 //           column j in registers, pivots and row k of R broadcast by shuffles, no barriers);
 //   trsm    one thread per column right of the micro-panel solves R_D^T x = a (8 steps);
 //   update  4x4 register tiles apply the rank-8 update to the trailing upper triangle.
-// The inverse: warp w inverts diagonal micro-block w, then block back-substitution from the
-// bottom block row up, X[I][J] = -X_II sum_{L>I} R[I][L] X[L][J] (two barriers per block row).
-// 3 barriers per micro-panel + 14 for the inverse instead of one per pivot and inverse step
-// (128) in the previous single-level version; the pivot chain is shuffle latency only.
+// The inverse: warp w inverts diagonal micro-block w, then recursive doubling over block
+// pairs, X12 = -X11 (R12 X22), with all pairs of a level in parallel (6 barriers at kb = 64).
 // Pivots below rel_tol * maxdiag set *fail (the caller falls back to Householder QR).
 constexpr int PB = 8;  // micro-panel width
 constexpr int PLD = CNB + 1;
-constexpr size_t kPotrfSmem = sizeof(double) * (2 * CNB * PLD + PB * PLD + CNB);
+constexpr size_t kPotrfSmem = sizeof(double) * (2 * CNB * PLD + (CNB / 2) * PLD + CNB);
 
+#ifdef DFCG_POTRF_TRACE  // phase timestamps for tools/potrf_bench.cu
+__device__ long long g_potrf_trace[64];
+#define POTRF_STAMP(i)                \
+  if (threadIdx.x == 0) {             \
+    const long long now_ = clock64(); \
+    g_potrf_trace[i] += now_ - tp_;   \
+    tp_ = now_;                       \
+  }
+#else
+#define POTRF_STAMP(i)
+#endif
 __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr,
                                                          const double* maxdiag, double rel_tol, int* fail) {
   extern __shared__ double psm[];
+#ifdef DFCG_POTRF_TRACE
+  long long tp_ = clock64();
+#endif
   double(*A)[PLD] = reinterpret_cast<double(*)[PLD]>(psm);                // R (upper)
   double(*X)[PLD] = reinterpret_cast<double(*)[PLD]>(psm + CNB * PLD);    // R^-1 (upper)
-  double(*S)[PLD] = reinterpret_cast<double(*)[PLD]>(psm + 2 * CNB * PLD);  // block-row scratch
-  double* dinv = psm + 2 * CNB * PLD + PB * PLD;                           // 1 / r_kk
+  double(*S)[PLD] = reinterpret_cast<double(*)[PLD]>(psm + 2 * CNB * PLD);  // doubling scratch (CNB/2 rows)
+  double* dinv = psm + 2 * CNB * PLD + (CNB / 2) * PLD;                    // 1 / r_kk
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const unsigned full = 0xffffffffu;
   const int kbp = (kb + PB - 1) / PB * PB;  // micro-panels that hold real columns
-  for (int e = t; e < kbp * kbp; e += 256) {
-    const int r = e / kbp, c = e % kbp;
-    A[r][c] = (r < kb && c < kb) ? (r <= c ? G[r * ldg + c] : 0.0) : (r == c ? 1.0 : 0.0);
-    X[r][c] = 0.0;
+  {  // all loads first (unconditional, address clamped), then the stores: every load in flight
+    double v[CNB * CNB / 256];
+#pragma unroll
+    for (int it = 0; it < CNB * CNB / 256; ++it) {
+      const int e = t + 256 * it, r = e / CNB, c = e % CNB;
+      const bool ok = r < kb && c < kb && r <= c;
+      v[it] = G[ok ? r * ldg + c : 0];
+    }
+#pragma unroll
+    for (int it = 0; it < CNB * CNB / 256; ++it) {
+      const int e = t + 256 * it, r = e / CNB, c = e % CNB;
+      const bool ok = r < kb && c < kb && r <= c;
+      A[r][c] = ok ? v[it] : (r == c && r >= kb ? 1.0 : 0.0);
+      X[r][c] = 0.0;
+    }
   }
   const double thr = rel_tol * (*maxdiag);
   __syncthreads();
+  POTRF_STAMP(1)
   for (int c0 = 0; c0 < kbp; c0 += PB) {
     if (warp == 0) {  // ---- factor the 8x8 diagonal micro-block
-      const int j = lane & (PB - 1);
-      double d[PB];
+      // every lane factors the whole upper triangle in registers (no shuffles on the pivot
+      // chain); lane j < 8 then stores column j
+      double a[PB][PB], ipv[PB];
 #pragma unroll
-      for (int i = 0; i < PB; ++i) d[i] = i <= j ? A[c0 + i][c0 + j] : 0.0;
+      for (int i = 0; i < PB; ++i)
+#pragma unroll
+        for (int j = i; j < PB; ++j) a[i][j] = A[c0 + i][c0 + j];
 #pragma unroll
       for (int k = 0; k < PB; ++k) {
-        const double piv = __shfl_sync(full, d[k], k);
+        const double piv = a[k][k];
         const bool bad = c0 + k < kb && (!(piv > thr) || !isfinite(piv));
         const double pv = bad ? 1.0 : piv;
         const double ip = rsqrt_nr(pv);
-        if (lane == 0) {
-          dinv[c0 + k] = ip;
-          if (bad) atomicExch(fail, 1);
-        }
-        d[k] = j == k ? pv * ip : (j > k ? d[k] * ip : 0.0);  // row k of R
+        if (bad) *fail = 1;  // warp-uniform (every lane holds the same block)
+        a[k][k] = pv * ip;
+        ipv[k] = ip;
 #pragma unroll
-        for (int i = k + 1; i < PB; ++i) {
-          const double rki = __shfl_sync(full, d[k], i);
-          if (j >= i) d[i] = fma(-rki, d[k], d[i]);
-        }
+        for (int j = k + 1; j < PB; ++j) a[k][j] *= ip;
+#pragma unroll
+        for (int i = k + 1; i < PB; ++i)
+#pragma unroll
+          for (int j = i; j < PB; ++j) a[i][j] = fma(-a[k][i], a[k][j], a[i][j]);
       }
-      if (lane < PB) {
+      if (lane == 0) {  // one writer: stores are cheap next to divergent per-lane column writes
 #pragma unroll
-        for (int i = 0; i < PB; ++i) A[c0 + i][c0 + j] = d[i];
+        for (int i = 0; i < PB; ++i) dinv[c0 + i] = ipv[i];
+#pragma unroll
+        for (int i = 0; i < PB; ++i) {
+#pragma unroll
+          for (int j = i; j < PB; ++j) A[c0 + i][c0 + j] = a[i][j];
+        }
       }
     }
     __syncthreads();
+    POTRF_STAMP(6)
     const int c1 = c0 + PB, n2 = kbp - c1;
     if (n2 == 0) break;
     if (t < n2) {  // ---- panel: R[c0:c1, c] = R_D^-T A[c0:c1, c]
@@ -138,6 +169,7 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
       }
     }
     __syncthreads();
+    POTRF_STAMP(7)
     {  // ---- trailing update of the upper triangle (4x4 tiles, tile row <= tile column)
       const int nt = n2 / 4;
       for (int e = t; e < nt * nt; e += 256) {
@@ -168,7 +200,9 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
       }
     }
     __syncthreads();
+    POTRF_STAMP(8)
   }
+  POTRF_STAMP(2)
   // ---- inverse: diagonal micro-blocks (warp w -> block w; lane j -> column j)
   if (PB * warp < kbp) {
     const int w0 = PB * warp, j = lane & (PB - 1);
@@ -193,36 +227,55 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
     }
   }
   __syncthreads();
-  // ---- block back-substitution, bottom block row first
-  for (int I = kbp / PB - 2; I >= 0; --I) {
-    const int r0 = PB * I, cb = r0 + PB, nc = kbp - cb;
-    for (int e = t; e < PB * nc; e += 256) {  // S = R[I, I+1:] X[I+1:, c]  (X upper: rows <= c)
-      const int i = e / nc, c = cb + e % nc;
-      double s0 = 0.0, s1 = 0.0;
-      int l = cb;
-      for (; l + 1 <= c; l += 2) {
-        s0 = fma(A[r0 + i][l], X[l][c], s0);
-        s1 = fma(A[r0 + i][l + 1], X[l + 1][c], s1);
+  POTRF_STAMP(3)
+  // ---- recursive doubling: for each pair of adjacent s-blocks, X12 = -X11 (R12 X22)
+  // (two triangular products, all pairs of a level in parallel): 2 log2(kb/8) barriers
+  // instead of a sequential block back-substitution.
+  for (int s = PB; s < kbp; s *= 2) {
+    const int npairs = (kbp + 2 * s - 1) / (2 * s);
+    for (int e = t; e < npairs * s * s; e += 256) {  // T = R12 X22 (X22's lower part is zero)
+      const int q = e / (s * s), i = (e / s) % s, j = e % s;
+      const int a0 = 2 * q * s, b0 = a0 + s, s2 = min(s, kbp - b0);  // s2: multiple of 8
+      if (j >= s2) continue;
+      double s0 = 0.0, s1 = 0.0, s2a = 0.0, s3 = 0.0;
+      for (int k = 0; k < s2; k += PB) {
+#pragma unroll
+        for (int u = 0; u < PB; u += 4) {
+          s0 = fma(A[a0 + i][b0 + k + u], X[b0 + k + u][b0 + j], s0);
+          s1 = fma(A[a0 + i][b0 + k + u + 1], X[b0 + k + u + 1][b0 + j], s1);
+          s2a = fma(A[a0 + i][b0 + k + u + 2], X[b0 + k + u + 2][b0 + j], s2a);
+          s3 = fma(A[a0 + i][b0 + k + u + 3], X[b0 + k + u + 3][b0 + j], s3);
+        }
       }
-      if (l <= c) s0 = fma(A[r0 + i][l], X[l][c], s0);
-      S[i][c] = s0 + s1;
+      S[q * s + i][j] = (s0 + s1) + (s2a + s3);
     }
     __syncthreads();
-    for (int e = t; e < PB * nc; e += 256) {  // X[I, c] = -X_II S
-      const int i = e / nc, c = cb + e % nc;
-      double v = 0.0;
+    for (int e = t; e < npairs * s * s; e += 256) {  // X12 = -X11 T (X11's lower part is zero)
+      const int q = e / (s * s), i = (e / s) % s, j = e % s;
+      const int a0 = 2 * q * s, b0 = a0 + s, s2 = min(s, kbp - b0);
+      if (j >= s2) continue;
+      double s0 = 0.0, s1 = 0.0, s2a = 0.0, s3 = 0.0;
+      for (int k = 0; k < s; k += PB) {
 #pragma unroll
-      for (int k = 0; k < PB; ++k)
-        if (k >= i) v = fma(X[r0 + i][r0 + k], S[k][c], v);
-      X[r0 + i][c] = -v;
+        for (int u = 0; u < PB; u += 4) {
+          s0 = fma(X[a0 + i][a0 + k + u], S[q * s + k + u][j], s0);
+          s1 = fma(X[a0 + i][a0 + k + u + 1], S[q * s + k + u + 1][j], s1);
+          s2a = fma(X[a0 + i][a0 + k + u + 2], S[q * s + k + u + 2][j], s2a);
+          s3 = fma(X[a0 + i][a0 + k + u + 3], S[q * s + k + u + 3][j], s3);
+        }
+      }
+      X[a0 + i][b0 + j] = -((s0 + s1) + (s2a + s3));
     }
     __syncthreads();
   }
+  POTRF_STAMP(4)
   for (int e = t; e < kb * kb; e += 256) {
     const int r = e / kb, c = e % kb;
     G[r * ldg + c] = r <= c ? A[r][c] : 0.0;
     Rinv[r * ldr + c] = r <= c ? X[r][c] : 0.0;
   }
+  __syncthreads();
+  POTRF_STAMP(5)
 }
 
 __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
