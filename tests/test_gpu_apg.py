@@ -22,6 +22,9 @@ pytestmark = pytest.mark.gpu
     (100, 100, 3, 5000, 0.1, 2),   # randomized partial-SVD path (min(m,n) > 64)
     (80, 300, 4, 9000, 0.1, 3),    # wide block (m < n)
     (300, 70, 4, 8000, 0.1, 4),    # tall block, min(m,n) = 70
+    (120, 100, 2, 12000, 0.0, 5),  # fully observed exact rank 2 < b: rank-deficient sketches ->
+                                   # CholQR breakdown -> Householder fallback in the range finder
+    (130, 75, 3, 3000, 0.1, 9),    # ragged 64x64 SDDMM tiles in both directions
 ])
 def test_apg_mc_parity(m, n, r, s, sigma, seed):
     L0, obs = P.gen_mc_instance(m, n, r, s, sigma, seed)
