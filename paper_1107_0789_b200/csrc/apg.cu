@@ -198,6 +198,10 @@ double dev_dot(cudaStream_t s, i64 n, const double* a, const double* b) {
 }
 
 // ---------------------------------------------------------------- operators
+// Sketch buffers use an even leading dimension (b rounded up) so the DMMA GEMMs take their
+// 16-byte operand loads; the padding column is never read (K / N extents stay b).
+inline i64 even_ld(i64 b) { return b + (b & 1); }
+
 // FactoredSparseOp (solvers.hpp:112-136): G = left right^T + coeff * R.
 struct OpMC {
   const DevOmega* om;
@@ -205,36 +209,41 @@ struct OpMC {
   const double* r_csc;  // the same residual in CSC order (transposed products)
   double coeff;
   i64 m, w, kY;
-  const double* left;   // m x kY row-major (ld kY)
-  const double* right;  // w x kY row-major
+  const double* left;   // m x kY row-major (ld ldy)
+  const double* right;  // w x kY row-major (ld ldy)
   i64 kc;               // the first kc columns of `left` are L_curr's left factor
+  i64 ldy;
   i64 rows() const { return m; }
   i64 cols() const { return w; }
-  void apply(cudaStream_t s, const double* X, i64 b, double* out) const {  // X w x b -> out m x b
+  void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {  // w x b -> m x b
     if (kY > 0) {
-      DBuf<double> T(kY * b, s);
-      gemm(s, true, false, kY, b, w, 1.0, right, kY, X, b, 0.0, T.get(), b);
-      gemm(s, false, false, m, b, kY, 1.0, left, kY, T.get(), b, 0.0, out, b);
-      spmm(s, *om, false, r_csr, b, coeff, X, b, 1.0, out, b);
+      const i64 ldt = even_ld(b);
+      DBuf<double> T(kY * ldt, s);
+      gemm(s, true, false, kY, b, w, 1.0, right, ldy, X, ldx, 0.0, T.get(), ldt);
+      gemm(s, false, false, m, b, kY, 1.0, left, ldy, T.get(), ldt, 0.0, out, ldo);
+      spmm(s, *om, false, r_csr, b, coeff, X, ldx, 1.0, out, ldo);
     } else {
-      spmm(s, *om, false, r_csr, b, coeff, X, b, 0.0, out, b);
+      spmm(s, *om, false, r_csr, b, coeff, X, ldx, 0.0, out, ldo);
     }
   }
-  // keep (optional): receives T = left^T X (kY x b), whose first kc rows are L_curr.left^T X.
-  void apply_adjoint(cudaStream_t s, const double* X, i64 b, double* out, DBuf<double>* keep = nullptr) const {
+  // keep (optional): receives T = left^T X (kY x b, ld even_ld(b)), whose first kc rows are
+  // L_curr.left^T X.
+  void apply_adjoint(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo,
+                     DBuf<double>* keep = nullptr) const {
     if (kY > 0) {
-      DBuf<double> T(kY * b, s);
-      gemm(s, true, false, kY, b, m, 1.0, left, kY, X, b, 0.0, T.get(), b);
-      gemm(s, false, false, w, b, kY, 1.0, right, kY, T.get(), b, 0.0, out, b);
-      spmm(s, *om, true, r_csr, b, coeff, X, b, 1.0, out, b, r_csc);
+      const i64 ldt = even_ld(b);
+      DBuf<double> T(kY * ldt, s);
+      gemm(s, true, false, kY, b, m, 1.0, left, ldy, X, ldx, 0.0, T.get(), ldt);
+      gemm(s, false, false, w, b, kY, 1.0, right, ldy, T.get(), ldt, 0.0, out, ldo);
+      spmm(s, *om, true, r_csr, b, coeff, X, ldx, 1.0, out, ldo, r_csc);
       if (keep) *keep = std::move(T);
     } else {
-      spmm(s, *om, true, r_csr, b, coeff, X, b, 0.0, out, b, r_csc);
+      spmm(s, *om, true, r_csr, b, coeff, X, ldx, 0.0, out, ldo, r_csc);
     }
   }
   i64 keep_rows() const { return kc; }
   void to_dense(cudaStream_t s, double* D) const {  // m x w row-major
-    if (kY > 0) gemm(s, false, true, m, w, kY, 1.0, left, kY, right, kY, 0.0, D, w);
+    if (kY > 0) gemm(s, false, true, m, w, kY, 1.0, left, ldy, right, ldy, 0.0, D, w);
     else DFCG_CUDA(cudaMemsetAsync(D, 0, sizeof(double) * m * w, s));
     scatter_add_dense(s, *om, r_csr, coeff, D, w);
   }
@@ -246,11 +255,12 @@ struct OpDense {
   i64 m, w;
   i64 rows() const { return m; }
   i64 cols() const { return w; }
-  void apply(cudaStream_t s, const double* X, i64 b, double* out) const {
-    gemm(s, true, false, m, b, w, 1.0, At, m, X, b, 0.0, out, b);
+  void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    gemm(s, true, false, m, b, w, 1.0, At, m, X, ldx, 0.0, out, ldo);
   }
-  void apply_adjoint(cudaStream_t s, const double* X, i64 b, double* out, DBuf<double>* = nullptr) const {
-    gemm(s, false, false, w, b, m, 1.0, At, m, X, b, 0.0, out, b);
+  void apply_adjoint(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo,
+                     DBuf<double>* = nullptr) const {
+    gemm(s, false, false, w, b, m, 1.0, At, m, X, ldx, 0.0, out, ldo);
   }
   i64 keep_rows() const { return -1; }  // no factor Grams for a dense operator
   void to_dense(cudaStream_t s, double* D) const { transpose(s, w, m, At, m, D, w); }
@@ -321,56 +331,57 @@ template <class Op>
 bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor& cur, double tau, SvtResult& res) {
   const i64 m = op.rows(), w = op.cols();
   const i64 b = std::min(k + p, std::min(m, w));
+  const i64 bl = even_ld(b);  // leading dimension of every sketch-width buffer
   // gaussian_matrix(w, b): column-major draws == row-major b x w; transpose to w x b.
-  DBuf<double> Gt(b * w, s), G(w * b, s), X(m * b, s), Z(w * b, s);
+  DBuf<double> Gt(b * w, s), G(w * bl, s), X(m * bl, s), Z(w * bl, s);
   cur.cache->fetch(cur.pos, w * b, Gt.get(), s);
   cur.pos += w * b;
-  transpose(s, b, w, Gt.get(), w, G.get(), b);
-  op.apply(s, G.get(), b, X.get());
+  transpose(s, b, w, Gt.get(), w, G.get(), bl);
+  op.apply(s, G.get(), bl, b, X.get(), bl);
   // m-side bases are kept lazily: the orthonormal basis is Q = X M (M = R^-1 of a CholQR
   // factor of X), and M is applied on the n side after the next product, A^T Q = (A^T X) M,
   // so the m x b x b triangular products of the intermediate bases (and of the second
   // CholQR pass of the final one) are never formed. Intermediate bases need one CholQR pass
   // (same span, well conditioned); the final projector gets two. Any Cholesky breakdown
   // falls back to the explicit thin_qr (Householder), with M = I.
-  DBuf<double> M(b * b, s), Xt;
+  DBuf<double> M(b * bl, s), Xt;
   bool lazy = false;
   auto orth_m = [&](bool final_basis) {
     lazy = false;
-    if (!cholqr_factor(s, m, b, X.get(), b, M.get(), b)) {
-      thin_qr(s, m, b, X.get(), b, nullptr, 0, final_basis ? 2 : 1);
+    if (!cholqr_factor(s, m, b, X.get(), bl, M.get(), bl)) {
+      thin_qr(s, m, b, X.get(), bl, nullptr, 0, final_basis ? 2 : 1);
       return;
     }
     if (!final_basis) {
       lazy = true;
       return;
     }
-    Xt.alloc(m * b, s);  // pass 1 explicit: X <- X R1^-1; pass 2 lazy
-    gemm_upper_b(s, m, b, 1.0, X.get(), b, M.get(), b, 0.0, Xt.get(), b);
+    Xt.alloc(m * bl, s);  // pass 1 explicit: X <- X R1^-1; pass 2 lazy
+    gemm_upper_b(s, m, b, 1.0, X.get(), bl, M.get(), bl, 0.0, Xt.get(), bl);
     std::swap(X, Xt);
-    if (cholqr_factor(s, m, b, X.get(), b, M.get(), b)) lazy = true;
-    else thin_qr(s, m, b, X.get(), b, nullptr, 0, 1);
+    if (cholqr_factor(s, m, b, X.get(), bl, M.get(), bl)) lazy = true;
+    else thin_qr(s, m, b, X.get(), bl, nullptr, 0, 1);
   };
   auto adjoint = [&](DBuf<double>* keep) {  // Z = A^T Q
-    op.apply_adjoint(s, X.get(), b, Z.get(), keep);
+    op.apply_adjoint(s, X.get(), bl, b, Z.get(), bl, keep);
     if (lazy) {
-      DBuf<double> Zm(w * b, s);
-      gemm_upper_b(s, w, b, 1.0, Z.get(), b, M.get(), b, 0.0, Zm.get(), b);
+      DBuf<double> Zm(w * bl, s);
+      gemm_upper_b(s, w, b, 1.0, Z.get(), bl, M.get(), bl, 0.0, Zm.get(), bl);
       std::swap(Z, Zm);
     }
   };
   orth_m(q == 0);
   for (i64 it = 0; it < q; ++it) {
     adjoint(nullptr);
-    thin_qr(s, w, b, Z.get(), b, nullptr, 0, 1);
-    op.apply(s, Z.get(), b, X.get());
+    thin_qr(s, w, b, Z.get(), bl, nullptr, 0, 1);
+    op.apply(s, Z.get(), bl, b, X.get(), bl);
     orth_m(it + 1 == q);
   }
   DBuf<double> T;
-  adjoint(&T);  // Z = A^T Q (w x b); T = Yl^T X (before M) for the factor Grams
-  DBuf<double> Uz(w * b, s), Vz(b * b, s);
+  adjoint(&T);  // Z = A^T Q (w x b); T = Yl^T X (before M, ld bl) for the factor Grams
+  DBuf<double> Uz(w * bl, s), Vz(b * bl, s);
   std::vector<double> sv;
-  thin_svd(s, w, b, Z.get(), b, Uz.get(), b, Vz.get(), b, sv, tau);
+  thin_svd(s, w, b, Z.get(), bl, Uz.get(), bl, Vz.get(), bl, sv, tau);
   const i64 kk = std::min<i64>(k, static_cast<i64>(sv.size()));
   sv.resize(static_cast<size_t>(kk));
   if (!(kk < k || sv[static_cast<size_t>(kk - 1)] <= tau)) return false;
@@ -384,28 +395,28 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
   res.left.alloc(m * r, s);
   res.right.alloc(w * r, s);
   DBuf<double> MV;
-  const double* coef = Vz.get();  // b x r block (ld b) mapping X to the left factor
-  i64 ldcoef = b;
+  const double* coef = Vz.get();  // b x r block mapping X to the left factor
+  i64 ldcoef = bl;
   if (lazy) {
-    MV.alloc(b * r, s);
-    gemm(s, false, false, b, r, b, 1.0, M.get(), b, Vz.get(), b, 0.0, MV.get(), r);
+    ldcoef = even_ld(r);
+    MV.alloc(b * ldcoef, s);
+    gemm(s, false, false, b, r, b, 1.0, M.get(), bl, Vz.get(), bl, 0.0, MV.get(), ldcoef);
     coef = MV.get();
-    ldcoef = r;
   }
-  gemm(s, false, false, m, r, b, 1.0, X.get(), b, coef, ldcoef, 0.0, res.left.get(), r);
+  gemm(s, false, false, m, r, b, 1.0, X.get(), bl, coef, ldcoef, 0.0, res.left.get(), r);
   const i64 kc = op.keep_rows();
-  if (kc >= 0 && T.size() >= kc * b) {  // left = Q Vz_r: left^T left = Vz_r^T Vz_r, Lc.left^T left = T[:kc] coef
+  if (kc >= 0 && T.size() >= kc * bl) {  // left = Q Vz_r: left^T left = Vz_r^T Vz_r, Lc.left^T left = T[:kc] coef
     res.grams = true;
     res.ll.alloc(r * r, s);
-    gemm(s, true, false, r, r, b, 1.0, Vz.get(), b, Vz.get(), b, 0.0, res.ll.get(), r);
+    gemm(s, true, false, r, r, b, 1.0, Vz.get(), bl, Vz.get(), bl, 0.0, res.ll.get(), r);
     if (kc > 0) {
       res.lc.alloc(kc * r, s);
-      gemm(s, false, false, kc, r, b, 1.0, T.get(), b, coef, ldcoef, 0.0, res.lc.get(), r);
+      gemm(s, false, false, kc, r, b, 1.0, T.get(), bl, coef, ldcoef, 0.0, res.lc.get(), r);
     }
   }
   DBuf<double> sc(r, s);
   DFCG_CUDA(cudaMemcpyAsync(sc.get(), res.s.data(), sizeof(double) * r, cudaMemcpyHostToDevice, s));
-  scale_cols_kernel<<<grid_for(w * r), 256, 0, s>>>(w, r, Uz.get(), b, sc.get(), res.right.get(), r);
+  scale_cols_kernel<<<grid_for(w * r), 256, 0, s>>>(w, r, Uz.get(), bl, sc.get(), res.right.get(), r);
   DFCG_LAUNCH_CHECK();
   DFCG_CUDA(cudaStreamSynchronize(s));
   return true;
@@ -437,12 +448,15 @@ void svt_operator(cudaStream_t s, const Op& op, double tau, i64 rank_hint, Norma
 }
 
 // factored_inner (solvers.hpp:179-184): sum((a.l^T b.l) .* (a.r^T b.r)).
+// lda / ldb: leading dimensions of a's / b's factors (0: the rank)
 double factored_inner(cudaStream_t s, i64 m, i64 n, i64 ka, const double* al, const double* ar, i64 kb,
-                      const double* bl, const double* br) {
+                      const double* bl, const double* br, i64 lda = 0, i64 ldb = 0) {
   if (ka == 0 || kb == 0) return 0.0;
+  if (lda == 0) lda = ka;
+  if (ldb == 0) ldb = kb;
   DBuf<double> L(ka * kb, s), R(ka * kb, s);
-  gemm(s, true, false, ka, kb, m, 1.0, al, ka, bl, kb, 0.0, L.get(), kb);
-  gemm(s, true, false, ka, kb, n, 1.0, ar, ka, br, kb, 0.0, R.get(), kb);
+  gemm(s, true, false, ka, kb, m, 1.0, al, lda, bl, ldb, 0.0, L.get(), kb);
+  gemm(s, true, false, ka, kb, n, 1.0, ar, lda, br, ldb, 0.0, R.get(), kb);
   return dev_dot(s, ka * kb, L.get(), R.get());
 }
 
@@ -611,16 +625,17 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   const bool concat = !(beta == 0.0 || Lp.k == 0);
   const i64 kY = concat ? Lc.k + Lp.k : Lc.k;
   DBuf<double> Yl, Yr;
+  const i64 ldy = std::max<i64>(1, even_ld(kY));  // even: 16-byte GEMM operand loads
   if (kY > 0) {
-    Yl.alloc(m * kY, s);
-    Yr.alloc(n * kY, s);
+    Yl.alloc(m * ldy, s);
+    Yr.alloc(n * ldy, s);
     if (Lc.k > 0) {
-      copy2d(s, m, Lc.k, Lc.left.get(), Lc.k, Yl.get(), kY);
-      copy2d(s, n, Lc.k, Lc.right.get(), Lc.k, Yr.get(), kY, 1.0 + beta);
+      copy2d(s, m, Lc.k, Lc.left.get(), Lc.k, Yl.get(), ldy);
+      copy2d(s, n, Lc.k, Lc.right.get(), Lc.k, Yr.get(), ldy, 1.0 + beta);
     }
     if (concat) {
-      copy2d(s, m, Lp.k, Lp.left.get(), Lp.k, Yl.get() + Lc.k, kY);
-      copy2d(s, n, Lp.k, Lp.right.get(), Lp.k, Yr.get() + Lc.k, kY, -beta);
+      copy2d(s, m, Lp.k, Lp.left.get(), Lp.k, Yl.get() + Lc.k, ldy);
+      copy2d(s, n, Lp.k, Lp.right.get(), Lp.k, Yr.get() + Lc.k, ldy, -beta);
     }
   }
   // R = P_Omega(Y) - P_Omega(M) = (1+beta) P_Omega(L_curr) - beta P_Omega(L_prev) - P_Omega(M)
@@ -631,7 +646,7 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   double step = 1.0;
   SvtResult f;
   for (;;) {
-    OpMC G{&st.om, st.r_csr.get(), st.r_csc.get(), -step, m, n, kY, Yl.get(), Yr.get(), Lc.k};
+    OpMC G{&st.om, st.r_csr.get(), st.r_csc.get(), -step, m, n, kY, Yl.get(), Yr.get(), Lc.k, ldy};
     f = SvtResult{};
     svt_operator(s, G, step * st.mu, st.rank_hint, st.cur, f);
     if (!cfg_.line_search || step <= 0.125) break;
@@ -643,8 +658,8 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
     const double f_y = 0.5 * rr;
     const double lin = dev_dot(s, nnz, st.r_csr.get(), nd.get()) - rr;  // sum (y-m)(next-y)
     const double d2 = factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), f.r, f.left.get(), f.right.get()) -
-                      2.0 * factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), kY, Yl.get(), Yr.get()) +
-                      factored_inner(s, m, n, kY, Yl.get(), Yr.get(), kY, Yl.get(), Yr.get());
+                      2.0 * factored_inner(s, m, n, f.r, f.left.get(), f.right.get(), kY, Yl.get(), Yr.get(), 0, ldy) +
+                      factored_inner(s, m, n, kY, Yl.get(), Yr.get(), kY, Yl.get(), Yr.get(), ldy, ldy);
     const double dist2 = std::sqrt(std::max(0.0, d2));
     if (f_next <= f_y + lin + dist2 * dist2 / (2.0 * step) + 1e-12) break;
     step *= 0.5;

@@ -8,6 +8,7 @@
 #include "common.cuh"
 
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 
 namespace dfcg {
@@ -25,40 +26,68 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // Shared-memory operand tile of ROWS (M or N index) x BK (k).
 //   KMajor == false: [rows][k] with k contiguous, row stride BK + 4
 //   KMajor == true : [k][rows] with rows contiguous, k stride ROWS + 4
-// Both paddings make every DMMA fragment load a 2-wavefront (conflict-free) access.
+// Both paddings make every DMMA fragment load a 2-wavefront (conflict-free) access and keep
+// even positions 16-byte aligned. (An unpadded XOR-swizzled layout measured 4-20% slower.)
+// VEC: 16-byte cp.async (even leading dimension, 16-byte aligned base; a pair straddling the
+// matrix edge copies 8 bytes and zero-fills the rest), else 8-byte cp.async.
 template <bool KMajor, int ROWS>
 struct Tile {
   static constexpr int PAD_K = BK + 4, PAD_R = ROWS + 4;
   static constexpr int elems = KMajor ? BK * PAD_R : ROWS * PAD_K;
-  template <int THREADS>
+  __device__ __forceinline__ static int pos(int r, int k) { return KMajor ? k * PAD_R + r : r * PAD_K + k; }
+  template <int THREADS, bool VEC>
   __device__ __forceinline__ static void load(double* sm, const double* g, i64 ld, i64 r0, i64 k0, i64 R, i64 Kend,
                                               int tid) {
+    if (VEC) {
 #pragma unroll
-    for (int it = 0; it < (ROWS * BK) / THREADS; ++it) {
-      const int e = tid + it * THREADS;
-      if (!KMajor) {
-        const int r = e / BK, k = e % BK;
-        const i64 gr = r0 + r, gk = k0 + k;
-        const bool ok = gr < R && gk < Kend;
-        cp_async8(sm + r * PAD_K + k, ok ? g + gr * ld + gk : g, ok);
-      } else {
-        const int k = e / ROWS, r = e % ROWS;
-        const i64 gr = r0 + r, gk = k0 + k;
-        const bool ok = gr < R && gk < Kend;
-        cp_async8(sm + k * PAD_R + r, ok ? g + gk * ld + gr : g, ok);
+      for (int it = 0; it < (ROWS * BK) / (2 * THREADS); ++it) {
+        const int e = tid + it * THREADS;
+        int r, k;
+        i64 rem;
+        const double* src;
+        if (!KMajor) {
+          r = e / (BK / 2);
+          k = 2 * (e % (BK / 2));
+          const i64 gr = r0 + r, gk = k0 + k;
+          rem = gr < R ? Kend - gk : 0;
+          src = rem > 0 ? g + gr * ld + gk : g;
+        } else {
+          k = e / (ROWS / 2);
+          r = 2 * (e % (ROWS / 2));
+          const i64 gr = r0 + r, gk = k0 + k;
+          rem = gk < Kend ? R - gr : 0;
+          src = rem > 0 ? g + gk * ld + gr : g;
+        }
+        const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+        const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(sm + pos(r, k)));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(src), "r"(bytes));
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < (ROWS * BK) / THREADS; ++it) {
+        const int e = tid + it * THREADS;
+        if (!KMajor) {
+          const int r = e / BK, k = e % BK;
+          const i64 gr = r0 + r, gk = k0 + k;
+          const bool ok = gr < R && gk < Kend;
+          cp_async8(sm + pos(r, k), ok ? g + gr * ld + gk : g, ok);
+        } else {
+          const int k = e / ROWS, r = e % ROWS;
+          const i64 gr = r0 + r, gk = k0 + k;
+          const bool ok = gr < R && gk < Kend;
+          cp_async8(sm + pos(r, k), ok ? g + gk * ld + gr : g, ok);
+        }
       }
     }
   }
-  __device__ __forceinline__ static double frag(const double* sm, int r, int k) {
-    return KMajor ? sm[k * PAD_R + r] : sm[r * PAD_K + k];
-  }
+  __device__ __forceinline__ static double frag(const double* sm, int r, int k) { return sm[pos(r, k)]; }
 };
 
 // C tile BM x BN per CTA; warps in a (BM/WM) x (BN/WN) grid, each computing WM x WN with
 // (WM/8) x (WN/8) DMMA 8x8 accumulators.
 // A tile: !TA -> A(i,k) at A[i*lda+k] -> [rows][k]; TA -> A(i,k) at A[k*lda+i] -> [k][rows].
 // B tile: !TB -> B(k,j) at B[k*ldb+j] -> [k][rows]; TB -> B(k,j) at B[j*ldb+k] -> [rows][k].
-template <bool TA, bool TB, int BM, int BN, int WM, int WN>
+template <bool TA, bool TB, int BM, int BN, int WM, int WN, bool VEC>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     gemm_kernel(i64 M, i64 N, i64 K, i64 kchunk, double alpha, const double* __restrict__ A, i64 lda,
                 const double* __restrict__ B, i64 ldb, double beta, double* __restrict__ C, i64 ldc,
@@ -91,8 +120,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
     if (st < ntiles) {
-      TileA::template load<THREADS>(sA + st * TileA::elems, A, lda, m0, kbeg + st * BK, M, kend, tid);
-      TileB::template load<THREADS>(sB + st * TileB::elems, B, ldb, n0, kbeg + st * BK, N, kend, tid);
+      TileA::template load<THREADS, VEC>(sA + st * TileA::elems, A, lda, m0, kbeg + st * BK, M, kend, tid);
+      TileB::template load<THREADS, VEC>(sB + st * TileB::elems, B, ldb, n0, kbeg + st * BK, N, kend, tid);
     }
     cp_async_commit();
   }
@@ -105,9 +134,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
       const int nt = t + STAGES - 1;
       if (nt < ntiles) {
         const int st = nt % STAGES;
-        TileA::template load<THREADS>(sA + st * TileA::elems, A, lda, m0, kbeg + static_cast<i64>(nt) * BK, M,
+        TileA::template load<THREADS, VEC>(sA + st * TileA::elems, A, lda, m0, kbeg + static_cast<i64>(nt) * BK, M,
                                       kend, tid);
-        TileB::template load<THREADS>(sB + st * TileB::elems, B, ldb, n0, kbeg + static_cast<i64>(nt) * BK, N,
+        TileB::template load<THREADS, VEC>(sB + st * TileB::elems, B, ldb, n0, kbeg + static_cast<i64>(nt) * BK, N,
                                       kend, tid);
       }
       cp_async_commit();
@@ -187,7 +216,8 @@ int num_sms() {
   return g_num_sms;
 }
 
-// CTAs of one GEMM configuration resident per SM (configures the shared-memory opt-in once).
+// CTAs of one GEMM configuration resident per SM (configures the shared-memory opt-in of both
+// load variants once).
 template <bool TA, bool TB, int BM, int BN, int WM, int WN>
 int gemm_resident() {
   constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
@@ -197,11 +227,16 @@ int gemm_resident() {
   int dev = 0;
   DFCG_CUDA(cudaGetDevice(&dev));
   if (!(configured & (1u << dev))) {
-    DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, BM, BN, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    int r = 0;
-    DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, gemm_kernel<TA, TB, BM, BN, WM, WN>, THREADS, smem));
-    resident = std::max(1, r);
+    DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, BM, BN, WM, WN, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, BM, BN, WM, WN, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int r0 = 0, r1 = 0;
+    DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r0, gemm_kernel<TA, TB, BM, BN, WM, WN, false>, THREADS,
+                                                            smem));
+    DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, gemm_kernel<TA, TB, BM, BN, WM, WN, true>, THREADS,
+                                                            smem));
+    resident = std::max(1, std::min(r0, r1));
     configured |= 1u << dev;
   }
   return resident;
@@ -237,19 +272,25 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
   i64 kchunk = (K + splits - 1) / splits;
   kchunk = (kchunk + BK - 1) / BK * BK;
   splits = static_cast<int>((K + kchunk - 1) / kchunk);
-  if (splits <= 1) {
-    gemm_kernel<TA, TB, BM, BN, WM, WN><<<dim3(gx, gy, 1), THREADS, smem, s>>>(M, N, K, std::max<i64>(K, 1), alpha, A,
-                                                                               lda, B, ldb, beta, C, ldc, nullptr,
-                                                                               upper_only);
+  // 16-byte operand loads when both operands allow them
+  const bool vec = lda % 2 == 0 && ldb % 2 == 0 && reinterpret_cast<std::uintptr_t>(A) % 16 == 0 &&
+                   reinterpret_cast<std::uintptr_t>(B) % 16 == 0;
+  auto run = [&](dim3 grid, i64 kc, double* ws) {
+    if (vec)
+      gemm_kernel<TA, TB, BM, BN, WM, WN, true><<<grid, THREADS, smem, s>>>(M, N, K, kc, alpha, A, lda, B, ldb, beta, C,
+                                                                            ldc, ws, upper_only);
+    else
+      gemm_kernel<TA, TB, BM, BN, WM, WN, false><<<grid, THREADS, smem, s>>>(M, N, K, kc, alpha, A, lda, B, ldb, beta,
+                                                                             C, ldc, ws, upper_only);
     DFCG_LAUNCH_CHECK();
+  };
+  if (splits <= 1) {
+    run(dim3(gx, gy, 1), std::max<i64>(K, 1), nullptr);
     return;
   }
   DBuf<double> ws(static_cast<i64>(splits) * M * N, s);
   if (upper_only & 1) ws.zero(s);  // skipped tiles leave their partials unwritten
-  gemm_kernel<TA, TB, BM, BN, WM, WN><<<dim3(gx, gy, splits), THREADS, smem, s>>>(M, N, K, kchunk, alpha, A, lda, B,
-                                                                                  ldb, beta, C, ldc, ws.get(),
-                                                                                  upper_only);
-  DFCG_LAUNCH_CHECK();
+  run(dim3(gx, gy, splits), kchunk, ws.get());
   const int rb = static_cast<int>(std::min<i64>((M * N + 255) / 256, 4L * num_sms()));
   splitk_reduce<<<rb, 256, 0, s>>>(M, N, splits, ws.get(), alpha, beta, C, ldc);
   DFCG_LAUNCH_CHECK();
@@ -258,8 +299,9 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
 // Tile policy (measured on B200 with tools/gemm_bench against cuBLAS, profiles/r01_gemm_*):
 // DMMA throughput needs many resident warps more than large warp tiles — 64x64 CTAs of four
 // 32x32 warps (127 registers, 4 CTAs / 16 warps per SM) beat 128x128 CTAs of 64x32 warps
-// (225 registers, one CTA per SM) by ~25% on the APG shapes; tile width and split-K count are
-// chosen to fill whole waves of resident CTAs. DFCG_GEMM_VARIANT forces a configuration.
+// (225 registers, one CTA per SM) by ~25% on the APG shapes (profiles/r01_gemm_variants_*);
+// tile width and split-K count are
+// chosen to fill whole waves of resident CTAs. DFCG_GEMM_VARIANT=4|7 forces 64x64|64x48.
 template <bool TA, bool TB>
 void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
                  i64 ldb, double beta, double* C, i64 ldc, int upper_only) {
@@ -267,9 +309,7 @@ void launch_gemm(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double
 #define DFCG_GEMM_CFG(bm, bn, wm, wn) \
   launch_gemm_cfg<TA, TB, bm, bn, wm, wn>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, upper_only)
   switch (variant) {
-    case 1: DFCG_GEMM_CFG(128, 128, 64, 32); return;
     case 4: DFCG_GEMM_CFG(64, 64, 32, 32); return;
-    case 5: DFCG_GEMM_CFG(32, 64, 16, 32); return;
     case 7: DFCG_GEMM_CFG(64, 48, 32, 24); return;
     default: break;
   }

@@ -30,6 +30,8 @@ struct Shape {
 int main() {
   const Shape shapes[] = {
       {"Yl*T        NN 10000x720x1437", false, false, 10000, 720, 1437, 0},
+      {"Yl*T even   NN 10000x720x1438", false, false, 10000, 720, 1438, 0},
+      {"Yl^T*X even TN 1438x720x10000", true, false, 1438, 720, 10000, 0},
       {"Yl^T*X      TN 1437x720x10000", true, false, 1437, 720, 10000, 0},
       {"X*Rinv      NN 10000x720x720", false, false, 10000, 720, 720, 0},
       {"X*Rinv tri  NN 10000x720x720", false, false, 10000, 720, 720, 1},
