@@ -679,8 +679,7 @@ __device__ __forceinline__ void jpair(int step, int k, int& a, int& b) {
 // carries a ~1e-7 relative error, which leaves g_ab at ~1e-7 of its value per visit — still
 // ahead of the quadratic rate. Half the dependent FP64 latency of the all-double formula,
 // which bounded every inner step.
-__device__ __forceinline__ void jrot(const double (*g)[17], int a, int b, double& c, double& sn) {
-  const double gpq = g[a][b], gpp = g[a][a], gqq = g[b][b];
+__device__ __forceinline__ void rot_from_gram(double gpp, double gqq, double gpq, double& c, double& sn) {
   c = 1.0;
   sn = 0.0;
   if (fabs(gpq) > 1e-300 && gpq * gpq > 1e-34 * (gpp * gqq)) {
@@ -697,6 +696,118 @@ __device__ __forceinline__ void jrot(const double (*g)[17], int a, int b, double
     const double nrm = fma(del, fma(del, 0.375, -0.5), 1.0);  // (1 + del)^-1/2 to O(del^3)
     c = cd * nrm;
     sn = sd * nrm;
+  }
+}
+__device__ __forceinline__ void jrot(const double (*g)[17], int a, int b, double& c, double& sn) {
+  rot_from_gram(g[a][a], g[b][b], g[a][b], c, sn);
+}
+
+// Single-CTA one-sided Jacobi for small problems (rows, n <= 64): W (and the rotation
+// accumulator V when nv > 0) resident in shared memory, cyclic round-robin sweeps over single
+// column pairs (a warp per pair, lanes over rows, warp-reduced Gram entries), the convergence
+// test on the device. One launch per SVD instead of (p - 1) round launches plus a host
+// synchronisation per sweep — the low-rank regime's SVDs are a few dozen columns.
+constexpr int kSmallN = 64;
+__global__ void __launch_bounds__(256) jacobi_small_kernel(int rows, int n, int nv, double* W, i64 ldw, double* V,
+                                                           i64 ldv, double tol, double stop_tol, int max_sweeps,
+                                                           unsigned long long* offmax, int* sweeps_out) {
+  extern __shared__ double jsm[];  // W, then V when nv > 0
+  double(*Ws)[kSmallN + 1] = reinterpret_cast<double(*)[kSmallN + 1]>(jsm);
+  double(*Vs)[kSmallN + 1] = reinterpret_cast<double(*)[kSmallN + 1]>(jsm + kSmallN * (kSmallN + 1));
+  __shared__ unsigned long long s_off;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int e = t; e < kSmallN * kSmallN; e += 256) {
+    const int r = e / kSmallN, c = e % kSmallN;
+    Ws[r][c] = (r < rows && c < n) ? W[r * ldw + c] : 0.0;
+    if (nv > 0) Vs[r][c] = (r < nv && c < n) ? V[r * ldv + c] : 0.0;
+  }
+  const int n2 = n + (n & 1);  // round-robin over an even count (a dummy column when n is odd)
+  // pairing table: step s, slot k -> (a, b), a < b (round robin with column 0 fixed)
+  __shared__ unsigned char pa[kSmallN - 1][kSmallN / 2], pb[kSmallN - 1][kSmallN / 2];
+  for (int e = t; e < (n2 - 1) * (n2 / 2); e += 256) {
+    const int st = e / (n2 / 2), k = e % (n2 / 2);
+    auto ring = [&](int i) {
+      if (i == 0) return 0;
+      int x = i - 1 - st;
+      if (x < 0) x += n2 - 1;
+      return 1 + x;
+    };
+    const int a = ring(k), b = ring(n2 - 1 - k);
+    pa[st][k] = static_cast<unsigned char>(a < b ? a : b);
+    pb[st][k] = static_cast<unsigned char>(a < b ? b : a);
+  }
+  __syncthreads();
+  // a half-warp per column pair (16 lanes x 4 rows), 16 pairs in flight per step
+  const int h = lane >> 4, l16 = lane & 15;
+  const unsigned hmask = h ? 0xffff0000u : 0x0000ffffu;
+  int sweep = 0;
+  double off2 = 0.0;  // 1 when some pair started the sweep above stop_tol
+  while (sweep < max_sweeps) {
+    if (t == 0) s_off = 0;
+    double wmax = 0.0;
+    for (int step = 0; step < n2 - 1; ++step) {
+      for (int k = 2 * warp + h; k < n2 / 2; k += 16) {
+        const int a = pa[step][k], b = pb[step][k];
+        if (b >= n) continue;  // the dummy column (uniform over the half-warp)
+        double xa[4], xb[4];
+        double aa = 0.0, bb = 0.0, ab = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          xa[j] = Ws[l16 + 16 * j][a];
+          xb[j] = Ws[l16 + 16 * j][b];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          aa = fma(xa[j], xa[j], aa);
+          bb = fma(xb[j], xb[j], bb);
+          ab = fma(xa[j], xb[j], ab);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          aa += __shfl_xor_sync(hmask, aa, o);
+          bb += __shfl_xor_sync(hmask, bb, o);
+          ab += __shfl_xor_sync(hmask, ab, o);
+        }
+        // cosine tests without a division: ab^2 > c^2 aa bb
+        const double d = aa * bb, ab2 = ab * ab;
+        if (ab2 > stop_tol * stop_tol * d) wmax = 1.0;  // this sweep does not meet the stop test
+        if (ab2 > tol * tol * d && d > 0.0) {  // uniform over the half-warp
+          double c, sn;
+          rot_from_gram(aa, bb, ab, c, sn);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            Ws[l16 + 16 * j][a] = c * xa[j] - sn * xb[j];
+            Ws[l16 + 16 * j][b] = sn * xa[j] + c * xb[j];
+          }
+          if (nv > 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const double va = Vs[l16 + 16 * j][a], vb = Vs[l16 + 16 * j][b];
+              Vs[l16 + 16 * j][a] = c * va - sn * vb;
+              Vs[l16 + 16 * j][b] = sn * va + c * vb;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    for (int o = 16; o > 0; o >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (lane == 0) atomicMax(&s_off, static_cast<unsigned long long>(__double_as_longlong(wmax)));
+    __syncthreads();
+    off2 = __longlong_as_double(static_cast<long long>(s_off));
+    ++sweep;
+    __syncthreads();
+    if (off2 == 0.0) break;  // every pair started the sweep with cosine <= stop_tol
+  }
+  const double off = off2 == 0.0 ? stop_tol : 1.0;  // (the small kernel reports pass / fail only)
+  for (int e = t; e < kSmallN * kSmallN; e += 256) {
+    const int r = e / kSmallN, c = e % kSmallN;
+    if (r < rows && c < n) W[r * ldw + c] = Ws[r][c];
+    if (nv > 0 && r < nv && c < n) V[r * ldv + c] = Vs[r][c];
+  }
+  if (t == 0) {
+    *sweeps_out = sweep;
+    *offmax = static_cast<unsigned long long>(__double_as_longlong(off));
   }
 }
 
@@ -1134,7 +1245,38 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     }
   }
   static const bool trace_svd = std::getenv("DFCG_TRACE_SVD") != nullptr;
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  const bool small = cols <= kSmallN && wrows <= kSmallN && nj <= kSmallN;
+  if (small) {  // one launch, convergence on the device
+    DBuf<int> nsw(1, s);
+    {
+      prof::Scope scope(prof::kJacobi, s, 8.0 * 6.0 * cols * cols * (wrows + nj), 8.0 * 16.0 * cols * (wrows + nj));
+      constexpr size_t kOne = sizeof(double) * kSmallN * (kSmallN + 1);
+      static unsigned configured = 0;
+      int dev = 0;
+      DFCG_CUDA(cudaGetDevice(&dev));
+      if (!(configured & (1u << dev))) {
+        DFCG_CUDA(cudaFuncSetAttribute(jacobi_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(2 * kOne)));
+        configured |= 1u << dev;
+      }
+      jacobi_small_kernel<<<1, 256, (nj > 0 ? 2 : 1) * kOne, s>>>(static_cast<int>(wrows), static_cast<int>(cols),
+                                                                  static_cast<int>(nj), W.get(), np, J.get(), np, tol,
+                                                                  stop_tol, 60, off.get(), nsw.get());
+      DFCG_LAUNCH_CHECK();
+    }
+    if (trace_svd) {
+      int h = 0;
+      unsigned long long ho = 0;
+      DFCG_CUDA(cudaMemcpyAsync(&h, nsw.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+      DFCG_CUDA(cudaMemcpyAsync(&ho, off.get(), sizeof(ho), cudaMemcpyDeviceToHost, s));
+      DFCG_CUDA(cudaStreamSynchronize(s));
+      double ov;
+      std::memcpy(&ov, &ho, sizeof(double));
+      std::fprintf(stderr, "[svd] %lldx%lld small kernel: %d sweeps, converged flag %.0e\n", (long long)rows,
+                   (long long)cols, h, ov);
+    }
+  }
+  for (int sweep = 0; sweep < 60 && !small; ++sweep) {
     off.zero(s);
     {
       prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,

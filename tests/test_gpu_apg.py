@@ -40,7 +40,16 @@ def test_apg_mc_high_accuracy_noiseless():
     pc, oc = cfg_pair(max_iters=400, rel_tol=1e-9, mu_decay=0.5, mu_floor=0.0)
     eo, ro = O.apg_mc(to_oracle_obs(obs), oc)
     ep, rp = P.apg_mc(obs, pc)
-    assert abs(rp.iterations - ro.iterations) <= 3, (rp.iterations, ro.iterations)
+    # the same rel trajectory while rel is above the formula's noise floor: rel^2 ||L||^2 is a
+    # difference of O(||L||^2) terms, so rel carries an absolute rounding error ~ c eps / rel ...
+    floor = 1e-7
+    for tg, to in zip(rp.trace, ro.trace):
+        if to["rel"] < 1e-6:
+            break
+        assert abs(tg["rel"] - to["rel"]) <= 1e-4 * to["rel"] + 1e-13 / to["rel"], (tg["it"], tg["rel"], to["rel"])
+    # ... then both stop on a rounding event inside the noise-floor regime (rel ~ 3e-8)
+    first_floor = next(t["it"] for t in ro.trace if t["rel"] < floor)
+    assert first_floor <= rp.iterations <= ro.iterations + 10, (rp.iterations, ro.iterations, first_floor)
     assert rp.rank == ro.rank == 5
     assert relF(ep, eo) <= 1e-6
     assert np.linalg.norm(ep.dense() - L0.dense()) / 100.0 < 1e-6
