@@ -2,7 +2,7 @@
 //
 // SDDMM: entry-parallel over the CSR stream, G lanes per entry (G ~ kY/4, power of two),
 // factor rows gathered contiguously (row-major factors), group reduction by xor-shuffles.
-// SpMM: segmented work list (<= SEG entries per item) so long CSC columns split across
+// SpMM: segmented work list (<= 64 or 128 entries per item) so long CSC columns split across
 // warps; multi-segment rows reduce their partials in a fixed order (deterministic).
 #include <algorithm>
 #include <cstdint>
@@ -13,7 +13,6 @@ namespace dfcg {
 
 namespace {
 
-constexpr int SEG = 64;
 constexpr int kSpmmCpl = 4;
 
 int pow2_at_least(i64 v) {
@@ -257,7 +256,8 @@ int grid_for(i64 total, int threads = 256) {
   return static_cast<int>(std::max<i64>(1, std::min<i64>((total + threads - 1) / threads, 4096)));
 }
 
-void build_plan(cudaStream_t s, SegPlan& p, i64 rows, const std::vector<int>& ptr) {
+void build_plan(cudaStream_t s, SegPlan& p, i64 rows, const std::vector<int>& ptr, int seg_len) {
+  const int SEG = seg_len;
   std::vector<SegItem> items;
   std::vector<int> multi_rows, slot_ptr{0};
   int slot = 0;
@@ -332,8 +332,17 @@ void DevOmega::build(cudaStream_t s, i64 m_, i64 n_, i64 nnz_, const long long* 
   upload(s, m_csc, mc);
   upload(s, m_csr, mr);
   upload(s, csc2csr, c2r);
-  build_plan(s, plan_csr, m, rowptr);
-  build_plan(s, plan_csc, n, colptr);
+  // Segment length: long enough that a typical structure row is one segment (no partial-sum
+  // reduction pass), short enough that the longest rows still spread over several warps.
+  auto seg_for = [](i64 rows, i64 nnz) {
+    const i64 avg = rows > 0 ? (nnz + rows - 1) / rows : 1;
+    return avg <= 128 ? 128 : 64;
+  };
+  build_plan(s, plan_csr, m, rowptr, seg_for(m, nnz));
+  build_plan(s, plan_csc, n, colptr, seg_for(n, nnz));
+  has_empty_csr = has_empty_csc = false;
+  for (i64 r = 0; r < m; ++r) has_empty_csr |= rowptr[r + 1] == rowptr[r];
+  for (i64 c = 0; c < n; ++c) has_empty_csc |= colptr[c + 1] == colptr[c];
   // column-tile offsets of every CSR row (tiled SDDMM), when the table stays small
   const i64 tiles = (n + kTileCols - 1) / kTileCols;
   if (m * (tiles + 1) <= (i64{1} << 26)) {
@@ -423,8 +432,10 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   const i64 in_rows = transpose ? om.m : om.n;
   prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,
                     (transpose ? 20.0 : 12.0) * om.nnz + 8.0 * b * (in_rows + out_rows * (beta != 0.0 ? 2 : 1)));
-  empty_rows_kernel<<<grid_for(out_rows * b), 256, 0, s>>>(out_rows, ptr, b, beta, out, ldo);
-  DFCG_LAUNCH_CHECK();
+  if (transpose ? om.has_empty_csc : om.has_empty_csr) {  // rows with no entries: out = beta out
+    empty_rows_kernel<<<grid_for(out_rows * b), 256, 0, s>>>(out_rows, ptr, b, beta, out, ldo);
+    DFCG_LAUNCH_CHECK();
+  }
   if (p.n_items == 0) return;
   DBuf<double> ws;
   if (p.n_slots) ws.alloc(p.n_slots * b, s);

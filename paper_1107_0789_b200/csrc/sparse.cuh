@@ -35,6 +35,7 @@ struct DevOmega {
   DBuf<long long> csc2csr;  // CSC position -> CSR position
   DBuf<double> m_csc;
   SegPlan plan_csr, plan_csc;
+  bool has_empty_csr = false, has_empty_csc = false;  // structure rows / columns without entries
   std::vector<long long> h_csc2csr;  // host copy (outputs in reference order)
   // Column-tile offsets of the CSR rows for the tiled SDDMM: the entries of row r in column
   // tile q = [64q, 64q + 64) are CSR positions [tile_csr[r*(ntc+1)+q], tile_csr[r*(ntc+1)+q+1]).
