@@ -340,10 +340,16 @@ def main():
     # basis broadcast + per-rank projection + row gather over NCCL when N > 1
     ests = {g: solvers[g].finish()[0] for g in mine}
     barrier()
+    P.prof_enable(True)
     t0 = time.perf_counter()
     combine(P, dist, groups, ests, wl, local)
     barrier()
     combine_ms = 1e3 * (time.perf_counter() - t0)
+    cprof = P.prof_collect()
+    P.prof_enable(False)
+    combine_ops = {k: dict(ms=round(v["ms"], 3), launches=v["launches"],
+                           tflops=round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3))
+                   for k, v in cprof.items() if v["launches"] > 0}
     for sv in solvers.values():
         sv.close()
 
@@ -413,7 +419,11 @@ def main():
                                 blocks_per_gpu=len(mine), l2="inputs > L2 (no flush)",
                                 parallelism=f"{wl['t']} blocks over {world} GPU(s), one CUDA stream per block"),
                     roofline=roof, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
-                    clocks=clocks.summary(), combine_ms=combine_ms, lowrank=lowrank)
+                    clocks=clocks.summary(), combine_ms=combine_ms,
+                    combine=dict(ms=combine_ms, device_ops=combine_ops,
+                                 note="DFC-Proj column_project of the 8 block estimates (host factors in and out; "
+                                      "device_ops = CUDA-event time per op class on this rank)"),
+                    lowrank=lowrank)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

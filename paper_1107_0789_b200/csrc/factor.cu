@@ -289,8 +289,8 @@ __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
 
 // In-place blocked Cholesky of G (n x n) -> upper R (lower part zeroed); Rinv = R^-1.
 // want_inverse == false: only R is produced (Rinv then holds just the diagonal-block inverses).
-void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol, int* fail,
-                      bool want_inverse = true) {
+void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol,
+                          int* fail, bool want_inverse) {
   static unsigned configured = 0;  // one bit per device: opt in to > 48 KB dynamic shared memory
   int dev = 0;
   DFCG_CUDA(cudaGetDevice(&dev));
@@ -331,6 +331,60 @@ void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i
       gemm(s, false, false, j0, jb, jb, -1.0, T.get(), jb, Rinv + j0 * ldr + j0, ldr, 0.0, Rinv + j0, ldr);
     }
   }
+}
+
+// Diagonal scaling for the Cholesky of a Gram: d = sqrt(diag G) (zero pivots keep d = 1), then
+// G <- D^-1 G D^-1 on the upper part (two kernels: the diagonal is read before it is rescaled)
+__global__ void gram_diag_kernel(i64 n, const double* G, i64 ldg, double* d) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const double g = G[i * ldg + i];
+    d[i] = g > 0.0 ? sqrt(g) : 1.0;
+  }
+}
+__global__ void gram_scale_kernel(i64 n, double* G, i64 ldg, const double* d) {
+  const i64 total = n * n;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = e / n, j = e % n;
+    if (i <= j) G[i * ldg + j] = G[i * ldg + j] / (d[i] * d[j]);
+  }
+}
+// R' -> R' D (columns, upper part), Rinv' -> D^-1 Rinv' (rows)
+__global__ void chol_unscale_kernel(i64 n, double* R, i64 ldg, double* Rinv, i64 ldr, const double* d, int inv) {
+  const i64 total = n * n;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = e / n, j = e % n;
+    if (i > j) continue;
+    R[i * ldg + j] *= d[j];
+    if (inv) Rinv[i * ldr + j] /= d[i];
+  }
+}
+
+// Cholesky of a Gram matrix, R^T R = G, with the inverse: the Gram is first scaled to unit
+// diagonal (Jacobi preconditioning, G' = D^-1 G D^-1, R = R' D, R^-1 = D^-1 R'^-1), so the
+// breakdown test (pivot < rel_tol * max pivot) fires on ill-conditioning of the column
+// directions only, not on column scaling — an SVT factor V diag(s), whose singular values span
+// many decades, stays on the CholQR path instead of the Householder fallback.
+// scale == false keeps the raw breakdown test (pivot < rel_tol * max diag G): it then also
+// certifies cond(X) < ~3e5, which the Gram-based R of thin_svd relies on for accuracy.
+void cholesky_inverse(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol, int* fail,
+                      bool want_inverse = true, bool scale = true) {
+  if (n <= 0) return;
+  static const int scale_mode = std::getenv("DFCG_CHOL_SCALE") ? std::atoi(std::getenv("DFCG_CHOL_SCALE")) : 1;
+  if (!scale || scale_mode == 0) {
+    cholesky_inverse_raw(s, n, G, ldg, Rinv, ldr, rel_tol, fail, want_inverse);
+    return;
+  }
+  DBuf<double> d(n, s);
+  gram_diag_kernel<<<grid_for(n), 256, 0, s>>>(n, G, ldg, d.get());
+  DFCG_LAUNCH_CHECK();
+  gram_scale_kernel<<<grid_for(n * n), 256, 0, s>>>(n, G, ldg, d.get());
+  DFCG_LAUNCH_CHECK();
+  cholesky_inverse_raw(s, n, G, ldg, Rinv, ldr, rel_tol, fail, want_inverse);
+  chol_unscale_kernel<<<grid_for(n * n), 256, 0, s>>>(n, G, ldg, Rinv, ldr, d.get(), want_inverse ? 1 : 0);
+  DFCG_LAUNCH_CHECK();
 }
 
 // ================================================================ Householder QR (fallback)
@@ -1201,7 +1255,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     DBuf<double> Rinv(cols * cols, s);
     fail.zero(s);
     gram_upper(s, rows, cols, Qx.get(), cols, R.get(), cols);
-    cholesky_inverse(s, cols, R.get(), cols, Rinv.get(), cols, 1e-11, fail.get(), false);
+    cholesky_inverse(s, cols, R.get(), cols, Rinv.get(), cols, 1e-11, fail.get(), false, false);
     int h_fail = 0;
     DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     DFCG_CUDA(cudaStreamSynchronize(s));
