@@ -123,7 +123,7 @@ def roofline_entry(prof, peaks, peak_kind):
     name, v = max(ops.items(), key=lambda kv: kv[1]["ms"])
     per_launch_ms = v["ms"] / v["launches"]
     share = v["ms"] / sum(x["ms"] for x in ops.values())
-    if name in ("gemm", "jacobi", "cholesky", "qr_fallback"):
+    if name in ("gemm", "gemm_small", "jacobi", "cholesky", "qr_fallback"):
         achieved = v["flops"] / (v["ms"] * 1e-3) / 1e12
         peak = FP64_DMMA_PEAK_TFLOPS
         entry = dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",

@@ -39,9 +39,10 @@ int dfcg_gen_rmf_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sig
                           double lo, double hi, dfcg_lowrank* L0, dfcg_sparse* S0, double* M);
 
 /* ---- kernel accounting (bench / profiling; off by default) ---------------------------
- * Op classes, in order: 0 gemm, 1 sddmm, 2 spmm, 3 cholesky, 4 qr_fallback, 5 jacobi,
- * 6 elementwise, 7 reduce, 8 other. dfcg_prof_enable clears previous records. */
-#define DFCG_PROF_NUM_OPS 9
+ * Op classes, in order: 0 gemm (>= 2 GFLOP), 1 sddmm, 2 spmm, 3 cholesky, 4 qr_fallback,
+ * 5 jacobi, 6 elementwise, 7 reduce, 8 other, 9 gemm_small (< 2 GFLOP).
+ * dfcg_prof_enable clears previous records. */
+#define DFCG_PROF_NUM_OPS 10
 void dfcg_prof_enable(int on);
 int64_t dfcg_launch_count(void);
 /* Per op class: launches, summed CUDA-event ms, algorithmic FLOPs and bytes. Returns the

@@ -93,41 +93,54 @@ double* dup_array(const std::vector<double>& v) {
   return p;
 }
 
-// LowRankEstimate ctor validation (matrix_io.hpp:73-84) on a host estimate.
-HostLowRank from_c(const dfcg_lowrank* e) {
-  if (!e) throw std::invalid_argument("LowRankEstimate: null estimate");
-  HostLowRank h;
-  h.m = e->m;
-  h.n = e->n;
-  h.k = e->k;
-  if (h.m < 1 || h.n < 1) throw std::invalid_argument("LowRankEstimate: dims must be positive");
-  if (h.k < 0 || h.k > std::min(h.m, h.n)) throw std::invalid_argument("LowRankEstimate: k exceeds min(m, n)");
-  h.left.assign(e->left, e->left + h.m * h.k);
-  h.right.assign(e->right, e->right + h.n * h.k);
-  for (double v : h.left)
-    if (!std::isfinite(v)) throw std::invalid_argument("LowRankEstimate: non-finite factor entry");
-  for (double v : h.right)
-    if (!std::isfinite(v)) throw std::invalid_argument("LowRankEstimate: non-finite factor entry");
-  return h;
-}
-
-void to_c(const HostLowRank& h, dfcg_lowrank* out) {
-  out->m = h.m;
-  out->n = h.n;
-  out->k = h.k;
-  out->left = dup_array(h.left);
-  out->right = dup_array(h.right);
-}
-
+// Device estimate -> caller-owned (malloc) column-major factors: transposed on the device,
+// copied straight into the output arrays (no intermediate host copies).
 void to_c(cudaStream_t s, const DevLowRank& d, dfcg_lowrank* out) {
-  HostLowRank h;
-  download_lowrank(s, d, h);
-  to_c(h, out);
+  out->m = d.m;
+  out->n = d.n;
+  out->k = d.k;
+  const size_t nl = static_cast<size_t>(d.m * d.k), nr = static_cast<size_t>(d.n * d.k);
+  out->left = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(1, nl)));
+  out->right = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(1, nr)));
+  if (!out->left || !out->right) {
+    std::free(out->left);
+    std::free(out->right);
+    out->left = out->right = nullptr;
+    throw std::bad_alloc();
+  }
+  if (d.k == 0) return;
+  DBuf<double> tl(d.m * d.k, s), tr(d.n * d.k, s);
+  transpose(s, d.m, d.k, d.left.get(), d.k, tl.get(), d.m);
+  transpose(s, d.n, d.k, d.right.get(), d.k, tr.get(), d.n);
+  DFCG_CUDA(cudaMemcpyAsync(out->left, tl.get(), sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaMemcpyAsync(out->right, tr.get(), sizeof(double) * nr, cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
 }
 
+// Caller's column-major estimate -> device (row-major): validated in place (LowRankEstimate
+// ctor, matrix_io.hpp:73-84), uploaded straight from the caller's arrays.
 DevLowRank to_dev(cudaStream_t s, const dfcg_lowrank* e) {
+  if (!e) throw std::invalid_argument("LowRankEstimate: null estimate");
+  if (e->m < 1 || e->n < 1) throw std::invalid_argument("LowRankEstimate: dims must be positive");
+  if (e->k < 0 || e->k > std::min(e->m, e->n)) throw std::invalid_argument("LowRankEstimate: k exceeds min(m, n)");
+  const i64 nl = e->m * e->k, nr = e->n * e->k;
+  for (i64 i = 0; i < nl; ++i)
+    if (!std::isfinite(e->left[i])) throw std::invalid_argument("LowRankEstimate: non-finite factor entry");
+  for (i64 i = 0; i < nr; ++i)
+    if (!std::isfinite(e->right[i])) throw std::invalid_argument("LowRankEstimate: non-finite factor entry");
   DevLowRank d;
-  upload_lowrank(s, from_c(e), d);
+  d.m = e->m;
+  d.n = e->n;
+  d.k = e->k;
+  if (e->k == 0) return d;
+  DBuf<double> tl(nl, s), tr(nr, s);
+  d.left.alloc(nl, s);
+  d.right.alloc(nr, s);
+  DFCG_CUDA(cudaMemcpyAsync(tl.get(), e->left, sizeof(double) * nl, cudaMemcpyHostToDevice, s));
+  DFCG_CUDA(cudaMemcpyAsync(tr.get(), e->right, sizeof(double) * nr, cudaMemcpyHostToDevice, s));
+  transpose(s, e->k, e->m, tl.get(), e->m, d.left.get(), e->k);  // column-major m x k == row-major k x m
+  transpose(s, e->k, e->n, tr.get(), e->n, d.right.get(), e->k);
+  DFCG_CUDA(cudaStreamSynchronize(s));
   return d;
 }
 

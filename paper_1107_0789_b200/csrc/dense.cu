@@ -456,7 +456,7 @@ int grid_for(i64 total, int threads = 256) {
 void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc) {
   if (M <= 0 || N <= 0) return;
-  prof::Scope scope(prof::kGemm, s, 2.0 * M * N * K,
+  prof::Scope scope(2.0 * M * N * K >= 2e9 ? prof::kGemm : prof::kGemmSmall, s, 2.0 * M * N * K,
                     8.0 * (M * K + K * N + M * N * (beta != 0.0 ? 2.0 : 1.0)));
   if (K <= 0 || alpha == 0.0) {
     scale_kernel<<<grid_for(M * N), 256, 0, s>>>(M, N, beta, C, ldc);
@@ -472,13 +472,15 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
 void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
                   double beta, double* C, i64 ldc) {
   if (M <= 0 || N <= 0) return;
-  prof::Scope scope(prof::kGemm, s, 1.0 * M * N * (N + 1), 8.0 * (M * N + N * N / 2 + M * N * (beta != 0.0 ? 2.0 : 1.0)));
+  prof::Scope scope(1.0 * M * N * (N + 1) >= 2e9 ? prof::kGemm : prof::kGemmSmall, s, 1.0 * M * N * (N + 1),
+                    8.0 * (M * N + N * N / 2 + M * N * (beta != 0.0 ? 2.0 : 1.0)));
   launch_gemm<false, false>(s, M, N, N, alpha, A, lda, B, ldb, beta, C, ldc, 2);
 }
 
 void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* G, i64 ldg) {
   if (rows <= 0 || cols <= 0) return;
-  prof::Scope scope(prof::kGemm, s, 1.0 * cols * (cols + 1) * rows, 8.0 * (rows * cols + cols * cols));
+  prof::Scope scope(1.0 * cols * (cols + 1) * rows >= 2e9 ? prof::kGemm : prof::kGemmSmall, s,
+                    1.0 * cols * (cols + 1) * rows, 8.0 * (rows * cols + cols * cols));
   launch_gemm<true, false>(s, cols, cols, rows, 1.0, X, ldx, X, ldx, 0.0, G, ldg, 1);
 }
 

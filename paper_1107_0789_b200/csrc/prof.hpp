@@ -22,6 +22,7 @@ enum Op : int {
   kElementwise,
   kReduce,
   kOther,
+  kGemmSmall,  // GEMMs below 2 GFLOP (factorisation internals, small products): latency-bound
   kNumOps
 };
 

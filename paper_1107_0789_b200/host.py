@@ -126,7 +126,8 @@ def gen_rmf_instance(m, n, r, s, sigma, seed, stream=0, lo=0.0, hi=1.0):
 
 
 # ------------------------------------------------------------------ kernel accounting
-PROF_OPS = ("gemm", "sddmm", "spmm", "cholesky", "qr_fallback", "jacobi", "elementwise", "reduce", "other")
+PROF_OPS = ("gemm", "sddmm", "spmm", "cholesky", "qr_fallback", "jacobi", "elementwise", "reduce", "other",
+            "gemm_small")
 
 
 def prof_enable(on: bool = True):
