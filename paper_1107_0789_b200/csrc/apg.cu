@@ -10,6 +10,7 @@
 // instead — the same matrix Y (the compaction only drops singular values <= 1e-12 *
 // max(m,n) * s_max), consumed only through Y*X, Y^T*X and P_Omega(Y).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -491,8 +492,14 @@ DeviceContext::~DeviceContext() {
   }
 }
 
+namespace {
+std::atomic<int> g_active_streams[64];
+}
+int active_streams(int dev) { return dev >= 0 && dev < 64 ? g_active_streams[dev].load() : 1; }
+
 cudaStream_t DeviceContext::acquire() {
   std::lock_guard<std::mutex> lock(mu);
+  if (device >= 0 && device < 64) g_active_streams[device]++;
   if (!free_streams.empty()) {
     cudaStream_t st = free_streams.back();
     free_streams.pop_back();
@@ -506,6 +513,7 @@ cudaStream_t DeviceContext::acquire() {
 
 void DeviceContext::release(cudaStream_t st) {
   std::lock_guard<std::mutex> lock(mu);
+  if (device >= 0 && device < 64) g_active_streams[device]--;
   free_streams.push_back(st);
 }
 

@@ -139,6 +139,10 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 #endif
 
+// Solves currently holding a stream of device `dev`'s context (DeviceContext acquire/release):
+// kernels with a latency / occupancy trade-off (the Jacobi cluster size) consult it.
+int active_streams(int dev);
+
 // ---------------------------------------------------------------- factorizations (factor.cu)
 struct Workspace;  // forward
 

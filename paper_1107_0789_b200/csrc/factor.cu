@@ -19,6 +19,9 @@
 
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace dfcg {
 
 namespace {
@@ -865,7 +868,11 @@ __global__ void __launch_bounds__(256) jacobi_small_kernel(int rows, int n, int 
   }
 }
 
-template <int NB>
+// CS > 1: a thread-block cluster of CS CTAs shares one block pair, each CTA staging, reducing
+// and rotating a contiguous slab of the rows; the 16x16 partial Grams are summed over the
+// cluster through distributed shared memory in rank order (every CTA gets the identical Gram
+// and runs the identical inner EVD). Used when few solves share the GPU (single-block latency).
+template <int NB, int CS>
 __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i64 nv_, double* W, i64 ldw, double* V,
                                                                     i64 ldv, int p, int round, double tol,
                                                                     unsigned long long* offmax, int inner_sweeps,
@@ -873,8 +880,19 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
   static_assert(NB == 8, "the swizzle and the step tables assume 16-column pairs");
   constexpr int JW = 16, T = 256;
   extern __shared__ __align__(16) double dyn[];
-  const int rows = static_cast<int>(rows_), nv = static_cast<int>(nv_);
-  const int rows4 = (rows + 3) & ~3, nv4 = (nv + 3) & ~3;
+  const int crank = static_cast<int>(blockIdx.x % CS), pk = static_cast<int>(blockIdx.x / CS);
+  int rows, nv, rows4, nv4;
+  {  // this CTA's slab of the W rows and of the V rows (multiples of 4)
+    const int R = static_cast<int>(rows_), R4 = (R + 3) & ~3, NV = static_cast<int>(nv_), NV4 = (NV + 3) & ~3;
+    const int cw = ((R4 / 4 + CS - 1) / CS) * 4, cv = ((NV4 / 4 + CS - 1) / CS) * 4;
+    const int rw = crank * cw, rv = crank * cv;
+    rows4 = max(0, min(cw, R4 - rw));
+    rows = max(0, min(cw, R - rw));
+    nv4 = max(0, min(cv, NV4 - rv));
+    nv = max(0, min(cv, NV - rv));
+    W += static_cast<i64>(rw) * ldw;
+    V += static_cast<i64>(rv) * ldv;
+  }
   const int cap = rows4 > nv4 ? rows4 : nv4;
   double* Wp = dyn;
   double* Vp = prefetch_v ? Wp + cap * JW : Wp;
@@ -886,7 +904,7 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
   // round-robin pairing (round_robin() on the host): ring[0] = 0, ring[i] = 1 + (i - 1 - round)
   // mod (p - 1); CTA k takes (ring[k], ring[p - 1 - k]). No global load before the staging.
   auto ring = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 - round) % (p - 1) + (p - 1)) % (p - 1); };
-  const int bi = ring(blockIdx.x), bj = ring(p - 1 - blockIdx.x);
+  const int bi = ring(pk), bj = ring(p - 1 - pk);
   auto gcol = [&](int c) -> i64 { return c < NB ? static_cast<i64>(bi) * NB + c : static_cast<i64>(bj) * NB + c - NB; };
 
   // staging: thread t moves 16-byte chunk q = t & 7 (pair columns 2q, 2q+1) of rows t/8, t/8+32, ...
@@ -950,6 +968,17 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
     g[0][r][c] = (red[e] + red[JW * JW + e]) + (red[2 * JW * JW + e] + red[3 * JW * JW + e]);
     rot[r][c] = r == c ? 1.0 : 0.0;
   }
+  if constexpr (CS > 1) {  // sum the cluster's partial Grams in rank order
+    __shared__ double gpart[JW * JW];
+    gpart[t] = g[0][t >> 4][t & 15];
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    double v = 0.0;
+#pragma unroll
+    for (int r = 0; r < CS; ++r) v += cluster.map_shared_rank(gpart, r)[t];
+    cluster.sync();  // every remote read done before any CTA of the cluster may exit
+    g[0][t >> 4][t & 15] = v;
+  }
   __syncthreads();
 
   // ---- off-diagonal measure (all pairs of the JW columns)
@@ -968,7 +997,7 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
     __syncthreads();
   }
   const double off0 = s_off;
-  if (t == 0) atomicMax(offmax, static_cast<unsigned long long>(__double_as_longlong(off0)));
+  if (t == 0 && crank == 0) atomicMax(offmax, static_cast<unsigned long long>(__double_as_longlong(off0)));
   if (off0 <= tol) {
     asm volatile("cp.async.wait_group 0;\n" ::);  // no copy may land after the CTA retires
     return;
@@ -1285,19 +1314,73 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   const int npairs = p / 2;
   const i64 cap_rows = std::max((wrows + 3) / 4 * 4, (nj + 3) / 4 * 4);
   const bool resident = cap_rows <= kResidentRows;
-  const int prefetch_v = nj > 0 && 2 * cap_rows <= kResidentRows ? 1 : 0;  // W and V pairs both fit
-  const size_t smem = sizeof(double) * ((prefetch_v ? 2 : 1) * cap_rows * JW + 4 * JW * JW);
+  int dev = 0;
+  DFCG_CUDA(cudaGetDevice(&dev));
+  // Cluster size: split each pair's rows over CS CTAs when few solves share the GPU, so a lone
+  // block's rounds use more SMs (the concurrent F step keeps CS = 1: same work, fewer CTAs).
+  static const int cs_env = std::getenv("DFCG_JACOBI_CLUSTER") ? std::atoi(std::getenv("DFCG_JACOBI_CLUSTER")) : 0;
+  int CS = 1;
+  if (resident) {
+    int nsm = 0;
+    DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const i64 slots = 2 * static_cast<i64>(nsm);
+    const i64 k = std::max(1, active_streams(dev));
+    for (int c : {4, 2})
+      if (k * npairs * c <= slots && wrows >= 64 * c) {
+        CS = c;
+        break;
+      }
+    if (cs_env == 1 || cs_env == 2 || cs_env == 4) CS = cs_env;
+  }
+  const i64 cw = ((cap_rows / 4 + CS - 1) / CS) * 4;  // rows per CTA (slab)
+  // the cluster variants carry 2 KB more static shared memory (the partial Gram they share)
+  const size_t dyn_cap = CS == 1 ? sizeof(double) * (kResidentRows * JW + 4 * JW * JW) : 220000;
+  int prefetch_v = nj > 0 && 2 * cw <= kResidentRows ? 1 : 0;  // W and V slabs both fit
+  if (sizeof(double) * (2 * cw * JW + 4 * JW * JW) > dyn_cap) prefetch_v = 0;
+  const size_t smem = sizeof(double) * ((prefetch_v ? 2 : 1) * cw * JW + 4 * JW * JW);
   if (resident) {
     static unsigned configured = 0;
-    int dev = 0;
-    DFCG_CUDA(cudaGetDevice(&dev));
     if (!(configured & (1u << dev))) {
       const size_t max_smem = sizeof(double) * (kResidentRows * JW + 4 * JW * JW);
-      DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(max_smem)));
+      DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     220000));
+      DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     220000));
       configured |= 1u << dev;
     }
   }
+  auto launch_round = [&](int r) {
+    const int inner = r == 0 ? 1 : 0;
+    if (CS == 1) {
+      jacobi_round_resident_kernel<NB, 1><<<npairs, 256, smem, s>>>(wrows, nj, W.get(), np, J.get(), np, p, r, tol,
+                                                                    off.get(), inner, prefetch_v);
+      return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(npairs * CS));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(CS);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    double* Wp = W.get();
+    double* Jp = J.get();
+    unsigned long long* op = off.get();
+    const i64 ld = np;
+    if (CS == 2)
+      DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_resident_kernel<NB, 2>, wrows, nj, Wp, ld, Jp, ld, p, r, tol, op,
+                                   inner, prefetch_v));
+    else
+      DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_resident_kernel<NB, 4>, wrows, nj, Wp, ld, Jp, ld, p, r, tol, op,
+                                   inner, prefetch_v));
+  };
   static const bool trace_svd = std::getenv("DFCG_TRACE_SVD") != nullptr;
   const bool small = cols <= kSmallN && wrows <= kSmallN && nj <= kSmallN;
   if (small) {  // one launch, convergence on the device
@@ -1338,8 +1421,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       for (int r = 0; r < p - 1; ++r) {
         const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
         if (resident)
-          jacobi_round_resident_kernel<NB><<<npairs, 256, smem, s>>>(wrows, nj, W.get(), np, J.get(), np, p, r, tol,
-                                                                     off.get(), r == 0 ? 1 : 0, prefetch_v);
+          launch_round(r);
         else
           jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol, off.get(),
                                                               2);
