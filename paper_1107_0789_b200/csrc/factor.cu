@@ -691,34 +691,34 @@ __global__ void __launch_bounds__(16 * NB) jacobi_round_kernel(i64 rows, i64 nv,
   apply(V, ldv, nv);
 }
 
-// Shared-memory-resident variant of the round (rows <= kResidentRows). One CTA per block pair:
-//   stage   the pair's 16 columns of W (and of V when both fit) with 16-byte cp.async into a
-//           swizzled 128-byte-row layout (chunk q of row r at q ^ 2(r & 3): conflict-free for
-//           both DMMA fragment patterns below, no padding, 16-byte aligned);
+// Shared-memory-resident variant of the round. One CTA (or a cluster of CS CTAs, each with a
+// slab of the rows) per block pair; NB = 8 or 16 columns per block:
+//   stage   the pair's 2NB columns of W (and of V when both fit) with 16-byte cp.async into a
+//           swizzled row layout (chunk q of row r at q ^ 2(r & 3): conflict-free for both DMMA
+//           fragment patterns below, no padding, 16-byte aligned);
 //   Gram    by DMMA over the 8 warps, fixed-order reduction through 4 shared slots;
-//   EVD     one cyclic sweep of the 16x16 Gram, one barrier per step: each of 64 threads owns a
-//           2x2 block (P, Q) of the pairing and applies J_P^T G J_Q into the other buffer of a
-//           double-buffered Gram, 128 threads rotate the accumulated rotation; every thread
-//           recomputes the rotations it needs from the pre-step Gram;
+//   EVD     the 2NB x 2NB Gram, one barrier per step: each thread owns a 2x2 block (P, Q) of the
+//           pairing and applies J_P^T G J_Q into the other buffer of a double-buffered Gram,
+//           the rest rotate the accumulated rotation; every thread recomputes the rotations it
+//           needs from the pre-step Gram;
 //   apply   W_pair <- W_pair rot by DMMA with the rotation fragments held in registers,
 //           16-byte stores; then the same for the V pair.
-// 1688 rows of 128 B + 4 partial Grams + ~7.4 KB static fit the 227 KB opt-in; a W pair alone
-// of <= ~800 rows leaves room for two CTAs per SM.
-constexpr int kResidentRows = 1688;
+// The host sizes the slab from the shared memory left by the static arrays (thin_svd).
 
-
-// swizzled position of column c (0..15) in row r of a staged pair
+// swizzled position of column c (0..2NB-1) in row r of a staged pair
 __device__ __forceinline__ int jswz(int r, int c) { return ((((c >> 1) ^ ((r & 3) << 1))) << 1) | (c & 1); }
 
-// pair k (0..7) of step `step` (0..14) of the 16-column round-robin ordering, a < b
+// pair k of step `step` of the JW-column round-robin ordering (column 0 fixed), a < b
+template <int JW>
 __device__ __forceinline__ void jpair(int step, int k, int& a, int& b) {
+  constexpr int M = JW - 1;
   if (k == 0) {
     a = 0;
     b = 1 + step;
   } else {
-    int x = step + k, y = step + 15 - k;
-    x = x >= 15 ? x - 15 : x;
-    y = y >= 15 ? y - 15 : y;
+    int x = step + k, y = step + M - k;
+    x = x >= M ? x - M : x;
+    y = y >= M ? y - M : y;
     a = 1 + x;
     b = 1 + y;
     if (a > b) {
@@ -755,7 +755,8 @@ __device__ __forceinline__ void rot_from_gram(double gpp, double gqq, double gpq
     sn = sd * nrm;
   }
 }
-__device__ __forceinline__ void jrot(const double (*g)[17], int a, int b, double& c, double& sn) {
+template <int LD>
+__device__ __forceinline__ void jrot(const double (*g)[LD], int a, int b, double& c, double& sn) {
   rot_from_gram(g[a][a], g[b][b], g[a][b], c, sn);
 }
 
@@ -873,12 +874,12 @@ __global__ void __launch_bounds__(256) jacobi_small_kernel(int rows, int n, int 
 // cluster through distributed shared memory in rank order (every CTA gets the identical Gram
 // and runs the identical inner EVD). Used when few solves share the GPU (single-block latency).
 template <int NB, int CS>
-__global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i64 nv_, double* W, i64 ldw, double* V,
+__global__ void __launch_bounds__(256, NB == 8 ? 2 : 1) jacobi_round_resident_kernel(i64 rows_, i64 nv_, double* W, i64 ldw, double* V,
                                                                     i64 ldv, int p, int round, double tol,
                                                                     unsigned long long* offmax, int inner_sweeps,
                                                                     int prefetch_v) {
-  static_assert(NB == 8, "the swizzle and the step tables assume 16-column pairs");
-  constexpr int JW = 16, T = 256;
+  static_assert(NB == 8 || NB == 16, "8- or 16-column blocks (16 or 32 columns per pair)");
+  constexpr int JW = 2 * NB, T = 256, NT = JW / 8, CH = JW / 2, KS = JW / 4;
   extern __shared__ __align__(16) double dyn[];
   const int crank = static_cast<int>(blockIdx.x % CS), pk = static_cast<int>(blockIdx.x / CS);
   int rows, nv, rows4, nv4;
@@ -896,7 +897,8 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
   const int cap = rows4 > nv4 ? rows4 : nv4;
   double* Wp = dyn;
   double* Vp = prefetch_v ? Wp + cap * JW : Wp;
-  double* red = Wp + (prefetch_v ? 2 : 1) * cap * JW;  // 4 x JW*JW partial Grams
+  double* red = Wp + (prefetch_v ? 2 : 1) * cap * JW;  // one JW x JW partial Gram (the other three
+                                                        // reduction slots reuse g and rot)
   __shared__ double g[2][JW][JW + 1];
   __shared__ double rot[JW][JW + 1];
   __shared__ double s_off;
@@ -907,14 +909,14 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
   const int bi = ring(pk), bj = ring(p - 1 - pk);
   auto gcol = [&](int c) -> i64 { return c < NB ? static_cast<i64>(bi) * NB + c : static_cast<i64>(bj) * NB + c - NB; };
 
-  // staging: thread t moves 16-byte chunk q = t & 7 (pair columns 2q, 2q+1) of rows t/8, t/8+32, ...
-  const int q = t & 7;
+  // staging: thread t moves 16-byte chunk q = t % CH (pair columns 2q, 2q+1) of rows t/CH, t/CH + T/CH, ...
+  const int q = t % CH, r0 = t / CH;
   const i64 gq = gcol(2 * q);
-  const int soff = (q ^ (((t >> 3) & 3) << 1)) << 1;  // swizzled chunk: r & 3 is fixed per thread
+  const int soff = (q ^ ((r0 & 3) << 1)) << 1;  // swizzled chunk: r & 3 is fixed per thread
   auto stage = [&](double* dst, const double* src, i64 ld, int n, int n4) {
-    const double* sp = src + (t >> 3) * ld + gq;
-    double* dp = dst + (t >> 3) * JW + soff;
-    for (int r = t >> 3; r < n4; r += T / 8, sp += (T / 8) * ld, dp += (T / 8) * JW) cp_async16(dp, r < n ? sp : src, r < n);
+    const double* sp = src + r0 * ld + gq;
+    double* dp = dst + r0 * JW + soff;
+    for (int r = r0; r < n4; r += T / CH, sp += (T / CH) * ld, dp += (T / CH) * JW) cp_async16(dp, r < n ? sp : src, r < n);
   };
   stage(Wp, W, ldw, rows, rows4);
   asm volatile("cp.async.commit_group;\n" ::);
@@ -927,67 +929,81 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
   }
   __syncthreads();
 
-  // ---- Gram (DMMA): lane reads column ti*8 + lane/4 of row k + lane%4 for both operands
+  // ---- Gram (DMMA): rows split over the warps; lane reads column ti*8 + lane/4 of row k + lane%4
   {
-    const int o0 = jswz(lane & 3, lane >> 2), o1 = jswz(lane & 3, 8 + (lane >> 2));
-    double acc[4][2];
+    int oc[NT];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) acc[e][0] = acc[e][1] = 0.0;
+    for (int ti = 0; ti < NT; ++ti) oc[ti] = jswz(lane & 3, ti * 8 + (lane >> 2));
+    double acc[NT * NT][2];
+#pragma unroll
+    for (int e = 0; e < NT * NT; ++e) acc[e][0] = acc[e][1] = 0.0;
     for (int k = 4 * warp; k < rows4; k += 32) {
       const double* row = Wp + (k + (lane & 3)) * JW;
-      const double x0 = row[o0], x1 = row[o1];
-      dmma(acc[0], x0, x0);
-      dmma(acc[1], x0, x1);
-      dmma(acc[2], x1, x0);
-      dmma(acc[3], x1, x1);
-    }
-    auto publish = [&](int slot) {
+      double x[NT];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = (e >> 1) * 8 + (lane >> 2), c = (e & 1) * 8 + (lane & 3) * 2;
-        red[slot * JW * JW + r * JW + c] = acc[e][0];
-        red[slot * JW * JW + r * JW + c + 1] = acc[e][1];
+      for (int ti = 0; ti < NT; ++ti) x[ti] = row[oc[ti]];
+#pragma unroll
+      for (int ti = 0; ti < NT; ++ti)
+#pragma unroll
+        for (int tj = 0; tj < NT; ++tj) dmma(acc[ti * NT + tj], x[ti], x[tj]);
+    }
+    // fixed-order reduction of the 8 warp partials through 4 slots (red, g[1], rot, g[0]):
+    // warps 4..7 publish, warps 0..3 fold them in (w + (w + 4)), publish, then sum slots 0..3
+    const int sl = warp & 3;  // this warp's slot (warps w and w + 4 share slot w)
+    double* const sp = sl == 0 ? red : (sl == 1 ? &g[1][0][0] : (sl == 2 ? &rot[0][0] : &g[0][0][0]));
+    const int sld = sl == 0 ? JW : JW + 1;
+    auto publish = [&]() {
+#pragma unroll
+      for (int e = 0; e < NT * NT; ++e) {
+        const int r = (e / NT) * 8 + (lane >> 2), c = (e % NT) * 8 + (lane & 3) * 2;
+        sp[r * sld + c] = acc[e][0];
+        sp[r * sld + c + 1] = acc[e][1];
       }
     };
-    if (warp >= 4) publish(warp - 4);
+    if (warp >= 4) publish();
     __syncthreads();
     if (warp < 4) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = (e >> 1) * 8 + (lane >> 2), c = (e & 1) * 8 + (lane & 3) * 2;
-        acc[e][0] += red[warp * JW * JW + r * JW + c];
-        acc[e][1] += red[warp * JW * JW + r * JW + c + 1];
+      for (int e = 0; e < NT * NT; ++e) {
+        const int r = (e / NT) * 8 + (lane >> 2), c = (e % NT) * 8 + (lane & 3) * 2;
+        acc[e][0] += sp[r * sld + c];
+        acc[e][1] += sp[r * sld + c + 1];
       }
     }
     __syncthreads();
-    if (warp < 4) publish(warp);
-  }
-  __syncthreads();
-  {
-    const int e = t, r = e >> 4, c = e & 15;  // T == JW * JW
-    g[0][r][c] = (red[e] + red[JW * JW + e]) + (red[2 * JW * JW + e] + red[3 * JW * JW + e]);
-    rot[r][c] = r == c ? 1.0 : 0.0;
+    if (warp < 4) publish();
+    __syncthreads();
+    for (int e = t; e < JW * JW; e += T) {  // thread e reads slot 3 == g[0] at e before writing it
+      const int r = e / JW, c = e % JW;
+      g[0][r][c] = (red[r * JW + c] + g[1][r][c]) + (rot[r][c] + g[0][r][c]);
+    }
+    __syncthreads();
+    for (int e = t; e < JW * JW; e += T) rot[e / JW][e % JW] = (e / JW == e % JW) ? 1.0 : 0.0;
   }
   if constexpr (CS > 1) {  // sum the cluster's partial Grams in rank order
     __shared__ double gpart[JW * JW];
-    gpart[t] = g[0][t >> 4][t & 15];
+    for (int e = t; e < JW * JW; e += T) gpart[e] = g[0][e / JW][e % JW];
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
-    double v = 0.0;
+    for (int e = t; e < JW * JW; e += T) {
+      double v = 0.0;
 #pragma unroll
-    for (int r = 0; r < CS; ++r) v += cluster.map_shared_rank(gpart, r)[t];
+      for (int r = 0; r < CS; ++r) v += cluster.map_shared_rank(gpart, r)[e];
+      g[0][e / JW][e % JW] = v;
+    }
     cluster.sync();  // every remote read done before any CTA of the cluster may exit
-    g[0][t >> 4][t & 15] = v;
   }
   __syncthreads();
 
   // ---- off-diagonal measure (all pairs of the JW columns)
   {
-    const int a = t >> 4, b = t & 15;
     double mx = 0.0;
-    if (a < b) {
-      const double d = sqrt(g[0][a][a]) * sqrt(g[0][b][b]);
-      if (d > 0.0) mx = fabs(g[0][a][b]) / d;
+    for (int e = t; e < JW * JW; e += T) {
+      const int a = e / JW, b = e % JW;
+      if (a < b) {
+        const double d = sqrt(g[0][a][a]) * sqrt(g[0][b][b]);
+        if (d > 0.0) mx = fmax(mx, fabs(g[0][a][b]) / d);
+      }
     }
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (t == 0) s_off = 0.0;
@@ -1004,8 +1020,8 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
   }
 
   // ---- inner Jacobi on the Gram, one barrier per step. inner_sweeps > 0: that many cyclic
-  // sweeps over all 120 column pairs (15 steps); inner_sweeps == 0: the 64 cross pairs only
-  // (8 steps, column i of block I with column (i + step) % 8 of block J). The host uses the
+  // sweeps over all column pairs (JW - 1 steps); inner_sweeps == 0: the NB^2 cross pairs only
+  // (NB steps, column i of block I with column (i + step) % NB of block J). The host uses the
   // full sweep in the first round of every outer sweep (each block appears once there, so its
   // internal pairs are rotated once per sweep) and cross steps elsewhere: every column pair is
   // then rotated exactly once per outer sweep, a cyclic Jacobi ordering.
@@ -1014,85 +1030,92 @@ __global__ void __launch_bounds__(256) jacobi_round_resident_kernel(i64 rows_, i
   const int nsteps = cross ? NB : (JW - 1) * inner_sweeps;
   for (int it = 0; it < nsteps; ++it) {
     const int step = cross ? it : it % (JW - 1);
-    {
-      auto pair_of = [&](int k, int& a, int& b) {
-        if (cross) {
-          a = k;
-          b = NB + ((k + step) & (NB - 1));
-        } else {
-          jpair(step, k, a, b);
-        }
-      };
-      if (t < 64) {
-        const int P = t >> 3, Q = t & 7;
-        int aP, bP, aQ, bQ;
-        pair_of(P, aP, bP);
-        pair_of(Q, aQ, bQ);
-        double cP, sP, cQ, sQ;
-        jrot(g[cur], aP, bP, cP, sP);
-        jrot(g[cur], aQ, bQ, cQ, sQ);
-        const double x00 = g[cur][aP][aQ], x01 = g[cur][aP][bQ], x10 = g[cur][bP][aQ], x11 = g[cur][bP][bQ];
-        const double y00 = cQ * x00 - sQ * x01, y01 = sQ * x00 + cQ * x01;  // columns: G J_Q
-        const double y10 = cQ * x10 - sQ * x11, y11 = sQ * x10 + cQ * x11;
-        const int nx = cur ^ 1;  // rows: J_P^T (G J_Q)
-        g[nx][aP][aQ] = cP * y00 - sP * y10;
-        g[nx][bP][aQ] = sP * y00 + cP * y10;
-        g[nx][aP][bQ] = cP * y01 - sP * y11;
-        g[nx][bP][bQ] = sP * y01 + cP * y11;
-      } else if (t < 64 + 128) {
-        const int u = t - 64, k = u >> 4, r = u & 15;
-        int a, b;
-        pair_of(k, a, b);
-        double c, sn;
-        jrot(g[cur], a, b, c, sn);
-        const double ra = rot[r][a], rb = rot[r][b];
-        rot[r][a] = c * ra - sn * rb;
-        rot[r][b] = sn * ra + c * rb;
+    auto pair_of = [&](int k, int& a, int& b) {
+      if (cross) {
+        a = k;
+        b = NB + ((k + step) & (NB - 1));
+      } else {
+        jpair<JW>(step, k, a, b);
       }
-      __syncthreads();
-      cur ^= 1;
+    };
+    // 2x2 blocks (P, Q) of the pairing: NB^2 of them, one per thread (NB = 16) or the first 64
+    if (t < NB * NB) {
+      const int P = t / NB, Q = t % NB;
+      int aP, bP, aQ, bQ;
+      pair_of(P, aP, bP);
+      pair_of(Q, aQ, bQ);
+      double cP, sP, cQ, sQ;
+      jrot(g[cur], aP, bP, cP, sP);
+      jrot(g[cur], aQ, bQ, cQ, sQ);
+      const double x00 = g[cur][aP][aQ], x01 = g[cur][aP][bQ], x10 = g[cur][bP][aQ], x11 = g[cur][bP][bQ];
+      const double y00 = cQ * x00 - sQ * x01, y01 = sQ * x00 + cQ * x01;  // columns: G J_Q
+      const double y10 = cQ * x10 - sQ * x11, y11 = sQ * x10 + cQ * x11;
+      const int nx = cur ^ 1;  // rows: J_P^T (G J_Q)
+      g[nx][aP][aQ] = cP * y00 - sP * y10;
+      g[nx][bP][aQ] = sP * y00 + cP * y10;
+      g[nx][aP][bQ] = cP * y01 - sP * y11;
+      g[nx][bP][bQ] = sP * y01 + cP * y11;
     }
+    // accumulated rotation: JW rows x NB pairs; NB = 8 uses the threads left over above
+    constexpr int RU = JW * NB;
+    for (int u = (NB == 8 ? t - 64 : t); u >= 0 && u < RU; u += (NB == 8 ? RU : T)) {
+      const int k = u / JW, r = u % JW;
+      int a, b;
+      pair_of(k, a, b);
+      double c, sn;
+      jrot(g[cur], a, b, c, sn);
+      const double ra = rot[r][a], rb = rot[r][b];
+      rot[r][a] = c * ra - sn * rb;
+      rot[r][b] = sn * ra + c * rb;
+    }
+    __syncthreads();
+    cur ^= 1;
   }
 
   // ---- apply: M_pair <- M_pair rot from the staged copy; B fragments (rot) live in registers
-  double bf[4][2];
+  double bf[KS][NT];
 #pragma unroll
-  for (int kk = 0; kk < 4; ++kk)
+  for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
-    for (int ct = 0; ct < 2; ++ct) bf[kk][ct] = rot[kk * 4 + (lane & 3)][ct * 8 + (lane >> 2)];
-  int ao[4];  // swizzled A-fragment offsets: row rt*8 + lane/4 (r & 3 == (lane/4) & 3), column kk*4 + lane%4
+    for (int ct = 0; ct < NT; ++ct) bf[kk][ct] = rot[kk * 4 + (lane & 3)][ct * 8 + (lane >> 2)];
+  int ao[KS];  // swizzled A-fragment offsets: row rt*8 + lane/4 (r & 3 == (lane/4) & 3), column kk*4 + lane%4
 #pragma unroll
-  for (int kk = 0; kk < 4; ++kk) ao[kk] = jswz((lane >> 2) & 3, kk * 4 + (lane & 3));
-  const i64 c0 = gcol((lane & 3) * 2), c1 = gcol(8 + (lane & 3) * 2);
-  // two row tiles per iteration: four independent DMMA chains hide the DMMA latency
+  for (int kk = 0; kk < KS; ++kk) ao[kk] = jswz((lane >> 2) & 3, kk * 4 + (lane & 3));
+  i64 cc[NT];
+#pragma unroll
+  for (int ct = 0; ct < NT; ++ct) cc[ct] = gcol(ct * 8 + (lane & 3) * 2);
+  // two row tiles per iteration: independent DMMA chains hide the DMMA latency
   auto apply = [&](const double* Sp, double* M, i64 ld, int n, int n4) {
     const int tiles = (n + 7) >> 3;
     for (int rt = warp; rt < tiles; rt += 2 * (T / 32)) {
       const bool two_tiles = rt + T / 32 < tiles;  // warp-uniform
       const int r = rt * 8 + (lane >> 2), r2 = r + 8 * (T / 32);
-      double o0[2] = {0.0, 0.0}, o1[2] = {0.0, 0.0}, p0[2] = {0.0, 0.0}, p1[2] = {0.0, 0.0};
-      double a[4], b[4];
+      double o[NT][2], pz[NT][2];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {  // rows past the staged block read as 0 (no divergence)
+      for (int ct = 0; ct < NT; ++ct) o[ct][0] = o[ct][1] = pz[ct][0] = pz[ct][1] = 0.0;
+      double a[KS], b[KS];
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {  // rows past the staged block read as 0 (no divergence)
         a[kk] = r < n4 ? Sp[r * JW + ao[kk]] : 0.0;
         b[kk] = two_tiles && r2 < n4 ? Sp[r2 * JW + ao[kk]] : 0.0;
       }
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        dmma(o0, a[kk], bf[kk][0]);
-        dmma(o1, a[kk], bf[kk][1]);
+      for (int kk = 0; kk < KS; ++kk) {
+#pragma unroll
+        for (int ct = 0; ct < NT; ++ct) dmma(o[ct], a[kk], bf[kk][ct]);
         if (two_tiles) {
-          dmma(p0, b[kk], bf[kk][0]);
-          dmma(p1, b[kk], bf[kk][1]);
+#pragma unroll
+          for (int ct = 0; ct < NT; ++ct) dmma(pz[ct], b[kk], bf[kk][ct]);
         }
       }
       if (r < n) {
-        *reinterpret_cast<double2*>(M + r * ld + c0) = make_double2(o0[0], o0[1]);
-        *reinterpret_cast<double2*>(M + r * ld + c1) = make_double2(o1[0], o1[1]);
+#pragma unroll
+        for (int ct = 0; ct < NT; ++ct) *reinterpret_cast<double2*>(M + r * ld + cc[ct]) = make_double2(o[ct][0], o[ct][1]);
       }
       if (two_tiles && r2 < n) {
-        *reinterpret_cast<double2*>(M + r2 * ld + c0) = make_double2(p0[0], p0[1]);
-        *reinterpret_cast<double2*>(M + r2 * ld + c1) = make_double2(p1[0], p1[1]);
+#pragma unroll
+        for (int ct = 0; ct < NT; ++ct)
+          *reinterpret_cast<double2*>(M + r2 * ld + cc[ct]) = make_double2(pz[ct][0], pz[ct][1]);
       }
     }
   };
@@ -1292,7 +1315,12 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   }
   if (!have_r) thin_qr(s, rows, cols, Qx.get(), cols, R.get(), cols);
 
-  constexpr int NB = 8, JW = 2 * NB;
+  // Block width: 8-column blocks (16-column pairs). 16-column blocks halve the rounds per sweep
+  // but measured slower on B200 at b ~ 720 (single block: 576 vs 477 ms per 40 iterations; the
+  // ~200 KB slab also takes a whole SM, which cost 2x in the concurrent F step), so they are
+  // only reachable through DFCG_JACOBI_NB=16 for experiments.
+  static const int nb_env = std::getenv("DFCG_JACOBI_NB") ? std::atoi(std::getenv("DFCG_JACOBI_NB")) : 0;
+  const int NB = nb_env == 16 ? 16 : 8;
   const int p0 = static_cast<int>((cols + NB - 1) / NB);
   const int p = std::max(2, p0 + (p0 & 1));
   const i64 np = static_cast<i64>(p) * NB;  // padded column count
@@ -1312,52 +1340,66 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   // measured ~1e-11 on the c2 shapes — too close to tol to serve as the stopping test too).
   const double tol = 1e-11, stop_tol = 1e-6;
   const int npairs = p / 2;
+  const int JW = 2 * NB;
   const i64 cap_rows = std::max((wrows + 3) / 4 * 4, (nj + 3) / 4 * 4);
-  const bool resident = cap_rows <= kResidentRows;
   int dev = 0;
   DFCG_CUDA(cudaGetDevice(&dev));
+  // Shared memory per CTA: the slab (cw rows of JW doubles, twice with the V prefetch) plus one
+  // JW x JW reduction slot, under the opt-in limit left by the static arrays (the Gram pair and
+  // rotation; the cluster variants add the shared partial Gram).
+  const size_t static_b = sizeof(double) * (3 * JW * (JW + 1) + 8) + (NB == 8 ? 1024 : 0);
+  auto dyn_cap = [&](int cs) {
+    return 232448 - static_b - (cs > 1 ? sizeof(double) * JW * JW : 0) - 1024;
+  };
+  auto dyn_for = [&](i64 cw, int pre) { return sizeof(double) * ((pre ? 2 : 1) * cw * JW + JW * JW); };
   // Cluster size: split each pair's rows over CS CTAs when few solves share the GPU, so a lone
-  // block's rounds use more SMs (the concurrent F step keeps CS = 1: same work, fewer CTAs).
+  // block's rounds use more SMs (the concurrent F step keeps CS = 1: same work, fewer CTAs), or
+  // when one CTA's shared memory cannot hold a slab.
   static const int cs_env = std::getenv("DFCG_JACOBI_CLUSTER") ? std::atoi(std::getenv("DFCG_JACOBI_CLUSTER")) : 0;
-  int CS = 1;
+  auto slab = [&](int cs) { return ((cap_rows / 4 + cs - 1) / cs) * 4; };
+  int CS = 0;  // 0: streaming (non-resident) round kernel
+  for (int c : {1, 2, 4})
+    if (dyn_for(slab(c), 0) <= dyn_cap(c)) {
+      CS = c;
+      break;
+    }
+  const bool resident = CS > 0;
   if (resident) {
     int nsm = 0;
     DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const i64 slots = 2 * static_cast<i64>(nsm);
     const i64 k = std::max(1, active_streams(dev));
     for (int c : {4, 2})
-      if (k * npairs * c <= slots && wrows >= 64 * c) {
+      if (c > CS && k * npairs * c <= slots && wrows >= 64 * c) {
         CS = c;
         break;
       }
-    if (cs_env == 1 || cs_env == 2 || cs_env == 4) CS = cs_env;
+    if (cs_env == 1 || cs_env == 2 || cs_env == 4)
+      if (dyn_for(slab(cs_env), 0) <= dyn_cap(cs_env)) CS = cs_env;
   }
-  const i64 cw = ((cap_rows / 4 + CS - 1) / CS) * 4;  // rows per CTA (slab)
-  // the cluster variants carry 2 KB more static shared memory (the partial Gram they share)
-  const size_t dyn_cap = CS == 1 ? sizeof(double) * (kResidentRows * JW + 4 * JW * JW) : 220000;
-  int prefetch_v = nj > 0 && 2 * cw <= kResidentRows ? 1 : 0;  // W and V slabs both fit
-  if (sizeof(double) * (2 * cw * JW + 4 * JW * JW) > dyn_cap) prefetch_v = 0;
-  const size_t smem = sizeof(double) * ((prefetch_v ? 2 : 1) * cw * JW + 4 * JW * JW);
+  if (!resident && NB != 8) throw std::runtime_error("thin_svd: no resident Jacobi configuration");
+  const i64 cw = resident ? slab(CS) : cap_rows;  // rows per CTA (slab)
+  const int prefetch_v = resident && nj > 0 && dyn_for(cw, 1) <= dyn_cap(CS) ? 1 : 0;  // W and V slabs both fit
+  const size_t smem = dyn_for(cw, prefetch_v);
   if (resident) {
     static unsigned configured = 0;
     if (!(configured & (1u << dev))) {
-      const size_t max_smem = sizeof(double) * (kResidentRows * JW + 4 * JW * JW);
-      DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(max_smem)));
-      DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     220000));
-      DFCG_CUDA(cudaFuncSetAttribute(jacobi_round_resident_kernel<NB, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     220000));
+      auto opt_in = [&](const void* fn, size_t b) {
+        DFCG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
+      };
+      const size_t s8 = 232448 - sizeof(double) * (3 * 16 * 17 + 8) - 1024 - 1024;
+      const size_t s16 = 232448 - sizeof(double) * (3 * 32 * 33 + 8) - 1024;
+      opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<8, 1>), s8);
+      opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<8, 2>), s8 - 2048);
+      opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<8, 4>), s8 - 2048);
+      opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<16, 1>), s16);
+      opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<16, 2>), s16 - 8192);
+      opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<16, 4>), s16 - 8192);
       configured |= 1u << dev;
     }
   }
   auto launch_round = [&](int r) {
     const int inner = r == 0 ? 1 : 0;
-    if (CS == 1) {
-      jacobi_round_resident_kernel<NB, 1><<<npairs, 256, smem, s>>>(wrows, nj, W.get(), np, J.get(), np, p, r, tol,
-                                                                    off.get(), inner, prefetch_v);
-      return;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(npairs * CS));
     cfg.blockDim = dim3(256);
@@ -1369,17 +1411,24 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = CS > 1 ? 1 : 0;
     double* Wp = W.get();
     double* Jp = J.get();
     unsigned long long* op = off.get();
     const i64 ld = np;
-    if (CS == 2)
-      DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_resident_kernel<NB, 2>, wrows, nj, Wp, ld, Jp, ld, p, r, tol, op,
-                                   inner, prefetch_v));
-    else
-      DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_resident_kernel<NB, 4>, wrows, nj, Wp, ld, Jp, ld, p, r, tol, op,
-                                   inner, prefetch_v));
+#define DFCG_JROUND(nb, cs)                                                                                        \
+  DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_resident_kernel<nb, cs>, wrows, nj, Wp, ld, Jp, ld, p, r, tol, op, \
+                               inner, prefetch_v))
+    if (NB == 8) {
+      if (CS == 1) DFCG_JROUND(8, 1);
+      else if (CS == 2) DFCG_JROUND(8, 2);
+      else DFCG_JROUND(8, 4);
+    } else {
+      if (CS == 1) DFCG_JROUND(16, 1);
+      else if (CS == 2) DFCG_JROUND(16, 2);
+      else DFCG_JROUND(16, 4);
+    }
+#undef DFCG_JROUND
   };
   static const bool trace_svd = std::getenv("DFCG_TRACE_SVD") != nullptr;
   const bool small = cols <= kSmallN && wrows <= kSmallN && nj <= kSmallN;
@@ -1423,8 +1472,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
         if (resident)
           launch_round(r);
         else
-          jacobi_round_kernel<NB><<<npairs, 16 * NB, 0, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol, off.get(),
-                                                              2);
+          jacobi_round_kernel<8><<<npairs, 16 * 8, 0, s>>>(wrows, nj, W.get(), np, J.get(), np, pr, tol, off.get(), 2);
         DFCG_LAUNCH_CHECK();
       }
     }
