@@ -335,6 +335,15 @@ def main():
     prof = P.prof_collect()
     P.prof_enable(False)
     roof = roofline_entry(prof, peaks, peak_kind)
+    # the tensor-core GEMMs (>= 2 GFLOP: the operator products, CholQR Grams / triangular
+    # products, the left factor) of that step, against the FP64 DMMA roofline
+    g = prof.get("gemm", {})
+    roof_gemm = None
+    if g.get("launches", 0) > 0 and g["ms"] > 0:
+        ach = g["flops"] / (g["ms"] * 1e-3) / 1e12
+        roof_gemm = dict(bound="tensor", achieved=ach, peak=FP64_DMMA_PEAK_TFLOPS, unit="TFLOP/s",
+                         frac=ach / FP64_DMMA_PEAK_TFLOPS, launches=g["launches"],
+                         avg_launch_ms=g["ms"] / g["launches"], kernel="gemm_kernel (DMMA m8n8k4)")
 
     # combine on the current block estimates (column_project, P/include/dfc/sketch.hpp:170-199):
     # basis broadcast + per-rank projection + row gather over NCCL when N > 1
@@ -418,7 +427,7 @@ def main():
                                        f"{args.prologue + args.warmup + args.steps} of every block",
                                 blocks_per_gpu=len(mine), l2="inputs > L2 (no flush)",
                                 parallelism=f"{wl['t']} blocks over {world} GPU(s), one CUDA stream per block"),
-                    roofline=roof, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
+                    roofline=roof, roofline_gemm=roof_gemm, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
                     clocks=clocks.summary(), combine_ms=combine_ms,
                     combine=dict(ms=combine_ms, device_ops=combine_ops,
                                  note="DFC-Proj column_project of the 8 block estimates (host factors in and out; "

@@ -494,12 +494,21 @@ DeviceContext::~DeviceContext() {
 
 namespace {
 std::atomic<int> g_active_streams[64];
-}
+// Counts a solve as active on its device while it is stepping (RAII).
+struct ActiveSolve {
+  int dev;
+  explicit ActiveSolve(int d) : dev(d) {
+    if (dev >= 0 && dev < 64) g_active_streams[dev]++;
+  }
+  ~ActiveSolve() {
+    if (dev >= 0 && dev < 64) g_active_streams[dev]--;
+  }
+};
+}  // namespace
 int active_streams(int dev) { return dev >= 0 && dev < 64 ? g_active_streams[dev].load() : 1; }
 
 cudaStream_t DeviceContext::acquire() {
   std::lock_guard<std::mutex> lock(mu);
-  if (device >= 0 && device < 64) g_active_streams[device]++;
   if (!free_streams.empty()) {
     cudaStream_t st = free_streams.back();
     free_streams.pop_back();
@@ -513,7 +522,6 @@ cudaStream_t DeviceContext::acquire() {
 
 void DeviceContext::release(cudaStream_t st) {
   std::lock_guard<std::mutex> lock(mu);
-  if (device >= 0 && device < 64) g_active_streams[device]--;
   free_streams.push_back(st);
 }
 
@@ -610,6 +618,7 @@ McSolver::~McSolver() = default;
 // One iteration of the apg_mc loop (solvers.hpp:275-317).
 bool McSolver::step(std::vector<IterTrace>* trace) {
   if (stopped_ || iters_ >= cfg_.max_iters) return false;
+  ActiveSolve busy(ctx_.device);
   // ncu --profile-from-start off: DFCG_PROFILE_ITER=k brackets iteration k of every solve.
   static const int profile_iter = std::getenv("DFCG_PROFILE_ITER") ? std::atoi(std::getenv("DFCG_PROFILE_ITER")) : -1;
   struct ProfRange {
@@ -752,6 +761,7 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
                     const ApgConfig& cfg, DevLowRank& out, std::vector<long long>& s_row, std::vector<long long>& s_col,
                     std::vector<double>& s_val, SolveReport& rep, std::vector<IterTrace>* trace) {
   const auto start = std::chrono::steady_clock::now();
+  ActiveSolve busy(ctx.device);
   if (!(lambda > 0)) throw std::invalid_argument("apg_rmf: lambda must be positive");
   const i64 mn = m * n;
   for (i64 i = 0; i < mn; ++i)

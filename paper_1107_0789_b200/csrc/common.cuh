@@ -139,8 +139,8 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 #endif
 
-// Solves currently holding a stream of device `dev`'s context (DeviceContext acquire/release):
-// kernels with a latency / occupancy trade-off (the Jacobi cluster size) consult it.
+// APG solves currently stepping on device `dev`: kernels with a latency / occupancy trade-off
+// (the Jacobi cluster size) consult it.
 int active_streams(int dev);
 
 // ---------------------------------------------------------------- factorizations (factor.cu)
