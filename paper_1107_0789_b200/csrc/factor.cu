@@ -292,6 +292,23 @@ __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
 
 // In-place blocked Cholesky of G (n x n) -> upper R (lower part zeroed); Rinv = R^-1.
 // want_inverse == false: only R is produced (Rinv then holds just the diagonal-block inverses).
+// Per host thread and device: a helper stream and two events (created once, never destroyed:
+// they live as long as the thread's CUDA context use).
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t updated = nullptr, factored = nullptr;
+};
+AuxStream& aux_stream(int dev) {
+  thread_local AuxStream aux[64];
+  AuxStream& a = aux[dev & 63];
+  if (!a.s) {
+    DFCG_CUDA(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
+    DFCG_CUDA(cudaEventCreateWithFlags(&a.updated, cudaEventDisableTiming));
+    DFCG_CUDA(cudaEventCreateWithFlags(&a.factored, cudaEventDisableTiming));
+  }
+  return a;
+}
+
 void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol,
                           int* fail, bool want_inverse) {
   static unsigned configured = 0;  // one bit per device: opt in to > 48 KB dynamic shared memory
@@ -306,22 +323,36 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   diag_max_kernel<<<1, 256, 0, s>>>(n, G, ldg, maxdiag.get());
   DFCG_LAUNCH_CHECK();
   DFCG_CUDA(cudaMemset2DAsync(Rinv, sizeof(double) * ldr, 0, sizeof(double) * n, n, s));
+  // Look-ahead: after the panel TRSM of block k, the next diagonal block is updated first and
+  // factored on a helper stream while the rest of the trailing update runs on s, so the
+  // latency-bound 64x64 potrf overlaps the trailing GEMM instead of following it.
+  AuxStream& aux = aux_stream(dev);
+  auto potrf = [&](cudaStream_t st, i64 k0, int kb) {
+    prof::Scope scope(prof::kCholesky, st, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
+    potrf_diag_kernel<<<1, 256, kPotrfSmem, st>>>(kb, G + k0 * ldg + k0, ldg, Rinv + k0 * ldr + k0, ldr,
+                                                  maxdiag.get(), rel_tol, fail);
+    DFCG_LAUNCH_CHECK();
+  };
+  potrf(s, 0, static_cast<int>(std::min<i64>(CNB, n)));
   for (i64 k0 = 0; k0 < n; k0 += CNB) {
     const int kb = static_cast<int>(std::min<i64>(CNB, n - k0));
-    double* Gkk = G + k0 * ldg + k0;
-    prof::Scope scope(prof::kCholesky, s, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
-    potrf_diag_kernel<<<1, 256, kPotrfSmem, s>>>(kb, Gkk, ldg, Rinv + k0 * ldr + k0, ldr, maxdiag.get(), rel_tol,
-                                                 fail);
-    DFCG_LAUNCH_CHECK();
+    if (k0 > 0) DFCG_CUDA(cudaStreamWaitEvent(s, aux.factored, 0));  // potrf(k) ran on the helper
     const i64 rem = n - k0 - kb;
-    if (rem > 0) {
-      double* panel = G + k0 * ldg + k0 + kb;  // kb x rem
-      // R[k, J] = Rkk^-T G[k, J]
-      gemm(s, true, false, kb, rem, kb, 1.0, Rinv + k0 * ldr + k0, ldr, panel, ldg, 0.0, panel, ldg);
-      // G[J, J] -= R[k,J]^T R[k,J]
-      double* trail = G + (k0 + kb) * ldg + k0 + kb;
-      gemm(s, true, false, rem, rem, kb, -1.0, panel, ldg, panel, ldg, 1.0, trail, ldg);
-    }
+    if (rem <= 0) break;
+    double* panel = G + k0 * ldg + k0 + kb;  // kb x rem
+    // R[k, J] = Rkk^-T G[k, J]
+    gemm(s, true, false, kb, rem, kb, 1.0, Rinv + k0 * ldr + k0, ldr, panel, ldg, 0.0, panel, ldg);
+    // next diagonal block: G[k1, k1] -= R[k, k1]^T R[k, k1], then factored on the helper stream
+    const i64 k1 = k0 + kb;
+    const int kb1 = static_cast<int>(std::min<i64>(CNB, rem));
+    gemm(s, true, false, kb1, kb1, kb, -1.0, panel, ldg, panel, ldg, 1.0, G + k1 * ldg + k1, ldg);
+    DFCG_CUDA(cudaEventRecord(aux.updated, s));
+    DFCG_CUDA(cudaStreamWaitEvent(aux.s, aux.updated, 0));
+    potrf(aux.s, k1, kb1);
+    DFCG_CUDA(cudaEventRecord(aux.factored, aux.s));
+    // the rest of the trailing update (rows k1.., columns past the next diagonal block)
+    if (rem > kb1)
+      gemm(s, true, false, rem, rem - kb1, kb, -1.0, panel, ldg, panel + kb1, ldg, 1.0, G + k1 * ldg + k1 + kb1, ldg);
   }
   zero_lower_kernel<<<grid_for(n * n), 256, 0, s>>>(n, G, ldg);
   DFCG_LAUNCH_CHECK();
