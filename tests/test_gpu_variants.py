@@ -1,0 +1,28 @@
+"""The kernel variants selected by heuristics (or only by environment switches) must give the
+same parity: Jacobi rounds on 2- and 4-CTA clusters and with 16-column blocks, the 64x64 /
+64x48 GEMM tiles, the unscaled Cholesky. Each variant runs in a child process (the switches are
+read once per process)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("env", [
+    {"DFCG_JACOBI_CLUSTER": "2"},
+    {"DFCG_JACOBI_CLUSTER": "4"},
+    {"DFCG_JACOBI_NB": "16"},
+    {"DFCG_JACOBI_NB": "16", "DFCG_JACOBI_CLUSTER": "2"},
+    {"DFCG_GEMM_VARIANT": "4"},
+    {"DFCG_GEMM_VARIANT": "7"},
+    {"DFCG_CHOL_SCALE": "0"},
+], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
+def test_variant_parity(env):
+    r = subprocess.run([sys.executable, os.path.join(HERE, "_variant_case.py")], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
