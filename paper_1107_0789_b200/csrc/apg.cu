@@ -61,6 +61,39 @@ void residual_combine(cudaStream_t s, i64 n, double a, const double* pc, double 
   DFCG_LAUNCH_CHECK();
 }
 
+// Dense APG-MC operator, column-major m x w (== row-major w x m): with step 1 the operator
+// G = Y - (P_Omega(Y) - P_Omega(M)) of FactoredSparseOp (solvers.hpp:112-136) is Y off the
+// observed set and M on it. Pass 1: A = a Dc + b Dp (a term with coefficient 0 is skipped,
+// its buffer may be stale).
+__global__ void dense_extrap_kernel(i64 n, double a, const double* __restrict__ dc, double b,
+                                    const double* __restrict__ dp, double* __restrict__ A) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    double v = 0.0;
+    if (a != 0.0) v = a * dc[i];
+    if (b != 0.0) v = fma(b, dp[i], v);
+    A[i] = v;
+  }
+}
+
+// Pass 2 (one CTA per column, CSC walk: rows ascend, so the stores of a column coalesce):
+// A[j, i] = M_e for every observed (i, j).
+__global__ void dense_observe_kernel(i64 m, const int* __restrict__ colptr, const int* __restrict__ crow,
+                                     const double* __restrict__ m_csc, double* __restrict__ A) {
+  const i64 j = blockIdx.x;
+  double* col = A + j * m;
+  for (int p = colptr[j] + threadIdx.x; p < colptr[j + 1]; p += blockDim.x) col[crow[p]] = m_csc[p];
+}
+
+// P_Omega of a dense column-major iterate, written in CSR order: out[csc2csr[p]] = D[j, row_p].
+__global__ void dense_gather_kernel(i64 m, const int* __restrict__ colptr, const int* __restrict__ crow,
+                                    const long long* __restrict__ csc2csr, const double* __restrict__ D,
+                                    double* __restrict__ out) {
+  const i64 j = blockIdx.x;
+  const double* col = D + j * m;
+  for (int p = colptr[j] + threadIdx.x; p < colptr[j + 1]; p += blockDim.x) out[csc2csr[p]] = col[crow[p]];
+}
+
 __global__ void fill_kernel(i64 n, double v, double* x) {
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x)
@@ -590,7 +623,40 @@ struct McSolver::State {
   std::vector<double> last_s;
   double mu_init = 0, mu_floor = 0, tau_prev = 1.0, tau_curr = 1.0, mu = 0, mu_used = 0;
   i64 rank_hint = 1;
+  // Dense-operator mode (high-rank iterations, see dense_operator()): the current / previous
+  // iterates as dense column-major m x n matrices (dc_ok / dp_ok: in sync with Lc / Lp) and
+  // the materialised operator.
+  DBuf<double> Dc, Dp, Ad;
+  bool dc_ok = false, dp_ok = false;
 };
+
+// Whether an iteration applies the SVT operator materialised (dense m x n, step 1:
+// Y off Omega, M on it) instead of factored (left right^T - R with SpMM). Six applications
+// per partial SVD cost 2 m n b FLOPs each dense, against 2 (m+n) kY b in the low-rank GEMMs
+// plus an SpMM over N entries (gather-bound: ~8x its FLOP count at GEMM rate); the dense
+// form adds one m x n x r GEMM per iteration (the new iterate) and two HBM passes. At a c2
+// block at default ApgConfig (m=1e4, n=1250, N=1.25e6, kY~1440) the dense form does ~20%
+// fewer FLOPs and no sparse gathers; in the low-rank regime (kY ~ 2r ~ 60) the factored
+// form wins. DFCG_DENSE_OP=0|1 forces a mode (tests). Not used with line search (step < 1).
+static bool dense_operator(i64 m, i64 n, i64 nnz, i64 kY, bool line_search) {
+  const char* env = std::getenv("DFCG_DENSE_OP");  // read per call: tests switch it in-process
+  const int mode = env ? std::atoi(env) : -1;
+  if (line_search || mode == 0) return false;
+  const double mn = static_cast<double>(m) * static_cast<double>(n);
+  if (3.0 * 8.0 * mn > 16e9) return false;  // three dense m x n buffers per solve
+  if (mode == 1) return true;
+  return static_cast<double>(m + n) * static_cast<double>(kY) + 8.0 * static_cast<double>(nnz) >= mn;
+}
+
+// D (column-major m x n == row-major n x m) = L.left L.right^T, or 0 for a zero estimate.
+static void densify(cudaStream_t s, const DevLowRank& L, i64 m, i64 n, DBuf<double>& D) {
+  D.ensure(m * n, s);
+  if (L.k == 0) {
+    D.zero(s);
+    return;
+  }
+  gemm(s, false, true, n, m, L.k, 1.0, L.right.get(), L.k, L.left.get(), L.k, 0.0, D.get(), m);
+}
 
 McSolver::McSolver(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows,
                    const long long* cols, const double* vals, const ApgConfig& cfg)
@@ -641,9 +707,27 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   DevLowRank& Lp = st.Lp;
   const bool concat = !(beta == 0.0 || Lp.k == 0);
   const i64 kY = concat ? Lc.k + Lp.k : Lc.k;
+  const bool dense = dense_operator(m, n, nnz, kY, cfg_.line_search);
+  if (dense) {
+    // A = (1+beta) Dc - beta Dp off Omega, M on Omega (column-major m x n)
+    if (!st.dc_ok) densify(s, Lc, m, n, st.Dc);
+    st.dc_ok = true;
+    if (concat && !st.dp_ok) {
+      densify(s, Lp, m, n, st.Dp);
+      st.dp_ok = true;
+    }
+    st.Ad.ensure(m * n, s);
+    prof::Scope scope(prof::kElementwise, s, 3.0 * m * n, 8.0 * m * n * (1.0 + (Lc.k > 0) + concat) + 20.0 * nnz);
+    dense_extrap_kernel<<<grid_for(m * n), 256, 0, s>>>(m * n, Lc.k > 0 ? 1.0 + beta : 0.0, st.Dc.get(),
+                                                        concat ? -beta : 0.0, st.Dp.get(), st.Ad.get());
+    DFCG_LAUNCH_CHECK();
+    dense_observe_kernel<<<static_cast<int>(n), 256, 0, s>>>(m, st.om.csc_colptr.get(), st.om.csc_row.get(),
+                                                             st.om.m_csc.get(), st.Ad.get());
+    DFCG_LAUNCH_CHECK();
+  }
   DBuf<double> Yl, Yr;
   const i64 ldy = std::max<i64>(1, even_ld(kY));  // even: 16-byte GEMM operand loads
-  if (kY > 0) {
+  if (kY > 0 && !dense) {
     Yl.alloc(m * ldy, s);
     Yr.alloc(n * ldy, s);
     if (Lc.k > 0) {
@@ -656,13 +740,19 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
     }
   }
   // R = P_Omega(Y) - P_Omega(M) = (1+beta) P_Omega(L_curr) - beta P_Omega(L_prev) - P_Omega(M)
-  residual_combine(s, nnz, Lc.k > 0 ? 1.0 + beta : 0.0, st.pc.get(), concat ? -beta : 0.0, st.pp.get(),
-                   st.om.m_csr.get(), st.r_csr.get());
-  csr_to_csc(s, st.om, st.r_csr.get(), st.r_csc.get());
+  if (!dense) {
+    residual_combine(s, nnz, Lc.k > 0 ? 1.0 + beta : 0.0, st.pc.get(), concat ? -beta : 0.0, st.pp.get(),
+                     st.om.m_csr.get(), st.r_csr.get());
+    csr_to_csc(s, st.om, st.r_csr.get(), st.r_csc.get());
+  }
 
   double step = 1.0;
   SvtResult f;
-  for (;;) {
+  if (dense) {
+    OpDense G{st.Ad.get(), m, n};
+    svt_operator(s, G, st.mu, st.rank_hint, st.cur, f);
+  }
+  for (; !dense;) {
     OpMC G{&st.om, st.r_csr.get(), st.r_csc.get(), -step, m, n, kY, Yl.get(), Yr.get(), Lc.k, ldy};
     f = SvtResult{};
     svt_operator(s, G, step * st.mu, st.rank_hint, st.cur, f);
@@ -683,7 +773,31 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   }
   // rel = ||L_next - L_curr|| / max(1, ||L_curr||) via factored inner products (:305-306)
   double inn, inc;
-  if (f.grams && f.r > 0) {  // m-side Grams come with the SVT result; only the n-side GEMMs remain
+  if (dense) {
+    // L_next densified (the next iteration's Dc); the factored inner products of the stop
+    // test (solvers.hpp:179-193) as Frobenius inner products of the dense iterates — the
+    // same quantities and the same cancellation formula below.
+    std::swap(st.Dc, st.Dp);
+    st.dp_ok = st.dc_ok;
+    DevLowRank nx;
+    nx.k = f.r;
+    nx.left = std::move(f.left);
+    nx.right = std::move(f.right);
+    densify(s, nx, m, n, st.Dc);
+    st.dc_ok = true;
+    f.left = std::move(nx.left);
+    f.right = std::move(nx.right);
+    const double* pn = st.Dc.get();
+    const double* pcur = st.Dp.get();
+    const bool have_c = Lc.k > 0;
+    auto sums = multi_sum<2>(s, m * n, [=] __device__(i64 i, double* acc) {
+      const double v = pn[i];
+      acc[0] += v * v;
+      if (have_c) acc[1] += v * pcur[i];
+    });
+    inn = f.r > 0 ? sums[0] : 0.0;
+    inc = (f.r > 0 && have_c) ? sums[1] : 0.0;
+  } else if (f.grams && f.r > 0) {  // m-side Grams come with the SVT result; only the n-side GEMMs remain
     DBuf<double> rr(f.r * f.r, s);
     gemm(s, true, false, f.r, f.r, n, 1.0, f.right.get(), f.r, f.right.get(), f.r, 0.0, rr.get(), f.r);
     inn = dev_dot(s, f.r * f.r, f.ll.get(), rr.get());
@@ -699,7 +813,17 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   }
   // P_Omega(L_next) for the next residual (pp <- pc <- new)
   std::swap(st.pc, st.pp);
-  if (f.r > 0) sddmm_residual(s, st.om, f.r, f.left.get(), f.r, f.right.get(), f.r, nullptr, st.pc.get());
+  if (dense) {
+    dense_gather_kernel<<<static_cast<int>(n), 256, 0, s>>>(m, st.om.csc_colptr.get(), st.om.csc_row.get(),
+                                                            st.om.csc2csr.get(), st.Dc.get(), st.pc.get());
+    DFCG_LAUNCH_CHECK();
+  } else {
+    if (f.r > 0) sddmm_residual(s, st.om, f.r, f.left.get(), f.r, f.right.get(), f.r, nullptr, st.pc.get());
+    // the dense copies (if any) shift with the iterates: old Dc is the new Dp
+    std::swap(st.Dc, st.Dp);
+    st.dp_ok = st.dc_ok;
+    st.dc_ok = false;
+  }
   const double d2 = inn - 2.0 * inc + st.icc;
   const double rel = std::sqrt(std::max(0.0, d2)) / std::max(1.0, std::sqrt(std::max(0.0, st.icc)));
   const double tau_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * st.tau_curr * st.tau_curr));

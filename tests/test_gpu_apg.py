@@ -26,7 +26,10 @@ pytestmark = pytest.mark.gpu
                                    # CholQR breakdown -> Householder fallback in the range finder
     (130, 75, 3, 3000, 0.1, 9),    # ragged 64x64 SDDMM tiles in both directions
 ])
-def test_apg_mc_parity(m, n, r, s, sigma, seed):
+@pytest.mark.parametrize("op_mode", ["0", "1"], ids=["factored_op", "dense_op"])
+def test_apg_mc_parity(m, n, r, s, sigma, seed, op_mode, monkeypatch):
+    # both SVT operator forms: factored (SDDMM + SpMM + low-rank GEMMs) and materialised
+    monkeypatch.setenv("DFCG_DENSE_OP", op_mode)
     L0, obs = P.gen_mc_instance(m, n, r, s, sigma, seed)
     assert_mc_parity(obs)
 
@@ -67,7 +70,10 @@ def test_apg_mc_acceptance_floor_500():  # acceptance criterion 3 setup (P/tests
     assert O.rmse(O.Estimate(L0.left, L0.right), O.Estimate(ep.left, ep.right)) < 0.15
 
 
-def test_apg_mc_c1_block_window():  # BASELINE c1 block shape 1000 x 250, default config, 60 iterations
+@pytest.mark.parametrize("op_mode", ["0", "1", "auto"])
+def test_apg_mc_c1_block_window(op_mode, monkeypatch):  # BASELINE c1 block 1000 x 250, default config, 60 its
+    if op_mode != "auto":
+        monkeypatch.setenv("DFCG_DENSE_OP", op_mode)
     L0, obs = P.gen_mc_instance(1000, 1000, 10, 200000, 0.1, 1)
     groups = P.partition_columns(1, 0xDFC0000000000001, 1000, 4)
     blk = P.extract_columns(obs, groups[0])
