@@ -61,10 +61,9 @@ void residual_combine(cudaStream_t s, i64 n, double a, const double* pc, double 
   DFCG_LAUNCH_CHECK();
 }
 
-// Dense APG-MC operator, column-major m x w (== row-major w x m): with step 1 the operator
-// G = Y - (P_Omega(Y) - P_Omega(M)) of FactoredSparseOp (solvers.hpp:112-136) is Y off the
-// observed set and M on it. Pass 1: A = a Dc + b Dp (a term with coefficient 0 is skipped,
-// its buffer may be stale).
+// Dense APG-MC operator, row-major m x w: with step 1 the operator G = Y - (P_Omega(Y) -
+// P_Omega(M)) of FactoredSparseOp (solvers.hpp:112-136) is Y off the observed set and M on it.
+// Pass 1: A = a Dc + b Dp (a term with coefficient 0 is skipped, its buffer may be stale).
 __global__ void dense_extrap_kernel(i64 n, double a, const double* __restrict__ dc, double b,
                                     const double* __restrict__ dp, double* __restrict__ A) {
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
@@ -76,22 +75,21 @@ __global__ void dense_extrap_kernel(i64 n, double a, const double* __restrict__ 
   }
 }
 
-// Pass 2 (one CTA per column, CSC walk: rows ascend, so the stores of a column coalesce):
-// A[j, i] = M_e for every observed (i, j).
-__global__ void dense_observe_kernel(i64 m, const int* __restrict__ colptr, const int* __restrict__ crow,
-                                     const double* __restrict__ m_csc, double* __restrict__ A) {
-  const i64 j = blockIdx.x;
-  double* col = A + j * m;
-  for (int p = colptr[j] + threadIdx.x; p < colptr[j + 1]; p += blockDim.x) col[crow[p]] = m_csc[p];
+// Pass 2 (one CTA per row, CSR walk: columns ascend, so the stores of a row coalesce):
+// A[i, j] = M_e for every observed (i, j).
+__global__ void dense_observe_kernel(i64 w, const int* __restrict__ rowptr, const int* __restrict__ ccol,
+                                     const double* __restrict__ m_csr, double* __restrict__ A) {
+  const i64 i = blockIdx.x;
+  double* row = A + i * w;
+  for (int e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) row[ccol[e]] = m_csr[e];
 }
 
-// P_Omega of a dense column-major iterate, written in CSR order: out[csc2csr[p]] = D[j, row_p].
-__global__ void dense_gather_kernel(i64 m, const int* __restrict__ colptr, const int* __restrict__ crow,
-                                    const long long* __restrict__ csc2csr, const double* __restrict__ D,
-                                    double* __restrict__ out) {
-  const i64 j = blockIdx.x;
-  const double* col = D + j * m;
-  for (int p = colptr[j] + threadIdx.x; p < colptr[j + 1]; p += blockDim.x) out[csc2csr[p]] = col[crow[p]];
+// P_Omega of a dense row-major iterate in CSR order: out[e] = D[row_e, col_e].
+__global__ void dense_gather_kernel(i64 w, const int* __restrict__ rowptr, const int* __restrict__ ccol,
+                                    const double* __restrict__ D, double* __restrict__ out) {
+  const i64 i = blockIdx.x;
+  const double* row = D + i * w;
+  for (int e = rowptr[i] + threadIdx.x; e < rowptr[i + 1]; e += blockDim.x) out[e] = row[ccol[e]];
 }
 
 __global__ void fill_kernel(i64 n, double v, double* x) {
@@ -281,6 +279,44 @@ struct OpMC {
     else DFCG_CUDA(cudaMemsetAsync(D, 0, sizeof(double) * m * w, s));
     scatter_add_dense(s, *om, r_csr, coeff, D, w);
   }
+};
+
+// The dense APG-MC operator (row-major m x w), see dense_operator().
+struct OpDenseRM {
+  const double* A;
+  i64 m, w;
+  i64 rows() const { return m; }
+  i64 cols() const { return w; }
+  void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    gemm(s, false, false, m, b, w, 1.0, A, w, X, ldx, 0.0, out, ldo);
+  }
+  void apply_adjoint(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo,
+                     DBuf<double>* = nullptr) const {
+    gemm(s, true, false, w, b, m, 1.0, A, w, X, ldx, 0.0, out, ldo);
+  }
+  i64 keep_rows() const { return -1; }
+  void to_dense(cudaStream_t s, double* D) const { copy2d(s, m, w, A, w, D, w); }
+};
+
+// The same operator compressed by a CholeskyQR2 factor A = Q_A R_A (m >= w, Q_A orthonormal,
+// never formed): every range-finder quantity of partial_svd is basis-invariant, so the SVT of A
+// runs on the w x w triangle R_A in Q_A's coordinates (orth(A Z) = Q_A orth(R_A Z), A^T Q_A Q~
+// = R_A^T Q~) and only the left factor maps back, U = Q_A U~ = A R_A^-1 U~. R_A is backward
+// stable (A = Q_A R_A + O(eps ||A||)), like the products with A it replaces.
+struct OpTri {
+  const double* R;  // w x w row-major, upper (lower part zero)
+  i64 w;
+  i64 rows() const { return w; }
+  i64 cols() const { return w; }
+  void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    gemm(s, false, false, w, b, w, 1.0, R, w, X, ldx, 0.0, out, ldo);
+  }
+  void apply_adjoint(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo,
+                     DBuf<double>* = nullptr) const {
+    gemm(s, true, false, w, b, w, 1.0, R, w, X, ldx, 0.0, out, ldo);
+  }
+  i64 keep_rows() const { return -1; }
+  void to_dense(cudaStream_t s, double* D) const { copy2d(s, w, w, R, w, D, w); }
 };
 
 // DenseOp (solvers.hpp:138-145) over a column-major m x w matrix A (== row-major w x m "At").
@@ -626,9 +662,39 @@ struct McSolver::State {
   // Dense-operator mode (high-rank iterations, see dense_operator()): the current / previous
   // iterates as dense column-major m x n matrices (dc_ok / dp_ok: in sync with Lc / Lp) and
   // the materialised operator.
-  DBuf<double> Dc, Dp, Ad;
+  DBuf<double> Dc, Dp, Ad[2];
   bool dc_ok = false, dp_ok = false;
+  // Compressed dense iterations: R_A, R_A^-1 of the current operator; an estimate whose left
+  // factor was not formed keeps (lazy_* = index of the operator buffer Ad[] it came from, cl_*
+  // = R_A^-1 U~, w x k): left = A cl.
+  DBuf<double> RA, RAinv, cl_c, cl_p;
+  int lazy_c = -1, lazy_p = -1;
+  int ad_next = 0;  // Ad[] buffer the next dense iteration writes
 };
+
+// left = Ad[src] cl (m x k) for an estimate produced by a compressed dense iteration.
+static void materialize_left(cudaStream_t s, i64 m, i64 n, const DBuf<double>& A, const DBuf<double>& cl,
+                             DevLowRank& L) {
+  L.left.alloc(m * L.k, s);
+  gemm(s, false, false, m, L.k, n, 1.0, A.get(), n, cl.get(), L.k, 0.0, L.left.get(), L.k);
+}
+
+// Whether a dense iteration compresses the operator (cost model in FLOPs, m >= n only):
+// uncompressed ~ m n (12 b + 2 r) + 5 m b^2 + 2 m b r (six products with A, the m-side
+// CholQR, the left factor, the densified iterate); compressed ~ 5 m n^2 (CholeskyQR2 of A:
+// two Grams and a triangular product, and the iterate as A (R_A^-1 P)). DFCG_DENSE_OP=1 / 2
+// forces uncompressed / compressed (when admissible).
+static bool compress_operator(i64 m, i64 n, i64 rank_hint) {
+  if (m < n) return false;
+  const char* env = std::getenv("DFCG_DENSE_OP");
+  const int mode = env ? std::atoi(env) : -1;
+  if (mode == 1) return false;
+  if (mode == 2) return true;
+  if (n < 128) return false;
+  const double b = static_cast<double>(std::min<i64>(rank_hint + 15, n)), r = static_cast<double>(rank_hint);
+  const double nn = static_cast<double>(n);
+  return 12.0 * b + 2.0 * r + 5.0 * b * b / nn + 2.0 * b * r / nn > 5.0 * nn;
+}
 
 // Whether an iteration applies the SVT operator materialised (dense m x n, step 1:
 // Y off Omega, M on it) instead of factored (left right^T - R with SpMM). Six applications
@@ -636,26 +702,27 @@ struct McSolver::State {
 // plus an SpMM over N entries (gather-bound: ~8x its FLOP count at GEMM rate); the dense
 // form adds one m x n x r GEMM per iteration (the new iterate) and two HBM passes. At a c2
 // block at default ApgConfig (m=1e4, n=1250, N=1.25e6, kY~1440) the dense form does ~20%
-// fewer FLOPs and no sparse gathers; in the low-rank regime (kY ~ 2r ~ 60) the factored
-// form wins. DFCG_DENSE_OP=0|1 forces a mode (tests). Not used with line search (step < 1).
+// fewer FLOPs and no sparse gathers (and its compressed variant, compress_operator(), ~45%
+// fewer); in the low-rank regime (kY ~ 2r ~ 60) the factored form wins. DFCG_DENSE_OP=0
+// forces the factored form, 1 / 2 the dense one (tests). Not used with line search (step < 1).
 static bool dense_operator(i64 m, i64 n, i64 nnz, i64 kY, bool line_search) {
   const char* env = std::getenv("DFCG_DENSE_OP");  // read per call: tests switch it in-process
   const int mode = env ? std::atoi(env) : -1;
   if (line_search || mode == 0) return false;
   const double mn = static_cast<double>(m) * static_cast<double>(n);
   if (3.0 * 8.0 * mn > 16e9) return false;  // three dense m x n buffers per solve
-  if (mode == 1) return true;
+  if (mode >= 1) return true;
   return static_cast<double>(m + n) * static_cast<double>(kY) + 8.0 * static_cast<double>(nnz) >= mn;
 }
 
-// D (column-major m x n == row-major n x m) = L.left L.right^T, or 0 for a zero estimate.
+// D (row-major m x n) = L.left L.right^T, or 0 for a zero estimate.
 static void densify(cudaStream_t s, const DevLowRank& L, i64 m, i64 n, DBuf<double>& D) {
   D.ensure(m * n, s);
   if (L.k == 0) {
     D.zero(s);
     return;
   }
-  gemm(s, false, true, n, m, L.k, 1.0, L.right.get(), L.k, L.left.get(), L.k, 0.0, D.get(), m);
+  gemm(s, false, true, m, n, L.k, 1.0, L.left.get(), L.k, L.right.get(), L.k, 0.0, D.get(), n);
 }
 
 McSolver::McSolver(DeviceContext& ctx, cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows,
@@ -708,22 +775,46 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   const bool concat = !(beta == 0.0 || Lp.k == 0);
   const i64 kY = concat ? Lc.k + Lp.k : Lc.k;
   const bool dense = dense_operator(m, n, nnz, kY, cfg_.line_search);
+  if (!dense) {  // the factored operator needs the left factors compressed iterations deferred
+    if (st.lazy_c >= 0) materialize_left(s, m, n, st.Ad[st.lazy_c], st.cl_c, Lc);
+    if (concat && st.lazy_p >= 0) materialize_left(s, m, n, st.Ad[st.lazy_p], st.cl_p, Lp);
+    if (st.lazy_c >= 0) st.lazy_c = -1;
+    if (concat && st.lazy_p >= 0) st.lazy_p = -1;
+  }
+  bool compressed = false;
+  int ai = -1;  // Ad[] buffer holding this iteration's dense operator
   if (dense) {
-    // A = (1+beta) Dc - beta Dp off Omega, M on Omega (column-major m x n)
+    // A = (1+beta) Dc - beta Dp off Omega, M on Omega (row-major m x n)
     if (!st.dc_ok) densify(s, Lc, m, n, st.Dc);
     st.dc_ok = true;
     if (concat && !st.dp_ok) {
       densify(s, Lp, m, n, st.Dp);
       st.dp_ok = true;
     }
-    st.Ad.ensure(m * n, s);
-    prof::Scope scope(prof::kElementwise, s, 3.0 * m * n, 8.0 * m * n * (1.0 + (Lc.k > 0) + concat) + 20.0 * nnz);
-    dense_extrap_kernel<<<grid_for(m * n), 256, 0, s>>>(m * n, Lc.k > 0 ? 1.0 + beta : 0.0, st.Dc.get(),
-                                                        concat ? -beta : 0.0, st.Dp.get(), st.Ad.get());
-    DFCG_LAUNCH_CHECK();
-    dense_observe_kernel<<<static_cast<int>(n), 256, 0, s>>>(m, st.om.csc_colptr.get(), st.om.csc_row.get(),
-                                                             st.om.m_csc.get(), st.Ad.get());
-    DFCG_LAUNCH_CHECK();
+    ai = st.ad_next;
+    st.ad_next ^= 1;
+    // Ad[ai] may be the source of a deferred left factor: L_curr's is formed first (it becomes
+    // L_prev, which a following factored iteration needs); L_prev's is dropped with L_prev.
+    if (st.lazy_c == ai) {
+      materialize_left(s, m, n, st.Ad[ai], st.cl_c, Lc);
+      st.lazy_c = -1;
+    }
+    if (st.lazy_p == ai) st.lazy_p = -2;  // lost: L_prev is not used in factored form again
+    st.Ad[ai].ensure(m * n, s);
+    {
+      prof::Scope scope(prof::kElementwise, s, 3.0 * m * n, 8.0 * m * n * (1.0 + (Lc.k > 0) + concat) + 20.0 * nnz);
+      dense_extrap_kernel<<<grid_for(m * n), 256, 0, s>>>(m * n, Lc.k > 0 ? 1.0 + beta : 0.0, st.Dc.get(),
+                                                          concat ? -beta : 0.0, st.Dp.get(), st.Ad[ai].get());
+      DFCG_LAUNCH_CHECK();
+      dense_observe_kernel<<<static_cast<int>(m), 256, 0, s>>>(n, st.om.csr_rowptr.get(), st.om.csr_col.get(),
+                                                               st.om.m_csr.get(), st.Ad[ai].get());
+      DFCG_LAUNCH_CHECK();
+    }
+    if (compress_operator(m, n, st.rank_hint)) {
+      st.RA.ensure(n * n, s);
+      st.RAinv.ensure(n * n, s);
+      compressed = cholqr2_r(s, m, n, st.Ad[ai].get(), n, st.RA.get(), st.RAinv.get(), 1e-13);
+    }
   }
   DBuf<double> Yl, Yr;
   const i64 ldy = std::max<i64>(1, even_ld(kY));  // even: 16-byte GEMM operand loads
@@ -748,8 +839,11 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
 
   double step = 1.0;
   SvtResult f;
-  if (dense) {
-    OpDense G{st.Ad.get(), m, n};
+  if (compressed) {
+    OpTri G{st.RA.get(), n};
+    svt_operator(s, G, st.mu, st.rank_hint, st.cur, f);
+  } else if (dense) {
+    OpDenseRM G{st.Ad[ai].get(), m, n};
     svt_operator(s, G, st.mu, st.rank_hint, st.cur, f);
   }
   for (; !dense;) {
@@ -779,14 +873,38 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
     // same quantities and the same cancellation formula below.
     std::swap(st.Dc, st.Dp);
     st.dp_ok = st.dc_ok;
-    DevLowRank nx;
-    nx.k = f.r;
-    nx.left = std::move(f.left);
-    nx.right = std::move(f.right);
-    densify(s, nx, m, n, st.Dc);
+    if (compressed) {
+      // f.left = U~ (Q_A coordinates): cl = R_A^-1 U~, L_next = A (cl right^T); the m x r left
+      // factor itself is deferred (materialize_left) until a factored iteration or finish().
+      st.Dc.ensure(m * n, s);
+      DBuf<double> cl;
+      if (f.r > 0) {
+        cl.alloc(n * f.r, s);
+        gemm(s, false, false, n, f.r, n, 1.0, st.RAinv.get(), n, f.left.get(), f.r, 0.0, cl.get(), f.r);
+        DBuf<double> T2(n * n, s);
+        gemm(s, false, true, n, n, f.r, 1.0, cl.get(), f.r, f.right.get(), f.r, 0.0, T2.get(), n);
+        gemm(s, false, false, m, n, n, 1.0, st.Ad[ai].get(), n, T2.get(), n, 0.0, st.Dc.get(), n);
+      } else {
+        st.Dc.zero(s);
+      }
+      f.left = DBuf<double>{};
+      st.lazy_p = st.lazy_c;
+      std::swap(st.cl_p, st.cl_c);
+      st.cl_c = std::move(cl);
+      st.lazy_c = f.r > 0 ? ai : -1;
+    } else {
+      DevLowRank nx;
+      nx.k = f.r;
+      nx.left = std::move(f.left);
+      nx.right = std::move(f.right);
+      densify(s, nx, m, n, st.Dc);
+      f.left = std::move(nx.left);
+      f.right = std::move(nx.right);
+      st.lazy_p = st.lazy_c;
+      std::swap(st.cl_p, st.cl_c);
+      st.lazy_c = -1;
+    }
     st.dc_ok = true;
-    f.left = std::move(nx.left);
-    f.right = std::move(nx.right);
     const double* pn = st.Dc.get();
     const double* pcur = st.Dp.get();
     const bool have_c = Lc.k > 0;
@@ -814,8 +932,8 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   // P_Omega(L_next) for the next residual (pp <- pc <- new)
   std::swap(st.pc, st.pp);
   if (dense) {
-    dense_gather_kernel<<<static_cast<int>(n), 256, 0, s>>>(m, st.om.csc_colptr.get(), st.om.csc_row.get(),
-                                                            st.om.csc2csr.get(), st.Dc.get(), st.pc.get());
+    dense_gather_kernel<<<static_cast<int>(m), 256, 0, s>>>(n, st.om.csr_rowptr.get(), st.om.csr_col.get(),
+                                                            st.Dc.get(), st.pc.get());
     DFCG_LAUNCH_CHECK();
   } else {
     if (f.r > 0) sddmm_residual(s, st.om, f.r, f.left.get(), f.r, f.right.get(), f.r, nullptr, st.pc.get());
@@ -823,6 +941,9 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
     std::swap(st.Dc, st.Dp);
     st.dp_ok = st.dc_ok;
     st.dc_ok = false;
+    st.lazy_p = st.lazy_c;
+    std::swap(st.cl_p, st.cl_c);
+    st.lazy_c = -1;
   }
   const double d2 = inn - 2.0 * inc + st.icc;
   const double rel = std::sqrt(std::max(0.0, d2)) / std::max(1.0, std::sqrt(std::max(0.0, st.icc)));
@@ -850,6 +971,10 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
 void McSolver::finish(DevLowRank& out, SolveReport& rep) {
   State& st = *st_;
   cudaStream_t s = s_;
+  if (st.lazy_c >= 0) {
+    materialize_left(s, m_, n_, st.Ad[st.lazy_c], st.cl_c, st.Lc);
+    st.lazy_c = -1;
+  }
   const DevLowRank& Lc = st.Lc;
   rep.iterations = iters_;
   rep.rank = Lc.k;

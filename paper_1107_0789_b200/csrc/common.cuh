@@ -157,6 +157,12 @@ bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, 
 // R^T R = X^T X, so X Rinv has orthonormal columns to ~eps cond(X)^2. Returns false (Rinv
 // unusable) when a Cholesky pivot signals cond(X) >~ 3e5.
 bool cholqr_factor(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* Rinv, i64 ldr);
+// CholeskyQR2 R factor of a tall row-major rows x cols matrix A (A = Q R, Q orthonormal and
+// never formed beyond the first pass): R (cols x cols, upper, lower part zero) and Rinv = R^-1.
+// rel_tol1: breakdown threshold of the first pass's (Jacobi-scaled) Cholesky pivots. Returns
+// false on breakdown (cond(A) too large for CholeskyQR2); R / Rinv are then unusable.
+bool cholqr2_r(cudaStream_t s, i64 rows, i64 cols, const double* A, i64 lda, double* R, double* Rinv,
+               double rel_tol1);
 // Householder QR only (tests / fallback).
 void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
 

@@ -1264,6 +1264,34 @@ bool cholqr_factor(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx,
   return h_fail == 0;
 }
 
+bool cholqr2_r(cudaStream_t s, i64 rows, i64 cols, const double* A, i64 lda, double* R, double* Rinv,
+               double rel_tol1) {
+  if (cols <= 0) return true;
+  DBuf<int> fail(1, s);
+  fail.zero(s);
+  DBuf<double> G(cols * cols, s), R1inv(cols * cols, s), Q1(rows * cols, s), R2inv(cols * cols, s);
+  // pass 1: R1^T R1 = A^T A, Q1 = A R1^-1 (orthogonal to ~eps cond(A)^2)
+  gram_upper(s, rows, cols, A, lda, G.get(), cols);
+  cholesky_inverse(s, cols, G.get(), cols, R1inv.get(), cols, rel_tol1, fail.get());
+  int h_fail = 0;
+  DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  if (h_fail) return false;
+  gemm_upper_b(s, rows, cols, 1.0, A, lda, R1inv.get(), cols, 0.0, Q1.get(), cols);
+  // pass 2 on the explicit Q1: R2^T R2 = Q1^T Q1; A = (Q1 R2^-1) (R2 R1)
+  gram_upper(s, rows, cols, Q1.get(), cols, R, cols);
+  cholesky_inverse(s, cols, R, cols, R2inv.get(), cols, 1e-11, fail.get());
+  DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaStreamSynchronize(s));
+  if (h_fail) return false;
+  // R = R2 R1 (G still holds R1), Rinv = R1^-1 R2^-1: products of upper triangles whose lower
+  // parts are stored as zeros (Q1 is free scratch now)
+  gemm_upper_b(s, cols, cols, 1.0, R, cols, G.get(), cols, 0.0, Q1.get(), cols);
+  copy2d(s, cols, cols, Q1.get(), cols, R, cols);
+  gemm_upper_b(s, cols, cols, 1.0, R1inv.get(), cols, R2inv.get(), cols, 0.0, Rinv, cols);
+  return true;
+}
+
 bool thin_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr, int passes) {
   if (cols <= 0) return false;
   if (rows < cols) throw std::invalid_argument("thin_qr: rows < cols");

@@ -26,9 +26,10 @@ pytestmark = pytest.mark.gpu
                                    # CholQR breakdown -> Householder fallback in the range finder
     (130, 75, 3, 3000, 0.1, 9),    # ragged 64x64 SDDMM tiles in both directions
 ])
-@pytest.mark.parametrize("op_mode", ["0", "1"], ids=["factored_op", "dense_op"])
+@pytest.mark.parametrize("op_mode", ["0", "1", "2"], ids=["factored_op", "dense_op", "dense_qr_op"])
 def test_apg_mc_parity(m, n, r, s, sigma, seed, op_mode, monkeypatch):
-    # both SVT operator forms: factored (SDDMM + SpMM + low-rank GEMMs) and materialised
+    # every SVT operator form: factored (SDDMM + SpMM + low-rank GEMMs), materialised, and
+    # materialised + CholeskyQR2-compressed (m >= n)
     monkeypatch.setenv("DFCG_DENSE_OP", op_mode)
     L0, obs = P.gen_mc_instance(m, n, r, s, sigma, seed)
     assert_mc_parity(obs)
@@ -70,7 +71,7 @@ def test_apg_mc_acceptance_floor_500():  # acceptance criterion 3 setup (P/tests
     assert O.rmse(O.Estimate(L0.left, L0.right), O.Estimate(ep.left, ep.right)) < 0.15
 
 
-@pytest.mark.parametrize("op_mode", ["0", "1", "auto"])
+@pytest.mark.parametrize("op_mode", ["0", "1", "2", "auto"])
 def test_apg_mc_c1_block_window(op_mode, monkeypatch):  # BASELINE c1 block 1000 x 250, default config, 60 its
     if op_mode != "auto":
         monkeypatch.setenv("DFCG_DENSE_OP", op_mode)
@@ -78,6 +79,17 @@ def test_apg_mc_c1_block_window(op_mode, monkeypatch):  # BASELINE c1 block 1000
     groups = P.partition_columns(1, 0xDFC0000000000001, 1000, 4)
     blk = P.extract_columns(obs, groups[0])
     assert_mc_parity(blk, max_iters=60)
+
+
+def test_apg_mc_operator_switching():
+    """A sparse block whose rank rises past and falls back below the dense-operator threshold
+    (acceptance-style floor, P/tests/acceptance.cpp:127-130): iterations switch between the
+    factored and the (compressed) dense operator and back, including the deferred left factors
+    of compressed iterations."""
+    m, n = 2000, 400
+    L0, obs = P.gen_mc_instance(m, n, 10, m * n // 20, 0.1, 13)
+    floor = 0.1 * np.sqrt(0.05) * (np.sqrt(m) + np.sqrt(n))
+    assert_mc_parity(obs, mu_floor=floor, max_iters=150)
 
 
 def test_apg_mc_all_zero_observations():  # P/tests/test_solvers.cpp:131-139

@@ -29,6 +29,10 @@ struct Shape {
 
 int main() {
   const Shape shapes[] = {
+      {"dense apply TN 10000x720x1250", true, false, 10000, 720, 1250, 0},
+      {"dense adj   NN 1250x720x10000", false, false, 1250, 720, 10000, 0},
+      {"densify     NT 1250x10000x700", false, true, 1250, 10000, 700, 0},
+      {"left X*coef NN 10000x700x720", false, false, 10000, 700, 720, 0},
       {"Yl*T        NN 10000x720x1437", false, false, 10000, 720, 1437, 0},
       {"Yl*T even   NN 10000x720x1438", false, false, 10000, 720, 1438, 0},
       {"Yl^T*X even TN 1438x720x10000", true, false, 1438, 720, 10000, 0},
