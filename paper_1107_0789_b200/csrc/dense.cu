@@ -8,6 +8,7 @@
 #include "common.cuh"
 
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 
@@ -463,10 +464,28 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
     DFCG_LAUNCH_CHECK();
     return;
   }
+  // DFCG_TRACE_GEMM=1 (diagnostics, while kernel accounting is enabled): time every call alone
+  static const bool trace = std::getenv("DFCG_TRACE_GEMM") != nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (trace && prof::g_enabled.load()) {
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, s);
+  }
   if (!ta && !tb) launch_gemm<false, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else if (ta && !tb) launch_gemm<true, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else if (!ta && tb) launch_gemm<false, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else launch_gemm<true, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+  if (t0) {
+    cudaEventRecord(t1, s);
+    cudaEventSynchronize(t1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    std::fprintf(stderr, "[gemm] %c%c M=%lld N=%lld K=%lld  %.1f us  %.2f TF/s\n", ta ? 'T' : 'N', tb ? 'T' : 'N',
+                 (long long)M, (long long)N, (long long)K, ms * 1e3, 2.0 * M * N * K / (ms * 1e-3) / 1e12);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
 }
 
 void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,

@@ -904,12 +904,28 @@ __global__ void __launch_bounds__(256) jacobi_small_kernel(int rows, int n, int 
 // and rotating a contiguous slab of the rows; the 16x16 partial Grams are summed over the
 // cluster through distributed shared memory in rank order (every CTA gets the identical Gram
 // and runs the identical inner EVD). Used when few solves share the GPU (single-block latency).
+// Per-SVD arguments of the round kernel, read from device memory so the p - 1 launches of a
+// sweep are identical across SVDs of one shape class and their CUDA graph is reused (the
+// round index and the inner-sweep count stay kernel parameters, fixed per graph node).
+struct JacobiArgs {
+  i64 rows, nv, ldw, ldv;
+  double* W;
+  double* V;
+  unsigned long long* offmax;
+  double tol;
+  int p, prefetch_v;
+};
+
 template <int NB, int CS>
-__global__ void __launch_bounds__(256, NB == 8 ? 2 : 1) jacobi_round_resident_kernel(i64 rows_, i64 nv_, double* W, i64 ldw, double* V,
-                                                                    i64 ldv, int p, int round, double tol,
-                                                                    unsigned long long* offmax, int inner_sweeps,
-                                                                    int prefetch_v) {
+__global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
+    jacobi_round_resident_kernel(const JacobiArgs* __restrict__ ja, int round, int inner_sweeps) {
   static_assert(NB == 8 || NB == 16, "8- or 16-column blocks (16 or 32 columns per pair)");
+  const i64 rows_ = ja->rows, nv_ = ja->nv, ldw = ja->ldw, ldv = ja->ldv;
+  double* W = ja->W;
+  double* V = ja->V;
+  unsigned long long* offmax = ja->offmax;
+  const double tol = ja->tol;
+  const int p = ja->p, prefetch_v = ja->prefetch_v;
   constexpr int JW = 2 * NB, T = 256, NT = JW / 8, CH = JW / 2, KS = JW / 4;
   extern __shared__ __align__(16) double dyn[];
   const int crank = static_cast<int>(blockIdx.x % CS), pk = static_cast<int>(blockIdx.x / CS);
@@ -1459,12 +1475,60 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       configured |= 1u << dev;
     }
   }
+  // Optional (DFCG_JACOBI_GRAPH=1): the p - 1 round launches of a sweep, identical from sweep
+  // to sweep, captured once into a CUDA graph and replayed per sweep — measured 9.7 -> 8.4 ms of
+  // Jacobi per c2 iteration for a lone block, but slower whenever several solves share the GPU
+  // (92 vs 109 block-it/s with eight; 65 when selected per call by the number of active solves,
+  // the instantiations of the per-thread graphs landing in the timed window), so the rounds are
+  // launched directly by default.
+  // Graph cache (per host thread): one captured sweep per shape class (device, block width,
+  // cluster size, pair count, V prefetch, shared-memory bucket), with its own argument block
+  // and off-diagonal accumulator at fixed addresses. The shared memory is bucketed to 64-row
+  // slabs so consecutive SVDs of slowly varying width share a graph.
+  static const int graph_env = std::getenv("DFCG_JACOBI_GRAPH") ? std::atoi(std::getenv("DFCG_JACOBI_GRAPH")) : -1;
+  const bool use_graph = graph_env == 1;
+  struct SweepGraph {
+    int dev, nb, cs, npairs, pre;
+    size_t smem;
+    cudaGraphExec_t exec;
+    JacobiArgs* d_args;
+    unsigned long long* d_off;
+  };
+  thread_local std::vector<SweepGraph> graphs;
+  const bool small_svd = cols <= kSmallN && wrows <= kSmallN && nj <= kSmallN;
+  size_t smem_launch = smem;
+  SweepGraph* sg = nullptr;
+  bool capture = false;
+  if (resident && !small_svd && use_graph) {
+    const i64 cw_b = (cw + 63) / 64 * 64;
+    if (dyn_for(cw_b, prefetch_v) <= dyn_cap(CS)) smem_launch = dyn_for(cw_b, prefetch_v);
+    for (SweepGraph& g : graphs)
+      if (g.dev == dev && g.nb == NB && g.cs == CS && g.npairs == npairs && g.pre == prefetch_v && g.smem == smem_launch)
+        sg = &g;
+    if (!sg && graphs.size() < 64) {
+      graphs.push_back(SweepGraph{dev, NB, CS, npairs, prefetch_v, smem_launch, nullptr, nullptr, nullptr});
+      sg = &graphs.back();
+      DFCG_CUDA(cudaMalloc(reinterpret_cast<void**>(&sg->d_args), sizeof(JacobiArgs)));
+      DFCG_CUDA(cudaMalloc(reinterpret_cast<void**>(&sg->d_off), sizeof(unsigned long long)));
+      capture = true;
+    }
+  }
+  // this SVD's argument block: the cached graph's, or a stream-ordered one
+  DBuf<JacobiArgs> own_args;
+  JacobiArgs* d_args = sg ? sg->d_args : nullptr;
+  unsigned long long* d_off = sg ? sg->d_off : off.get();
+  if (!sg) {
+    own_args.alloc(1, s);
+    d_args = own_args.get();
+  }
+  const JacobiArgs h_args{wrows, nj, np, np, W.get(), J.get(), d_off, tol, p, prefetch_v};
+  DFCG_CUDA(cudaMemcpyAsync(d_args, &h_args, sizeof(JacobiArgs), cudaMemcpyHostToDevice, s));
   auto launch_round = [&](int r) {
     const int inner = r == 0 ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(npairs * CS));
     cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = smem_launch;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1473,13 +1537,8 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = CS > 1 ? 1 : 0;
-    double* Wp = W.get();
-    double* Jp = J.get();
-    unsigned long long* op = off.get();
-    const i64 ld = np;
-#define DFCG_JROUND(nb, cs)                                                                                        \
-  DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_resident_kernel<nb, cs>, wrows, nj, Wp, ld, Jp, ld, p, r, tol, op, \
-                               inner, prefetch_v))
+    const JacobiArgs* ap = d_args;
+#define DFCG_JROUND(nb, cs) DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_resident_kernel<nb, cs>, ap, r, inner))
     if (NB == 8) {
       if (CS == 1) DFCG_JROUND(8, 1);
       else if (CS == 2) DFCG_JROUND(8, 2);
@@ -1523,9 +1582,24 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
                    (long long)cols, h, ov);
     }
   }
+  if (capture) {
+    DFCG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    DFCG_CUDA(cudaMemsetAsync(sg->d_off, 0, sizeof(unsigned long long), s));
+    for (int r = 0; r < p - 1; ++r) launch_round(r);
+    cudaGraph_t graph = nullptr;
+    DFCG_CUDA(cudaStreamEndCapture(s, &graph));
+    DFCG_CUDA(cudaGraphInstantiate(&sg->exec, graph, 0));
+    DFCG_CUDA(cudaGraphDestroy(graph));
+  }
+  cudaGraphExec_t sweep_exec = sg ? sg->exec : nullptr;
   for (int sweep = 0; sweep < 60 && !small; ++sweep) {
-    off.zero(s);
-    {
+    if (sweep_exec) {
+      prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
+                        (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW);
+      DFCG_CUDA(cudaGraphLaunch(sweep_exec, s));
+      prof::count_launch(p - 1);
+    } else {
+      off.zero(s);
       prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
                         (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW);
       for (int r = 0; r < p - 1; ++r) {
@@ -1538,7 +1612,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       }
     }
     unsigned long long h_off = 0;
-    DFCG_CUDA(cudaMemcpyAsync(&h_off, off.get(), sizeof(h_off), cudaMemcpyDeviceToHost, s));
+    DFCG_CUDA(cudaMemcpyAsync(&h_off, d_off, sizeof(h_off), cudaMemcpyDeviceToHost, s));
     DFCG_CUDA(cudaStreamSynchronize(s));
     double offv;
     std::memcpy(&offv, &h_off, sizeof(double));

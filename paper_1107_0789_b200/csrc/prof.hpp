@@ -29,7 +29,7 @@ enum Op : int {
 extern std::atomic<bool> g_enabled;
 extern std::atomic<long long> g_launches;
 
-inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // RAII scope: records start/stop events on `s` when profiling is enabled.
 class Scope {

@@ -10,10 +10,11 @@ groups = P.partition_columns(1, 0xDFC0000000000001, 10000, 8)
 blocks = [P.extract_columns(obs, g) for g in groups]
 pool = ThreadPoolExecutor(8)
 P.apg_mc(blocks[0], P.ApgConfig(max_iters=2))  # context + normal cache warm
-t0 = time.time()
-outs = list(pool.map(lambda b: (time.time(), P.apg_mc(b, P.ApgConfig()), time.time()), blocks))
-wall = time.time() - t0
-print(f"wall {wall:.2f}s")
+for rep_i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 1):
+    t0 = time.time()
+    outs = list(pool.map(lambda b: (time.time(), P.apg_mc(b, P.ApgConfig()), time.time()), blocks))
+    wall = time.time() - t0
+    print(f"run {rep_i}: wall {wall:.2f}s", flush=True)
 edges = [0, 10, 30, 100, 200, 300, 400, 500]
 for g, (ts, (est, rep), te) in enumerate(outs):
     ms = np.array([t["ms"] for t in rep.trace])
