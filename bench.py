@@ -20,9 +20,16 @@ H2D/D2H inside the timed region): block-iterations/s over the whole solve, plus 
 """
 from __future__ import annotations
 
+import os
+
+# Eight solves (each with a Cholesky look-ahead helper stream) plus the normal-stream upload share
+# the GPU: with the default 8 hardware work queues, streams alias onto the same queue and
+# serialise against each other (measured 45-112 block-it/s run to run; 97-122 with 32 queues).
+# Read when the CUDA context is created, so it is set before torch initialises CUDA.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import argparse
 import json
-import os
 import subprocess
 import sys
 import threading
@@ -54,34 +61,55 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region: ONE long-running
+    `nvidia-smi --query-gpu=... -lms 200` (the profiling recipe's clocks line), started before the
+    warm-up so its NVML initialisation stays out of the timed region (spawning nvidia-smi per
+    sample measured as a stall of the concurrent solves); only samples taken between mark() and
+    exit are kept."""
 
     QUERY = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device, self.samples, self._stop = device, [], threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self.device, self.samples, self._t0 = device, [], None
+        self._proc = None
+        self._reader = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            for line in self._proc.stdout:
+                if self._t0 is not None and line.strip():
+                    self.samples.append([x.strip() for x in line.strip().split(",")])
+        except Exception:
+            pass
+
+    def start(self):
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                                           "--format=csv,noheader,nounits", "-lms", "200"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._reader.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def mark(self):
+        self._t0 = time.perf_counter()
 
     def __enter__(self):
-        self._t.start()
+        self.mark()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        time.sleep(0.25)  # at least one sample covering the end of the region
+        self._t0 = None
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
 
     def summary(self):
         if not self.samples:
@@ -299,6 +327,7 @@ def main():
             dist.barrier()
 
     advance(args.prologue)
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         advance(1)
     barrier()
@@ -307,7 +336,7 @@ def main():
     # The K steps run back to back per block: every block's thread advances it K iterations on
     # its own stream, as the F step runs (blocks are independent, P/include/dfc/dfc.hpp:133-147);
     # a host barrier per iteration would only line the blocks' phases up against each other.
-    with ClockSampler(local) as clocks:
+    with clocks:
         e0.record()
         iters = advance(args.steps)
         torch.cuda.synchronize()

@@ -9,7 +9,14 @@ orchestrator. This module is a thin ctypes mirror of that ABI with the reference
 There is no CPU fallback: importing works anywhere, but every compute call needs the CUDA
 library and a GPU and raises if either is missing.
 """
-from ._lib import (  # noqa: F401
+import os as _os
+
+# Concurrent block solves use two streams each; 32 hardware work queues keep them from aliasing
+# onto shared queues (read at CUDA context creation: effective when this package is imported
+# before the process initialises CUDA; bench.py sets it first thing).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+from ._lib import (  # noqa: F401,E402
     ApgConfig,
     BlockError,
     DfcError,
@@ -32,7 +39,7 @@ from ._lib import (  # noqa: F401
     random_project,
     svd_of_product,
 )
-from .host import (  # noqa: F401
+from .host import (  # noqa: F401,E402
     extract_columns,
     extract_rows,
     gen_mc_instance,

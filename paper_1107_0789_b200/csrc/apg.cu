@@ -549,6 +549,12 @@ DeviceContext::DeviceContext(int dev) : device(dev) {
   DFCG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
   std::uint64_t threshold = UINT64_MAX;
   DFCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  // Solves share the device pool from concurrent streams: memory freed on one solve's stream
+  // must not be handed to another with an inserted wait on the first stream's pending work
+  // (that couples independent blocks); reuse is only stream-local, opportunistic (the free has
+  // already completed) or along existing event dependencies.
+  int no = 0;
+  DFCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no));
   normals_mc = std::make_unique<NormalCache>(dev, 0x737674u, 0);
   normals_rmf = std::make_unique<NormalCache>(dev, 0x737674u, 1);
 }

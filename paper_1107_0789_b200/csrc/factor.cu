@@ -1075,7 +1075,58 @@ __global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
   int cur = 0;
   const bool cross = inner_sweeps == 0;
   const int nsteps = cross ? NB : (JW - 1) * inner_sweeps;
-  for (int it = 0; it < nsteps; ++it) {
+  if constexpr (NB == 8) {
+    // Warp-synchronous EVD (16 x 16): warp 0 runs every step with __syncwarp between steps
+    // instead of a CTA barrier. Lane l computes rotation k = l % 8 (four copies), owns the Gram
+    // 2x2 blocks (P = l / 4, Q = 2 (l % 4) + {0, 1}) with the other rotations taken by shuffles,
+    // and rotates rows l / 8 + 4 j (j < 4) of the accumulator for its own pair k.
+    if (warp == 0) {
+      for (int it = 0; it < nsteps; ++it) {
+        const int step = cross ? it : it % (JW - 1);
+        auto pair_of = [&](int k, int& a, int& b) {
+          if (cross) {
+            a = k;
+            b = NB + ((k + step) & (NB - 1));
+          } else {
+            jpair<JW>(step, k, a, b);
+          }
+        };
+        const int k = lane & 7, P = lane >> 2;
+        int a, b, aP, bP;
+        pair_of(k, a, b);
+        pair_of(P, aP, bP);
+        double c, sn;
+        jrot(g[cur], a, b, c, sn);
+        const double cP = __shfl_sync(0xffffffffu, c, P), sP = __shfl_sync(0xffffffffu, sn, P);
+        const int nx = cur ^ 1;
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int Q = 2 * (lane & 3) + qq;
+          int aQ, bQ;
+          pair_of(Q, aQ, bQ);
+          const double cQ = __shfl_sync(0xffffffffu, c, Q), sQ = __shfl_sync(0xffffffffu, sn, Q);
+          const double x00 = g[cur][aP][aQ], x01 = g[cur][aP][bQ], x10 = g[cur][bP][aQ], x11 = g[cur][bP][bQ];
+          const double y00 = cQ * x00 - sQ * x01, y01 = sQ * x00 + cQ * x01;  // columns: G J_Q
+          const double y10 = cQ * x10 - sQ * x11, y11 = sQ * x10 + cQ * x11;
+          g[nx][aP][aQ] = cP * y00 - sP * y10;  // rows: J_P^T (G J_Q)
+          g[nx][bP][aQ] = sP * y00 + cP * y10;
+          g[nx][aP][bQ] = cP * y01 - sP * y11;
+          g[nx][bP][bQ] = sP * y01 + cP * y11;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = (lane >> 3) + 4 * j;
+          const double ra = rot[r][a], rb = rot[r][b];
+          rot[r][a] = c * ra - sn * rb;
+          rot[r][b] = sn * ra + c * rb;
+        }
+        __syncwarp();
+        cur = nx;
+      }
+    }
+    __syncthreads();
+  }
+  for (int it = 0; NB != 8 && it < nsteps; ++it) {
     const int step = cross ? it : it % (JW - 1);
     auto pair_of = [&](int k, int& a, int& b) {
       if (cross) {
