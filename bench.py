@@ -318,8 +318,17 @@ def main():
     solvers = {g: P.McSolver(blocks[g], cfg, device=local) for g in mine}
     pool = ThreadPoolExecutor(max_workers=max(1, len(mine)))
 
-    def advance(n):
-        return sum(pool.map(lambda g: solvers[g].step(n), mine))
+    trace_window = os.environ.get("DFCG_BENCH_TRACE") == "1"  # diagnostics: per-iteration host times
+
+    def advance(n, trace=False):
+        if not trace:
+            return sum(pool.map(lambda g: solvers[g].step(n), mine))
+        t0 = time.perf_counter()
+        outs = list(pool.map(lambda g: (g, solvers[g].step(n, trace=True), time.perf_counter() - t0), mine))
+        for g, (done, tr), t_end in outs:
+            print(f"[window] block {g}: end {t_end * 1e3:.1f} ms, its " +
+                  " ".join(f"{t['it']}:{t['ms']:.1f}/r{t['rank']}/c{t['svd_calls']}" for t in tr), file=sys.stderr)
+        return sum(d for _, (d, _), _ in outs)
 
     def barrier():
         torch.cuda.synchronize()
@@ -338,7 +347,7 @@ def main():
     # a host barrier per iteration would only line the blocks' phases up against each other.
     with clocks:
         e0.record()
-        iters = advance(args.steps)
+        iters = advance(args.steps, trace_window)
         torch.cuda.synchronize()
         e1.record()
         e1.synchronize()

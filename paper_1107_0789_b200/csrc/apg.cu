@@ -555,6 +555,22 @@ DeviceContext::DeviceContext(int dev) : device(dev) {
   // already completed) or along existing event dependencies.
   int no = 0;
   DFCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no));
+  // Reserve the pool up front (DFCG_POOL_RESERVE_GB, default 16; 0 disables): growing it maps new
+  // memory under a context-wide driver lock, a stall every concurrent solve then shares.
+  const char* res_env = std::getenv("DFCG_POOL_RESERVE_GB");
+  const double reserve_gb = res_env ? std::atof(res_env) : 16.0;
+  size_t free_b = 0, total_b = 0;
+  DFCG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t reserve = static_cast<size_t>(std::min(reserve_gb * 1e9, 0.5 * static_cast<double>(free_b)));
+  if (reserve > 0) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, reserve, nullptr) == cudaSuccess) {
+      DFCG_CUDA(cudaFreeAsync(p, nullptr));
+      DFCG_CUDA(cudaStreamSynchronize(nullptr));
+    } else {
+      cudaGetLastError();
+    }
+  }
   normals_mc = std::make_unique<NormalCache>(dev, 0x737674u, 0);
   normals_rmf = std::make_unique<NormalCache>(dev, 0x737674u, 1);
 }

@@ -73,7 +73,7 @@ class SeededRng {
 class NormalCache {
  public:
   static constexpr i64 kChunk = i64{1} << 22;  // 4 Mi normals = 32 MiB per chunk
-  static constexpr i64 kAhead = 2;
+  static constexpr i64 kAhead = 4;
 
   NormalCache(int device, std::uint64_t seed, std::uint64_t stream) : device_(device), rng_(seed, stream) {}
   ~NormalCache() {
@@ -133,7 +133,9 @@ class NormalCache {
         // Raw 64-bit draws are sequential (mt19937_64); the Box-Muller transform runs on host
         // threads so the stream stays bit-identical to the reference's std::log/std::cos.
         for (auto& r : raw) r = rng_.next_u64();
-        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        // A few transform threads only: the generator runs beside the solves' host threads, and a
+        // burst that takes every core delays their kernel launches (the GPU then idles).
+        const unsigned nt = std::max(1u, std::min(4u, std::thread::hardware_concurrency() / 4));
         std::vector<std::thread> pool;
         for (unsigned t = 0; t < nt; ++t)
           pool.emplace_back([&, t] {
