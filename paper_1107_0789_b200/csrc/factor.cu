@@ -1651,9 +1651,11 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       prof::count_launch(p - 1);
     } else {
       off.zero(s);
-      prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
-                        (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW);
       for (int r = 0; r < p - 1; ++r) {
+        // accounting per round launch (algorithmic: Gram + rotation of the pair's columns,
+        // every W / V element read and written once)
+        prof::Scope scope(prof::kJacobi, s, 1.0 * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
+                          1.0 * npairs * 16.0 * (wrows + nj) * JW);
         const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
         if (resident)
           launch_round(r);
