@@ -169,6 +169,9 @@ int dfcg_random_project(dfcg_ctx* ctx, int64_t t, const dfcg_lowrank* blocks, co
 /* Compact SVD of left * right^T (svd_of_product); out = (U, V diag(s)), s copied to s_out
  * (caller buffer of size >= min(m, n, k)) when non-null, rank in *rank. */
 int dfcg_svd_of_product(dfcg_ctx* ctx, const dfcg_lowrank* in, dfcg_lowrank* out, double* s_out, int64_t* rank);
+/* Diagnostics: normals [pos, pos+n) of the device-cached SVT stream SeededRng(0x737674, stream_id)
+ * (stream_id 0: apg_mc, 1: apg_rmf; P/include/dfc/solvers.hpp:263,344) copied to host out[n]. */
+int dfcg_normals_fetch(dfcg_ctx* ctx, int stream_id, int64_t pos, int64_t n, double* out);
 
 /* One block of the DFC-Proj combine, for the multi-GPU split of column_project
  * (sketch.hpp:194-196): Rg = block.right (Ub^T block.left)^T, Ub m x kb column-major, Rg

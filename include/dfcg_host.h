@@ -20,6 +20,8 @@ extern "C" {
 #endif
 
 void dfcg_rng_u64(uint64_t seed, uint64_t stream, int64_t n, uint64_t* out);
+/* The same raw stream from the bulk (vectorised) mt19937_64 the device normal cache uses. */
+void dfcg_rng_u64_bulk(uint64_t seed, uint64_t stream, int64_t n, uint64_t* out);
 void dfcg_rng_uniform(uint64_t seed, uint64_t stream, int64_t n, double* out);
 void dfcg_rng_normal(uint64_t seed, uint64_t stream, int64_t n, double* out);
 int dfcg_rng_index(uint64_t seed, uint64_t stream, int64_t count, uint64_t bound, uint64_t* out);

@@ -247,6 +247,10 @@ struct OpMC {
   i64 ldy;
   i64 rows() const { return m; }
   i64 cols() const { return w; }
+  i64 zrows() const { return w; }  // rows of the n-side range-finder vectors
+  void apply_g0(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    apply(s, X, ldx, b, out, ldo);
+  }
   void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {  // w x b -> m x b
     if (kY > 0) {
       const i64 ldt = even_ld(b);
@@ -287,6 +291,10 @@ struct OpDenseRM {
   i64 m, w;
   i64 rows() const { return m; }
   i64 cols() const { return w; }
+  i64 zrows() const { return w; }
+  void apply_g0(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    apply(s, X, ldx, b, out, ldo);
+  }
   void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
     gemm(s, false, false, m, b, w, 1.0, A, w, X, ldx, 0.0, out, ldo);
   }
@@ -308,6 +316,10 @@ struct OpTri {
   i64 w;
   i64 rows() const { return w; }
   i64 cols() const { return w; }
+  i64 zrows() const { return w; }
+  void apply_g0(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    apply(s, X, ldx, b, out, ldo);
+  }
   void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
     gemm(s, false, false, w, b, w, 1.0, R, w, X, ldx, 0.0, out, ldo);
   }
@@ -319,12 +331,41 @@ struct OpTri {
   void to_dense(cudaStream_t s, double* D) const { copy2d(s, w, w, R, w, D, w); }
 };
 
+// Wide dense operator (m < n) compressed by CholeskyQR2 of its transpose: A^T = Q_B R, i.e.
+// A = R^T Q_B^T (R m x m upper). The first range-finder product is A G0 itself; every later
+// n-side vector lies in span(Q_B) and is kept in its coordinates (Z = Q_B Z~): A Z = R^T Z~,
+// A^T Q = Q_B (R Q). The right factor maps back as V = Q_B V~ = A^T R^-1 V~ (deferred).
+struct OpWideQR {
+  const double* A;  // m x n row-major
+  const double* R;  // m x m row-major, upper (lower part zero)
+  i64 m, n;
+  i64 rows() const { return m; }
+  i64 cols() const { return n; }
+  i64 zrows() const { return m; }
+  void apply_g0(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    gemm(s, false, false, m, b, n, 1.0, A, n, X, ldx, 0.0, out, ldo);
+  }
+  void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    gemm(s, true, false, m, b, m, 1.0, R, m, X, ldx, 0.0, out, ldo);
+  }
+  void apply_adjoint(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo,
+                     DBuf<double>* = nullptr) const {
+    gemm(s, false, false, m, b, m, 1.0, R, m, X, ldx, 0.0, out, ldo);
+  }
+  i64 keep_rows() const { return -1; }
+  void to_dense(cudaStream_t s, double* D) const { transpose(s, m, m, R, m, D, m); }  // R^T
+};
+
 // DenseOp (solvers.hpp:138-145) over a column-major m x w matrix A (== row-major w x m "At").
 struct OpDense {
   const double* At;
   i64 m, w;
   i64 rows() const { return m; }
   i64 cols() const { return w; }
+  i64 zrows() const { return w; }
+  void apply_g0(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
+    apply(s, X, ldx, b, out, ldo);
+  }
   void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
     gemm(s, true, false, m, b, w, 1.0, At, m, X, ldx, 0.0, out, ldo);
   }
@@ -373,7 +414,7 @@ void shrink_into(cudaStream_t s, i64 m, i64 w, const double* U, i64 ldu, const d
 // svt_factors_dense (solvers.hpp:90-93) on the materialised operator.
 template <class Op>
 void svt_dense(cudaStream_t s, const Op& op, double tau, SvtResult& res) {
-  const i64 m = op.rows(), w = op.cols();
+  const i64 m = op.rows(), w = op.zrows();  // (compressed operators: w = the coordinate count)
   DBuf<double> D(m * w, s);
   op.to_dense(s, D.get());
   std::vector<double> sv;
@@ -399,15 +440,17 @@ struct NormalCursor {
 // result was accepted (f.rank() < k or s[k-1] <= tau), filling res.
 template <class Op>
 bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor& cur, double tau, SvtResult& res) {
-  const i64 m = op.rows(), w = op.cols();
+  const i64 m = op.rows(), w = op.cols(), wz = op.zrows();  // wz: rows of the n-side vectors
   const i64 b = std::min(k + p, std::min(m, w));
   const i64 bl = even_ld(b);  // leading dimension of every sketch-width buffer
   // gaussian_matrix(w, b): column-major draws == row-major b x w; transpose to w x b.
-  DBuf<double> Gt(b * w, s), G(w * bl, s), X(m * bl, s), Z(w * bl, s);
+  DBuf<double> Gt(b * w, s), G(w * bl, s), X(m * bl, s), Z(wz * bl, s);
   cur.cache->fetch(cur.pos, w * b, Gt.get(), s);
   cur.pos += w * b;
   transpose(s, b, w, Gt.get(), w, G.get(), bl);
-  op.apply(s, G.get(), bl, b, X.get(), bl);
+  op.apply_g0(s, G.get(), bl, b, X.get(), bl);
+  G.release();
+  Gt.release();
   // m-side bases are kept lazily: the orthonormal basis is Q = X M (M = R^-1 of a CholQR
   // factor of X), and M is applied on the n side after the next product, A^T Q = (A^T X) M,
   // so the m x b x b triangular products of the intermediate bases (and of the second
@@ -435,23 +478,23 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
   auto adjoint = [&](DBuf<double>* keep) {  // Z = A^T Q
     op.apply_adjoint(s, X.get(), bl, b, Z.get(), bl, keep);
     if (lazy) {
-      DBuf<double> Zm(w * bl, s);
-      gemm_upper_b(s, w, b, 1.0, Z.get(), bl, M.get(), bl, 0.0, Zm.get(), bl);
+      DBuf<double> Zm(wz * bl, s);
+      gemm_upper_b(s, wz, b, 1.0, Z.get(), bl, M.get(), bl, 0.0, Zm.get(), bl);
       std::swap(Z, Zm);
     }
   };
   orth_m(q == 0);
   for (i64 it = 0; it < q; ++it) {
     adjoint(nullptr);
-    thin_qr(s, w, b, Z.get(), bl, nullptr, 0, 1);
+    thin_qr(s, wz, b, Z.get(), bl, nullptr, 0, 1);
     op.apply(s, Z.get(), bl, b, X.get(), bl);
     orth_m(it + 1 == q);
   }
   DBuf<double> T;
   adjoint(&T);  // Z = A^T Q (w x b); T = Yl^T X (before M, ld bl) for the factor Grams
-  DBuf<double> Uz(w * bl, s), Vz(b * bl, s);
+  DBuf<double> Uz(wz * bl, s), Vz(b * bl, s);
   std::vector<double> sv;
-  thin_svd(s, w, b, Z.get(), bl, Uz.get(), bl, Vz.get(), bl, sv, tau);
+  thin_svd(s, wz, b, Z.get(), bl, Uz.get(), bl, Vz.get(), bl, sv, tau);
   const i64 kk = std::min<i64>(k, static_cast<i64>(sv.size()));
   sv.resize(static_cast<size_t>(kk));
   if (!(kk < k || sv[static_cast<size_t>(kk - 1)] <= tau)) return false;
@@ -463,7 +506,7 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
   for (double& x : res.s) x -= tau;
   if (r == 0) return true;
   res.left.alloc(m * r, s);
-  res.right.alloc(w * r, s);
+  res.right.alloc(wz * r, s);
   DBuf<double> MV;
   const double* coef = Vz.get();  // b x r block mapping X to the left factor
   i64 ldcoef = bl;
@@ -486,7 +529,7 @@ bool partial_svt(cudaStream_t s, const Op& op, i64 k, i64 p, i64 q, NormalCursor
   }
   DBuf<double> sc(r, s);
   DFCG_CUDA(cudaMemcpyAsync(sc.get(), res.s.data(), sizeof(double) * r, cudaMemcpyHostToDevice, s));
-  scale_cols_kernel<<<grid_for(w * r), 256, 0, s>>>(w, r, Uz.get(), bl, sc.get(), res.right.get(), r);
+  scale_cols_kernel<<<grid_for(wz * r), 256, 0, s>>>(wz, r, Uz.get(), bl, sc.get(), res.right.get(), r);
   DFCG_LAUNCH_CHECK();
   DFCG_CUDA(cudaStreamSynchronize(s));
   return true;
@@ -541,6 +584,21 @@ double sum_of(const std::vector<double>& v) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------- normal stream
+__global__ void box_muller_kernel(const std::uint64_t* __restrict__ raw, double* __restrict__ out, i64 n) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const double u1 = (static_cast<double>(raw[2 * i] >> 11) + 1.0) * 0x1.0p-53;
+    const double u2 = static_cast<double>(raw[2 * i + 1] >> 11) * 0x1.0p-53;
+    out[i] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925286766559 * u2);
+  }
+}
+
+void box_muller_device(cudaStream_t s, const std::uint64_t* raw, double* out, i64 n) {
+  box_muller_kernel<<<grid_for(n), 256, 0, s>>>(raw, out, n);
+  DFCG_LAUNCH_CHECK();
+}
 
 // ---------------------------------------------------------------- context / streams
 DeviceContext::DeviceContext(int dev) : device(dev) {
@@ -691,30 +749,38 @@ struct McSolver::State {
   // = R_A^-1 U~, w x k): left = A cl.
   DBuf<double> RA, RAinv, cl_c, cl_p;
   int lazy_c = -1, lazy_p = -1;
+  bool wide = false;  // the deferred factor: the left one (tall, m >= n) or the right one (m < n)
   int ad_next = 0;  // Ad[] buffer the next dense iteration writes
 };
 
-// left = Ad[src] cl (m x k) for an estimate produced by a compressed dense iteration.
-static void materialize_left(cudaStream_t s, i64 m, i64 n, const DBuf<double>& A, const DBuf<double>& cl,
-                             DevLowRank& L) {
-  L.left.alloc(m * L.k, s);
-  gemm(s, false, false, m, L.k, n, 1.0, A.get(), n, cl.get(), L.k, 0.0, L.left.get(), L.k);
+// The deferred factor of an estimate produced by a compressed dense iteration: left = A cl
+// (m x k, tall operator) or right = A^T cl (n x k, wide operator), A = Ad[src] row-major m x n.
+static void materialize(cudaStream_t s, i64 m, i64 n, bool wide, const DBuf<double>& A, const DBuf<double>& cl,
+                        DevLowRank& L) {
+  if (!wide) {
+    L.left.alloc(m * L.k, s);
+    gemm(s, false, false, m, L.k, n, 1.0, A.get(), n, cl.get(), L.k, 0.0, L.left.get(), L.k);
+  } else {
+    L.right.alloc(n * L.k, s);
+    gemm(s, true, false, n, L.k, m, 1.0, A.get(), n, cl.get(), L.k, 0.0, L.right.get(), L.k);
+  }
 }
 
-// Whether a dense iteration compresses the operator (cost model in FLOPs, m >= n only):
+// Whether a dense iteration compresses the operator (cost model in FLOPs, written for m >= n;
+// a wide block, m < n, is compressed on its rows — OpWideQR — with m and n exchanged):
 // uncompressed ~ m n (12 b + 2 r) + 5 m b^2 + 2 m b r (six products with A, the m-side
 // CholQR, the left factor, the densified iterate); compressed ~ 5 m n^2 (CholeskyQR2 of A:
 // two Grams and a triangular product, and the iterate as A (R_A^-1 P)). DFCG_DENSE_OP=1 / 2
 // forces uncompressed / compressed (when admissible).
 static bool compress_operator(i64 m, i64 n, i64 rank_hint) {
-  if (m < n) return false;
   const char* env = std::getenv("DFCG_DENSE_OP");
   const int mode = env ? std::atoi(env) : -1;
   if (mode == 1) return false;
   if (mode == 2) return true;
-  if (n < 128) return false;
-  const double b = static_cast<double>(std::min<i64>(rank_hint + 15, n)), r = static_cast<double>(rank_hint);
-  const double nn = static_cast<double>(n);
+  const i64 lo = std::min(m, n);  // the compressed side (n for a tall block, m for a wide one)
+  if (lo < 128) return false;
+  const double b = static_cast<double>(std::min<i64>(rank_hint + 15, lo)), r = static_cast<double>(rank_hint);
+  const double nn = static_cast<double>(lo);
   return 12.0 * b + 2.0 * r + 5.0 * b * b / nn + 2.0 * b * r / nn > 5.0 * nn;
 }
 
@@ -798,8 +864,8 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
   const i64 kY = concat ? Lc.k + Lp.k : Lc.k;
   const bool dense = dense_operator(m, n, nnz, kY, cfg_.line_search);
   if (!dense) {  // the factored operator needs the left factors compressed iterations deferred
-    if (st.lazy_c >= 0) materialize_left(s, m, n, st.Ad[st.lazy_c], st.cl_c, Lc);
-    if (concat && st.lazy_p >= 0) materialize_left(s, m, n, st.Ad[st.lazy_p], st.cl_p, Lp);
+    if (st.lazy_c >= 0) materialize(s, m, n, st.wide, st.Ad[st.lazy_c], st.cl_c, Lc);
+    if (concat && st.lazy_p >= 0) materialize(s, m, n, st.wide, st.Ad[st.lazy_p], st.cl_p, Lp);
     if (st.lazy_c >= 0) st.lazy_c = -1;
     if (concat && st.lazy_p >= 0) st.lazy_p = -1;
   }
@@ -818,7 +884,7 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
     // Ad[ai] may be the source of a deferred left factor: L_curr's is formed first (it becomes
     // L_prev, which a following factored iteration needs); L_prev's is dropped with L_prev.
     if (st.lazy_c == ai) {
-      materialize_left(s, m, n, st.Ad[ai], st.cl_c, Lc);
+      materialize(s, m, n, st.wide, st.Ad[ai], st.cl_c, Lc);
       st.lazy_c = -1;
     }
     if (st.lazy_p == ai) st.lazy_p = -2;  // lost: L_prev is not used in factored form again
@@ -833,9 +899,12 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
       DFCG_LAUNCH_CHECK();
     }
     if (compress_operator(m, n, st.rank_hint)) {
-      st.RA.ensure(n * n, s);
-      st.RAinv.ensure(n * n, s);
-      compressed = cholqr2_r(s, m, n, st.Ad[ai].get(), n, st.RA.get(), st.RAinv.get(), 1e-13);
+      const i64 lo = std::min(m, n);
+      st.RA.ensure(lo * lo, s);
+      st.RAinv.ensure(lo * lo, s);
+      st.wide = m < n;
+      compressed = st.wide ? cholqr2_r(s, n, m, st.Ad[ai].get(), n, st.RA.get(), st.RAinv.get(), 1e-13, true)
+                           : cholqr2_r(s, m, n, st.Ad[ai].get(), n, st.RA.get(), st.RAinv.get(), 1e-13);
     }
   }
   DBuf<double> Yl, Yr;
@@ -861,7 +930,10 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
 
   double step = 1.0;
   SvtResult f;
-  if (compressed) {
+  if (compressed && st.wide) {
+    OpWideQR G{st.Ad[ai].get(), st.RA.get(), m, n};
+    svt_operator(s, G, st.mu, st.rank_hint, st.cur, f);
+  } else if (compressed) {
     OpTri G{st.RA.get(), n};
     svt_operator(s, G, st.mu, st.rank_hint, st.cur, f);
   } else if (dense) {
@@ -895,9 +967,28 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
     // same quantities and the same cancellation formula below.
     std::swap(st.Dc, st.Dp);
     st.dp_ok = st.dc_ok;
-    if (compressed) {
+    if (compressed && st.wide) {
+      // f.right = V~ S (Q_B coordinates): cl = R^-1 V~ S, L_next = (left cl^T) A; the n x r
+      // right factor itself is deferred (materialize) until a factored iteration or finish().
+      st.Dc.ensure(m * n, s);
+      DBuf<double> cl;
+      if (f.r > 0) {
+        cl.alloc(m * f.r, s);
+        gemm(s, false, false, m, f.r, m, 1.0, st.RAinv.get(), m, f.right.get(), f.r, 0.0, cl.get(), f.r);
+        DBuf<double> T2(m * m, s);
+        gemm(s, false, true, m, m, f.r, 1.0, f.left.get(), f.r, cl.get(), f.r, 0.0, T2.get(), m);
+        gemm(s, false, false, m, n, m, 1.0, T2.get(), m, st.Ad[ai].get(), n, 0.0, st.Dc.get(), n);
+      } else {
+        st.Dc.zero(s);
+      }
+      f.right = DBuf<double>{};
+      st.lazy_p = st.lazy_c;
+      std::swap(st.cl_p, st.cl_c);
+      st.cl_c = std::move(cl);
+      st.lazy_c = f.r > 0 ? ai : -1;
+    } else if (compressed) {
       // f.left = U~ (Q_A coordinates): cl = R_A^-1 U~, L_next = A (cl right^T); the m x r left
-      // factor itself is deferred (materialize_left) until a factored iteration or finish().
+      // factor itself is deferred (materialize) until a factored iteration or finish().
       st.Dc.ensure(m * n, s);
       DBuf<double> cl;
       if (f.r > 0) {
@@ -994,7 +1085,7 @@ void McSolver::finish(DevLowRank& out, SolveReport& rep) {
   State& st = *st_;
   cudaStream_t s = s_;
   if (st.lazy_c >= 0) {
-    materialize_left(s, m_, n_, st.Ad[st.lazy_c], st.cl_c, st.Lc);
+    materialize(s, m_, n_, st.wide, st.Ad[st.lazy_c], st.cl_c, st.Lc);
     st.lazy_c = -1;
   }
   const DevLowRank& Lc = st.Lc;

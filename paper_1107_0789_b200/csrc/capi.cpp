@@ -184,6 +184,18 @@ int dfcg_ctx_create(int device, dfcg_ctx** out) {
   });
 }
 
+int dfcg_normals_fetch(dfcg_ctx* ctx, int stream_id, int64_t pos, int64_t n, double* out) {
+  return guard([&] {
+    if (!ctx || !out || pos < 0 || n < 0 || (stream_id != 0 && stream_id != 1))
+      throw std::invalid_argument("dfcg_normals_fetch: bad argument");
+    CallStream cs(*ctx->dev);
+    DBuf<double> d(n, cs.s);
+    ctx->dev->normals(stream_id).fetch(pos, n, d.get(), cs.s);
+    DFCG_CUDA(cudaMemcpyAsync(out, d.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, cs.s));
+    DFCG_CUDA(cudaStreamSynchronize(cs.s));
+  });
+}
+
 void dfcg_ctx_destroy(dfcg_ctx* ctx) {
   if (!ctx) return;
   delete ctx->dev;

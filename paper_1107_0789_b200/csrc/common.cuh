@@ -106,6 +106,12 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
 void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
                   double beta, double* C, i64 ldc);
 void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* G, i64 ldg);
+// Upper triangle of G = A A^T (rows x rows), A row-major rows x k.
+void gram_upper_nt(cudaStream_t s, i64 rows, i64 k, const double* A, i64 lda, double* G, i64 ldg);
+// C (M x N) = alpha A^T B + beta C with A stored row-major N x M (A^T(i,k) = A[k*lda + i]) and
+// B (N x N) upper triangular (lower part stored as zeros): the TRMM of a transposed operand.
+void gemm_ta_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
+                     double beta, double* C, i64 ldc);
 
 // dst (rows x cols, ldd) = alpha * src (rows x cols, lds)  [alpha may be 1]
 void copy2d(cudaStream_t s, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd, double alpha = 1.0);
@@ -139,6 +145,10 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 #endif
 
+// out[i] = sqrt(-2 log(u1)) cos(2 pi u2), u1 = ((raw[2i] >> 11) + 1) 2^-53, u2 = (raw[2i+1] >> 11)
+// 2^-53: SeededRng::normal (P/include/dfc/rng.hpp:62-66) on raw mt19937_64 words, on the device.
+void box_muller_device(cudaStream_t s, const std::uint64_t* raw, double* out, i64 n);
+
 // APG solves currently stepping on device `dev`: kernels with a latency / occupancy trade-off
 // (the Jacobi cluster size) consult it.
 int active_streams(int dev);
@@ -161,8 +171,9 @@ bool cholqr_factor(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx,
 // never formed beyond the first pass): R (cols x cols, upper, lower part zero) and Rinv = R^-1.
 // rel_tol1: breakdown threshold of the first pass's (Jacobi-scaled) Cholesky pivots. Returns
 // false on breakdown (cond(A) too large for CholeskyQR2); R / Rinv are then unusable.
+// trans: the tall matrix is A^T, A stored row-major cols x rows (lda).
 bool cholqr2_r(cudaStream_t s, i64 rows, i64 cols, const double* A, i64 lda, double* R, double* Rinv,
-               double rel_tol1);
+               double rel_tol1, bool trans = false);
 // Householder QR only (tests / fallback).
 void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
 

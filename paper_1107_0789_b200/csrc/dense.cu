@@ -496,6 +496,21 @@ void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i
   launch_gemm<false, false>(s, M, N, N, alpha, A, lda, B, ldb, beta, C, ldc, 2);
 }
 
+void gram_upper_nt(cudaStream_t s, i64 rows, i64 k, const double* A, i64 lda, double* G, i64 ldg) {
+  if (rows <= 0 || k <= 0) return;
+  prof::Scope scope(1.0 * rows * (rows + 1) * k >= 2e9 ? prof::kGemm : prof::kGemmSmall, s,
+                    1.0 * rows * (rows + 1) * k, 8.0 * (rows * k + rows * rows));
+  launch_gemm<false, true>(s, rows, rows, k, 1.0, A, lda, A, lda, 0.0, G, ldg, 1);
+}
+
+void gemm_ta_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
+                     double beta, double* C, i64 ldc) {
+  if (M <= 0 || N <= 0) return;
+  prof::Scope scope(1.0 * M * N * (N + 1) >= 2e9 ? prof::kGemm : prof::kGemmSmall, s, 1.0 * M * N * (N + 1),
+                    8.0 * (M * N + N * N / 2 + M * N * (beta != 0.0 ? 2.0 : 1.0)));
+  launch_gemm<true, false>(s, M, N, N, alpha, A, lda, B, ldb, beta, C, ldc, 2);
+}
+
 void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* G, i64 ldg) {
   if (rows <= 0 || cols <= 0) return;
   prof::Scope scope(1.0 * cols * (cols + 1) * rows >= 2e9 ? prof::kGemm : prof::kGemmSmall, s,

@@ -1332,19 +1332,21 @@ bool cholqr_factor(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx,
 }
 
 bool cholqr2_r(cudaStream_t s, i64 rows, i64 cols, const double* A, i64 lda, double* R, double* Rinv,
-               double rel_tol1) {
+               double rel_tol1, bool trans) {
   if (cols <= 0) return true;
   DBuf<int> fail(1, s);
   fail.zero(s);
   DBuf<double> G(cols * cols, s), R1inv(cols * cols, s), Q1(rows * cols, s), R2inv(cols * cols, s);
   // pass 1: R1^T R1 = A^T A, Q1 = A R1^-1 (orthogonal to ~eps cond(A)^2)
-  gram_upper(s, rows, cols, A, lda, G.get(), cols);
+  if (trans) gram_upper_nt(s, cols, rows, A, lda, G.get(), cols);
+  else gram_upper(s, rows, cols, A, lda, G.get(), cols);
   cholesky_inverse(s, cols, G.get(), cols, R1inv.get(), cols, rel_tol1, fail.get());
   int h_fail = 0;
   DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
   DFCG_CUDA(cudaStreamSynchronize(s));
   if (h_fail) return false;
-  gemm_upper_b(s, rows, cols, 1.0, A, lda, R1inv.get(), cols, 0.0, Q1.get(), cols);
+  if (trans) gemm_ta_upper_b(s, rows, cols, 1.0, A, lda, R1inv.get(), cols, 0.0, Q1.get(), cols);
+  else gemm_upper_b(s, rows, cols, 1.0, A, lda, R1inv.get(), cols, 0.0, Q1.get(), cols);
   // pass 2 on the explicit Q1: R2^T R2 = Q1^T Q1; A = (Q1 R2^-1) (R2 R1)
   gram_upper(s, rows, cols, Q1.get(), cols, R, cols);
   cholesky_inverse(s, cols, R, cols, R2inv.get(), cols, 1e-11, fail.get());
@@ -1646,16 +1648,16 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   for (int sweep = 0; sweep < 60 && !small; ++sweep) {
     if (sweep_exec) {
       prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
-                        (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW);
+                        (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW, p - 1);
       DFCG_CUDA(cudaGraphLaunch(sweep_exec, s));
       prof::count_launch(p - 1);
     } else {
       off.zero(s);
+      // one event pair per sweep, counted as p - 1 round launches (algorithmic per round: Gram +
+      // rotation of each pair's columns, every W / V element read and written once)
+      prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
+                        (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW, p - 1);
       for (int r = 0; r < p - 1; ++r) {
-        // accounting per round launch (algorithmic: Gram + rotation of the pair's columns,
-        // every W / V element read and written once)
-        prof::Scope scope(prof::kJacobi, s, 1.0 * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
-                          1.0 * npairs * 16.0 * (wrows + nj) * JW);
         const int* pr = pairs.get() + 2 * static_cast<i64>(r) * npairs;
         if (resident)
           launch_round(r);

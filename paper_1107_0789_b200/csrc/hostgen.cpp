@@ -42,7 +42,72 @@ double row_dot(const std::vector<double>& A, i64 m, i64 i, const std::vector<dou
 
 }  // namespace
 
+
+namespace dfcg {
+
+void Mt64::seed(std::uint64_t s) {
+  mt[0] = s;
+  for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + static_cast<std::uint64_t>(i);
+  idx = 312;
+}
+
+namespace {
+constexpr std::uint64_t kUM = 0xFFFFFFFF80000000ULL, kLM = 0x7FFFFFFFULL, kMA = 0xB5026F5AA96619E9ULL;
+
+// One MT19937-64 twist: new[i] for i < 156 reads old words only; i in [156, 311) reads new[i - 156]
+// and old[i], old[i + 1]; i = 311 reads new[0] and new[155] — three loops without carried
+// dependences (the in-place reference loop is the same recurrence).
+__attribute__((optimize("O3"), target_clones("avx512f", "avx2", "default"))) void mt64_twist(std::uint64_t* __restrict__ mt, std::uint64_t* __restrict__ nw) {
+  for (int i = 0; i < 156; ++i) {
+    const std::uint64_t x = (mt[i] & kUM) | (mt[i + 1] & kLM);
+    nw[i] = mt[i + 156] ^ (x >> 1) ^ ((0 - (x & 1ULL)) & kMA);
+  }
+  for (int i = 156; i < 311; ++i) {
+    const std::uint64_t x = (mt[i] & kUM) | (mt[i + 1] & kLM);
+    nw[i] = nw[i - 156] ^ (x >> 1) ^ ((0 - (x & 1ULL)) & kMA);
+  }
+  const std::uint64_t x = (mt[311] & kUM) | (nw[0] & kLM);
+  nw[311] = nw[155] ^ (x >> 1) ^ ((0 - (x & 1ULL)) & kMA);
+}
+
+__attribute__((optimize("O3"), target_clones("avx512f", "avx2", "default"))) void mt64_temper(const std::uint64_t* __restrict__ mt, std::uint64_t* __restrict__ out,
+                                                 int n) {
+  for (int i = 0; i < n; ++i) {
+    std::uint64_t y = mt[i];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    out[i] = y;
+  }
+}
+}  // namespace
+
+void mt64_fill(Mt64& g, std::uint64_t* out, std::int64_t n) {
+  std::uint64_t nw[312];
+  while (n > 0) {
+    if (g.idx == 312) {
+      mt64_twist(g.mt, nw);
+      std::memcpy(g.mt, nw, sizeof(nw));
+      g.idx = 0;
+    }
+    const int take = static_cast<int>(std::min<std::int64_t>(n, 312 - g.idx));
+    mt64_temper(g.mt + g.idx, out, take);
+    g.idx += take;
+    out += take;
+    n -= take;
+  }
+}
+
+}  // namespace dfcg
+
 extern "C" {
+
+void dfcg_rng_u64_bulk(uint64_t seed, uint64_t stream, int64_t n, uint64_t* out) {
+  Mt64 g;
+  g.seed(SeededRng::engine_seed(seed, stream));
+  mt64_fill(g, out, n);
+}
 
 void dfcg_rng_u64(uint64_t seed, uint64_t stream, int64_t n, uint64_t* out) {
   SeededRng r(seed, stream);

@@ -16,14 +16,15 @@ namespace {
 struct Rec {
   Op op;
   double flops, bytes;
+  int launches;
   cudaEvent_t e0, e1;
 };
 std::mutex g_mu;
 std::vector<Rec> g_recs;
 }  // namespace
 
-Scope::Scope(Op op, cudaStream_t s, double flops, double bytes)
-    : op_(op), s_(s), flops_(flops), bytes_(bytes) {
+Scope::Scope(Op op, cudaStream_t s, double flops, double bytes, int launches)
+    : op_(op), s_(s), flops_(flops), bytes_(bytes), launches_(launches) {
   if (!g_enabled.load(std::memory_order_relaxed)) return;
   on_ = true;
   cudaEventCreate(&e0_);
@@ -35,7 +36,7 @@ Scope::~Scope() {
   if (!on_) return;
   cudaEventRecord(e1_, s_);
   std::lock_guard<std::mutex> lock(g_mu);
-  g_recs.push_back({op_, flops_, bytes_, e0_, e1_});
+  g_recs.push_back({op_, flops_, bytes_, launches_, e0_, e1_});
 }
 
 }  // namespace prof
@@ -67,7 +68,7 @@ int dfcg_prof_collect(int64_t* launches, double* ms, double* flops, double* byte
     if (cudaEventSynchronize(r.e1) != cudaSuccess) return -4;
     float t = 0.f;
     cudaEventElapsedTime(&t, r.e0, r.e1);
-    launches[r.op] += 1;
+    launches[r.op] += r.launches;
     ms[r.op] += t;
     flops[r.op] += r.flops;
     bytes[r.op] += r.bytes;

@@ -34,7 +34,9 @@ inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_
 // RAII scope: records start/stop events on `s` when profiling is enabled.
 class Scope {
  public:
-  Scope(Op op, cudaStream_t s, double flops, double bytes);
+  // launches: kernel launches the scope spans (e.g. the rounds of a Jacobi sweep), so per-launch
+  // rates stay per kernel without an event pair around every launch.
+  Scope(Op op, cudaStream_t s, double flops, double bytes, int launches = 1);
   ~Scope();
   Scope(const Scope&) = delete;
   Scope& operator=(const Scope&) = delete;
@@ -44,6 +46,7 @@ class Scope {
   Op op_;
   cudaStream_t s_;
   double flops_, bytes_;
+  int launches_ = 1;
   cudaEvent_t e0_ = nullptr, e1_ = nullptr;
 };
 

@@ -29,13 +29,28 @@ inline std::uint64_t splitmix64(std::uint64_t& state) {
   return z ^ (z >> 31);
 }
 
+// mt19937_64 with bulk output (bit-identical to std::mt19937_64: same parameters, seeding and
+// tempering), its twist written as three dependence-free loops over a second state array so
+// the compiler vectorises it — the sequential part of the normal stream (hostgen.cpp).
+struct Mt64 {
+  std::uint64_t mt[312];
+  int idx = 312;
+  void seed(std::uint64_t s);
+};
+// out[0:n) = the engine's next n outputs.
+void mt64_fill(Mt64& g, std::uint64_t* out, std::int64_t n);
+
 class SeededRng {
  public:
-  explicit SeededRng(std::uint64_t seed, std::uint64_t stream = 0) : seed_(seed), stream_(stream) {
+  // The mt19937_64 seed SeededRng(seed, stream) uses (P/include/dfc/rng.hpp:19-26 restated).
+  static std::uint64_t engine_seed(std::uint64_t seed, std::uint64_t stream) {
     std::uint64_t x = seed;
     const std::uint64_t h = splitmix64(x);
     x = h ^ (0xD1B54A32D192ED03ULL * (stream + 1));
-    engine_.seed(splitmix64(x));
+    return splitmix64(x);
+  }
+  explicit SeededRng(std::uint64_t seed, std::uint64_t stream = 0) : seed_(seed), stream_(stream) {
+    engine_.seed(engine_seed(seed, stream));
   }
   std::uint64_t next_u64() { return engine_(); }
   double uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
@@ -75,7 +90,9 @@ class NormalCache {
   static constexpr i64 kChunk = i64{1} << 22;  // 4 Mi normals = 32 MiB per chunk
   static constexpr i64 kAhead = 4;
 
-  NormalCache(int device, std::uint64_t seed, std::uint64_t stream) : device_(device), rng_(seed, stream) {}
+  NormalCache(int device, std::uint64_t seed, std::uint64_t stream) : device_(device) {
+    mt_.seed(SeededRng::engine_seed(seed, stream));
+  }
   ~NormalCache() {
     {
       std::lock_guard<std::mutex> lock(mu_);
@@ -83,8 +100,10 @@ class NormalCache {
     }
     cv_.notify_all();
     if (worker_.joinable()) worker_.join();
+    if (transformer_.joinable()) transformer_.join();
     for (double* p : chunks_) cudaFree(p);
-    if (pinned_) cudaFreeHost(pinned_);
+    for (std::uint64_t* p : raw_buf_)
+      if (p) cudaFreeHost(p);
     if (stream_) cudaStreamDestroy(stream_);
   }
 
@@ -99,7 +118,10 @@ class NormalCache {
       static const i64 ahead = std::getenv("DFCG_NORMALS_AHEAD") ? std::atoll(std::getenv("DFCG_NORMALS_AHEAD")) : kAhead;
       if (need + ahead > wanted_) {
         wanted_ = need + ahead;
-        if (!worker_.joinable()) worker_ = std::thread([this] { run(); });
+        if (!worker_.joinable()) {
+          worker_ = std::thread([this] { run_raw(); });
+          transformer_ = std::thread([this] { run_transform(); });
+        }
         cv_.notify_all();
       }
       cv_.wait(lock, [&] { return static_cast<i64>(chunks_.size()) >= need || error_; });
@@ -118,62 +140,98 @@ class NormalCache {
   }
 
  private:
-  void run() {
+  // Two-stage pipeline: this thread draws the raw 64-bit words of chunk k + 1 (sequential
+  // mt19937_64, the stream's only serial part) while run_transform() uploads chunk k and turns
+  // it into normals on the device — a chunk every max(draw, transform) instead of their sum. Wide
+  // blocks consume w * b normals per partial SVD (7.2 M for a 1250 x 10000 DFC-Nys row block),
+  // so the generator's rate bounds them otherwise.
+  void run_raw() {
     try {
       DFCG_CUDA(cudaSetDevice(device_));
-      DFCG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-      DFCG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pinned_), sizeof(double) * kChunk));
-      std::vector<std::uint64_t> raw(2 * kChunk);
+      // three pinned raw buffers cycle between the two stages (no allocation or first-touch
+      // page faults per chunk, DMA-speed uploads)
+      for (int i = 0; i < kRawBufs; ++i) {
+        DFCG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&raw_buf_[i]), sizeof(std::uint64_t) * 2 * kChunk));
+        std::lock_guard<std::mutex> lock(mu_);
+        raw_free_.push_back(i);
+      }
       for (;;) {
+        int b = -1;
         {
           std::unique_lock<std::mutex> lock(mu_);
-          cv_.wait(lock, [&] { return stop_ || static_cast<i64>(chunks_.size()) < wanted_; });
+          cv_.wait(lock, [&] { return stop_ || (raw_made_ < wanted_ && !raw_free_.empty()); });
           if (stop_) return;
+          b = raw_free_.back();
+          raw_free_.pop_back();
         }
-        // Raw 64-bit draws are sequential (mt19937_64); the Box-Muller transform runs on host
-        // threads so the stream stays bit-identical to the reference's std::log/std::cos.
-        for (auto& r : raw) r = rng_.next_u64();
-        // A few transform threads only: the generator runs beside the solves' host threads, and a
-        // burst that takes every core delays their kernel launches (the GPU then idles).
-        const unsigned nt = std::max(1u, std::min(4u, std::thread::hardware_concurrency() / 4));
-        std::vector<std::thread> pool;
-        for (unsigned t = 0; t < nt; ++t)
-          pool.emplace_back([&, t] {
-            for (i64 i = t; i < kChunk; i += nt) {
-              const double u1 = (static_cast<double>(raw[2 * i] >> 11) + 1.0) * 0x1.0p-53;
-              const double u2 = static_cast<double>(raw[2 * i + 1] >> 11) * 0x1.0p-53;
-              pinned_[i] = SeededRng::box_muller(u1, u2);
-            }
-          });
-        for (auto& th : pool) th.join();
-        double* d = nullptr;
-        DFCG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(double) * kChunk, stream_));
-        DFCG_CUDA(cudaMemcpyAsync(d, pinned_, sizeof(double) * kChunk, cudaMemcpyHostToDevice, stream_));
-        DFCG_CUDA(cudaStreamSynchronize(stream_));
+        mt64_fill(mt_, raw_buf_[b], 2 * kChunk);
         {
           std::lock_guard<std::mutex> lock(mu_);
-          chunks_.push_back(d);
+          raw_q_.push_back(b);
+          ++raw_made_;
         }
         cv_.notify_all();
       }
     } catch (const std::exception& e) {
-      std::lock_guard<std::mutex> lock(mu_);
-      error_ = true;
-      err_msg_ = std::string("NormalCache: ") + e.what();
-      cv_.notify_all();
+      fail(e.what());
     }
   }
 
+  void run_transform() {
+    try {
+      DFCG_CUDA(cudaSetDevice(device_));
+      DFCG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+      std::uint64_t* raw_dev = nullptr;
+      DFCG_CUDA(cudaMalloc(reinterpret_cast<void**>(&raw_dev), sizeof(std::uint64_t) * 2 * kChunk));
+      for (;;) {
+        int b = -1;
+        {
+          std::unique_lock<std::mutex> lock(mu_);
+          cv_.wait(lock, [&] { return stop_ || !raw_q_.empty(); });
+          if (stop_) break;
+          b = raw_q_.front();
+          raw_q_.erase(raw_q_.begin());
+        }
+        // Box-Muller on the device (CUDA's log / cos, <= 1 ulp from the host libm the oracle
+        // uses; the raw words are bit-identical): the host keeps only the serial draws.
+        double* d = nullptr;
+        DFCG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(double) * kChunk, stream_));
+        DFCG_CUDA(cudaMemcpyAsync(raw_dev, raw_buf_[b], sizeof(std::uint64_t) * 2 * kChunk, cudaMemcpyHostToDevice,
+                                  stream_));
+        box_muller_device(stream_, raw_dev, d, kChunk);
+        DFCG_CUDA(cudaStreamSynchronize(stream_));
+        {
+          std::lock_guard<std::mutex> lock(mu_);
+          raw_free_.push_back(b);
+          chunks_.push_back(d);
+        }
+        cv_.notify_all();
+      }
+      cudaFree(raw_dev);
+    } catch (const std::exception& e) {
+      fail(e.what());
+    }
+  }
+
+  void fail(const char* what) {
+    std::lock_guard<std::mutex> lock(mu_);
+    error_ = true;
+    err_msg_ = std::string("NormalCache: ") + what;
+    cv_.notify_all();
+  }
+
   int device_;
-  SeededRng rng_;
+  Mt64 mt_;
   std::mutex mu_;
   std::condition_variable cv_;
-  std::thread worker_;
+  std::thread worker_, transformer_;
   bool stop_ = false, error_ = false;
   std::string err_msg_;
-  i64 wanted_ = 0;
+  i64 wanted_ = 0, raw_made_ = 0;
+  static constexpr int kRawBufs = 3;
+  std::uint64_t* raw_buf_[kRawBufs] = {nullptr, nullptr, nullptr};
+  std::vector<int> raw_q_, raw_free_;
   std::vector<double*> chunks_;
-  double* pinned_ = nullptr;
   cudaStream_t stream_ = nullptr;
 };
 

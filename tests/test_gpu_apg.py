@@ -81,6 +81,17 @@ def test_apg_mc_c1_block_window(op_mode, monkeypatch):  # BASELINE c1 block 1000
     assert_mc_parity(blk, max_iters=60)
 
 
+@pytest.mark.parametrize("op_mode", ["0", "1", "2", "auto"])
+def test_apg_mc_wide_row_block_window(op_mode, monkeypatch):
+    """A DFC-Nys row subproblem (R-hat) shape at c1 scale: 250 x 1000 (m < n), default config,
+    60 iterations — the wide operator path (CholeskyQR2 of the transposed dense operator)."""
+    if op_mode != "auto":
+        monkeypatch.setenv("DFCG_DENSE_OP", op_mode)
+    L0, obs = P.gen_mc_instance(1000, 1000, 10, 200000, 0.1, 1)
+    rows = np.sort(P.sample_without_replacement(1, 0xDFC0000000000003, 1000, 250))
+    assert_mc_parity(P.extract_rows(obs, rows), max_iters=60)
+
+
 def test_apg_mc_operator_switching():
     """A sparse block whose rank rises past and falls back below the dense-operator threshold
     (acceptance-style floor, P/tests/acceptance.cpp:127-130): iterations switch between the

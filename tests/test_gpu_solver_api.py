@@ -70,3 +70,23 @@ def test_bench_multi_rank_path_on_one_gpu():
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["gpu_launches"] > 0
+
+
+def test_device_normal_stream_matches_reference_rng():
+    """The SVT's Gaussian draws (SeededRng(0x737674, 0|1), P/include/dfc/rng.hpp:62-66): raw
+    mt19937_64 words drawn on the host (bit-identical), Box-Muller on the device with CUDA's
+    log / cos — within a few ulp of the host libm values the oracle uses, across chunk
+    boundaries (4 Mi normals per chunk)."""
+    import ctypes as C
+
+    L = P.lib()
+    for stream in (0, 1):
+        for pos, n in ((0, 20000), ((1 << 22) - 5000, 10000)):
+            out = np.zeros(n)
+            rc = L.dfcg_normals_fetch(P.context(0), C.c_int(stream), C.c_int64(pos), C.c_int64(n),
+                                      out.ctypes.data_as(C.c_void_p))
+            assert rc == 0
+            ref = P.SeededRng(0x737674, stream).normal(pos + n)[pos:]
+            ulp = np.abs(out - ref) / np.spacing(np.abs(ref))
+            assert ulp.max() <= 4, (stream, pos, ulp.max())
+            assert np.mean(out == ref) > 0.5

@@ -48,6 +48,24 @@ def test_host_normal_stream_matches_oracle():  # the SVT draws from SeededRng(0x
         assert np.array_equal(P.SeededRng(0x737674, stream).normal(5000), O.rng_normal(0x737674, stream, 5000))
 
 
+def test_bulk_mt19937_64_matches_engine():
+    """The device normal cache draws its raw words with the vectorised bulk mt19937_64
+    (rng.hpp Mt64): the same words as the reference's SeededRng engine, across twist
+    boundaries, for both SVT streams and another seed."""
+    import ctypes as C
+
+    L = P.lib()
+    L.dfcg_rng_u64.restype = None
+    L.dfcg_rng_u64_bulk.restype = None
+    for seed, stream, n in ((0x737674, 0, 312 * 7 + 5), (0x737674, 1, 100_000), (42, 3, 1)):
+        a = np.zeros(n, np.uint64)
+        b = np.zeros(n, np.uint64)
+        L.dfcg_rng_u64(C.c_uint64(seed), C.c_uint64(stream), C.c_int64(n), a.ctypes.data_as(C.c_void_p))
+        L.dfcg_rng_u64_bulk(C.c_uint64(seed), C.c_uint64(stream), C.c_int64(n), b.ctypes.data_as(C.c_void_p))
+        assert np.array_equal(a, b), (seed, stream, n)
+    assert int(P.SeededRng(42, 3).u64(1)[0]) == int(b[0])
+
+
 def test_generators_match_oracle_bitwise():
     L0p, obp = P.gen_mc_instance(60, 50, 3, 900, 0.1, 5)
     L0o, obo = O.gen_mc_instance(60, 50, 3, 900, 0.1, 5, 0)
