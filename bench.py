@@ -175,6 +175,54 @@ def roofline_entry(prof, peaks, peak_kind):
     return entry
 
 
+def nys_run(P, obs, wl):
+    """DFC-Nys at the c2 shape (BASELINE configs[1]): l = d = n/t sampled columns / rows, the
+    two subproblems (C-hat m x l, R-hat d x n) solved concurrently, gen_nystrom combine — the whole
+    dfc_run through the C ABI, host triplets in and host factors out."""
+    l = wl["n"] // wl["t"]
+    t0 = time.perf_counter()
+    est, info = P.dfc_run(obs, variant="nys", l=l, d=l, seed=wl["seed"], workers=2)
+    wall = time.perf_counter() - t0
+    its = [s.iterations for s in info["subproblems"]]
+    return dict(solve_s=wall, factor_s=info["factor_ms"] / 1e3, combine_ms=info["combine_ms"], rank=est.rank,
+                subproblem_iterations=its, subproblem_ranks=[s.rank for s in info["subproblems"]],
+                value=sum(its) / (info["factor_ms"] * 1e-3), unit="subproblem-iterations/s",
+                note=f"DFC-Nys l = d = {l}: C-hat {wl['m']}x{l} and R-hat {l}x{wl['n']} on 2 streams + gen_nystrom")
+
+
+def rmf_c3(P, device):
+    """BASELINE configs[2] (c3): DFC-Proj robust matrix factorisation, 10000 x 10000, r = 10, 10%
+    outliers U[-10, 10], dense noise N(0, 0.01^2), t = 8 dense column blocks solved concurrently by
+    apg_rmf (lambda = 1/sqrt(max(m, w)), P/include/dfc/dfc.hpp:74), column_project combine; host
+    buffers in and out. Plus one profiled iteration of block 0 (the fused extrapolate / gradient /
+    soft-threshold pass is the RMF's HBM kernel)."""
+    m = n = 10000
+    t = 8
+    L0, S0, M = P.gen_rmf_instance(m, n, 10, m * n // 10, 0.01, 1, lo=-10.0, hi=1.0 * 10)
+    groups = P.partition_columns(1, PARTITION_STREAM, n, t)
+    blocks = [np.asfortranarray(M[:, g]) for g in groups]
+    pool = ThreadPoolExecutor(max_workers=t)
+    t0 = time.perf_counter()
+    outs = list(pool.map(lambda b: P.apg_rmf(b, 1.0 / np.sqrt(max(b.shape)), device=device), blocks))
+    f_s = time.perf_counter() - t0
+    ests = [o[0] for o in outs]
+    est = P.column_project(ests[0], ests, groups, device=device)
+    solve_s = time.perf_counter() - t0
+    its = [o[2].iterations for o in outs]
+    P.prof_enable(True)
+    P.apg_rmf(blocks[0], 1.0 / np.sqrt(max(blocks[0].shape)), P.ApgConfig(max_iters=1), device=device)
+    prof = P.prof_collect()
+    P.prof_enable(False)
+    ew = prof.get("elementwise", {})
+    shrink = None
+    if ew.get("launches", 0) and ew["ms"] > 0:
+        shrink = dict(gbs=ew["bytes"] / (ew["ms"] * 1e-3) / 1e9, launches=ew["launches"], ms=ew["ms"])
+    return dict(solve_s=solve_s, factor_s=f_s, block_iterations=its, ranks=[o[2].rank for o in outs],
+                value=sum(its) / f_s, unit="block-iterations/s", rank=est.rank, shrink_kernel=shrink,
+                note="c3: 8 dense 10000x1250 blocks, apg_rmf concurrently on one GPU + column_project; "
+                     "shrink_kernel = the fused RMF elementwise pass (algorithmic bytes / event time)")
+
+
 def lowrank_window(P, block, wl, skip=60, win=20):
     import math
 
@@ -285,6 +333,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-lowrank", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the DFC-Nys (c2) and RMF (c3) runs")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
@@ -443,6 +492,12 @@ def main():
     if rank == 0 and not args.no_lowrank:
         lowrank = lowrank_window(P, blocks[0], wl)
 
+    # the other BASELINE F-step configurations on this GPU (rank 0, N = 1): DFC-Nys at c2, c3
+    nys = rmf = None
+    if rank == 0 and world == 1 and not args.no_extra and args.workload == "c2":
+        nys = nys_run(P, obs, wl)
+        rmf = rmf_c3(P, local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle as O
@@ -470,7 +525,7 @@ def main():
                     combine=dict(ms=combine_ms, device_ops=combine_ops,
                                  note="DFC-Proj column_project of the 8 block estimates (host factors in and out; "
                                       "device_ops = CUDA-event time per op class on this rank)"),
-                    lowrank=lowrank)
+                    lowrank=lowrank, nys_c2=nys, rmf_c3=rmf)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
