@@ -454,6 +454,34 @@ int grid_for(i64 total, int threads = 256) {
 
 }  // namespace
 
+// DFCG_TRACE_GEMM=1 (diagnostics, while kernel accounting is enabled): time every call alone
+struct GemmTrace {
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaStream_t s;
+  const char* tag;
+  i64 M, N, K;
+  double flops;
+  GemmTrace(cudaStream_t s_, const char* tag_, i64 M_, i64 N_, i64 K_, double flops_)
+      : s(s_), tag(tag_), M(M_), N(N_), K(K_), flops(flops_) {
+    static const bool on = std::getenv("DFCG_TRACE_GEMM") != nullptr;
+    if (!on || !prof::g_enabled.load()) return;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, s);
+  }
+  ~GemmTrace() {
+    if (!t0) return;
+    cudaEventRecord(t1, s);
+    cudaEventSynchronize(t1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    std::fprintf(stderr, "[gemm] %s M=%lld N=%lld K=%lld  %.1f us  %.2f TF/s\n", tag, (long long)M, (long long)N,
+                 (long long)K, ms * 1e3, flops / (ms * 1e-3) / 1e12);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
+};
+
 void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc) {
   if (M <= 0 || N <= 0) return;
@@ -464,28 +492,12 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
     DFCG_LAUNCH_CHECK();
     return;
   }
-  // DFCG_TRACE_GEMM=1 (diagnostics, while kernel accounting is enabled): time every call alone
-  static const bool trace = std::getenv("DFCG_TRACE_GEMM") != nullptr;
-  cudaEvent_t t0 = nullptr, t1 = nullptr;
-  if (trace && prof::g_enabled.load()) {
-    cudaEventCreate(&t0);
-    cudaEventCreate(&t1);
-    cudaEventRecord(t0, s);
-  }
+  static const char* tags[4] = {"NN", "TN", "NT", "TT"};
+  GemmTrace tr(s, tags[(ta ? 1 : 0) + (tb ? 2 : 0)], M, N, K, 2.0 * M * N * K);
   if (!ta && !tb) launch_gemm<false, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else if (ta && !tb) launch_gemm<true, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else if (!ta && tb) launch_gemm<false, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else launch_gemm<true, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
-  if (t0) {
-    cudaEventRecord(t1, s);
-    cudaEventSynchronize(t1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, t0, t1);
-    std::fprintf(stderr, "[gemm] %c%c M=%lld N=%lld K=%lld  %.1f us  %.2f TF/s\n", ta ? 'T' : 'N', tb ? 'T' : 'N',
-                 (long long)M, (long long)N, (long long)K, ms * 1e3, 2.0 * M * N * K / (ms * 1e-3) / 1e12);
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
-  }
 }
 
 void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
@@ -493,6 +505,7 @@ void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i
   if (M <= 0 || N <= 0) return;
   prof::Scope scope(1.0 * M * N * (N + 1) >= 2e9 ? prof::kGemm : prof::kGemmSmall, s, 1.0 * M * N * (N + 1),
                     8.0 * (M * N + N * N / 2 + M * N * (beta != 0.0 ? 2.0 : 1.0)));
+  GemmTrace tr(s, "TRMM", M, N, N, 1.0 * M * N * (N + 1));
   launch_gemm<false, false>(s, M, N, N, alpha, A, lda, B, ldb, beta, C, ldc, 2);
 }
 
@@ -515,6 +528,7 @@ void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, do
   if (rows <= 0 || cols <= 0) return;
   prof::Scope scope(1.0 * cols * (cols + 1) * rows >= 2e9 ? prof::kGemm : prof::kGemmSmall, s,
                     1.0 * cols * (cols + 1) * rows, 8.0 * (rows * cols + cols * cols));
+  GemmTrace tr(s, "SYRK", cols, cols, rows, 1.0 * cols * (cols + 1) * rows);
   launch_gemm<true, false>(s, cols, cols, rows, 1.0, X, ldx, X, ldx, 0.0, G, ldg, 1);
 }
 
