@@ -159,7 +159,7 @@ __global__ void rmf_step_kernel(i64 n, double step, double thr, const double* __
 
 // Deterministic multi-output reductions over n elements: fixed grid, per-block partials,
 // single-block final sum. K quantities per element.
-constexpr int RB = 256, RT = 256;
+constexpr int RB = 1024, RT = 256;  // 1024 blocks: a 256-block grid streamed a 200 MB pair at 3.3 TB/s (ncu)
 
 template <int K, class F>
 __global__ void multi_sum_partial(i64 n, F f, double* part) {
