@@ -6,6 +6,7 @@
 // warps; multi-segment rows reduce their partials in a fixed order (deterministic).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sparse.cuh"
 
@@ -96,6 +97,121 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
         ws[static_cast<i64>(it.slot) * b + c] = acc[q];
       }
     }
+  }
+}
+
+// Tiled SpMM (experimental, see spmm()) for sketches up to 64 columns: out[o, :] (+)= alpha sum_e v_e X[idx_e, :] over the
+// entries e of outer line o (a CSR row for R X, a CSC column for R^T X). One CTA per 128 outer
+// lines (16 warps x 8 lines, accumulators in registers: lane l holds columns l and l + 32) and
+// one chunk of the inner dimension; the chunk's X rows stream through shared memory 256 at a
+// time, so X is read from L2 once per 128 lines instead of once per entry (the segmented kernel
+// gathers a b-wide X row per entry: L2-bound, ~10% of the HBM roofline at the c5 block). Each
+// line's entries of a 256-row X slab are one contiguous range of the per-line 64-tile table.
+// Deterministic: a line's entries are summed in storage order; chunk partials (ws, when the
+// inner dimension is split for parallelism) are combined in chunk order by spmm_chunk_reduce.
+constexpr int TSP_LINES = 8, TSP_WARPS = 16, TSP_OB = TSP_LINES * TSP_WARPS, TSP_SLAB = 256;
+
+__global__ void __launch_bounds__(TSP_WARPS * 32)
+    spmm_tile_kernel(i64 n_outer, i64 n_inner, int nt, const int* __restrict__ tptr, const int* __restrict__ idx,
+                     const double* __restrict__ vals, int b, double alpha, const double* __restrict__ X, i64 ldx,
+                     double beta, double* __restrict__ out, i64 ldo, int chunk_tiles, double* __restrict__ ws) {
+  extern __shared__ double xs[];  // [TSP_SLAB][b]
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const i64 o0 = static_cast<i64>(blockIdx.x) * TSP_OB + warp * TSP_LINES;
+  const int q_begin = blockIdx.y * chunk_tiles, q_end = min(nt, q_begin + chunk_tiles);
+  constexpr int TPS = TSP_SLAB / DevOmega::kTileCols;  // 64-tiles per slab
+  double acc[TSP_LINES][2];
+#pragma unroll
+  for (int r = 0; r < TSP_LINES; ++r) acc[r][0] = acc[r][1] = 0.0;
+  const bool c1 = lane + 32 < b;
+  for (int q0 = q_begin; q0 < q_end; q0 += TPS) {
+    const int q1 = min(q_end, q0 + TPS);
+    const i64 in0 = static_cast<i64>(q0) * DevOmega::kTileCols;
+    const int rows_in = static_cast<int>(min(static_cast<i64>(q1 - q0) * DevOmega::kTileCols, n_inner - in0));
+    __syncthreads();  // the previous slab is consumed
+    // asynchronous 8-byte copies: no register round trip, every load in flight at once
+    for (int e = t; e < rows_in * b; e += blockDim.x) {
+      const int r = e / b, c = e - r * b;
+      cp_async8(xs + e, X + (in0 + r) * ldx + c, true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    // the warp's 8 lines: slab ranges [e0, e1) via two table loads per line (lanes 0-15), and
+    // each line's first 32 entries loaded up front, one per lane (coalesced); the FMAs then take
+    // (index, value) by shuffle — no dependent global load inside the entry loop
+    int tv = 0;
+    if (lane < 2 * TSP_LINES) {
+      const i64 o = o0 + (lane & (TSP_LINES - 1));
+      tv = o < n_outer ? tptr[o * (nt + 1) + (lane < TSP_LINES ? q0 : q1)] : 0;
+    }
+    int e0[TSP_LINES], e1[TSP_LINES], ix0[TSP_LINES];
+    double v0[TSP_LINES];
+#pragma unroll
+    for (int r = 0; r < TSP_LINES; ++r) {
+      e0[r] = __shfl_sync(0xffffffffu, tv, r);
+      e1[r] = __shfl_sync(0xffffffffu, tv, TSP_LINES + r);
+      const int e = e0[r] + lane;
+      ix0[r] = 0;
+      v0[r] = 0.0;
+      if (e < e1[r]) {
+        ix0[r] = static_cast<int>(idx[e] - in0);
+        v0[r] = vals[e];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < TSP_LINES; ++r) {
+      const int cnt_all = e1[r] - e0[r];
+      for (int base = 0; base < cnt_all; base += 32) {
+        int ixc = ix0[r];
+        double vc = v0[r];
+        if (base > 0) {  // lines with more than 32 entries in this slab
+          const int e = e0[r] + base + lane;
+          ixc = 0;
+          vc = 0.0;
+          if (e < e1[r]) {
+            ixc = static_cast<int>(idx[e] - in0);
+            vc = vals[e];
+          }
+        }
+        const int cnt = min(32, cnt_all - base);
+        for (int jj = 0; jj < cnt; ++jj) {
+          const double* xr = xs + __shfl_sync(0xffffffffu, ixc, jj) * b;
+          const double v = __shfl_sync(0xffffffffu, vc, jj);
+          acc[r][0] = fma(v, lane < b ? xr[lane] : 0.0, acc[r][0]);
+          if (c1) acc[r][1] = fma(v, xr[lane + 32], acc[r][1]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < TSP_LINES; ++r) {
+    const i64 o = o0 + r;
+    if (o >= n_outer) break;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c >= b) continue;
+      if (ws) {
+        ws[(static_cast<i64>(blockIdx.y) * n_outer + o) * b + c] = acc[r][h];
+      } else {
+        double* p = out + o * ldo + c;
+        *p = beta == 0.0 ? alpha * acc[r][h] : fma(beta, *p, alpha * acc[r][h]);
+      }
+    }
+  }
+}
+
+__global__ void spmm_chunk_reduce(i64 n_outer, int b, int chunks, const double* __restrict__ ws, double alpha,
+                                  double beta, double* __restrict__ out, i64 ldo) {
+  const i64 total = n_outer * b;
+  for (i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<i64>(gridDim.x) * blockDim.x) {
+    double sacc = 0.0;
+    for (int y = 0; y < chunks; ++y) sacc += ws[y * total + t];
+    const i64 o = t / b, c = t - o * b;
+    double* p = out + o * ldo + c;
+    *p = beta == 0.0 ? alpha * sacc : fma(beta, *p, alpha * sacc);
   }
 }
 
@@ -359,6 +475,22 @@ void DevOmega::build(cudaStream_t s, i64 m_, i64 n_, i64 nnz_, const long long* 
     upload(s, tile_csr, h);
     DFCG_CUDA(cudaStreamSynchronize(s));
   }
+  // row-tile offsets of every CSC column (rows ascend within a column)
+  const i64 rtiles = (m + kTileCols - 1) / kTileCols;
+  if (n * (rtiles + 1) <= (i64{1} << 26)) {
+    ntr = static_cast<int>(rtiles);
+    std::vector<int> h(static_cast<size_t>(n * (rtiles + 1)));
+    for (i64 c = 0; c < n; ++c) {
+      int e = colptr[c];
+      for (i64 q = 0; q <= rtiles; ++q) {
+        const long long lim = q * kTileCols;
+        while (e < colptr[c + 1] && crow[e] < lim) ++e;
+        h[static_cast<size_t>(c * (rtiles + 1) + q)] = q == rtiles ? colptr[c + 1] : e;
+      }
+    }
+    upload(s, tile_csc, h);
+    DFCG_CUDA(cudaStreamSynchronize(s));
+  }
   h_csc2csr = std::move(c2r);
 }
 
@@ -367,7 +499,9 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
   if (om.nnz == 0) return;
   // algorithmic bytes: row+col index, M_e, r_e per entry + both factors once
   prof::Scope scope(prof::kSddmm, s, 2.0 * kY * om.nnz, 24.0 * om.nnz + 8.0 * (om.m + om.n) * kY);
-  if (om.ntc > 0) {
+  const char* tile_env = std::getenv("DFCG_SDDMM_TILE");  // 0 / 1 force the entry-parallel / tiled kernel
+  const int tile_mode = tile_env ? std::atoi(tile_env) : -1;
+  if (om.ntc > 0 && tile_mode != 0) {
     static unsigned configured = 0;  // one bit per device
     int dev = 0;
     DFCG_CUDA(cudaGetDevice(&dev));
@@ -432,6 +566,45 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   const i64 in_rows = transpose ? om.m : om.n;
   prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,
                     (transpose ? 20.0 : 12.0) * om.nnz + 8.0 * b * (in_rows + out_rows * (beta != 0.0 ? 2 : 1)));
+  {  // tiled kernel: 2 <= b <= 64, the tile table of the walk, CSC values streamed (transpose)
+    // Experimental (DFCG_SPMM_TILE=1): measured slower than the segmented kernel at the c5 block
+    // (567 vs 273 us per call at b = 35, N = 1e7: one CTA per SM at 126 registers, slab staging
+    // and the per-slab barriers are not overlapped with the entry loop), so off by default.
+    static const bool tiled_env = std::getenv("DFCG_SPMM_TILE") && std::atoi(std::getenv("DFCG_SPMM_TILE")) == 1;
+    const int nt = transpose ? om.ntr : om.ntc;
+    const double* tv = transpose ? vals_csc : vals_csr;
+    if (tiled_env && b >= 2 && b <= 64 && nt > 0 && tv) {
+      const int* tptr = transpose ? om.tile_csc.get() : om.tile_csr.get();
+      const int* tidx = transpose ? om.csc_row.get() : om.csr_col.get();
+      const i64 outer_blocks = (out_rows + TSP_OB - 1) / TSP_OB;
+      // split the inner dimension until the grid covers ~2 CTAs per SM (chunks of >= one slab)
+      const int max_chunks = std::max(1, (nt + 3) / 4);
+      int chunks = static_cast<int>(std::min<i64>(max_chunks, std::max<i64>(1, (2 * 148 + outer_blocks - 1) / outer_blocks)));
+      const int chunk_tiles = (nt + chunks - 1) / chunks;
+      chunks = (nt + chunk_tiles - 1) / chunk_tiles;
+      const size_t smem = sizeof(double) * TSP_SLAB * b;
+      static unsigned configured = 0;
+      int dev = 0;
+      DFCG_CUDA(cudaGetDevice(&dev));
+      if (!(configured & (1u << dev))) {
+        DFCG_CUDA(cudaFuncSetAttribute(spmm_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(double) * TSP_SLAB * 64)));
+        configured |= 1u << dev;
+      }
+      DBuf<double> ws;
+      if (chunks > 1) ws.alloc(static_cast<i64>(chunks) * out_rows * b, s);
+      spmm_tile_kernel<<<dim3(static_cast<unsigned>(outer_blocks), static_cast<unsigned>(chunks)), TSP_WARPS * 32,
+                         smem, s>>>(out_rows, in_rows, nt, tptr, tidx, tv, static_cast<int>(b), alpha, X, ldx, beta,
+                                    out, ldo, chunk_tiles, chunks > 1 ? ws.get() : nullptr);
+      DFCG_LAUNCH_CHECK();
+      if (chunks > 1) {
+        spmm_chunk_reduce<<<grid_for(out_rows * b), 256, 0, s>>>(out_rows, static_cast<int>(b), chunks, ws.get(),
+                                                                 alpha, beta, out, ldo);
+        DFCG_LAUNCH_CHECK();
+      }
+      return;
+    }
+  }
   if (transpose ? om.has_empty_csc : om.has_empty_csr) {  // rows with no entries: out = beta out
     empty_rows_kernel<<<grid_for(out_rows * b), 256, 0, s>>>(out_rows, ptr, b, beta, out, ldo);
     DFCG_LAUNCH_CHECK();

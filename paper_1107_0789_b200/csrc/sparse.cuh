@@ -43,6 +43,9 @@ struct DevOmega {
   static constexpr int kTileCols = 64;
   int ntc = 0;
   DBuf<int> tile_csr;
+  // The same for the CSC columns over 64-row tiles (tiled transposed SpMM): ntr = 0 when too large.
+  int ntr = 0;
+  DBuf<int> tile_csc;
 
   // rows/cols: CSC-sorted (column-major order, as ObservedMatrix guarantees).
   void build(cudaStream_t s, i64 m, i64 n, i64 nnz, const long long* rows, const long long* cols, const double* vals);
