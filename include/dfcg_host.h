@@ -37,6 +37,14 @@ int dfcg_gen_mc_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigm
 
 /* gen_rmf_instance; outliers U[lo, hi] (the reference draws U[0,1]); M is a caller buffer of
  * m * n doubles (column-major); S0 in draw order (library-allocated). */
+/* BASELINE c4 stand-in (no reference generator): recommender-shaped instance, Zipf(1) row/column
+ * popularity, cells ~ row_pop * col_pop (alias sampling + dedup, ~density * m * n * subset mass),
+ * values clip(round(3.6 + A B^T + N(0, noise^2)), 1, 5), A, B iid N(0, fsd^2). ncols_sub > 0
+ * restricts to a column subset (returned columns are subset positions). Triplets column-major,
+ * library-allocated (free with dfcg_free). */
+int dfcg_gen_recsys_instance(int64_t m, int64_t n, int64_t r, double density, double fsd, double noise,
+                             int64_t ncols_sub, const int64_t* cols_sub, uint64_t seed, uint64_t stream,
+                             int64_t* count, int64_t** rows, int64_t** cols, double** vals);
 int dfcg_gen_rmf_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigma, uint64_t seed, uint64_t stream,
                           double lo, double hi, dfcg_lowrank* L0, dfcg_sparse* S0, double* M);
 

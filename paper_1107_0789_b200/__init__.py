@@ -43,6 +43,7 @@ from .host import (  # noqa: F401,E402
     extract_columns,
     extract_rows,
     gen_mc_instance,
+    gen_recsys_instance,
     launch_count,
     prof_collect,
     prof_enable,

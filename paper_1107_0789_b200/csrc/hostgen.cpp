@@ -1,6 +1,7 @@
 // Host utilities (include/dfcg_host.h): the reference's RNG, sampling and instance
 // generators (P/include/dfc/rng.hpp, sampling.hpp, simgen.hpp), restated so the bench can
 // synthesise the reference's exact inputs on the GPU box.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -154,6 +155,119 @@ int dfcg_partition_columns(uint64_t seed, uint64_t stream, int64_t n, int64_t t,
       for (i64 c : plan[g]) cols[at++] = c;
       offsets[g + 1] = at;
     }
+  });
+}
+
+// BASELINE configs[3] (c4) stand-in — recommender-shaped matrix completion, which the
+// reference's generators cannot produce: m x n with Zipf(s = 1) row and column
+// popularity (the Zipf ranks assigned by random permutations), cells drawn with probability
+// proportional to row_pop * col_pop (Walker alias tables) and deduplicated, values
+// clip(round(3.6 + A B^T + N(0, noise^2)), 1, 5) with A, B iid N(0, fsd^2). Restricted to a column
+// subset (a D-step block), the cells are drawn conditional on the column lying in the subset and
+// the target count scales with the subset's popularity mass, so each block is the block of the
+// full instance in distribution. Everything on SeededRng(seed, stream); parity of this generator
+// is unpinned (no reference), the solves on its output are checked against the oracle.
+namespace {
+struct Alias {
+  std::vector<double> prob;
+  std::vector<int> alias;
+  explicit Alias(const std::vector<double>& w) : prob(w.size()), alias(w.size()) {
+    const i64 k = static_cast<i64>(w.size());
+    double tot = 0.0;
+    for (double x : w) tot += x;
+    std::vector<double> q(w.size());
+    std::vector<int> small, large;
+    for (i64 i = 0; i < k; ++i) {
+      q[i] = w[i] * k / tot;
+      (q[i] < 1.0 ? small : large).push_back(static_cast<int>(i));
+    }
+    while (!small.empty() && !large.empty()) {
+      const int a = small.back(), b = large.back();
+      small.pop_back();
+      prob[a] = q[a];
+      alias[a] = b;
+      q[b] -= 1.0 - q[a];
+      if (q[b] < 1.0) {
+        large.pop_back();
+        small.push_back(b);
+      }
+    }
+    for (int i : large) prob[i] = 1.0, alias[i] = i;
+    for (int i : small) prob[i] = 1.0, alias[i] = i;
+  }
+  int sample(SeededRng& r) const {
+    const i64 i = static_cast<i64>(r.index(prob.size()));
+    return r.uniform() < prob[i] ? static_cast<int>(i) : alias[i];
+  }
+};
+std::vector<double> zipf_popularity(i64 k, SeededRng& r) {  // 1 / rank, ranks a random permutation
+  std::vector<i64> perm(k);
+  for (i64 i = 0; i < k; ++i) perm[i] = i;
+  for (i64 i = k - 1; i > 0; --i) std::swap(perm[i], perm[static_cast<i64>(r.index(i + 1))]);
+  std::vector<double> w(k);
+  for (i64 i = 0; i < k; ++i) w[i] = 1.0 / static_cast<double>(perm[i] + 1);
+  return w;
+}
+}  // namespace
+
+int dfcg_gen_recsys_instance(int64_t m, int64_t n, int64_t r, double density, double fsd, double noise,
+                             int64_t ncols_sub, const int64_t* cols_sub, uint64_t seed, uint64_t stream,
+                             int64_t* count, int64_t** rows, int64_t** cols, double** vals) {
+  return dfcg_guard_call([&] {
+    if (m < 1 || n < 1 || r < 1 || !(density > 0 && density <= 1))
+      throw std::invalid_argument("gen_recsys_instance: bad shape or density");
+    SeededRng rng(seed, stream);
+    std::vector<double> A(static_cast<size_t>(m * r)), B(static_cast<size_t>(n * r));
+    for (double& x : A) x = rng.normal(0.0, fsd);
+    for (double& x : B) x = rng.normal(0.0, fsd);
+    const std::vector<double> rp = zipf_popularity(m, rng), cp = zipf_popularity(n, rng);
+    std::vector<i64> sub;
+    if (ncols_sub > 0) {
+      sub.assign(cols_sub, cols_sub + ncols_sub);
+      for (i64 c : sub)
+        if (c < 0 || c >= n) throw std::out_of_range("gen_recsys_instance: column subset out of range");
+    } else {
+      sub.resize(static_cast<size_t>(n));
+      for (i64 j = 0; j < n; ++j) sub[static_cast<size_t>(j)] = j;
+    }
+    const i64 w = static_cast<i64>(sub.size());
+    std::vector<double> wq(static_cast<size_t>(w));
+    double mass = 0.0, tot = 0.0;
+    for (double x : cp) tot += x;
+    for (i64 j = 0; j < w; ++j) mass += (wq[static_cast<size_t>(j)] = cp[static_cast<size_t>(sub[static_cast<size_t>(j)])]);
+    const i64 target = std::max<i64>(1, std::llround(density * static_cast<double>(m) * static_cast<double>(n) * mass / tot));
+    const Alias ar(rp), ac(wq);
+    std::vector<std::uint64_t> keys;  // local column * m + row: column-major order
+    for (int round = 0; round < 8 && static_cast<i64>(keys.size()) < target - target / 100; ++round) {
+      const i64 want = target - static_cast<i64>(keys.size());
+      for (i64 d = 0; d < want; ++d) {
+        const std::uint64_t row = static_cast<std::uint64_t>(ar.sample(rng));
+        const std::uint64_t col = static_cast<std::uint64_t>(ac.sample(rng));
+        keys.push_back(col * static_cast<std::uint64_t>(m) + row);
+      }
+      std::sort(keys.begin(), keys.end());
+      keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    }
+    const i64 cnt = static_cast<i64>(keys.size());
+    int64_t* ro = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<i64>(cnt, 1)));
+    int64_t* co = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<i64>(cnt, 1)));
+    double* va = static_cast<double*>(std::malloc(sizeof(double) * std::max<i64>(cnt, 1)));
+    if (!ro || !co || !va) throw std::bad_alloc();
+    for (i64 e = 0; e < cnt; ++e) {
+      const i64 i = static_cast<i64>(keys[static_cast<size_t>(e)] % static_cast<std::uint64_t>(m));
+      const i64 jl = static_cast<i64>(keys[static_cast<size_t>(e)] / static_cast<std::uint64_t>(m));
+      const i64 j = sub[static_cast<size_t>(jl)];
+      double dot = 0.0;
+      for (i64 k = 0; k < r; ++k) dot += A[static_cast<size_t>(k * m + i)] * B[static_cast<size_t>(k * n + j)];
+      const double v = std::round(3.6 + dot + rng.normal(0.0, noise));
+      ro[e] = i;
+      co[e] = jl;
+      va[e] = std::min(5.0, std::max(1.0, v));
+    }
+    *count = cnt;
+    *rows = ro;
+    *cols = co;
+    *vals = va;
   });
 }
 

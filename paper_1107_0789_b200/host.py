@@ -110,6 +110,27 @@ def gen_mc_instance(m, n, r, s, sigma, seed, stream=0):
     return _lowrank_out(L0), Observed(m, n, R, Cc, V)
 
 
+def gen_recsys_instance(m, n, r, density, seed, stream=0, cols=None, fsd=None, noise=0.8):
+    """BASELINE c4 stand-in (dfcg_gen_recsys_instance): Zipf row/column popularity, values
+    clip(round(3.6 + A B^T + N(0, noise^2)), 1, 5), A, B iid N(0, 0.3^2 / r); `cols` restricts the
+    instance to a column subset (a D-step block; columns renumbered by subset position)."""
+    fsd = 0.3 / np.sqrt(r) if fsd is None else fsd
+    sub = np.asarray(cols if cols is not None else [], np.int64)
+    cnt = i64()
+    rows_p, cols_p, vals_p = i64ptr(), i64ptr(), C.POINTER(C.c_double)()
+    _check(lib().dfcg_gen_recsys_instance(i64(m), i64(n), i64(r), C.c_double(density), C.c_double(fsd),
+                                          C.c_double(noise), i64(len(sub)), _i(sub) if len(sub) else None,
+                                          u64(seed), u64(stream), C.byref(cnt), C.byref(rows_p), C.byref(cols_p),
+                                          C.byref(vals_p)))
+    k = cnt.value
+    R = np.ctypeslib.as_array(rows_p, shape=(max(k, 1),))[:k].copy()
+    Cc = np.ctypeslib.as_array(cols_p, shape=(max(k, 1),))[:k].copy()
+    V = np.ctypeslib.as_array(vals_p, shape=(max(k, 1),))[:k].copy()
+    for p in (rows_p, cols_p, vals_p):
+        lib().dfcg_free(C.cast(p, C.c_void_p))
+    return Observed(m, len(sub) if len(sub) else n, R, Cc, V)
+
+
 def gen_rmf_instance(m, n, r, s, sigma, seed, stream=0, lo=0.0, hi=1.0):
     """gen_rmf_instance (simgen.hpp:64-82); outliers U[lo, hi] (reference: U[0,1])."""
     L0 = LowRankC()

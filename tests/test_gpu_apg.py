@@ -92,6 +92,15 @@ def test_apg_mc_wide_row_block_window(op_mode, monkeypatch):
     assert_mc_parity(P.extract_rows(obs, rows), max_iters=60)
 
 
+def test_apg_mc_c4_standin_block():
+    """A block of the recommender-shaped c4 stand-in (Zipf popularity, integer ratings with a
+    3.6 offset: a large rank-one mean component), default config, 60 iterations."""
+    m, n = 400, 3000
+    groups = P.partition_columns(3, 0xDFC0000000000001, n, 8)
+    blk = P.gen_recsys_instance(m, n, 5, 0.05, 3, cols=groups[0])
+    assert_mc_parity(blk, max_iters=60)
+
+
 def test_apg_mc_operator_switching():
     """A sparse block whose rank rises past and falls back below the dense-operator threshold
     (acceptance-style floor, P/tests/acceptance.cpp:127-130): iterations switch between the

@@ -137,3 +137,26 @@ def test_compute_fails_loudly_without_gpu():
     L0, obs = P.gen_mc_instance(20, 20, 2, 200, 0.1, 1)
     with pytest.raises(P.DfcError):
         P.apg_mc(obs)
+
+
+def test_recsys_generator_c4_standin():
+    """BASELINE c4 stand-in (no reference generator; parity of the generator itself is unpinned):
+    deterministic, column-major sorted unique cells, ratings in {1..5} with the 3.6 offset, Zipf
+    skew (the most popular row far above the mean), and a column-subset block that is the same as
+    the cells of the full instance restricted to those columns in distribution (checked on the
+    density and the rating mean)."""
+    m, n, r = 400, 3000, 5
+    full = P.gen_recsys_instance(m, n, r, 0.02, 7)
+    again = P.gen_recsys_instance(m, n, r, 0.02, 7)
+    assert np.array_equal(full.rows, again.rows) and np.array_equal(full.vals, again.vals)
+    key = full.cols * m + full.rows
+    assert np.all(np.diff(key) > 0)  # sorted column-major, no duplicates
+    assert set(np.unique(full.vals)) <= {1.0, 2.0, 3.0, 4.0, 5.0}
+    assert 3.2 < full.vals.mean() < 4.0
+    assert 0.5 * 0.02 * m * n < full.count <= 0.02 * m * n * 1.001
+    rc = np.bincount(full.rows, minlength=m)
+    assert rc.max() > 5 * rc.mean()
+    groups = P.partition_columns(7, 0xDFC0000000000001, n, 8)
+    blk = P.gen_recsys_instance(m, n, r, 0.02, 7, cols=groups[0])
+    assert blk.n == len(groups[0]) and blk.cols.max() < blk.n
+    assert 3.2 < blk.vals.mean() < 4.0
