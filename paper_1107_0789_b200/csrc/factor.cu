@@ -965,8 +965,13 @@ __global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
     double* dp = dst + r0 * JW + soff;
     for (int r = r0; r < n4; r += T / CH, sp += (T / CH) * ld, dp += (T / CH) * JW) cp_async16(dp, r < n ? sp : src, r < n);
   };
+  // Programmatic dependent launch (when the host enables it): everything above only reads the
+  // argument block; the previous round's writes to W are visible after griddepcontrol.wait, and
+  // the next round may start launching once every CTA of this one has issued its loads.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   stage(Wp, W, ldw, rows, rows4);
   asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("griddepcontrol.launch_dependents;\n" ::);
   if (prefetch_v) {  // second group: the V pair, consumed only after the rotation is known
     stage(Vp, V, ldv, nv, nv4);
     asm volatile("cp.async.commit_group;\n" ::);
@@ -1576,6 +1581,8 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   }
   const JacobiArgs h_args{wrows, nj, np, np, W.get(), J.get(), d_off, tol, p, prefetch_v};
   DFCG_CUDA(cudaMemcpyAsync(d_args, &h_args, sizeof(JacobiArgs), cudaMemcpyHostToDevice, s));
+  static const int pdl_env = std::getenv("DFCG_JACOBI_PDL") ? std::atoi(std::getenv("DFCG_JACOBI_PDL")) : 1;
+  const bool use_pdl = pdl_env == 1;
   auto launch_round = [&](int r) {
     const int inner = r == 0 ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
@@ -1583,13 +1590,22 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = smem_launch;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(CS);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (CS > 1) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = static_cast<unsigned>(CS);
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    if (use_pdl && r > 0) {  // round r overlaps its launch with round r - 1 (griddepcontrol in the kernel)
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = CS > 1 ? 1 : 0;
+    cfg.numAttrs = na;
     const JacobiArgs* ap = d_args;
 #define DFCG_JROUND(nb, cs) DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_round_resident_kernel<nb, cs>, ap, r, inner))
     if (NB == 8) {
