@@ -149,6 +149,32 @@ __device__ __forceinline__ void cp_async_wait() {
 // 2^-53: SeededRng::normal (P/include/dfc/rng.hpp:62-66) on raw mt19937_64 words, on the device.
 void box_muller_device(cudaStream_t s, const std::uint64_t* raw, double* out, i64 n);
 
+// Programmatic dependent launch (PDL): a kernel launched with pdl_launch may begin while its
+// stream predecessor is still running; it must call pdl_wait() before it touches any global
+// memory the predecessor reads or writes (the wait returns once the predecessor grid has
+// completed and its writes are visible), and may call pdl_trigger() to let its own successor
+// launch early. Hides the launch gap of the latency-bound chains (blocked Cholesky, small GEMMs,
+// Jacobi rounds) of a solve that has the GPU to itself (see pdl_enabled(), dense.cu).
+bool pdl_enabled();
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  DFCG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+#endif
+
 // APG solves currently stepping on device `dev`: kernels with a latency / occupancy trade-off
 // (the Jacobi cluster size) consult it.
 int active_streams(int dev);

@@ -100,6 +100,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   double* sA = smem;
   double* sB = smem + STAGES * TileA::elems;
 
+  pdl_wait();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp / (BN / WN)) * WM, wn = (warp % (BN / WN)) * WN;
   const i64 m0 = static_cast<i64>(blockIdx.y) * BM, n0 = static_cast<i64>(blockIdx.x) * BN;
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     }
     cp_async_commit();
   }
+  pdl_trigger();
 
   const int fr = lane >> 2, fk = lane & 3;
   for (int t = 0; t < ntiles; ++t) {
@@ -185,6 +187,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 
 __global__ void splitk_reduce(i64 M, i64 N, int splits, const double* __restrict__ ws, double alpha, double beta,
                               double* __restrict__ C, i64 ldc) {
+  pdl_wait();
+  pdl_trigger();
   const i64 total = M * N;
   for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<i64>(gridDim.x) * blockDim.x) {
@@ -207,6 +211,24 @@ __global__ void scale_kernel(i64 M, i64 N, double beta, double* C, i64 ldc) {
 }
 
 int g_num_sms = 0;
+
+}  // namespace
+
+// On when at most two solves share the device (latency mode: a lone block per GPU, the two
+// DFC-Nys subproblems): measured 24.3 -> 23.2 ms per lone c2 iteration, but 128.6 -> 120.2
+// block-it/s with eight concurrent solves (dependent CTAs waiting at griddepcontrol.wait hold SM
+// slots other streams would use). DFCG_PDL=0 / 2 forces off / on.
+bool pdl_enabled() {
+  static const int env = std::getenv("DFCG_PDL") ? std::atoi(std::getenv("DFCG_PDL")) : 1;
+  if (env == 0) return false;
+  if (env == 2) return true;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return active_streams(dev) <= 2;
+}
+
+namespace {
+
 int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;
@@ -278,11 +300,11 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
                    reinterpret_cast<std::uintptr_t>(B) % 16 == 0;
   auto run = [&](dim3 grid, i64 kc, double* ws) {
     if (vec)
-      gemm_kernel<TA, TB, BM, BN, WM, WN, true><<<grid, THREADS, smem, s>>>(M, N, K, kc, alpha, A, lda, B, ldb, beta, C,
-                                                                            ldc, ws, upper_only);
+      pdl_launch(gemm_kernel<TA, TB, BM, BN, WM, WN, true>, grid, dim3(THREADS), smem, s, M, N, K, kc, alpha, A, lda, B,
+                 ldb, beta, C, ldc, ws, upper_only);
     else
-      gemm_kernel<TA, TB, BM, BN, WM, WN, false><<<grid, THREADS, smem, s>>>(M, N, K, kc, alpha, A, lda, B, ldb, beta,
-                                                                             C, ldc, ws, upper_only);
+      pdl_launch(gemm_kernel<TA, TB, BM, BN, WM, WN, false>, grid, dim3(THREADS), smem, s, M, N, K, kc, alpha, A, lda,
+                 B, ldb, beta, C, ldc, ws, upper_only);
     DFCG_LAUNCH_CHECK();
   };
   if (splits <= 1) {
@@ -293,7 +315,7 @@ void launch_gemm_cfg(cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const do
   if (upper_only & 1) ws.zero(s);  // skipped tiles leave their partials unwritten
   run(dim3(gx, gy, splits), kchunk, ws.get());
   const int rb = static_cast<int>(std::min<i64>((M * N + 255) / 256, 4L * num_sms()));
-  splitk_reduce<<<rb, 256, 0, s>>>(M, N, splits, ws.get(), alpha, beta, C, ldc);
+  pdl_launch(splitk_reduce, dim3(rb), dim3(256), 0, s, M, N, splits, ws.get(), alpha, beta, C, ldc);
   DFCG_LAUNCH_CHECK();
 }
 

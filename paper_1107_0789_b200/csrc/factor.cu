@@ -92,6 +92,8 @@ __device__ long long g_potrf_trace[64];
 __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr,
                                                          const double* maxdiag, double rel_tol, int* fail) {
   extern __shared__ double psm[];
+  pdl_wait();
+  pdl_trigger();
 #ifdef DFCG_POTRF_TRACE
   long long tp_ = clock64();
 #endif
@@ -329,8 +331,8 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   AuxStream& aux = aux_stream(dev);
   auto potrf = [&](cudaStream_t st, i64 k0, int kb) {
     prof::Scope scope(prof::kCholesky, st, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
-    potrf_diag_kernel<<<1, 256, kPotrfSmem, st>>>(kb, G + k0 * ldg + k0, ldg, Rinv + k0 * ldr + k0, ldr,
-                                                  maxdiag.get(), rel_tol, fail);
+    pdl_launch(potrf_diag_kernel, dim3(1), dim3(256), kPotrfSmem, st, kb, G + k0 * ldg + k0, ldg,
+               Rinv + k0 * ldr + k0, ldr, static_cast<const double*>(maxdiag.get()), rel_tol, fail);
     DFCG_LAUNCH_CHECK();
   };
   potrf(s, 0, static_cast<int>(std::min<i64>(CNB, n)));

@@ -23,6 +23,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
     {"DFCG_GEMM_VARIANT": "7"},
     {"DFCG_CHOL_SCALE": "0"},
     {"DFCG_JACOBI_GRAPH": "1"},
+    {"DFCG_PDL": "2"},
+    {"DFCG_PDL": "0", "DFCG_JACOBI_PDL": "0"},
     {"DFCG_DENSE_OP": "0", "DFCG_SPMM_TILE": "1"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_TILE": "0"},
     {"DFCG_JACOBI_GRAPH": "1", "DFCG_JACOBI_CLUSTER": "1"},
