@@ -5,6 +5,8 @@
        broadcasts it (NCCL over NVLink when the process group is "nccl"),
     2. every rank projects its own blocks: R_g = right_g (U_b^T left_g)^T,
     3. the projected rows are gathered to rank 0 and scattered to their original columns.
+DFC-Nys (nystrom_distributed): the two subproblems (C-hat, R-hat) solve concurrently on two
+ranks; R-hat's factors are broadcast from its rank (the only exchange) and rank 0 combines.
 The compute steps are injected (GPU C ABI in bench.py, the CPU oracle in the gloo tests), so
 the same host logic runs under both backends.
 """
@@ -88,3 +90,20 @@ def column_project_distributed(dist, groups: Sequence[np.ndarray], local_ests: D
     for g, idx in enumerate(groups):
         right[np.asarray(idx)] = rows[g][: len(idx)]
     return Ub, right
+
+
+def nystrom_distributed(dist, local_ests: Dict[int, object], rows, cols, nystrom_fn: Callable, make_est: Callable,
+                        device="cpu"):
+    """DFC-Nys combine over ranks (P/include/dfc/dfc.hpp:250-324, gen_nystrom
+    P/include/dfc/sketch.hpp:241-266): subproblem 0 (C-hat = M[:, cols]) lives on rank 0 and
+    subproblem 1 (R-hat = M[rows, :]) on rank shard(2, world, .)'s owner of block 1; R-hat's
+    factors (d x k_R, n x k_R) are broadcast from that rank and rank 0 returns
+    nystrom_fn(C_hat, make_est(R_left, R_right), rows, cols). None on the other ranks."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    src = 1 % world
+    R = local_ests.get(1)
+    rl = broadcast_array(dist, R.left if rank == src else None, src, device)
+    rr = broadcast_array(dist, R.right if rank == src else None, src, device)
+    if rank != 0:
+        return None
+    return nystrom_fn(local_ests[0], make_est(rl, rr), rows, cols)

@@ -69,6 +69,40 @@ def test_sharded_dfc_proj_matches_single_process(tmp_path):
     assert err < 1e-10, err
 
 
+def _worker_nys(rank, world, port, out_path):
+    import torch.distributed as dist
+
+    from paper_1107_0789_b200.distributed import nystrom_distributed, shard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, n, l, d, seed = 120, 90, 30, 40, 5
+    L0, obs = O.gen_mc_instance(m, n, 3, 5000, 0.1, 3, 0)
+    # dfc_nys's D step (P/include/dfc/dfc.hpp:250-290): sorted row / column samples
+    rows = np.sort(O.sample_without_replacement(seed, 0xDFC0000000000002, m, d))
+    cols = np.sort(O.sample_without_replacement(seed, 0xDFC0000000000003, n, l))
+    subs = {0: lambda: O.extract_columns(obs, cols), 1: lambda: O.extract_rows(obs, rows)}
+    local = {g: O.apg_mc(subs[g]())[0] for g in shard(2, world, rank)}
+    res = nystrom_distributed(dist, local, rows, cols, O.gen_nystrom, O.Estimate)
+    if rank == 0:
+        ref, _ = O.dfc_run(obs, "nys", l=l, d=d, seed=seed)
+        err = np.linalg.norm(res.dense() - ref.dense()) / np.linalg.norm(ref.dense())
+        with open(out_path, "w") as f:
+            f.write(repr(float(err)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_dfc_nys_matches_single_process(tmp_path):
+    """DFC-Nys with its two subproblems on two ranks (R-hat's factors broadcast to rank 0)."""
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "err.txt")
+    mp.spawn(_worker_nys, args=(2, _free_port(), out), nprocs=2, join=True)
+    err = float(open(out).read())
+    assert err < 1e-10, err
+
+
 def test_shard_covers_blocks_once():
     from paper_1107_0789_b200.distributed import shard
 
