@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <random>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -79,12 +80,13 @@ class SeededRng {
   std::mt19937_64 engine_;
 };
 
-// Device-resident prefix of the normal stream of SeededRng(seed, stream), in fixed chunks that
-// are immutable once published (concurrent solves read them without locking). A background
-// thread generates ahead of the furthest position any solve has asked for (kAhead chunks), so
-// the sequential mt19937_64 draws and the host Box-Muller never sit on a solve's critical
-// path in steady state; the upload goes through pinned memory on the cache's own non-blocking
-// stream (no legacy-stream synchronisation with the solves' streams).
+// Device-resident window of the normal stream of SeededRng(seed, stream), in fixed chunks that
+// are immutable while resident (a fetch pins the chunks it copies from). Background threads draw
+// the chunks each fetch will need next (kAhead past its window), so the sequential mt19937_64
+// draws never sit on a solve's critical path in steady state; least-recently-fetched chunks
+// are evicted beyond a device budget and redrawn from their engine snapshot if a later solve
+// (every solve restarts at position 0) asks again. Uploads run on the cache's own
+// non-blocking stream (no legacy-stream synchronisation with the solves' streams).
 class NormalCache {
  public:
   static constexpr i64 kChunk = i64{1} << 22;  // 4 Mi normals = 32 MiB per chunk
@@ -92,6 +94,8 @@ class NormalCache {
 
   NormalCache(int device, std::uint64_t seed, std::uint64_t stream) : device_(device) {
     mt_.seed(SeededRng::engine_seed(seed, stream));
+    const char* env = std::getenv("DFCG_NORMALS_MAX_CHUNKS");
+    max_resident_ = env ? std::max<i64>(2 * kAhead + 2, std::atoll(env)) : 64;
   }
   ~NormalCache() {
     {
@@ -101,7 +105,10 @@ class NormalCache {
     cv_.notify_all();
     if (worker_.joinable()) worker_.join();
     if (transformer_.joinable()) transformer_.join();
-    for (double* p : chunks_) cudaFree(p);
+    for (double* p : chunks_)
+      if (p) cudaFree(p);
+    for (cudaEvent_t e : use_ev_)
+      if (e) cudaEventDestroy(e);
     for (std::uint64_t* p : raw_buf_)
       if (p) cudaFreeHost(p);
     if (stream_) cudaStreamDestroy(stream_);
@@ -110,41 +117,77 @@ class NormalCache {
   // dst[0:count) <- normals[pos : pos+count) on stream s.
   void fetch(i64 pos, i64 count, double* dst, cudaStream_t s) {
     if (count <= 0) return;
-    const i64 need = (pos + count + kChunk - 1) / kChunk;
-    std::vector<double*> src;
+    const i64 c0 = pos / kChunk, c1 = (pos + count + kChunk - 1) / kChunk;  // chunks [c0, c1)
+    static const i64 ahead = std::getenv("DFCG_NORMALS_AHEAD") ? std::atoll(std::getenv("DFCG_NORMALS_AHEAD")) : kAhead;
+    std::vector<double*> src(static_cast<size_t>(c1 - c0));
     {
       std::unique_lock<std::mutex> lock(mu_);
       if (error_) throw std::runtime_error(err_msg_);
-      static const i64 ahead = std::getenv("DFCG_NORMALS_AHEAD") ? std::atoll(std::getenv("DFCG_NORMALS_AHEAD")) : kAhead;
-      if (need + ahead > wanted_) {
-        wanted_ = need + ahead;
+      grow(c1 + ahead);
+      bool more = false;
+      for (i64 c = c0; c < c1 + ahead; ++c)
+        if (!chunks_[c] && !inflight_[c] && want_.insert(c).second) more = true;
+      if (more) {
         if (!worker_.joinable()) {
           worker_ = std::thread([this] { run_raw(); });
           transformer_ = std::thread([this] { run_transform(); });
         }
         cv_.notify_all();
       }
-      cv_.wait(lock, [&] { return static_cast<i64>(chunks_.size()) >= need || error_; });
-      if (error_) throw std::runtime_error(err_msg_);
-      src = chunks_;
+      for (;;) {  // (a needed chunk evicted before this fetch pinned it is requested again)
+        if (error_) throw std::runtime_error(err_msg_);
+        bool ready = true, ask = false;
+        for (i64 c = c0; c < c1; ++c)
+          if (!chunks_[c]) {
+            ready = false;
+            if (!inflight_[c] && want_.insert(c).second) ask = true;
+          }
+        if (ready) break;
+        if (ask) cv_.notify_all();
+        cv_.wait(lock);
+      }
+      for (i64 c = c0; c < c1; ++c) {
+        src[static_cast<size_t>(c - c0)] = chunks_[c];
+        ++pins_[c];  // not evicted until this fetch's copies are ordered before its free
+        last_use_[c] = ++clock_;
+      }
     }
     i64 done = 0;
     while (done < count) {
       const i64 p = pos + done;
       const i64 c = p / kChunk, off = p % kChunk;
       const i64 n = std::min(count - done, kChunk - off);
-      DFCG_CUDA(cudaMemcpyAsync(dst + done, src[static_cast<size_t>(c)] + off, sizeof(double) * n,
+      DFCG_CUDA(cudaMemcpyAsync(dst + done, src[static_cast<size_t>(c - c0)] + off, sizeof(double) * n,
                                 cudaMemcpyDeviceToDevice, s));
       done += n;
+    }
+    std::lock_guard<std::mutex> lock(mu_);
+    for (i64 c = c0; c < c1; ++c) {
+      if (!use_ev_[c]) DFCG_CUDA(cudaEventCreateWithFlags(&use_ev_[c], cudaEventDisableTiming));
+      DFCG_CUDA(cudaEventRecord(use_ev_[c], s));
+      --pins_[c];
     }
   }
 
  private:
-  // Two-stage pipeline: this thread draws the raw 64-bit words of chunk k + 1 (sequential
-  // mt19937_64, the stream's only serial part) while run_transform() uploads chunk k and turns
-  // it into normals on the device — a chunk every max(draw, transform) instead of their sum. Wide
-  // blocks consume w * b normals per partial SVD (7.2 M for a 1250 x 10000 DFC-Nys row block),
-  // so the generator's rate bounds them otherwise.
+  // Chunk bookkeeping (under mu_): device chunk or nullptr (not resident), the engine state at
+  // the start of every chunk drawn so far (an evicted chunk is redrawn from it), pin counts of
+  // in-progress fetches, and LRU stamps. At most max_resident_ chunks stay on the device
+  // (DFCG_NORMALS_MAX_CHUNKS, default 64 = 2 GiB): a solve draws w * b normals per partial SVD,
+  // so an unbounded prefix reached 29 GB for a 500-iteration DFC-Nys row block and growing the
+  // device pool for it stalled every concurrent solve.
+  void grow(i64 n) {
+    if (static_cast<i64>(chunks_.size()) >= n) return;
+    chunks_.resize(static_cast<size_t>(n), nullptr);
+    inflight_.resize(static_cast<size_t>(n), 0);
+    pins_.resize(static_cast<size_t>(n), 0);
+    last_use_.resize(static_cast<size_t>(n), 0);
+    use_ev_.resize(static_cast<size_t>(n), nullptr);
+  }
+
+  // Two-stage pipeline: this thread draws the raw 64-bit words of a chunk (sequential
+  // mt19937_64, the stream's only serial part; an evicted chunk restarts from its snapshot)
+  // while run_transform() uploads the previous one and turns it into normals on the device.
   void run_raw() {
     try {
       DFCG_CUDA(cudaSetDevice(device_));
@@ -157,18 +200,35 @@ class NormalCache {
       }
       for (;;) {
         int b = -1;
+        i64 c = -1;
+        Mt64 g;
+        bool sequential = false;
         {
           std::unique_lock<std::mutex> lock(mu_);
-          cv_.wait(lock, [&] { return stop_ || (raw_made_ < wanted_ && !raw_free_.empty()); });
+          cv_.wait(lock, [&] { return stop_ || (!want_.empty() && !raw_free_.empty()); });
           if (stop_) return;
+          c = *want_.begin();
+          const i64 next = static_cast<i64>(snap_.size());
+          if (c >= next) {  // draw forward: the next chunk in sequence (a prerequisite of c)
+            if (c == next) want_.erase(want_.begin());
+            c = next;
+            snap_.push_back(mt_);
+            sequential = true;
+            grow(c + 1);
+          } else {  // redraw an evicted chunk from its snapshot
+            want_.erase(want_.begin());
+            if (chunks_[c] || inflight_[c]) continue;
+            g = snap_[static_cast<size_t>(c)];
+          }
+          inflight_[c] = 1;
           b = raw_free_.back();
           raw_free_.pop_back();
         }
-        mt64_fill(mt_, raw_buf_[b], 2 * kChunk);
+        if (sequential) mt64_fill(mt_, raw_buf_[b], 2 * kChunk);
+        else mt64_fill(g, raw_buf_[b], 2 * kChunk);
         {
           std::lock_guard<std::mutex> lock(mu_);
-          raw_q_.push_back(b);
-          ++raw_made_;
+          raw_q_.push_back({c, b});
         }
         cv_.notify_all();
       }
@@ -184,13 +244,32 @@ class NormalCache {
       std::uint64_t* raw_dev = nullptr;
       DFCG_CUDA(cudaMalloc(reinterpret_cast<void**>(&raw_dev), sizeof(std::uint64_t) * 2 * kChunk));
       for (;;) {
+        i64 c = -1;
         int b = -1;
+        std::vector<std::pair<double*, cudaEvent_t>> victims;
         {
           std::unique_lock<std::mutex> lock(mu_);
           cv_.wait(lock, [&] { return stop_ || !raw_q_.empty(); });
           if (stop_) break;
-          b = raw_q_.front();
+          c = raw_q_.front().first;
+          b = raw_q_.front().second;
           raw_q_.erase(raw_q_.begin());
+          // evict least-recently fetched, unpinned chunks down to the budget (this one included)
+          i64 resident = 1;
+          for (double* p : chunks_) resident += p != nullptr;
+          while (resident > max_resident_) {
+            i64 v = -1;
+            for (i64 k = 0; k < static_cast<i64>(chunks_.size()); ++k)
+              if (chunks_[k] && pins_[k] == 0 && (v < 0 || last_use_[k] < last_use_[v])) v = k;
+            if (v < 0) break;
+            victims.push_back({chunks_[v], use_ev_[v]});
+            chunks_[v] = nullptr;
+            --resident;
+          }
+        }
+        for (auto& [p, ev] : victims) {  // freed on this stream after the chunk's last copy
+          if (ev) DFCG_CUDA(cudaStreamWaitEvent(stream_, ev, 0));
+          DFCG_CUDA(cudaFreeAsync(p, stream_));
         }
         // Box-Muller on the device (CUDA's log / cos, <= 1 ulp from the host libm the oracle
         // uses; the raw words are bit-identical): the host keeps only the serial draws.
@@ -203,7 +282,9 @@ class NormalCache {
         {
           std::lock_guard<std::mutex> lock(mu_);
           raw_free_.push_back(b);
-          chunks_.push_back(d);
+          chunks_[c] = d;
+          inflight_[c] = 0;
+          last_use_[c] = ++clock_;
         }
         cv_.notify_all();
       }
@@ -221,17 +302,25 @@ class NormalCache {
   }
 
   int device_;
-  Mt64 mt_;
+  Mt64 mt_;  // the engine after the last chunk drawn in sequence
   std::mutex mu_;
   std::condition_variable cv_;
   std::thread worker_, transformer_;
   bool stop_ = false, error_ = false;
   std::string err_msg_;
-  i64 wanted_ = 0, raw_made_ = 0;
+  i64 max_resident_ = 64;
+  std::uint64_t clock_ = 0;
+  std::set<i64> want_;
+  std::vector<Mt64> snap_;
+  std::vector<double*> chunks_;
+  std::vector<char> inflight_;
+  std::vector<int> pins_;
+  std::vector<std::uint64_t> last_use_;
+  std::vector<cudaEvent_t> use_ev_;
   static constexpr int kRawBufs = 3;
   std::uint64_t* raw_buf_[kRawBufs] = {nullptr, nullptr, nullptr};
-  std::vector<int> raw_q_, raw_free_;
-  std::vector<double*> chunks_;
+  std::vector<std::pair<i64, int>> raw_q_;
+  std::vector<int> raw_free_;
   cudaStream_t stream_ = nullptr;
 };
 

@@ -90,3 +90,33 @@ def test_device_normal_stream_matches_reference_rng():
             ulp = np.abs(out - ref) / np.spacing(np.abs(ref))
             assert ulp.max() <= 4, (stream, pos, ulp.max())
             assert np.mean(out == ref) > 0.5
+
+
+def test_normal_stream_eviction_and_redraw():
+    """With a 10-chunk device budget (DFCG_NORMALS_MAX_CHUNKS), reading far ahead evicts the
+    first chunks; reading them again redraws them from their engine snapshots — the same values
+    (a child process: the budget is read once per cache)."""
+    code = r"""
+import ctypes as C, numpy as np, sys
+sys.path.insert(0, %r)
+import paper_1107_0789_b200 as P
+L = P.lib()
+def fetch(pos, n):
+    out = np.zeros(n)
+    assert L.dfcg_normals_fetch(P.context(0), C.c_int(0), C.c_int64(pos), C.c_int64(n),
+                                out.ctypes.data_as(C.c_void_p)) == 0
+    return out
+K = 1 << 22
+first = fetch(0, 5000)
+mid = fetch(K - 100, 300)
+for c in range(1, 40):
+    fetch(c * K + 7, 1000)  # walk 40 chunks: the budget forces evictions
+assert np.array_equal(fetch(0, 5000), first)
+assert np.array_equal(fetch(K - 100, 300), mid)
+ref = P.SeededRng(0x737674, 0).normal(5000)
+assert np.abs(first - ref).max() <= 4 * np.spacing(np.abs(ref)).max()
+print("OK")
+""" % ROOT
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "DFCG_NORMALS_MAX_CHUNKS": "10"})
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
