@@ -253,14 +253,19 @@ __global__ void scatter_dense_kernel(i64 N, const int* __restrict__ row, const i
 // entries from there: each factor row is read from L2 once per tile instead of once per entry
 // (~6x less L2 traffic at 10% density). Each lane walks a chunk starting at k = lane, so the
 // 16 lanes of a shared-memory phase hit 16 distinct banks whatever rows they read.
-constexpr int STR = 64, STC = 64, SKC = 32, SDD_T = 256, SEPT = 4;
-constexpr size_t kSddmmSmem = sizeof(double) * 2 * (STR + STC) * SKC;
-static_assert(STC == DevOmega::kTileCols, "tile width must match the CSR column-tile table");
+// Tile widths: TW column tiles of the CSR table per CTA (TW = 1: 64 x 64 tiles, the high-rank
+// c2 setting; TW = 4 with 16-wide k chunks at kY <= 32: 64 x 256 tiles, four times the entries
+// per CTA to amortise the per-tile setup at low rank and low density).
+constexpr int STR = 64, SDD_T = 256, SEPT = 4;
+template <int TW, int SKC>
+constexpr size_t sddmm_smem() { return sizeof(double) * 2 * (STR + TW * DevOmega::kTileCols) * SKC; }
 
+template <int TW, int SKC>
 __global__ void __launch_bounds__(SDD_T) sddmm_tile_kernel(i64 m, i64 n, i64 kY, int ntc, const int* __restrict__ tptr,
                                                            const int* __restrict__ col, const double* __restrict__ Yl,
                                                            i64 ldl, const double* __restrict__ Yr, i64 ldr,
                                                            const double* __restrict__ sub, double* __restrict__ out) {
+  constexpr int STC = TW * DevOmega::kTileCols;
   extern __shared__ double sm[];  // [2][STR][SKC] then [2][STC][SKC]
   double* sl = sm;
   double* sr = sm + 2 * STR * SKC;
@@ -268,21 +273,26 @@ __global__ void __launch_bounds__(SDD_T) sddmm_tile_kernel(i64 m, i64 n, i64 kY,
   __shared__ int base_pos[STR];
   const int t = threadIdx.x, lane = t & 31;
   const i64 i0 = static_cast<i64>(blockIdx.y) * STR, j0 = static_cast<i64>(blockIdx.x) * STC;
-  if (t < STR) {
+  const int q0 = blockIdx.x * TW, q1 = min(ntc, q0 + TW);
+  if (t < STR) {  // the tile's row counts, prefix-summed by warp scans (two warps)
     const i64 i = i0 + t;
     int b0 = 0, c = 0;
     if (i < m) {
-      b0 = tptr[i * (ntc + 1) + blockIdx.x];
-      c = tptr[i * (ntc + 1) + blockIdx.x + 1] - b0;
+      b0 = tptr[i * (ntc + 1) + q0];
+      c = tptr[i * (ntc + 1) + q1] - b0;
     }
     base_pos[t] = b0;
-    pre[t + 1] = c;
+    int v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    pre[t + 1] = v;  // inclusive within the warp
   }
   __syncthreads();
-  if (t == 0) {
-    pre[0] = 0;
-    for (int r = 0; r < STR; ++r) pre[r + 1] += pre[r];
-  }
+  if (t >= 32 && t < STR) pre[t + 1] += pre[32];  // second warp: add the first warp's total
+  if (t == 0) pre[0] = 0;
   __syncthreads();
   const int total = pre[STR];
   if (total == 0) return;
@@ -312,6 +322,7 @@ __global__ void __launch_bounds__(SDD_T) sddmm_tile_kernel(i64 m, i64 n, i64 kY,
     cp_async_commit();
   };
   for (int first = 0; first < total; first += SDD_T * SEPT) {
+    __syncthreads();  // previous pass done with the staging buffers
     int li[SEPT], lj[SEPT], pos[SEPT];
     double acc[SEPT];
 #pragma unroll
@@ -506,8 +517,10 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
     int dev = 0;
     DFCG_CUDA(cudaGetDevice(&dev));
     if (!(configured & (1u << dev))) {
-      DFCG_CUDA(cudaFuncSetAttribute(sddmm_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kSddmmSmem)));
+      DFCG_CUDA(cudaFuncSetAttribute(sddmm_tile_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sddmm_smem<1, 32>())));
+      DFCG_CUDA(cudaFuncSetAttribute(sddmm_tile_kernel<4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sddmm_smem<4, 16>())));
       configured |= 1u << dev;
     }
     // 16-byte staging needs even leading dimensions and an even k extent: repack the factors
@@ -530,9 +543,15 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
       Yr = pr.get();
       ldl = ldr = k2;
     }
-    const dim3 grid(om.ntc, static_cast<unsigned>((om.m + STR - 1) / STR));
-    sddmm_tile_kernel<<<grid, SDD_T, kSddmmSmem, s>>>(om.m, om.n, k2, om.ntc, om.tile_csr.get(), om.csr_col.get(), Yl,
-                                                      ldl, Yr, ldr, sub, r_csr);
+    static const int tw_env = std::getenv("DFCG_SDDMM_TW") ? std::atoi(std::getenv("DFCG_SDDMM_TW")) : 0;
+    const bool wide = tw_env ? tw_env == 4 : k2 <= 32;
+    const unsigned gy = static_cast<unsigned>((om.m + STR - 1) / STR);
+    if (wide)
+      sddmm_tile_kernel<4, 16><<<dim3((om.ntc + 3) / 4, gy), SDD_T, sddmm_smem<4, 16>(), s>>>(
+          om.m, om.n, k2, om.ntc, om.tile_csr.get(), om.csr_col.get(), Yl, ldl, Yr, ldr, sub, r_csr);
+    else
+      sddmm_tile_kernel<1, 32><<<dim3(om.ntc, gy), SDD_T, sddmm_smem<1, 32>(), s>>>(
+          om.m, om.n, k2, om.ntc, om.tile_csr.get(), om.csr_col.get(), Yl, ldl, Yr, ldr, sub, r_csr);
     DFCG_LAUNCH_CHECK();
     return;
   }

@@ -27,6 +27,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
     {"DFCG_PDL": "0", "DFCG_JACOBI_PDL": "0"},
     {"DFCG_DENSE_OP": "0", "DFCG_SPMM_TILE": "1"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_TILE": "0"},
+    {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_TW": "1"},
+    {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_TW": "4"},
     {"DFCG_JACOBI_GRAPH": "1", "DFCG_JACOBI_CLUSTER": "1"},
 ], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
 def test_variant_parity(env):
