@@ -321,11 +321,11 @@ struct OpTri {
     apply(s, X, ldx, b, out, ldo);
   }
   void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
-    gemm(s, false, false, w, b, w, 1.0, R, w, X, ldx, 0.0, out, ldo);
+    gemm_tri_a(s, false, w, b, 1.0, R, w, X, ldx, 0.0, out, ldo);
   }
   void apply_adjoint(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo,
                      DBuf<double>* = nullptr) const {
-    gemm(s, true, false, w, b, w, 1.0, R, w, X, ldx, 0.0, out, ldo);
+    gemm_tri_a(s, true, w, b, 1.0, R, w, X, ldx, 0.0, out, ldo);
   }
   i64 keep_rows() const { return -1; }
   void to_dense(cudaStream_t s, double* D) const { copy2d(s, w, w, R, w, D, w); }
@@ -346,11 +346,11 @@ struct OpWideQR {
     gemm(s, false, false, m, b, n, 1.0, A, n, X, ldx, 0.0, out, ldo);
   }
   void apply(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo) const {
-    gemm(s, true, false, m, b, m, 1.0, R, m, X, ldx, 0.0, out, ldo);
+    gemm_tri_a(s, true, m, b, 1.0, R, m, X, ldx, 0.0, out, ldo);
   }
   void apply_adjoint(cudaStream_t s, const double* X, i64 ldx, i64 b, double* out, i64 ldo,
                      DBuf<double>* = nullptr) const {
-    gemm(s, false, false, m, b, m, 1.0, R, m, X, ldx, 0.0, out, ldo);
+    gemm_tri_a(s, false, m, b, 1.0, R, m, X, ldx, 0.0, out, ldo);
   }
   i64 keep_rows() const { return -1; }
   void to_dense(cudaStream_t s, double* D) const { transpose(s, m, m, R, m, D, m); }  // R^T
@@ -974,7 +974,7 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
       DBuf<double> cl;
       if (f.r > 0) {
         cl.alloc(m * f.r, s);
-        gemm(s, false, false, m, f.r, m, 1.0, st.RAinv.get(), m, f.right.get(), f.r, 0.0, cl.get(), f.r);
+        gemm_tri_a(s, false, m, f.r, 1.0, st.RAinv.get(), m, f.right.get(), f.r, 0.0, cl.get(), f.r);
         DBuf<double> T2(m * m, s);
         gemm(s, false, true, m, m, f.r, 1.0, f.left.get(), f.r, cl.get(), f.r, 0.0, T2.get(), m);
         gemm(s, false, false, m, n, m, 1.0, T2.get(), m, st.Ad[ai].get(), n, 0.0, st.Dc.get(), n);
@@ -993,7 +993,7 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
       DBuf<double> cl;
       if (f.r > 0) {
         cl.alloc(n * f.r, s);
-        gemm(s, false, false, n, f.r, n, 1.0, st.RAinv.get(), n, f.left.get(), f.r, 0.0, cl.get(), f.r);
+        gemm_tri_a(s, false, n, f.r, 1.0, st.RAinv.get(), n, f.left.get(), f.r, 0.0, cl.get(), f.r);
         DBuf<double> T2(n * n, s);
         gemm(s, false, true, n, n, f.r, 1.0, cl.get(), f.r, f.right.get(), f.r, 0.0, T2.get(), n);
         gemm(s, false, false, m, n, n, 1.0, st.Ad[ai].get(), n, T2.get(), n, 0.0, st.Dc.get(), n);

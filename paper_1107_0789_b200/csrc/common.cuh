@@ -106,6 +106,11 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
 void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
                   double beta, double* C, i64 ldc);
 void gram_upper(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx, double* G, i64 ldg);
+// C (M x N) = alpha op(A) B + beta C for an upper-triangular M x M matrix A (lower part stored
+// as zeros): op(A) = A (ta = false) or A^T (ta = true); the K loop of each row tile skips the
+// zero half (half the FLOPs).
+void gemm_tri_a(cudaStream_t s, bool ta, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B,
+                i64 ldb, double beta, double* C, i64 ldc);
 // Upper triangle of G = A A^T (rows x rows), A row-major rows x k.
 void gram_upper_nt(cudaStream_t s, i64 rows, i64 k, const double* A, i64 lda, double* G, i64 ldg);
 // C (M x N) = alpha A^T B + beta C with A stored row-major N x M (A^T(i,k) = A[k*lda + i]) and

@@ -107,10 +107,14 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   // flags & 1 (SYRK-style): tiles strictly below the diagonal are skipped (C left as is).
   // flags & 2 (B upper triangular, TRMM-style): B(k, j) = 0 for k > j, so the K loop of this
   // column tile stops at n0 + BN.
+  // flags & 4 (op(A) upper triangular): op(A)(i, k) = 0 for k < i, the K loop of this row tile
+  // starts at m0; flags & 8 (op(A) lower triangular): it stops at m0 + BM.
   if ((upper_only & 1) && m0 >= n0 + BN) return;
-  const i64 kbeg = static_cast<i64>(blockIdx.z) * kchunk;
+  i64 kbeg = static_cast<i64>(blockIdx.z) * kchunk;
   i64 kend = min(K, kbeg + kchunk);
   if (upper_only & 2) kend = min(kend, n0 + BN);
+  if (upper_only & 4) kbeg = max(kbeg, m0);
+  if (upper_only & 8) kend = min(kend, m0 + BM);
   const int ntiles = kend > kbeg ? static_cast<int>((kend - kbeg + BK - 1) / BK) : 0;
 
   double acc[FM][FN][2];
@@ -520,6 +524,16 @@ void gemm(cudaStream_t s, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, c
   else if (ta && !tb) launch_gemm<true, false>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else if (!ta && tb) launch_gemm<false, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else launch_gemm<true, true>(s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+}
+
+void gemm_tri_a(cudaStream_t s, bool ta, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B,
+                i64 ldb, double beta, double* C, i64 ldc) {
+  if (M <= 0 || N <= 0) return;
+  prof::Scope scope(1.0 * M * M * N >= 2e9 ? prof::kGemm : prof::kGemmSmall, s, 1.0 * M * (M + 1) * N,
+                    8.0 * (M * M / 2 + M * N + M * N * (beta != 0.0 ? 2.0 : 1.0)));
+  GemmTrace tr(s, ta ? "TRLT" : "TRUP", M, N, M, 1.0 * M * (M + 1) * N);
+  if (ta) launch_gemm<true, false>(s, M, N, M, alpha, A, lda, B, ldb, beta, C, ldc, 8);
+  else launch_gemm<false, false>(s, M, N, M, alpha, A, lda, B, ldb, beta, C, ldc, 4);
 }
 
 void gemm_upper_b(cudaStream_t s, i64 M, i64 N, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
