@@ -147,12 +147,14 @@ def test_apg_mc_deterministic_bitwise():  # P/tests/test_solvers.cpp:159-169
 
 
 def test_apg_mc_c2_block_properties():
-    """BASELINE c2 block (10000 x 1250, 10% observed): first 4 iterations against the oracle,
-    then 30 GPU iterations checked through properties (objective bound, residual
-    consistency, orthonormal left factor)."""
+    """BASELINE c2 block (10000 x 1250, 10% observed): the first 9 iterations against the oracle
+    (ranks climb to ~500 with a k doubling: iterations 5-9 run the dense and the
+    CholeskyQR2-compressed operators at the real block shape; ~1-2 min of oracle time), then 30
+    GPU iterations checked through properties (objective bound, residual consistency,
+    orthonormal left factor)."""
     m, n = 10000, 1250
     L0, obs = P.gen_mc_instance(m, n, 10, m * n // 10, 0.1, 1)
-    assert_mc_parity(obs, max_iters=4)
+    assert_mc_parity(obs, max_iters=9)
     est, rep = P.apg_mc(obs, P.ApgConfig(max_iters=30))
     assert rep.iterations == 30
     # residual reported == residual recomputed from the factors on Omega
