@@ -187,3 +187,37 @@ def test_dfc_worker_invariance_bitwise():  # P/tests/test_dfc.cpp:322-342
         a, _ = P.dfc_run(obs, variant, ensemble=True, seed=11, workers=1, **kw)
         b, _ = P.dfc_run(obs, variant, ensemble=True, seed=11, workers=4, **kw)
         assert np.array_equal(a.left, b.left) and np.array_equal(a.right, b.right)
+
+
+def test_experiment_harness_matches_oracle():
+    """run_experiment on the GPU path (bench.hpp:158-336): per-seed RMSE of every method equal to
+    the oracle's dfc_run / apg_mc / F-step-only estimate on the same seeds, summary rows appended."""
+    import io
+
+    from paper_1107_0789_b200.experiment import ExperimentSpec, run_experiment, write_csv
+
+    spec = ExperimentSpec(m=100, n=90, r=3, s=4000, sigma=0.1, methods=["base", "part", "proj", "nys", "rp"],
+                          seeds=[1, 2], t=3, l_frac=0.3, d_frac=0.3)
+    rows = run_experiment(spec)
+    assert [r.method for r in rows[-10:]] == sorted(m + s for m in spec.methods for s in ("_mean", "_std"))
+    for r in rows[:-10]:
+        L0, obs = O.gen_mc_instance(100, 90, 3, 4000, 0.1, r.seed, 0)
+        if r.method == "base":
+            est, _ = O.apg_mc(obs)
+        elif r.method == "part":
+            groups = O.partition_columns(r.seed, 0xDFC0000000000001, 90, 3)
+            ests = [O.apg_mc(O.extract_columns(obs, g))[0] for g in groups]
+            left = np.hstack([e.left for e in ests])
+            right = np.zeros((90, left.shape[1]))
+            at = 0
+            for e, g in zip(ests, groups):
+                right[np.asarray(g), at:at + e.rank] = e.right
+                at += e.rank
+            est = O.Estimate(left, right)
+        else:
+            est, _ = O.dfc_run(obs, r.method, t=3, l=27, d=30, rp_p=5, rp_q=2, seed=r.seed)
+        ref = O.rmse(L0, est)
+        assert abs(r.rmse - ref) <= 1e-6 * ref, (r.method, r.seed, r.rmse, ref)
+    buf = io.StringIO()
+    write_csv(buf, rows)
+    assert len(buf.getvalue().splitlines()) == len(rows) + 1

@@ -160,3 +160,23 @@ def test_recsys_generator_c4_standin():
     blk = P.gen_recsys_instance(m, n, r, 0.02, 7, cols=groups[0])
     assert blk.n == len(groups[0]) and blk.cols.max() < blk.n
     assert 3.2 < blk.vals.mean() < 4.0
+
+
+def test_experiment_csv_schema():
+    """The experiment harness writes the reference's CSV (P/include/dfc/bench.hpp:339-351):
+    header, %.12g RMSE, %.6g timings; summary rows follow the per-seed rows."""
+    import io
+
+    from paper_1107_0789_b200.experiment import ExperimentSpec, ResultRow, _validate, config_echo, write_csv
+
+    buf = io.StringIO()
+    write_csv(buf, [ResultRow("proj", 3, 0.123456789012345, 1.0, 2345.678901, 0.5, 2347.2, 12),
+                    ResultRow("proj_mean", 1, 0.1, 0, 0, 0, 0, 12)])
+    lines = buf.getvalue().splitlines()
+    assert lines[0] == "method,seed,rmse,ms_divide,ms_factor,ms_combine,ms_total,rank"
+    assert lines[1] == "proj,3,0.123456789012,1,2345.68,0.5,2347.2,12"
+    spec = ExperimentSpec(m=10, n=10, r=2, s=50, sigma=0.1, methods=["proj", "nys"], seeds=[1])
+    assert config_echo(spec).startswith("task=mc;m=10;n=10;r=2;s=50;sigma=0.1;t=4")
+    for bad in (dict(seeds=[]), dict(methods=["nope"]), dict(t=0), dict(l_frac=0.0)):
+        with pytest.raises(ValueError):
+            _validate(ExperimentSpec(**{**spec.__dict__, **bad}))
