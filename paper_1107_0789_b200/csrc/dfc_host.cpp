@@ -5,6 +5,7 @@
 #include "dfc_host.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -53,10 +54,40 @@ HostObs HostObs::make(i64 m, i64 n, std::vector<long long> row, std::vector<long
   return o;
 }
 
-// sampling.hpp:15-26
+// sampling.hpp:15-26. For a large population the partial Fisher-Yates runs on a hash map of
+// the displaced positions (open addressing, ~32 bytes per draw) instead of an n-element
+// permutation: the same RNG calls and swaps, so the same output, without the 12.8 GB index
+// vector of BASELINE c5 (n = 1.6e9 cells, l = 8e7). DFCG_SWR_SPARSE=0 / 1 forces a path.
 std::vector<i64> sample_without_replacement(i64 n, i64 l, SeededRng& rng) {
   if (n < 1) throw std::invalid_argument("sample_without_replacement: empty population");
   if (l < 1 || l > n) throw std::invalid_argument("sample_without_replacement: need 1 <= l <= n");
+  const char* env = std::getenv("DFCG_SWR_SPARSE");
+  const int mode = env ? std::atoi(env) : -1;
+  const bool sparse = mode == 1 || (mode != 0 && n > (i64{1} << 27) && l < n / 4);
+  if (sparse) {
+    size_t cap = 16;
+    while (cap < static_cast<size_t>(2 * l + 16)) cap <<= 1;
+    std::vector<i64> key(cap, -1), val(cap);
+    auto slot = [&](i64 x) {
+      size_t h = static_cast<size_t>((static_cast<std::uint64_t>(x) * 0x9E3779B97F4A7C15ULL) >> 17) & (cap - 1);
+      while (key[h] != -1 && key[h] != x) h = (h + 1) & (cap - 1);
+      return h;
+    };
+    auto get = [&](i64 x) {
+      const size_t h = slot(x);
+      return key[h] == x ? val[h] : x;
+    };
+    std::vector<i64> out(static_cast<size_t>(l));
+    for (i64 i = 0; i < l; ++i) {
+      const i64 j = i + static_cast<i64>(rng.index(static_cast<std::uint64_t>(n - i)));
+      const i64 vi = get(i), vj = get(j);
+      out[static_cast<size_t>(i)] = vj;  // perm[i] <- perm[j]; position i is never read again
+      const size_t h = slot(j);
+      key[h] = j;
+      val[h] = vi;  // perm[j] <- old perm[i]
+    }
+    return out;
+  }
   std::vector<i64> perm(static_cast<size_t>(n));
   std::iota(perm.begin(), perm.end(), i64{0});
   for (i64 i = 0; i < l; ++i) {

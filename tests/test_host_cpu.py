@@ -180,3 +180,15 @@ def test_experiment_csv_schema():
     for bad in (dict(seeds=[]), dict(methods=["nope"]), dict(t=0), dict(l_frac=0.0)):
         with pytest.raises(ValueError):
             _validate(ExperimentSpec(**{**spec.__dict__, **bad}))
+
+
+@pytest.mark.parametrize("n,l", [(1_000_003, 50_000), (5000, 5000), (777, 1), (200_000, 150_000)])
+def test_sample_without_replacement_sparse_path_identical(n, l, monkeypatch):
+    """The hash-map partial Fisher-Yates (large populations: BASELINE c5 draws 8e7 of 1.6e9
+    cells) returns exactly the dense permutation's sample (P/include/dfc/sampling.hpp:15-26)."""
+    monkeypatch.setenv("DFCG_SWR_SPARSE", "0")
+    dense = P.sample_without_replacement(11, 3, n, l)
+    monkeypatch.setenv("DFCG_SWR_SPARSE", "1")
+    sparse = P.sample_without_replacement(11, 3, n, l)
+    assert np.array_equal(dense, sparse)
+    assert np.array_equal(dense, O.sample_without_replacement(11, 3, n, l))
