@@ -9,6 +9,9 @@
 // exact svd_of_product when kc + kp > min(m, n); the device keeps the concatenated factors
 // instead — the same matrix Y (the compaction only drops singular values <= 1e-12 *
 // max(m,n) * s_max), consumed only through Y*X, Y^T*X and P_Omega(Y).
+// High-rank iterations apply the same operator materialised (dense_operator: Y off Omega, M on
+// it) and, when cheaper, compressed by a CholeskyQR2 factor (OpTri for m >= n, OpWideQR for
+// m < n): the randomized SVT then runs in the R factor's coordinates — same spans, same draws.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
