@@ -148,10 +148,16 @@ def roofline_entry(prof, peaks, peak_kind):
     ops = {k: v for k, v in prof.items() if v["launches"] > 0}
     if not ops:
         return None
-    name, v = max(ops.items(), key=lambda kv: kv[1]["ms"])
+    # the dominant KERNEL: the accounting splits gemm_kernel launches into >= 2 GFLOP ("gemm")
+    # and smaller ("gemm_small") classes; as a kernel they are one
+    kern = {k: v for k, v in ops.items() if k not in ("gemm", "gemm_small")}
+    g = [ops[k] for k in ("gemm", "gemm_small") if k in ops]
+    if g:
+        kern["gemm_kernel"] = {f: sum(x[f] for x in g) for f in ("ms", "launches", "flops", "bytes")}
+    name, v = max(kern.items(), key=lambda kv: kv[1]["ms"])
     per_launch_ms = v["ms"] / v["launches"]
     share = v["ms"] / sum(x["ms"] for x in ops.values())
-    if name in ("gemm", "gemm_small", "jacobi", "cholesky", "qr_fallback"):
+    if name in ("gemm_kernel", "jacobi", "cholesky", "qr_fallback"):
         achieved = v["flops"] / (v["ms"] * 1e-3) / 1e12
         peak = FP64_DMMA_PEAK_TFLOPS
         entry = dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
@@ -169,7 +175,7 @@ def roofline_entry(prof, peaks, peak_kind):
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(traffic_file):
         try:
-            entry["traffic"] = json.load(open(traffic_file)).get(name)
+            entry["traffic"] = json.load(open(traffic_file)).get("gemm" if name == "gemm_kernel" else name)
         except Exception:
             pass
     return entry
