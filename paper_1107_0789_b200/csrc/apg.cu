@@ -1173,6 +1173,8 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
 
   NormalCursor cur{&ctx.normals(1), 0};
   SvtResult last;
+  DBuf<double> RA, RAinv, cl_last;  // compressed iterations (see below)
+  bool left_deferred = false;
   double tau_prev = 1.0, tau_curr = 1.0, mu = mu_init, mu_used = mu_init;
   i64 rank_hint = 1;
   int iters = 0;
@@ -1206,14 +1208,42 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
         }
         DFCG_LAUNCH_CHECK();
       }
-      OpDense op{GL.get(), m, n};
       f = SvtResult{};
-      svt_operator(s, op, step * mu, rank_hint, cur, f);
-      // Ld_next = U diag(s) V^T  (column-major m x n == row-major n x m: V diag(s) U^T)
-      if (f.r == 0) {
-        Ldn.zero(s);
+      // The dense operator GL (column-major m x n) compressed by CholeskyQR2 when tall and the
+      // cost model says so (OpTri, as in apg_mc): the SVT runs on R_A, the next L_d is
+      // GL (R_A^-1 U~ S V^T) and the left factor is deferred (only the last one is output).
+      bool compressed = false;
+      if (!cfg.line_search && m >= n && compress_operator(m, n, rank_hint)) {
+        RA.ensure(n * n, s);
+        RAinv.ensure(n * n, s);
+        compressed = cholqr2_r(s, m, n, GL.get(), m, RA.get(), RAinv.get(), 1e-13, true);
+      }
+      if (compressed) {
+        OpTri op{RA.get(), n};
+        svt_operator(s, op, step * mu, rank_hint, cur, f);
+        cl_last = DBuf<double>{};
+        if (f.r > 0) {
+          cl_last.alloc(n * f.r, s);
+          gemm_tri_a(s, false, n, f.r, 1.0, RAinv.get(), n, f.left.get(), f.r, 0.0, cl_last.get(), f.r);
+          DBuf<double> T2(n * n, s);
+          gemm(s, false, true, n, n, f.r, 1.0, cl_last.get(), f.r, f.right.get(), f.r, 0.0, T2.get(), n);
+          // L_d (column-major == row-major n x m) = T2^T GL^T
+          gemm(s, true, false, n, m, n, 1.0, T2.get(), n, GL.get(), m, 0.0, Ldn.get(), m);
+        } else {
+          Ldn.zero(s);
+        }
+        f.left = DBuf<double>{};
+        left_deferred = f.r > 0;
       } else {
-        gemm(s, false, true, n, m, f.r, 1.0, f.right.get(), f.r, f.left.get(), f.r, 0.0, Ldn.get(), m);
+        OpDense op{GL.get(), m, n};
+        svt_operator(s, op, step * mu, rank_hint, cur, f);
+        left_deferred = false;
+        // Ld_next = U diag(s) V^T  (column-major m x n == row-major n x m: V diag(s) U^T)
+        if (f.r == 0) {
+          Ldn.zero(s);
+        } else {
+          gemm(s, false, true, n, m, f.r, 1.0, f.right.get(), f.r, f.left.get(), f.r, 0.0, Ldn.get(), m);
+        }
       }
       if (!cfg.line_search || step <= 0.0625) break;
       const double* pM = M.get();
@@ -1295,6 +1325,10 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
   out.m = m;
   out.n = n;
   out.k = last.r;
+  if (left_deferred) {  // the last iteration's left factor: GL R_A^-1 U~ (GL is that iteration's)
+    last.left.alloc(m * last.r, s);
+    gemm(s, true, false, m, last.r, n, 1.0, GL.get(), m, cl_last.get(), last.r, 0.0, last.left.get(), last.r);
+  }
   out.left = std::move(last.left);
   out.right = std::move(last.right);
   rep.wall_ms = ms_since(start);

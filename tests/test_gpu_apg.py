@@ -174,7 +174,10 @@ def test_apg_mc_c2_block_properties():
     (30, 30, 2, 90, 0.05, 8),      # determinism case (:253-262)
     (120, 90, 3, 1000, 0.05, 4),   # partial-SVD path (min > 64)
 ])
-def test_apg_rmf_parity(m, n, r, s, sigma, seed):
+@pytest.mark.parametrize("op_mode", ["1", "2"], ids=["dense_op", "dense_qr_op"])
+def test_apg_rmf_parity(m, n, r, s, sigma, seed, op_mode, monkeypatch):
+    # the dense RMF operator as is, and CholeskyQR2-compressed (m >= n)
+    monkeypatch.setenv("DFCG_DENSE_OP", op_mode)
     L0, S0, M = P.gen_rmf_instance(m, n, r, s, sigma, seed)
     assert_rmf_parity(M, O.default_rmf_lambda(m, n))
 
@@ -185,7 +188,10 @@ def test_apg_rmf_acceptance_floor_300():  # acceptance criterion 4 setup (P/test
     assert_rmf_parity(M, O.default_rmf_lambda(m, n), mu_floor=0.1 * 2 * np.sqrt(300))
 
 
-def test_apg_rmf_bounded_outliers_c3_shape():  # BASELINE c3 value model (U[-10,10], sigma 0.01), scaled
+@pytest.mark.parametrize("op_mode", ["1", "2", "auto"])
+def test_apg_rmf_bounded_outliers_c3_shape(op_mode, monkeypatch):  # BASELINE c3 value model (U[-10,10], sigma 0.01), scaled
+    if op_mode != "auto":
+        monkeypatch.setenv("DFCG_DENSE_OP", op_mode)
     L0, S0, M = P.gen_rmf_instance(400, 100, 4, 4000, 0.01, 3, lo=-10.0, hi=10.0)
     assert_rmf_parity(M, O.default_rmf_lambda(400, 100), max_iters=120)
 
