@@ -90,7 +90,8 @@ __device__ long long g_potrf_trace[64];
 #define POTRF_STAMP(i)
 #endif
 __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr,
-                                                         const double* maxdiag, double rel_tol, int* fail) {
+                                                         const double* maxdiag, double rel_tol, int* fail,
+                                                         int want_inv) {
   extern __shared__ double psm[];
   pdl_wait();
   pdl_trigger();
@@ -208,6 +209,13 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
     POTRF_STAMP(8)
   }
   POTRF_STAMP(2)
+  if (!want_inv) {  // the blocked Cholesky's critical path: R only (inverses batched later)
+    for (int e = t; e < kb * kb; e += 256) {
+      const int r = e / kb, c = e % kb;
+      G[r * ldg + c] = r <= c ? A[r][c] : 0.0;
+    }
+    return;
+  }
   // ---- inverse: diagonal micro-blocks (warp w -> block w; lane j -> column j)
   if (PB * warp < kbp) {
     const int w0 = PB * warp, j = lane & (PB - 1);
@@ -283,6 +291,120 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
   POTRF_STAMP(5)
 }
 
+// Panel TRSM of the blocked Cholesky without an explicit inverse: X = R_kk^-T P for the kb x rem
+// panel P (in place). One warp per panel column, lane l holding rows l and l + 32: per pivot i
+// the owner scales x_i, a shuffle broadcasts it and every lane updates its later rows — a
+// 64-step chain of (shuffle, FMA) per column, all columns in parallel; R_kk in shared memory.
+constexpr int TRSM_T = 256;
+__global__ void __launch_bounds__(TRSM_T) trsm_panel_kernel(int kb, i64 rem, const double* __restrict__ Rkk, i64 ldg,
+                                                            double* __restrict__ P) {
+  __shared__ double R[CNB][CNB + 1];
+  __shared__ double rd[CNB];
+  pdl_wait();
+  pdl_trigger();
+  const int t = threadIdx.x, lane = t & 31;
+  for (int e = t; e < kb * kb; e += TRSM_T) {
+    const int r = e / kb, c = e % kb;
+    R[r][c] = r <= c ? Rkk[r * ldg + c] : 0.0;
+  }
+  __syncthreads();
+  if (t < kb) rd[t] = 1.0 / R[t][t];
+  __syncthreads();
+  const i64 c = static_cast<i64>(blockIdx.x) * (TRSM_T / 32) + (t >> 5);
+  if (c >= rem) return;
+  double x0 = lane < kb ? P[lane * ldg + c] : 0.0;
+  double x1 = lane + 32 < kb ? P[(lane + 32) * ldg + c] : 0.0;
+  for (int i = 0; i < kb; ++i) {
+    double xi;
+    if (i < 32) {
+      if (lane == i) x0 *= rd[i];
+      xi = __shfl_sync(0xffffffffu, x0, i);
+    } else {
+      if (lane == i - 32) x1 *= rd[i];
+      xi = __shfl_sync(0xffffffffu, x1, i - 32);
+    }
+    if (lane > i && lane < kb) x0 = fma(-R[i][lane], xi, x0);
+    if (lane + 32 > i && lane + 32 < kb) x1 = fma(-R[i][lane + 32], xi, x1);
+  }
+  if (lane < kb) P[lane * ldg + c] = x0;
+  if (lane + 32 < kb) P[(lane + 32) * ldg + c] = x1;
+}
+
+// Inverses of every CNB x CNB diagonal block of an upper-triangular R (one CTA per block, all at
+// once after the factorisation — off the blocked Cholesky's critical path), by the same micro-
+// block inversion + recursive doubling as potrf_diag_kernel.
+__global__ void __launch_bounds__(256) trinv_diag_kernel(i64 n, const double* __restrict__ G, i64 ldg,
+                                                         double* __restrict__ Rinv, i64 ldr) {
+  extern __shared__ double psm[];
+  pdl_wait();
+  pdl_trigger();
+  double(*A)[PLD] = reinterpret_cast<double(*)[PLD]>(psm);
+  double(*X)[PLD] = reinterpret_cast<double(*)[PLD]>(psm + CNB * PLD);
+  double(*S)[PLD] = reinterpret_cast<double(*)[PLD]>(psm + 2 * CNB * PLD);
+  double* dinv = psm + 2 * CNB * PLD + (CNB / 2) * PLD;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const i64 k0 = static_cast<i64>(blockIdx.x) * CNB;
+  const int kb = static_cast<int>(min(static_cast<i64>(CNB), n - k0));
+  const int kbp = (kb + PB - 1) / PB * PB;
+  for (int e = t; e < CNB * CNB; e += 256) {
+    const int r = e / CNB, c = e % CNB;
+    const bool ok = r < kb && c < kb && r <= c;
+    A[r][c] = ok ? G[(k0 + r) * ldg + k0 + c] : (r == c && r >= kb ? 1.0 : 0.0);
+    X[r][c] = 0.0;
+  }
+  __syncthreads();
+  if (t < CNB) dinv[t] = 1.0 / A[t][t];
+  __syncthreads();
+  if (PB * warp < kbp) {  // diagonal micro-blocks (warp w -> block w; lane j -> column j)
+    const int w0 = PB * warp, j = lane & (PB - 1);
+    double x[PB];
+#pragma unroll
+    for (int i = PB - 1; i >= 0; --i) {
+      double v = 0.0;
+      if (i == j) {
+        v = dinv[w0 + i];
+      } else if (i < j) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int l = i + 1; l < PB; ++l)
+          if (l <= j) sacc = fma(A[w0 + i][w0 + l], x[l], sacc);
+        v = -dinv[w0 + i] * sacc;
+      }
+      x[i] = v;
+    }
+    if (lane < PB) {
+#pragma unroll
+      for (int i = 0; i < PB; ++i) X[w0 + i][w0 + j] = x[i];
+    }
+  }
+  __syncthreads();
+  for (int sz = PB; sz < kbp; sz *= 2) {  // recursive doubling: X12 = -X11 (R12 X22)
+    const int npairs = (kbp + 2 * sz - 1) / (2 * sz);
+    for (int e = t; e < npairs * sz * sz; e += 256) {
+      const int q = e / (sz * sz), i = (e / sz) % sz, j = e % sz;
+      const int a0 = 2 * q * sz, b0 = a0 + sz, s2 = min(sz, kbp - b0);
+      if (j >= s2) continue;
+      double acc = 0.0;
+      for (int k = 0; k < s2; ++k) acc = fma(A[a0 + i][b0 + k], X[b0 + k][b0 + j], acc);
+      S[q * sz + i][j] = acc;
+    }
+    __syncthreads();
+    for (int e = t; e < npairs * sz * sz; e += 256) {
+      const int q = e / (sz * sz), i = (e / sz) % sz, j = e % sz;
+      const int a0 = 2 * q * sz, b0 = a0 + sz, s2 = min(sz, kbp - b0);
+      if (j >= s2) continue;
+      double acc = 0.0;
+      for (int k = 0; k < sz; ++k) acc = fma(X[a0 + i][a0 + k], S[q * sz + k][j], acc);
+      X[a0 + i][b0 + j] = -acc;
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < kb * kb; e += 256) {
+    const int r = e / kb, c = e % kb;
+    Rinv[(k0 + r) * ldr + k0 + c] = r <= c ? X[r][c] : 0.0;
+  }
+}
+
 __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
   const i64 total = n * n;
   for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
@@ -319,8 +441,14 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   if (!(configured & (1u << dev))) {
     DFCG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(kPotrfSmem)));
+    DFCG_CUDA(cudaFuncSetAttribute(trinv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kPotrfSmem)));
     configured |= 1u << dev;
   }
+  // DFCG_CHOL_INV_LATE=0: the diagonal inverses inside potrf and the panel TRSM as a GEMM with
+  // them (the previous critical path); default: potrf without the inverse, substitution TRSM,
+  // all diagonal inverses in one launch after the factorisation.
+  static const bool late = !(std::getenv("DFCG_CHOL_INV_LATE") && std::atoi(std::getenv("DFCG_CHOL_INV_LATE")) == 0);
   DBuf<double> maxdiag(1, s);
   diag_max_kernel<<<1, 256, 0, s>>>(n, G, ldg, maxdiag.get());
   DFCG_LAUNCH_CHECK();
@@ -332,7 +460,7 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   auto potrf = [&](cudaStream_t st, i64 k0, int kb) {
     prof::Scope scope(prof::kCholesky, st, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
     pdl_launch(potrf_diag_kernel, dim3(1), dim3(256), kPotrfSmem, st, kb, G + k0 * ldg + k0, ldg,
-               Rinv + k0 * ldr + k0, ldr, static_cast<const double*>(maxdiag.get()), rel_tol, fail);
+               Rinv + k0 * ldr + k0, ldr, static_cast<const double*>(maxdiag.get()), rel_tol, fail, late ? 0 : 1);
     DFCG_LAUNCH_CHECK();
   };
   potrf(s, 0, static_cast<int>(std::min<i64>(CNB, n)));
@@ -343,7 +471,14 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
     if (rem <= 0) break;
     double* panel = G + k0 * ldg + k0 + kb;  // kb x rem
     // R[k, J] = Rkk^-T G[k, J]
-    gemm(s, true, false, kb, rem, kb, 1.0, Rinv + k0 * ldr + k0, ldr, panel, ldg, 0.0, panel, ldg);
+    if (late) {
+      prof::Scope scope(prof::kCholesky, s, 1.0 * kb * kb * rem, 16.0 * kb * rem);
+      pdl_launch(trsm_panel_kernel, dim3(static_cast<unsigned>((rem + TRSM_T / 32 - 1) / (TRSM_T / 32))), dim3(TRSM_T), 0, s, kb,
+                 rem, static_cast<const double*>(G + k0 * ldg + k0), ldg, panel);
+      DFCG_LAUNCH_CHECK();
+    } else {
+      gemm(s, true, false, kb, rem, kb, 1.0, Rinv + k0 * ldr + k0, ldr, panel, ldg, 0.0, panel, ldg);
+    }
     // next diagonal block: G[k1, k1] -= R[k, k1]^T R[k, k1], then factored on the helper stream
     const i64 k1 = k0 + kb;
     const int kb1 = static_cast<int>(std::min<i64>(CNB, rem));
@@ -358,6 +493,12 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   }
   zero_lower_kernel<<<grid_for(n * n), 256, 0, s>>>(n, G, ldg);
   DFCG_LAUNCH_CHECK();
+  if (late && want_inverse) {
+    prof::Scope scope(prof::kCholesky, s, n * CNB * CNB / 3.0, 16.0 * n * CNB);
+    pdl_launch(trinv_diag_kernel, dim3(static_cast<unsigned>((n + CNB - 1) / CNB)), dim3(256), kPotrfSmem, s, n,
+               static_cast<const double*>(G), ldg, Rinv, ldr);
+    DFCG_LAUNCH_CHECK();
+  }
   // Off-diagonal blocks of the inverse: Rinv[0:J, J] = -Rinv[0:J,0:J] R[0:J, J] Rinv[J,J].
   if (want_inverse && n > CNB) {
     DBuf<double> T(n * CNB, s);

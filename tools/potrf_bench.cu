@@ -30,7 +30,7 @@ int main() {
     for (int r = 0; r < reps; ++r) {
       cudaMemcpy(G, h.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice);
       cudaEventRecord(e0);
-      potrf_diag_kernel<<<1, 256, kPotrfSmem>>>(kb, G, n, R, n, md, 1e-11, fail);
+      potrf_diag_kernel<<<1, 256, kPotrfSmem>>>(kb, G, n, R, n, md, 1e-11, fail, 1);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float t = 0;
