@@ -1647,7 +1647,10 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const i64 slots = 2 * static_cast<i64>(nsm);
     const i64 k = std::max(1, active_streams(dev));
-    for (int c : {4, 2})
+    // 2-CTA clusters when they fit (a lone c2 block: 8.1 ms of Jacobi per iteration against 8.5
+    // with 4 and 9.2 with 1, with programmatic dependent launch of the rounds); 4 when a slab
+    // needs it
+    for (int c : {2, 4})
       if (c > CS && k * npairs * c <= slots && wrows >= 64 * c) {
         CS = c;
         break;
