@@ -12,11 +12,17 @@ Metric: base-APG iterations/s ("block-iterations/s": one APG iteration of one 10
 block = one unit). A step = one APG iteration on every block (blocks sharded over the ranks,
 each advancing on its own CUDA stream). Before the W warm-up steps every block runs a fixed
 prologue of --prologue iterations (default 26) so the timed window sits in the steady
-rank ~700 regime that dominates a c2 solve; the reference arm measures the same window.
+rank ~700 regime that dominates a c2 solve. The reference arm (--impl reference: the oracle
+port on the host cores, inputs from the oracle's own generator) runs the same prologue and
+warm-up untimed and times the same iterations of block 0.
 Inputs are larger than L2 (the 10k x 10k factors alone exceed 126 MB); no flush needed.
 
-e2e: the full DFC-Proj solve through the public C ABI (host triplets in, host estimate out,
-H2D/D2H inside the timed region): block-iterations/s over the whole solve, plus the solve time.
+e2e: the full DFC-Proj pipeline (D step, F step, combine) through the public C ABI (host
+triplets in, host estimate out, H2D/D2H inside the timed region): block-iterations/s over the
+whole solve, plus the solve time and its divide / factor / combine phases.
+
+roofline: the dominant kernel on one extra iteration of one block run alone (per-launch CUDA
+events); roofline_step: all tensor-path FLOPs of the packed timed window / its device time.
 """
 from __future__ import annotations
 
@@ -257,75 +263,101 @@ def lowrank_window(P, block, wl, skip=60, win=20):
                      "kernels this small (~17 MB per SpMM) are launch- and latency-bound")
 
 
-def _oracle_run(O, block, threads):
-    import ctypes as C
-
-    L = O.lib()
-    L.orc_set_blas_threads(threads)
-    h = O._obs_handle(O.Observed(block.m, block.n, block.rows, block.cols, block.vals))
-    run = C.c_void_p()
-    O._check(L.orc_mc_run_new(h.ptr, C.byref(O.apg_cfg()), C.byref(run)))
-    return L, h, run
-
-
-def _oracle_steps(O, L, run, n):
-    import ctypes as C
-
-    done = C.c_longlong()
-    O._check(L.orc_mc_run_step(run, C.c_longlong(n), C.byref(done)))
-    return done.value
-
-
-def cpu_sample(O, block, budget_s, threads):
-    """Oracle (restated reference, CPU) on one block: whole APG iterations from the start of
-    the solve until `budget_s` seconds of CPU work (bounded sample)."""
-    L, h, run = _oracle_run(O, block, threads)
-    iters, t0 = 0, time.perf_counter()
+def cpu_sample(O, block, budget_s, threads, min_rank=400, max_total_s=150.0):
+    """Oracle (restated reference, CPU) on one block, bounded sample of the regime the GPU
+    window measures: APG iterations from the start of the solve run UNTIMED until the incoming
+    rank reaches `min_rank` (the first ~6 iterations at ranks 1..400 are cheap and unlike the
+    rank ~700 window), then whole iterations are timed until `budget_s` seconds of CPU work
+    (or `max_total_s` overall). Returns (timed iterations, seconds, first timed iteration)."""
+    O.lib().orc_set_blas_threads(threads)
+    run = O.McRun(O.Observed(block.m, block.n, block.rows, block.cols, block.vals))
+    t_start = time.perf_counter()
+    it, rank = 0, 0
     try:
-        while time.perf_counter() - t0 < budget_s:
-            k = _oracle_steps(O, L, run, 1)
-            if k == 0:
+        while rank < min_rank and time.perf_counter() - t_start < max_total_s:
+            tr = run.step(1)
+            if not tr:
                 break
-            iters += k
+            it, rank = tr[-1]["it"], tr[-1]["rank"]
+        first, iters, t0 = it + 1, 0, time.perf_counter()
+        while time.perf_counter() - t0 < budget_s and time.perf_counter() - t_start < max_total_s:
+            if not run.step(1):
+                break
+            iters += 1
         dt = time.perf_counter() - t0
     finally:
-        L.orc_mc_run_free(run)
-        L.orc_set_blas_threads(1)
-    return iters, dt
+        run.close()
+        O.lib().orc_set_blas_threads(1)
+    return iters, dt, first
 
 
 def run_reference(args, wl):
-    """--impl reference: the reference's CPU path (oracle port — the C++/Eigen reference cannot
-    be built here) on the host cores, same workload / metric / unit. Bounded sample: block 0 of
-    the c2 partition, W untimed warm-up iterations from the start of the solve, then K timed
-    iterations (each step = one APG iteration of the sampled block)."""
+    """--impl reference: the reference's CPU path on the host cores, same workload / metric /
+    unit / window as the GPU arm. The C++/Eigen reference cannot be built here (Eigen3,
+    GoogleTest and the vendored CLI11 are absent, no network), so this runs the oracle port
+    (oracle/, a C++ restatement of P/include/dfc/*.hpp) — and only the oracle: the inputs come
+    from the oracle's own restated generator / partition / extract (gen_mc_instance,
+    partition_columns, extract_columns), nothing of the product package is imported.
+    Window: block 0 of the c2 partition; --prologue + W untimed iterations from the start of
+    the solve, then K timed iterations (each step = one APG iteration of that block) — the GPU
+    arm's window, iterations prologue+W+1 .. prologue+W+K."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle as O
-    import paper_1107_0789_b200 as P  # host-side generator only (no GPU work)
 
     threads = os.cpu_count() or 1
-    L0, obs, groups, blocks = make_blocks(P, wl)
-    L, h, run = _oracle_run(O, blocks[0], threads)
-    _oracle_steps(O, L, run, args.warmup)
+    L0, obs = O.gen_mc_instance(wl["m"], wl["n"], wl["r"], wl["s"], wl["sigma"], wl["seed"])
+    groups = O.partition_columns(wl["seed"], PARTITION_STREAM, wl["n"], wl["t"])
+    blk = O.extract_columns(obs, groups[0])
+    del obs
+    O.lib().orc_set_blas_threads(threads)
+    run = O.McRun(blk)
+    t_pro = time.perf_counter()
+    run.step(args.prologue + args.warmup)
+    pro_s = time.perf_counter() - t_pro
     t0 = time.perf_counter()
-    done = _oracle_steps(O, L, run, args.steps)
+    tr = run.step(args.steps)
     dt = time.perf_counter() - t0
-    L.orc_mc_run_free(run)
+    run.close()
+    done = len(tr)
     value = done / dt
-    window = f"APG iterations {args.warmup + 1}..{args.warmup + done} of block 0 (10000x1250)"
+    first = args.prologue + args.warmup + 1
+    window = f"APG iterations {first}..{first + done - 1} of block 0 (10000x1250)"
     line = dict(impl="reference", metric=METRIC, value=value, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * dt / max(done, 1), higher_is_better=True,
-                scaling="strong", vs_baseline=None, dtype="f64", data="synthetic (reference generator, seed 1)",
+                scaling="strong", vs_baseline=None, dtype="f64",
+                data="synthetic (oracle restatement of the reference generator gen_mc_instance, seed 1)",
                 config=dict(workload=f"{args.workload}: DFC-Proj MC {wl['m']}x{wl['n']} r={wl['r']} "
                                      f"{wl['s']} obs sigma={wl['sigma']} t={wl['t']} default ApgConfig",
-                            window=window),
+                            window=window, prologue_s=round(pro_s, 1),
+                            ranks=[t["rank"] for t in tr]),
                 cpu_baseline=dict(value=value, unit=UNIT, cores=threads, kind="port",
                                   sample=f"{window}; oracle/ restatement of apg_mc (single-threaded sparse "
                                          f"ops as in the reference, OpenBLAS/LAPACK with {threads} threads)"),
                 e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
+
+
+def step_roofline(w0, w1, ms, steps, peaks, peak_kind):
+    """Packed-step roofline: the algorithmic work of every library op executed inside the timed
+    window (always-on counters, no events) over the window's device time. Tensor-path work =
+    GEMMs + Cholesky + Jacobi + Householder fallback FLOPs (FP64 DMMA); HBM-path work = the
+    SDDMM / SpMM / elementwise / reduction bytes."""
+    d = {k: {f: w1[k][f] - w0[k][f] for f in ("launches", "flops", "bytes")} for k in w1}
+    tensor_ops = ("gemm", "gemm_small", "cholesky", "jacobi", "qr_fallback")
+    fl = sum(d[k]["flops"] for k in tensor_ops)
+    by = sum(d[k]["bytes"] for k in d if k not in tensor_ops)
+    sec = ms * 1e-3
+    ach = fl / sec / 1e12
+    return dict(bound="tensor", achieved=ach, peak=FP64_DMMA_PEAK_TFLOPS, unit="TFLOP/s",
+                frac=ach / FP64_DMMA_PEAK_TFLOPS, flops_per_step=fl / max(steps, 1),
+                gemm_flops_per_step=(d["gemm"]["flops"] + d["gemm_small"]["flops"]) / max(steps, 1),
+                hbm_bytes_per_step=by / max(steps, 1), hbm_gbs=by / sec / 1e9,
+                launches_per_step=sum(v["launches"] for v in d.values()) / max(steps, 1),
+                peak_source="measured FP64 DMMA (tools/fp64_peak.cu, profiles/fp64_peak.txt)",
+                note="algorithmic FLOPs of all tensor-path ops in the timed window (all blocks) / window "
+                     "device time (CUDA events); Jacobi FLOPs are the executed sweeps' rotation work")
 
 
 def main():
@@ -340,7 +372,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-lowrank", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the DFC-Nys (c2) and RMF (c3) runs")
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of timed CPU work for cpu_baseline")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -396,6 +428,7 @@ def main():
         advance(1)
     barrier()
     launches0 = P.launch_count()
+    work0 = P.work_counters()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # The K steps run back to back per block: every block's thread advances it K iterations on
     # its own stream, as the F step runs (blocks are independent, P/include/dfc/dfc.hpp:133-147);
@@ -407,6 +440,7 @@ def main():
         e1.record()
         e1.synchronize()
     launches = P.launch_count() - launches0
+    work1 = P.work_counters()
     ms = e0.elapsed_time(e1)
     cdev = "cuda" if (dist is None or dist.get_backend() == "nccl") else "cpu"
     tot = torch.tensor([ms, float(iters)], dtype=torch.float64, device=cdev)
@@ -419,6 +453,7 @@ def main():
     else:
         iters_all = float(iters)
     value = iters_all / (ms * 1e-3)
+    roof_step = step_roofline(work0, work1, ms, args.steps, *measured_peaks())
 
     # kernel accounting on one extra iteration of one block, run alone (outside the timed
     # region) so every op's CUDA-event interval is its own device time
@@ -455,31 +490,38 @@ def main():
     for sv in solvers.values():
         sv.close()
 
-    # e2e: full DFC-Proj solve through the public C ABI (host buffers in and out)
+    # e2e: the full DFC-Proj pipeline through the public C ABI, D step included
+    # (P/include/dfc/dfc.hpp:166-200: partition + extract, F, combine; DfcReport.total_ms covers
+    # all three): host triplets in, host factors out. N = 1: one dfcg_dfc_run call. N > 1: every
+    # rank partitions, extracts its own blocks, solves them and joins the distributed combine.
     e2e = None
     if not args.no_e2e:
         barrier()
         t0 = time.perf_counter()
         h2d = d2h = 0
-        rep_iters = []
-
-        def solve(g):
-            est, rep = P.apg_mc(blocks[g], cfg, device=local)
-            return g, est, rep
-
-        outs = list(pool.map(solve, mine))
-        for g, est, rep in outs:
-            h2d += blocks[g].count * 24
-            d2h += (est.left.size + est.right.size) * 8
-            rep_iters.append(rep.iterations)
-        local_ests = {g: est for g, est, _ in outs}
-        final = combine(P, dist, groups, local_ests, wl, local)
-        if final is not None:
-            d2h += (final[0].size + final[1].size) * 8
-        it_t = torch.tensor([float(sum(rep_iters))], dtype=torch.float64, device=cdev)
-        if dist:
+        if dist is None:
+            est, info = P.dfc_run(obs, "proj", t=wl["t"], seed=wl["seed"], workers=wl["t"], device=local)
+            tot_iters = float(sum(r.iterations for r in info["subproblems"]))
+            h2d = obs.count * 24
+            d2h = (est.left.size + est.right.size) * 8
+            phases = dict(divide_ms=info["divide_ms"], factor_ms=info["factor_ms"], combine_ms=info["combine_ms"],
+                          total_ms=info["total_ms"])
+        else:
+            t_d = time.perf_counter()
+            groups_e = P.partition_columns(wl["seed"], PARTITION_STREAM, wl["n"], wl["t"])
+            blocks_e = {g: P.extract_columns(obs, groups_e[g]) for g in mine}
+            divide_ms = 1e3 * (time.perf_counter() - t_d)
+            outs = list(pool.map(lambda g: (g, *P.apg_mc(blocks_e[g], cfg, device=local)), mine))
+            for g, est, rep in outs:
+                h2d += blocks_e[g].count * 24
+                d2h += (est.left.size + est.right.size) * 8
+            final = combine(P, dist, groups_e, {g: est for g, est, _ in outs}, wl, local)
+            if final is not None:
+                d2h += (final[0].size + final[1].size) * 8
+            it_t = torch.tensor([float(sum(rep.iterations for _, _, rep in outs))], dtype=torch.float64, device=cdev)
             dist.all_reduce(it_t)
-        tot_iters = it_t.item()
+            tot_iters = it_t.item()
+            phases = dict(divide_ms=divide_ms)
         barrier()
         wall = time.perf_counter() - t0
         wt = torch.tensor([wall], dtype=torch.float64, device=cdev)
@@ -487,9 +529,9 @@ def main():
             dist.all_reduce(wt, op=dist.ReduceOp.MAX)
         wall = wt.item()
         e2e = dict(value=tot_iters / wall, unit=UNIT, h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
-                   dfc_proj_solve_s=wall, block_iterations=int(tot_iters),
-                   note="one e2e step = the whole DFC-Proj solve (all blocks to convergence + combine) "
-                        "through the C ABI from host triplets to host factors")
+                   dfc_proj_solve_s=wall, block_iterations=int(tot_iters), **phases,
+                   note="one e2e step = the whole DFC-Proj pipeline (D: partition + extract, F: all blocks to "
+                        "convergence, C: column_project) through the C ABI from host triplets to host factors")
 
     # Secondary regime ("report both regimes"): the acceptance-style floor
     # (P/tests/acceptance.cpp:127-130) drives block 0 to its low-rank tail, where the sparse
@@ -509,12 +551,12 @@ def main():
         import oracle as O
 
         threads = os.cpu_count() or 1
-        done, dt = cpu_sample(O, blocks[0], args.cpu_budget, threads)
-        cpu = dict(value=done / dt, unit=UNIT, cores=threads, kind="port",
-                   sample=f"block 0 (10000x1250): APG iterations 1..{done} from the start of the solve "
-                          f"({dt:.1f} s); oracle/ restatement of apg_mc (single-threaded sparse ops as in the "
-                          f"reference, OpenBLAS/LAPACK with {threads} threads). Early iterations are cheaper "
-                          f"than the GPU's steady-state window, so this overstates the CPU rate.")
+        done, dt, first = cpu_sample(O, blocks[0], args.cpu_budget, threads)
+        cpu = dict(value=done / max(dt, 1e-9), unit=UNIT, cores=threads, kind="port",
+                   sample=f"block 0 (10000x1250): APG iterations {first}..{first + done - 1} ({dt:.1f} s), the "
+                          f"first iterations entered at rank >= 400 (earlier, cheaper iterations run untimed); "
+                          f"oracle/ restatement of apg_mc (single-threaded sparse ops as in the reference, "
+                          f"OpenBLAS/LAPACK with {threads} threads)")
 
     if rank == 0:
         line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
@@ -526,7 +568,7 @@ def main():
                                        f"{args.prologue + args.warmup + args.steps} of every block",
                                 blocks_per_gpu=len(mine), l2="inputs > L2 (no flush)",
                                 parallelism=f"{wl['t']} blocks over {world} GPU(s), one CUDA stream per block"),
-                    roofline=roof, roofline_gemm=roof_gemm, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
+                    roofline=roof, roofline_step=roof_step, roofline_gemm=roof_gemm, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
                     clocks=clocks.summary(), combine_ms=combine_ms,
                     combine=dict(ms=combine_ms, device_ops=combine_ops,
                                  note="DFC-Proj column_project of the 8 block estimates (host factors in and out; "

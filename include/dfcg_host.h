@@ -58,6 +58,9 @@ int64_t dfcg_launch_count(void);
 /* Per op class: launches, summed CUDA-event ms, algorithmic FLOPs and bytes. Returns the
  * number of classes filled (DFCG_PROF_NUM_OPS) or a negative error. */
 int dfcg_prof_collect(int64_t* launches, double* ms, double* flops, double* bytes);
+/* Always-on cumulative work counters per op class since the library loaded (no events):
+ * launches, algorithmic FLOPs and bytes. Difference two reads around a timed window. */
+int dfcg_work_counters(int64_t* launches, double* flops, double* bytes);
 
 #ifdef __cplusplus
 }

@@ -460,3 +460,33 @@ def dfc_run(obs: Observed, variant="proj", ensemble=False, t=4, l=0, d=0, rp_p=5
     return est, dict(divide_ms=rep.divide_ms, factor_ms=rep.factor_ms, combine_ms=rep.combine_ms,
                      total_ms=rep.total_ms, chosen_k=rep.chosen_k, k_clamped=bool(rep.k_clamped),
                      rank_deficient=bool(rep.rank_deficient), subproblems=sub)
+
+
+class McRun:
+    """Resumable apg_mc (orc_mc_run_*): step(n) -> per-iteration trace; finish() -> (Estimate,
+    Report) of the current iterate without ending the run (bench windows, fixture generation)."""
+
+    def __init__(self, obs: Observed, cfg: OrcApgCfg | None = None):
+        self._h = _obs_handle(obs)
+        self.ptr = C.c_void_p()
+        _check(lib().orc_mc_run_new(self._h.ptr, C.byref(cfg or apg_cfg()), C.byref(self.ptr)))
+
+    def step(self, n: int):
+        tr = (OrcTrace * max(n, 1))()
+        done, ln = i64(), i64()
+        _check(lib().orc_mc_run_step_trace(self.ptr, i64(n), C.byref(done), tr, i64(max(n, 1)), C.byref(ln)))
+        return _report(OrcReport(), tr, min(ln.value, max(n, 1))).trace
+
+    def finish(self):
+        out = C.c_void_p()
+        rep = OrcReport()
+        _check(lib().orc_mc_run_finish(self.ptr, C.byref(out), C.byref(rep)))
+        return _est_from_handle(out), _report(rep, None, 0)
+
+    def close(self):
+        if self.ptr:
+            lib().orc_mc_run_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        self.close()

@@ -272,6 +272,17 @@ int orc_mc_run_step(orc::ApgMcRun* r, long long n, long long* done) {
     *done = k;
   });
 }
+// Same, with the per-iteration trace of the stepped iterations (fixture generation).
+int orc_mc_run_step_trace(orc::ApgMcRun* r, long long n, long long* done, OrcTrace* trace, long long cap,
+                          long long* len) {
+  return guard([&] {
+    std::vector<orc::IterTrace> tr;
+    long long k = 0;
+    while (k < n && r->step(&tr)) ++k;
+    *done = k;
+    to_trace(tr, trace, cap, len);
+  });
+}
 int orc_mc_run_finish(orc::ApgMcRun* r, OrcEst** out, OrcReport* rep) {
   return guard([&] {
     auto [L, rp] = r->finish();

@@ -45,6 +45,7 @@ from .host import (  # noqa: F401,E402
     gen_mc_instance,
     gen_recsys_instance,
     launch_count,
+    work_counters,
     prof_collect,
     prof_enable,
     gen_rmf_instance,

@@ -11,6 +11,7 @@ namespace prof {
 
 std::atomic<bool> g_enabled{false};
 std::atomic<long long> g_launches{0};
+std::atomic<long long> g_work_flops[kNumOps], g_work_bytes[kNumOps], g_work_launches[kNumOps];
 
 namespace {
 struct Rec {
@@ -25,6 +26,9 @@ std::vector<Rec> g_recs;
 
 Scope::Scope(Op op, cudaStream_t s, double flops, double bytes, int launches)
     : op_(op), s_(s), flops_(flops), bytes_(bytes), launches_(launches) {
+  g_work_flops[op].fetch_add(static_cast<long long>(flops), std::memory_order_relaxed);
+  g_work_bytes[op].fetch_add(static_cast<long long>(bytes), std::memory_order_relaxed);
+  g_work_launches[op].fetch_add(launches, std::memory_order_relaxed);
   if (!g_enabled.load(std::memory_order_relaxed)) return;
   on_ = true;
   cudaEventCreate(&e0_);
@@ -57,6 +61,15 @@ void dfcg_prof_enable(int on) {
 }
 
 int64_t dfcg_launch_count(void) { return g_launches.load(); }
+
+int dfcg_work_counters(int64_t* launches, double* flops, double* bytes) {
+  for (int i = 0; i < kNumOps; ++i) {
+    launches[i] = g_work_launches[i].load();
+    flops[i] = static_cast<double>(g_work_flops[i].load());
+    bytes[i] = static_cast<double>(g_work_bytes[i].load());
+  }
+  return kNumOps;
+}
 
 int dfcg_prof_collect(int64_t* launches, double* ms, double* flops, double* bytes) {
   std::lock_guard<std::mutex> lock(g_mu);

@@ -28,6 +28,9 @@ enum Op : int {
 
 extern std::atomic<bool> g_enabled;
 extern std::atomic<long long> g_launches;
+// Always-on work counters per op class (algorithmic FLOPs / bytes / launches of every scope,
+// no events): bench.py reads them around its timed window for the packed-step roofline.
+extern std::atomic<long long> g_work_flops[kNumOps], g_work_bytes[kNumOps], g_work_launches[kNumOps];
 
 inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 

@@ -168,6 +168,16 @@ def prof_collect() -> dict:
             for i, op in enumerate(PROF_OPS)}
 
 
+def work_counters() -> dict:
+    """{op: dict(launches, flops, bytes)}: cumulative always-on counters (no events)."""
+    n = len(PROF_OPS)
+    launches = np.zeros(n, np.int64)
+    fl, by = np.zeros(n), np.zeros(n)
+    _check(min(0, lib().dfcg_work_counters(_i(launches), _d(fl), _d(by))))
+    return {op: dict(launches=int(launches[i]), flops=float(fl[i]), bytes=float(by[i]))
+            for i, op in enumerate(PROF_OPS)}
+
+
 def launch_count() -> int:
     """Total kernels launched by libdfcg in this process."""
     lib().dfcg_launch_count.restype = i64
