@@ -19,7 +19,9 @@
  * All arithmetic is FP64. Every function returns DFCG_OK (0) or a negative error code;
  * dfcg_last_error() returns the thread's last message. Error codes map onto the
  * reference's exceptions: DFCG_EINVAL = std::invalid_argument, DFCG_ERANGE =
- * std::out_of_range, DFCG_EBLOCK = BlockError (dfc.hpp:50-54, see dfcg_last_error_block).
+ * std::out_of_range, DFCG_EBLOCK = BlockError (dfc.hpp:50-54, see dfcg_last_error_block;
+ * for DFCG_EBLOCK dfcg_last_error() is the failing block's own message, without the
+ * "block N: " prefix that BlockError's constructor adds).
  * Result arrays are allocated by the library (malloc) and released with dfcg_free.
  */
 #ifndef DFCG_H_
@@ -111,6 +113,9 @@ typedef struct {
   int32_t task;
   double lambda;
   int32_t workers;
+  /* Proj-Ens anchors: 0 = every block (the reference, dfc.hpp:191-195); A > 0 = the first
+   * min(A, t) plan groups (BASELINE c5's "ensemble of 4"; an extension of the reference). */
+  int64_t ensemble_anchors;
 } dfcg_dfc_cfg;
 
 /* DfcReport, P/include/dfc/dfc.hpp:56-65. subproblems has n_sub entries (library-allocated). */

@@ -48,7 +48,7 @@ class OrcTrace(C.Structure):
 class OrcDfcCfg(C.Structure):
     _fields_ = [("variant", C.c_int), ("ensemble", C.c_int), ("t", i64), ("l", i64), ("d", i64),
                 ("rp_k", i64), ("rp_p", i64), ("rp_q", i64), ("seed", u64), ("solver", OrcApgCfg),
-                ("task", C.c_int), ("lambda_", C.c_double), ("workers", C.c_int)]
+                ("task", C.c_int), ("lambda_", C.c_double), ("workers", C.c_int), ("ensemble_anchors", i64)]
 
 
 class OrcDfcReport(C.Structure):
@@ -445,10 +445,10 @@ TASKS = {"mc": 0, "rmf": 1}
 
 
 def dfc_run(obs: Observed, variant="proj", ensemble=False, t=4, l=0, d=0, rp_p=5, rp_q=2, seed=0,
-            solver_cfg: OrcApgCfg | None = None, task="mc", lam=0.0, workers=1):
+            solver_cfg: OrcApgCfg | None = None, task="mc", lam=0.0, workers=1, ensemble_anchors=0):
     """dfc_run (P/include/dfc/dfc.hpp:326-335) with the reference's DfcConfig fields."""
     cfg = OrcDfcCfg(VARIANTS[variant], int(ensemble), t, l, d, 1, rp_p, rp_q, seed,
-                    solver_cfg or apg_cfg(), TASKS[task], lam, workers)
+                    solver_cfg or apg_cfg(), TASKS[task], lam, workers, ensemble_anchors)
     h = _obs_handle(obs)
     out = C.c_void_p()
     rep = OrcDfcReport()

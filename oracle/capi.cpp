@@ -83,6 +83,7 @@ struct OrcDfcCfg {
   int task;
   double lambda;
   int workers;
+  long long ensemble_anchors;
 };
 struct OrcDfcReport {
   double divide_ms, factor_ms, combine_ms, total_ms;
@@ -378,6 +379,9 @@ int orc_dfc_run(const OrcObs* obs, const OrcDfcCfg* c, OrcEst** out, OrcDfcRepor
     cfg.task = static_cast<orc::Task>(c->task);
     cfg.lambda = c->lambda;
     cfg.workers = c->workers;
+    cfg.ensemble_anchors = c->ensemble_anchors;
+    if (cfg.ensemble_anchors != 0 && cfg.variant != orc::DfcVariant::Proj)
+      throw std::invalid_argument("dfc_run: ensemble_anchors applies to DFC-Proj-Ens only");
     auto [L, r] = orc::dfc_run(obs->obs, cfg);
     *out = new OrcEst{std::move(L)};
     rep->divide_ms = r.divide_ms;

@@ -1126,6 +1126,9 @@ Index median_rank(const std::vector<Index>& ranks) {
 std::pair<LowRankEstimate, DfcReport> dfc_proj(const ObservedMatrix& obs, const DfcConfig& cfg, const BaseSolver& solver) {
   if (cfg.variant != DfcVariant::Proj) throw std::invalid_argument("dfc_proj: wrong variant");
   if (cfg.t < 1 || cfg.t > obs.cols()) throw std::invalid_argument("dfc_proj: need 1 <= t <= n");
+  if (cfg.ensemble_anchors < 0) throw std::invalid_argument("dfc_proj: ensemble_anchors must be >= 0");
+  if (cfg.ensemble_anchors > 0 && !cfg.ensemble)
+    throw std::invalid_argument("dfc_proj: ensemble_anchors needs ensemble = true");
   DfcReport report;
   detail::PhaseClock total, phase;
   SeededRng prng(cfg.seed, streams::partition);
@@ -1140,8 +1143,13 @@ std::pair<LowRankEstimate, DfcReport> dfc_proj(const ObservedMatrix& obs, const 
   if (!cfg.ensemble) {
     out = column_project(ests[0], ests, plan);
   } else {
-    std::vector<LowRankEstimate> projected(ests.size(), LowRankEstimate::zero(1, 1));
-    detail::parallel_for(ests.size(), cfg.workers, [&](std::size_t i) { projected[i] = column_project(ests[i], ests, plan); });
+    // extension: the first `ensemble_anchors` plan groups anchor the ensemble (0 = all t, the
+    // reference's dfc.hpp:191-195); the recompression target stays the median of ALL block ranks
+    const std::size_t anchors = cfg.ensemble_anchors > 0
+                                    ? std::min<std::size_t>(static_cast<std::size_t>(cfg.ensemble_anchors), ests.size())
+                                    : ests.size();
+    std::vector<LowRankEstimate> projected(anchors, LowRankEstimate::zero(1, 1));
+    detail::parallel_for(anchors, cfg.workers, [&](std::size_t i) { projected[i] = column_project(ests[i], ests, plan); });
     out = average_estimates(projected, median_rank(detail::block_ranks(ests)));
   }
   report.combine_ms = phase.lap();

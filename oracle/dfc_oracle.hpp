@@ -319,6 +319,7 @@ struct DfcConfig {
   Task task = Task::MC;
   double lambda = 0.0;
   int workers = 1;
+  Index ensemble_anchors = 0;  // extension (BASELINE c5 "ensemble of 4"): 0 = all t blocks
 };
 struct BlockError : std::runtime_error {
   BlockError(std::size_t block, const std::string& what)

@@ -33,8 +33,9 @@ class BlockError(RuntimeError):
     """dfc::BlockError (P/include/dfc/dfc.hpp:50-54): lowest failing block index + message."""
 
     def __init__(self, block: int, msg: str):
-        super().__init__(msg)
+        super().__init__(f"block {block}: {msg}")  # the reference's what() (dfc.hpp:51-52)
         self.block = block
+        self.inner = msg
 
 
 class ApgCfgC(C.Structure):
@@ -68,7 +69,7 @@ class TraceC(C.Structure):
 class DfcCfgC(C.Structure):
     _fields_ = [("variant", C.c_int32), ("ensemble", C.c_int32), ("t", i64), ("l", i64), ("d", i64),
                 ("rp_p", i64), ("rp_q", i64), ("seed", u64), ("solver", ApgCfgC), ("task", C.c_int32),
-                ("lambda_", C.c_double), ("workers", C.c_int32)]
+                ("lambda_", C.c_double), ("workers", C.c_int32), ("ensemble_anchors", i64)]
 
 
 class DfcReportC(C.Structure):
@@ -413,12 +414,15 @@ TASKS = {"mc": 0, "rmf": 1}
 
 
 def dfc_run(obs: Observed, variant="proj", ensemble=False, t=4, l=0, d=0, rp_p=5, rp_q=2, seed=0,
-            solver_cfg: ApgConfig | None = None, task="mc", lam=0.0, workers=1, device: int = 0):
-    """dfc_run (P/include/dfc/dfc.hpp:326-335): D on host, F and C on the GPU."""
+            solver_cfg: ApgConfig | None = None, task="mc", lam=0.0, workers=1, device: int = 0,
+            ensemble_anchors: int = 0):
+    """dfc_run (P/include/dfc/dfc.hpp:326-335): D on host, F and C on the GPU. ensemble_anchors
+    (Proj-Ens only): 0 = every block anchors the ensemble, as in the reference; A > 0 = the first
+    min(A, t) plan groups (BASELINE c5's "ensemble of 4")."""
     keep = _Keep()
     o = _obs_in(obs, keep)
     cfg = DfcCfgC(VARIANTS[variant], int(ensemble), t, l, d, rp_p, rp_q, seed, (solver_cfg or ApgConfig()).c(),
-                  TASKS[task], lam, workers)
+                  TASKS[task], lam, workers, ensemble_anchors)
     out = LowRankC()
     rep = DfcReportC()
     _check(lib().dfcg_dfc_run(context(device), C.byref(o), C.byref(cfg), C.byref(out), C.byref(rep)))

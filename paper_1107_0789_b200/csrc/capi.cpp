@@ -37,7 +37,9 @@ int guard(F&& f) {
     f();
     return DFCG_OK;
   } catch (const BlockError& e) {
-    g_err = e.what();
+    // the inner message: a caller rethrowing BlockError(dfcg_last_error_block(), msg) adds the
+    // "block N: " prefix itself (P/include/dfc/dfc.hpp:50-54), exactly once
+    g_err = e.inner;
     g_err_block = static_cast<int64_t>(e.block);
     return DFCG_EBLOCK;
   } catch (const CudaError& e) {
@@ -472,6 +474,7 @@ int dfcg_dfc_run(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_dfc_cfg* c, dfcg_
     cfg.task = c->task == 1 ? Task::RMF : Task::MC;
     cfg.lambda = c->lambda;
     cfg.workers = c->workers;
+    cfg.ensemble_anchors = c->ensemble_anchors;
     auto [est, r] = dfc_run(*ctx->dev, obs, cfg);
     {
       CallStream cs(*ctx->dev);

@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -40,6 +41,14 @@ struct CudaError : std::runtime_error {
   } while (0)
 
 inline int cdiv(i64 a, i64 b) { return static_cast<int>((a + b - 1) / b); }
+
+// Bit of `dev` in a per-device flag word (one-time kernel attribute opt-ins). The flag words
+// are std::atomic<std::uint64_t>: concurrent first callers may both run the (idempotent)
+// setup, then set the bit; ordinals >= 64 are rejected instead of shifting out of range.
+inline std::uint64_t dev_bit(int dev) {
+  if (dev < 0 || dev >= 64) throw std::runtime_error("device ordinal outside [0, 64)");
+  return std::uint64_t{1} << dev;
+}
 
 // Stream-ordered device buffer (cudaMallocAsync from the device's default pool,
 // whose release threshold is raised at context creation so reuse is cheap).

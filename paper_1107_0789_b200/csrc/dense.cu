@@ -249,11 +249,11 @@ template <bool TA, bool TB, int BM, int BN, int WM, int WN>
 int gemm_resident() {
   constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
   const size_t smem = sizeof(double) * STAGES * (Tile<TA, BM>::elems + Tile<!TB, BN>::elems);
-  static unsigned configured = 0;  // one bit per device
+  static std::atomic<std::uint64_t> configured{0};  // one bit per device
   static int resident = 0;
   int dev = 0;
   DFCG_CUDA(cudaGetDevice(&dev));
-  if (!(configured & (1u << dev))) {
+  if (!(configured.load() & dev_bit(dev))) {
     DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, BM, BN, WM, WN, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DFCG_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, BM, BN, WM, WN, true>,
@@ -264,7 +264,7 @@ int gemm_resident() {
     DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, gemm_kernel<TA, TB, BM, BN, WM, WN, true>, THREADS,
                                                             smem));
     resident = std::max(1, std::min(r0, r1));
-    configured |= 1u << dev;
+    configured.fetch_or(dev_bit(dev));
   }
   return resident;
 }

@@ -278,6 +278,9 @@ std::pair<DevLowRank, DfcReport> dfc_proj(DeviceContext& ctx, const HostObs& obs
                                           const BaseSolver& solver) {
   if (cfg.variant != DfcVariant::Proj) throw std::invalid_argument("dfc_proj: wrong variant");
   if (cfg.t < 1 || cfg.t > obs.n) throw std::invalid_argument("dfc_proj: need 1 <= t <= n");
+  if (cfg.ensemble_anchors < 0) throw std::invalid_argument("dfc_proj: ensemble_anchors must be >= 0");
+  if (cfg.ensemble_anchors > 0 && !cfg.ensemble)
+    throw std::invalid_argument("dfc_proj: ensemble_anchors needs ensemble = true");
   DfcReport report;
   PhaseClock total, phase;
   SeededRng prng(cfg.seed, streams::partition);
@@ -296,8 +299,13 @@ std::pair<DevLowRank, DfcReport> dfc_proj(DeviceContext& ctx, const HostObs& obs
     CallStream cs(ctx);
     column_project(cs.s, ests[0], bl, plan, obs.n, out);
   } else {
-    std::vector<DevLowRank> projected(ests.size());
-    parallel_for(ctx, ests.size(), cfg.workers,
+    // every block projected onto each anchor's column space (all t blocks in the reference;
+    // the first ensemble_anchors plan groups when that knob is set)
+    const std::size_t anchors = cfg.ensemble_anchors > 0
+                                    ? std::min<std::size_t>(static_cast<std::size_t>(cfg.ensemble_anchors), ests.size())
+                                    : ests.size();
+    std::vector<DevLowRank> projected(anchors);
+    parallel_for(ctx, anchors, cfg.workers,
                  [&](std::size_t i, cudaStream_t s) { column_project(s, ests[i], bl, plan, obs.n, projected[i]); });
     CallStream cs(ctx);
     average_estimates(cs.s, ptrs(projected), median_rank(block_ranks(ests)), out);
@@ -430,6 +438,8 @@ std::pair<DevLowRank, DfcReport> dfc_nys(DeviceContext& ctx, const HostObs& obs,
 
 // dfc_run, dfc.hpp:326-335.
 std::pair<DevLowRank, DfcReport> dfc_run(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg) {
+  if (cfg.ensemble_anchors != 0 && cfg.variant != DfcVariant::Proj)
+    throw std::invalid_argument("dfc_run: ensemble_anchors applies to DFC-Proj-Ens only");
   const BaseSolver solver = make_base_solver(ctx, cfg.task, cfg.solver_cfg, cfg.lambda);
   switch (cfg.variant) {
     case DfcVariant::Proj: return dfc_proj(ctx, obs, cfg, solver);

@@ -42,12 +42,16 @@ struct DfcConfig {
   Task task = Task::MC;
   double lambda = 0.0;
   int workers = 1;
+  // Proj-Ens anchors (BASELINE c5 "ensemble of 4"; not in the reference, whose ensemble anchors
+  // on every block, dfc.hpp:191-195): 0 = all t blocks, else the first min(A, t) plan groups.
+  i64 ensemble_anchors = 0;
 };
 
 struct BlockError : std::runtime_error {
   BlockError(std::size_t block, const std::string& what)
-      : std::runtime_error("block " + std::to_string(block) + ": " + what), block(block) {}
+      : std::runtime_error("block " + std::to_string(block) + ": " + what), block(block), inner(what) {}
   std::size_t block;
+  std::string inner;  // the failing block's own message, without the "block N: " prefix
 };
 
 struct DfcReport {

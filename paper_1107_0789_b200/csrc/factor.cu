@@ -17,6 +17,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <mutex>
+
 #include "common.cuh"
 
 #include <cooperative_groups.h>
@@ -415,35 +417,63 @@ __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
 }
 
 // In-place blocked Cholesky of G (n x n) -> upper R (lower part zeroed); Rinv = R^-1.
-// want_inverse == false: only R is produced (Rinv then holds just the diagonal-block inverses).
-// Per host thread and device: a helper stream and two events (created once, never destroyed:
-// they live as long as the thread's CUDA context use).
+// want_inverse == false: only R is produced and Rinv's contents are unspecified (scratch).
+// The look-ahead helper stream and its two events are leased from a per-device pool for the
+// duration of one factorisation (worker threads come and go with every dfc_run / combine;
+// the pool holds at most as many helpers as factorisations ever ran concurrently).
 struct AuxStream {
   cudaStream_t s = nullptr;
   cudaEvent_t updated = nullptr, factored = nullptr;
 };
-AuxStream& aux_stream(int dev) {
-  thread_local AuxStream aux[64];
-  AuxStream& a = aux[dev & 63];
-  if (!a.s) {
-    DFCG_CUDA(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
-    DFCG_CUDA(cudaEventCreateWithFlags(&a.updated, cudaEventDisableTiming));
-    DFCG_CUDA(cudaEventCreateWithFlags(&a.factored, cudaEventDisableTiming));
+class AuxLease {
+ public:
+  explicit AuxLease(int dev) : dev_(dev) {
+    {
+      std::lock_guard<std::mutex> lock(mu());
+      auto& fl = free_list(dev);
+      if (!fl.empty()) {
+        a_ = fl.back();
+        fl.pop_back();
+        return;
+      }
+    }
+    DFCG_CUDA(cudaStreamCreateWithFlags(&a_.s, cudaStreamNonBlocking));
+    DFCG_CUDA(cudaEventCreateWithFlags(&a_.updated, cudaEventDisableTiming));
+    DFCG_CUDA(cudaEventCreateWithFlags(&a_.factored, cudaEventDisableTiming));
   }
-  return a;
-}
+  ~AuxLease() {
+    // work still queued on the helper stays ordered: the next lessee's launches queue behind it
+    std::lock_guard<std::mutex> lock(mu());
+    free_list(dev_).push_back(a_);
+  }
+  AuxLease(const AuxLease&) = delete;
+  AuxLease& operator=(const AuxLease&) = delete;
+  AuxStream& get() { return a_; }
+
+ private:
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<AuxStream>& free_list(int dev) {
+    static std::vector<AuxStream> lists[64];
+    return lists[dev_bit(dev) ? dev : 0];
+  }
+  int dev_;
+  AuxStream a_;
+};
 
 void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol,
                           int* fail, bool want_inverse) {
-  static unsigned configured = 0;  // one bit per device: opt in to > 48 KB dynamic shared memory
+  static std::atomic<std::uint64_t> configured{0};  // one bit per device: opt in to > 48 KB dynamic shared memory
   int dev = 0;
   DFCG_CUDA(cudaGetDevice(&dev));
-  if (!(configured & (1u << dev))) {
+  if (!(configured.load() & dev_bit(dev))) {
     DFCG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(kPotrfSmem)));
     DFCG_CUDA(cudaFuncSetAttribute(trinv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(kPotrfSmem)));
-    configured |= 1u << dev;
+    configured.fetch_or(dev_bit(dev));
   }
   // DFCG_CHOL_INV_LATE=0: the diagonal inverses inside potrf and the panel TRSM as a GEMM with
   // them (the previous critical path); default: potrf without the inverse, substitution TRSM,
@@ -456,7 +486,8 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   // Look-ahead: after the panel TRSM of block k, the next diagonal block is updated first and
   // factored on a helper stream while the rest of the trailing update runs on s, so the
   // latency-bound 64x64 potrf overlaps the trailing GEMM instead of following it.
-  AuxStream& aux = aux_stream(dev);
+  AuxLease aux_lease(dev);
+  AuxStream& aux = aux_lease.get();
   auto potrf = [&](cudaStream_t st, i64 k0, int kb) {
     prof::Scope scope(prof::kCholesky, st, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
     pdl_launch(potrf_diag_kernel, dim3(1), dim3(256), kPotrfSmem, st, kb, G + k0 * ldg + k0, ldg,
@@ -1648,13 +1679,9 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     const i64 slots = 2 * static_cast<i64>(nsm);
     const i64 k = std::max(1, active_streams(dev));
     // 2-CTA clusters when they fit (a lone c2 block: 8.1 ms of Jacobi per iteration against 8.5
-    // with 4 and 9.2 with 1, with programmatic dependent launch of the rounds); 4 when a slab
-    // needs it
-    for (int c : {2, 4})
-      if (c > CS && k * npairs * c <= slots && wrows >= 64 * c) {
-        CS = c;
-        break;
-      }
+    // with 4 and 9.2 with 1, with programmatic dependent launch of the rounds); 4 only when the
+    // slab already needed it (the loop above)
+    if (CS == 1 && k * npairs * 2 <= slots && wrows >= 128 && dyn_for(slab(2), 0) <= dyn_cap(2)) CS = 2;
     if (cs_env == 1 || cs_env == 2 || cs_env == 4)
       if (dyn_for(slab(cs_env), 0) <= dyn_cap(cs_env)) CS = cs_env;
   }
@@ -1663,8 +1690,8 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
   const int prefetch_v = resident && nj > 0 && dyn_for(cw, 1) <= dyn_cap(CS) ? 1 : 0;  // W and V slabs both fit
   const size_t smem = dyn_for(cw, prefetch_v);
   if (resident) {
-    static unsigned configured = 0;
-    if (!(configured & (1u << dev))) {
+    static std::atomic<std::uint64_t> configured{0};
+    if (!(configured.load() & dev_bit(dev))) {
       auto opt_in = [&](const void* fn, size_t b) {
         DFCG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b)));
       };
@@ -1676,7 +1703,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<16, 1>), s16);
       opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<16, 2>), s16 - 8192);
       opt_in(reinterpret_cast<const void*>(jacobi_round_resident_kernel<16, 4>), s16 - 8192);
-      configured |= 1u << dev;
+      configured.fetch_or(dev_bit(dev));
     }
   }
   // Optional (DFCG_JACOBI_GRAPH=1): the p - 1 round launches of a sweep, identical from sweep
@@ -1772,13 +1799,13 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     {
       prof::Scope scope(prof::kJacobi, s, 8.0 * 6.0 * cols * cols * (wrows + nj), 8.0 * 16.0 * cols * (wrows + nj));
       constexpr size_t kOne = sizeof(double) * kSmallN * (kSmallN + 1);
-      static unsigned configured = 0;
+      static std::atomic<std::uint64_t> configured{0};
       int dev = 0;
       DFCG_CUDA(cudaGetDevice(&dev));
-      if (!(configured & (1u << dev))) {
+      if (!(configured.load() & dev_bit(dev))) {
         DFCG_CUDA(cudaFuncSetAttribute(jacobi_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(2 * kOne)));
-        configured |= 1u << dev;
+        configured.fetch_or(dev_bit(dev));
       }
       jacobi_small_kernel<<<1, 256, (nj > 0 ? 2 : 1) * kOne, s>>>(static_cast<int>(wrows), static_cast<int>(cols),
                                                                   static_cast<int>(nj), W.get(), np, J.get(), np, tol,

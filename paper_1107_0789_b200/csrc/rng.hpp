@@ -107,8 +107,9 @@ class NormalCache {
     if (transformer_.joinable()) transformer_.join();
     for (double* p : chunks_)
       if (p) cudaFree(p);
-    for (cudaEvent_t e : use_ev_)
-      if (e) cudaEventDestroy(e);
+    for (auto& evs : use_ev_)
+      for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_free_) cudaEventDestroy(e);
     for (std::uint64_t* p : raw_buf_)
       if (p) cudaFreeHost(p);
     if (stream_) cudaStreamDestroy(stream_);
@@ -161,10 +162,29 @@ class NormalCache {
                                 cudaMemcpyDeviceToDevice, s));
       done += n;
     }
+    // One event per fetch and chunk: fetches on different streams each keep their own record,
+    // and eviction orders the free after ALL of them (completed ones are recycled here).
     std::lock_guard<std::mutex> lock(mu_);
     for (i64 c = c0; c < c1; ++c) {
-      if (!use_ev_[c]) DFCG_CUDA(cudaEventCreateWithFlags(&use_ev_[c], cudaEventDisableTiming));
-      DFCG_CUDA(cudaEventRecord(use_ev_[c], s));
+      auto& evs = use_ev_[c];
+      for (size_t i = 0; i < evs.size();) {
+        if (cudaEventQuery(evs[i]) == cudaSuccess) {
+          ev_free_.push_back(evs[i]);
+          evs[i] = evs.back();
+          evs.pop_back();
+        } else {
+          ++i;
+        }
+      }
+      cudaEvent_t ev = nullptr;
+      if (!ev_free_.empty()) {
+        ev = ev_free_.back();
+        ev_free_.pop_back();
+      } else {
+        DFCG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      }
+      DFCG_CUDA(cudaEventRecord(ev, s));
+      evs.push_back(ev);
       --pins_[c];
     }
   }
@@ -182,7 +202,7 @@ class NormalCache {
     inflight_.resize(static_cast<size_t>(n), 0);
     pins_.resize(static_cast<size_t>(n), 0);
     last_use_.resize(static_cast<size_t>(n), 0);
-    use_ev_.resize(static_cast<size_t>(n), nullptr);
+    use_ev_.resize(static_cast<size_t>(n));
   }
 
   // Two-stage pipeline: this thread draws the raw 64-bit words of a chunk (sequential
@@ -246,7 +266,7 @@ class NormalCache {
       for (;;) {
         i64 c = -1;
         int b = -1;
-        std::vector<std::pair<double*, cudaEvent_t>> victims;
+        std::vector<std::pair<double*, std::vector<cudaEvent_t>>> victims;
         {
           std::unique_lock<std::mutex> lock(mu_);
           cv_.wait(lock, [&] { return stop_ || !raw_q_.empty(); });
@@ -262,14 +282,19 @@ class NormalCache {
             for (i64 k = 0; k < static_cast<i64>(chunks_.size()); ++k)
               if (chunks_[k] && pins_[k] == 0 && (v < 0 || last_use_[k] < last_use_[v])) v = k;
             if (v < 0) break;
-            victims.push_back({chunks_[v], use_ev_[v]});
+            victims.push_back({chunks_[v], std::move(use_ev_[v])});
+            use_ev_[v].clear();
             chunks_[v] = nullptr;
             --resident;
           }
         }
-        for (auto& [p, ev] : victims) {  // freed on this stream after the chunk's last copy
-          if (ev) DFCG_CUDA(cudaStreamWaitEvent(stream_, ev, 0));
+        for (auto& [p, evs] : victims) {  // freed on this stream after every fetch's copies
+          for (cudaEvent_t ev : evs) DFCG_CUDA(cudaStreamWaitEvent(stream_, ev, 0));
           DFCG_CUDA(cudaFreeAsync(p, stream_));
+        }
+        if (!victims.empty()) {  // the waits captured the records; the events can be reused
+          std::lock_guard<std::mutex> lock(mu_);
+          for (auto& [p, evs] : victims) ev_free_.insert(ev_free_.end(), evs.begin(), evs.end());
         }
         // Box-Muller on the device (CUDA's log / cos, <= 1 ulp from the host libm the oracle
         // uses; the raw words are bit-identical): the host keeps only the serial draws.
@@ -316,7 +341,8 @@ class NormalCache {
   std::vector<char> inflight_;
   std::vector<int> pins_;
   std::vector<std::uint64_t> last_use_;
-  std::vector<cudaEvent_t> use_ev_;
+  std::vector<std::vector<cudaEvent_t>> use_ev_;  // per chunk: one event per fetch not known done
+  std::vector<cudaEvent_t> ev_free_;
   static constexpr int kRawBufs = 3;
   std::uint64_t* raw_buf_[kRawBufs] = {nullptr, nullptr, nullptr};
   std::vector<std::pair<i64, int>> raw_q_;

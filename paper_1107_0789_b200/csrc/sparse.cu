@@ -513,15 +513,15 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
   const char* tile_env = std::getenv("DFCG_SDDMM_TILE");  // 0 / 1 force the entry-parallel / tiled kernel
   const int tile_mode = tile_env ? std::atoi(tile_env) : -1;
   if (om.ntc > 0 && tile_mode != 0) {
-    static unsigned configured = 0;  // one bit per device
+    static std::atomic<std::uint64_t> configured{0};  // one bit per device
     int dev = 0;
     DFCG_CUDA(cudaGetDevice(&dev));
-    if (!(configured & (1u << dev))) {
+    if (!(configured.load() & dev_bit(dev))) {
       DFCG_CUDA(cudaFuncSetAttribute(sddmm_tile_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(sddmm_smem<1, 32>())));
       DFCG_CUDA(cudaFuncSetAttribute(sddmm_tile_kernel<4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(sddmm_smem<4, 16>())));
-      configured |= 1u << dev;
+      configured.fetch_or(dev_bit(dev));
     }
     // 16-byte staging needs even leading dimensions and an even k extent: repack the factors
     // (a few tens of microseconds) unless they already qualify; the padding column is zero.
@@ -602,13 +602,13 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
       const int chunk_tiles = (nt + chunks - 1) / chunks;
       chunks = (nt + chunk_tiles - 1) / chunk_tiles;
       const size_t smem = sizeof(double) * TSP_SLAB * b;
-      static unsigned configured = 0;
+      static std::atomic<std::uint64_t> configured{0};
       int dev = 0;
       DFCG_CUDA(cudaGetDevice(&dev));
-      if (!(configured & (1u << dev))) {
+      if (!(configured.load() & dev_bit(dev))) {
         DFCG_CUDA(cudaFuncSetAttribute(spmm_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sizeof(double) * TSP_SLAB * 64)));
-        configured |= 1u << dev;
+        configured.fetch_or(dev_bit(dev));
       }
       DBuf<double> ws;
       if (chunks > 1) ws.alloc(static_cast<i64>(chunks) * out_rows * b, s);

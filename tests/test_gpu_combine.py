@@ -145,6 +145,23 @@ def test_dfc_run_parity(variant, ens, kw):
     assert ip["chosen_k"] == io["chosen_k"] and ip["rank_deficient"] == io["rank_deficient"]
 
 
+@pytest.mark.parametrize("anchors", [1, 4])
+def test_dfc_proj_ens_anchor_parity(anchors):
+    """BASELINE c5's "ensemble of 4" (an extension of dfc.hpp:189-195): Proj-Ens anchored on the
+    first A plan groups, GPU against the oracle extension."""
+    L0, obs = P.gen_mc_instance(200, 200, 3, 16000, 0.1, 1)
+    pc, oc = cfg_pair()
+    eo, io = O.dfc_run(to_oracle_obs(obs), "proj", ensemble=True, t=6, solver_cfg=oc, seed=1,
+                       ensemble_anchors=anchors)
+    ep, ip = P.dfc_run(obs, "proj", ensemble=True, t=6, solver_cfg=pc, seed=1, workers=3,
+                       ensemble_anchors=anchors)
+    assert [s.iterations for s in ip["subproblems"]] == [s.iterations for s in io["subproblems"]]
+    assert ep.rank == eo.rank
+    assert relF(ep, eo) <= REL_TOL
+    with pytest.raises(ValueError):
+        P.dfc_run(obs, "rp", ensemble=True, t=3, ensemble_anchors=2)
+
+
 def test_dfc_rmf_parity():  # DfcTask RMF path (P/tests/test_dfc.cpp:304-320 shape)
     L0, S0, M = P.gen_rmf_instance(60, 72, 2, 200, 0.01, 3)
     r, c = np.meshgrid(np.arange(60), np.arange(72), indexing="ij")

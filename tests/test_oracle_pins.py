@@ -172,6 +172,32 @@ def test_dfc_identities():  # P/tests/test_dfc.cpp:51-62, 226-239, 322-342
         assert np.array_equal(a.left, b.left) and np.array_equal(a.right, b.right)
 
 
+def test_dfc_proj_ens_anchors():
+    """Extension knob for BASELINE c5's "ensemble of 4": Proj-Ens anchored on the first A plan
+    groups. A = 0 and A >= t are the reference's all-block ensemble (dfc.hpp:189-195) bit for bit;
+    A = 1 is the plain projection onto block 0 recompressed to the median block rank."""
+    L0, obs = O.gen_mc_instance(60, 60, 2, 2400, 0.05, 3, 0)
+    base, _ = O.dfc_run(obs, "proj", ensemble=True, t=6, seed=4)
+    for A in (6, 9):
+        a, _ = O.dfc_run(obs, "proj", ensemble=True, t=6, seed=4, ensemble_anchors=A)
+        assert np.array_equal(a.left, base.left) and np.array_equal(a.right, base.right)
+    four, info = O.dfc_run(obs, "proj", ensemble=True, t=6, seed=4, ensemble_anchors=4)
+    assert four.rank <= max(s.rank for s in info["subproblems"])
+    assert np.linalg.norm(four.dense() - base.dense()) < 0.5 * np.linalg.norm(base.dense())
+    one, info = O.dfc_run(obs, "proj", ensemble=True, t=6, seed=4, ensemble_anchors=1)
+    proj, _ = O.dfc_run(obs, "proj", t=6, seed=4)
+    ranks = sorted(s.rank for s in info["subproblems"])
+    if ranks[(len(ranks) - 1) // 2] >= proj.rank:  # no truncation: the same matrix
+        assert np.linalg.norm(one.dense() - proj.dense()) <= 1e-9 * np.linalg.norm(proj.dense())
+    for bad in (dict(ensemble_anchors=-1), dict(ensemble=False, ensemble_anchors=2)):
+        kw = dict(ensemble=True, t=6, seed=4)
+        kw.update(bad)
+        with pytest.raises(ValueError):
+            O.dfc_run(obs, "proj", **kw)
+    with pytest.raises(ValueError):
+        O.dfc_run(obs, "rp", ensemble=True, t=3, seed=4, ensemble_anchors=2)
+
+
 def test_dfc_block_error_lowest_index():  # P/tests/test_dfc.cpp:118-144 (fault surfaces as BlockError)
     L0, obs = O.gen_mc_instance(6, 5, 1, 30, 0.0, 1, 0)
     with pytest.raises(ValueError):
