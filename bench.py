@@ -136,19 +136,6 @@ def make_blocks(P, wl):
     return L0, obs, groups, blocks
 
 
-def combine(P, dist, groups, ests, wl, device):
-    """DFC-Proj combine of the block estimates; returns (U_b, right) on rank 0 (else None)."""
-    if dist is None:
-        est = P.column_project(ests[0], [ests[g] for g in range(wl["t"])], groups, device=device)
-        return est.left, est.right
-    from paper_1107_0789_b200.distributed import column_project_distributed
-
-    return column_project_distributed(
-        dist, groups, ests, wl["m"],
-        basis_fn=lambda e: P.svd_of_product(e.left, e.right, device=device)[0].left,
-        project_fn=lambda Ub, e: P.project_block(Ub, e, device=device),
-        device=f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu")
-
 
 def roofline_entry(prof, peaks, peak_kind):
     ops = {k: v for k, v in prof.items() if v["launches"] > 0}
@@ -400,7 +387,17 @@ def main():
 
     peaks, peak_kind = measured_peaks()
     L0, obs, groups, blocks = make_blocks(P, wl)
-    mine = [g for g in range(wl["t"]) if g % world == rank]
+    comm = None
+    if dist is not None:
+        # libdfcg's own transport: NCCL inside the library (the uid travels over the process
+        # group), or its host-callback transport over gloo when ranks share one GPU
+        from paper_1107_0789_b200.distributed import Comm, assign_blocks, dfc_run_dist
+
+        comm = Comm.nccl(device=local) if backend == "nccl" else Comm.host()
+        owner = assign_blocks([b.count for b in blocks], world)  # LPT by nnz, as dfc_run_dist assigns
+    else:
+        owner = [0] * wl["t"]
+    mine = [g for g in range(wl["t"]) if owner[g] == rank]
     cfg = P.ApgConfig()
     solvers = {g: P.McSolver(blocks[g], cfg, device=local) for g in mine}
     pool = ThreadPoolExecutor(max_workers=max(1, len(mine)))
@@ -473,20 +470,22 @@ def main():
                          frac=ach / FP64_DMMA_PEAK_TFLOPS, launches=g["launches"],
                          avg_launch_ms=g["ms"] / g["launches"], kernel="gemm_kernel (DMMA m8n8k4)")
 
-    # combine on the current block estimates (column_project, P/include/dfc/sketch.hpp:170-199):
-    # basis broadcast + per-rank projection + row gather over NCCL when N > 1
-    ests = {g: solvers[g].finish()[0] for g in mine}
-    barrier()
-    P.prof_enable(True)
-    t0 = time.perf_counter()
-    combine(P, dist, groups, ests, wl, local)
-    barrier()
-    combine_ms = 1e3 * (time.perf_counter() - t0)
-    cprof = P.prof_collect()
-    P.prof_enable(False)
-    combine_ops = {k: dict(ms=round(v["ms"], 3), launches=v["launches"],
-                           tflops=round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3))
-                   for k, v in cprof.items() if v["launches"] > 0}
+    # combine on the current block estimates (column_project, P/include/dfc/sketch.hpp:170-199);
+    # at N > 1 the combine runs inside dfc_run_dist (e2e below: basis broadcast + row gather)
+    combine_ms, combine_ops = None, None
+    if dist is None:
+        ests = {g: solvers[g].finish()[0] for g in mine}
+        barrier()
+        P.prof_enable(True)
+        t0 = time.perf_counter()
+        P.column_project(ests[0], [ests[g] for g in range(wl["t"])], groups, device=local)
+        barrier()
+        combine_ms = 1e3 * (time.perf_counter() - t0)
+        cprof = P.prof_collect()
+        P.prof_enable(False)
+        combine_ops = {k: dict(ms=round(v["ms"], 3), launches=v["launches"],
+                               tflops=round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3))
+                       for k, v in cprof.items() if v["launches"] > 0}
     for sv in solvers.values():
         sv.close()
 
@@ -507,21 +506,16 @@ def main():
             phases = dict(divide_ms=info["divide_ms"], factor_ms=info["factor_ms"], combine_ms=info["combine_ms"],
                           total_ms=info["total_ms"])
         else:
-            t_d = time.perf_counter()
-            groups_e = P.partition_columns(wl["seed"], PARTITION_STREAM, wl["n"], wl["t"])
-            blocks_e = {g: P.extract_columns(obs, groups_e[g]) for g in mine}
-            divide_ms = 1e3 * (time.perf_counter() - t_d)
-            outs = list(pool.map(lambda g: (g, *P.apg_mc(blocks_e[g], cfg, device=local)), mine))
-            for g, est, rep in outs:
-                h2d += blocks_e[g].count * 24
-                d2h += (est.left.size + est.right.size) * 8
-            final = combine(P, dist, groups_e, {g: est for g, est, _ in outs}, wl, local)
-            if final is not None:
-                d2h += (final[0].size + final[1].size) * 8
-            it_t = torch.tensor([float(sum(rep.iterations for _, _, rep in outs))], dtype=torch.float64, device=cdev)
-            dist.all_reduce(it_t)
-            tot_iters = it_t.item()
-            phases = dict(divide_ms=divide_ms)
+            # every rank: the whole observation set in, its LPT share solved, the combine's
+            # exchange over libdfcg's communicator, the final estimate out (dfcg_dfc_run_dist)
+            est, info = dfc_run_dist(obs, comm, "proj", t=wl["t"], seed=wl["seed"], workers=max(1, len(mine)),
+                                     device=local)
+            tot_iters = float(sum(r.iterations for r in info["subproblems"]))
+            h2d = obs.count * 24
+            d2h = (est.left.size + est.right.size) * 8
+            phases = dict(divide_ms=info["divide_ms"], factor_ms=info["factor_ms"], combine_ms=info["combine_ms"],
+                          total_ms=info["total_ms"], owner=info["owner"])
+            combine_ms = info["combine_ms"]
         barrier()
         wall = time.perf_counter() - t0
         wt = torch.tensor([wall], dtype=torch.float64, device=cdev)
@@ -567,14 +561,19 @@ def main():
                                 window=f"APG iterations {args.prologue + args.warmup + 1}.."
                                        f"{args.prologue + args.warmup + args.steps} of every block",
                                 blocks_per_gpu=len(mine), l2="inputs > L2 (no flush)",
-                                parallelism=f"{wl['t']} blocks over {world} GPU(s), one CUDA stream per block"),
+                                parallelism=f"{wl['t']} blocks over {world} GPU(s) (LPT by nnz), one CUDA "
+                                            f"stream per block; combine over libdfcg's "
+                                            f"{'NCCL' if backend == 'nccl' or world == 1 else 'host'} transport"),
                     roofline=roof, roofline_step=roof_step, roofline_gemm=roof_gemm, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
                     clocks=clocks.summary(), combine_ms=combine_ms,
                     combine=dict(ms=combine_ms, device_ops=combine_ops,
-                                 note="DFC-Proj column_project of the 8 block estimates (host factors in and out; "
-                                      "device_ops = CUDA-event time per op class on this rank)"),
+                                 note="DFC-Proj column_project of the 8 block estimates (N = 1: host factors in and "
+                                      "out, device_ops = CUDA-event time per op class; N > 1: the combine phase of "
+                                      "dfc_run_dist, basis broadcast + projected-row gather)"),
                     lowrank=lowrank, nys_c2=nys, rmf_c3=rmf)
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if dist:
         dist.destroy_process_group()
 

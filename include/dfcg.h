@@ -184,6 +184,39 @@ int dfcg_normals_fetch(dfcg_ctx* ctx, int stream_id, int64_t pos, int64_t n, dou
 int dfcg_project_block(dfcg_ctx* ctx, const double* Ub, int64_t m, int64_t kb, const dfcg_lowrank* block,
                        double* Rg);
 
+/* ---- multi-GPU: one process per GPU (the reference's single-process
+ * parallel_for over subproblems, P/include/dfc/dfc.hpp:84-147, split over ranks) ------------- */
+typedef struct dfcg_comm dfcg_comm;
+/* Caller-provided collective layer on HOST buffers (e.g. torch.distributed over gloo): the
+ * library stages device data through pinned memory. Each callback returns 0 on success and is
+ * invoked by every participating rank in the same global order. */
+typedef struct {
+  void* user;
+  int (*bcast)(void* user, void* buf, int64_t bytes, int32_t root);
+  int (*send)(void* user, const void* buf, int64_t bytes, int32_t peer);
+  int (*recv)(void* user, void* buf, int64_t bytes, int32_t peer);
+} dfcg_host_transport;
+/* NCCL (loaded at run time: the process's libnccl.so.2, else $DFCG_NCCL_LIB): rank 0 draws the
+ * id, the caller distributes it, every rank creates its communicator on ctx's device. */
+int dfcg_nccl_unique_id(unsigned char id[128]);
+int dfcg_comm_init_nccl(dfcg_ctx* ctx, int32_t nranks, int32_t rank, const unsigned char id[128], dfcg_comm** out);
+int dfcg_comm_init_host(int32_t nranks, int32_t rank, const dfcg_host_transport* t, dfcg_comm** out);
+void dfcg_comm_destroy(dfcg_comm* comm);
+/* Host-only traffic pattern through the transport (every root broadcasts, a ring of sends);
+ * *errors = mismatched words seen by this rank. No CUDA for a host transport. */
+int dfcg_comm_selftest(dfcg_comm* comm, int64_t* errors);
+/* LPT assignment of count subproblems to nranks by observation count (descending nnz, ties to
+ * the lower index; each to the least-loaded rank, ties to fewer blocks then the lower rank). */
+int dfcg_assign_blocks(int64_t count, const int64_t* nnz, int32_t nranks, int32_t* owner);
+/* dfc_run over the ranks of comm: every rank passes the same obs and cfg, solves its LPT share
+ * of the subproblems (cfg->workers concurrent streams), and the combine moves factors only
+ * (basis broadcast + row gather for Proj; R-hat for Nys; block factors for Rp). Every rank
+ * returns the final estimate and the report of every subproblem; owner (optional, n_sub
+ * entries up to owner_cap) receives the assignment. A failing subproblem raises DFCG_EBLOCK
+ * with the lowest failing index on every rank. */
+int dfcg_dfc_run_dist(dfcg_ctx* ctx, dfcg_comm* comm, const dfcg_obs* in, const dfcg_dfc_cfg* cfg, dfcg_lowrank* out,
+                      dfcg_dfc_report* rep, int32_t* owner, int64_t owner_cap);
+
 /* ---- whole D-F-C pipeline (replaces dfc_run) --------------------------------------------- */
 int dfcg_dfc_run(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_dfc_cfg* cfg, dfcg_lowrank* out,
                  dfcg_dfc_report* rep);

@@ -30,6 +30,15 @@ int dfcg_sample_without_replacement(uint64_t seed, uint64_t stream, int64_t n, i
 /* cols: n entries, offsets: t + 1 entries (group g = cols[offsets[g]:offsets[g+1]], sorted). */
 int dfcg_partition_columns(uint64_t seed, uint64_t stream, int64_t n, int64_t t, int64_t* cols, int64_t* offsets);
 
+/* The D step as dfc_run runs it (sampling.hpp:83-113 extract_columns / extract_rows): ngroups
+ * disjoint column groups (CSR plan) then, when nrows > 0, one row sample, extracted in one
+ * parallel stable pass (DFCG_DSTEP_THREADS host threads). counts[i] (ngroups + (nrows > 0)
+ * entries) and the triplets of every subproblem, concatenated in that order (column-major within
+ * each, indices relabelled; library-allocated). */
+int dfcg_extract_subproblems(const dfcg_obs* in, int64_t ngroups, const int64_t* group_offsets,
+                             const int64_t* group_cols, int64_t nrows, const int64_t* rows, int64_t* counts,
+                             int64_t** out_rows, int64_t** out_cols, double** out_vals);
+
 /* gen_mc_instance with SeededRng(seed, stream). L0 factors column-major (library-allocated),
  * observations sorted column-major (library-allocated, s entries). */
 int dfcg_gen_mc_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigma, uint64_t seed, uint64_t stream,

@@ -41,6 +41,7 @@ from ._lib import (  # noqa: F401,E402
 )
 from .host import (  # noqa: F401,E402
     extract_columns,
+    extract_subproblems,
     extract_rows,
     gen_mc_instance,
     gen_recsys_instance,

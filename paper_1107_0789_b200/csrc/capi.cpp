@@ -11,11 +11,16 @@
 #include <string>
 
 #include "dfc_host.hpp"
+#include "dist.hpp"
 
 using namespace dfcg;
 
 struct dfcg_ctx {
   DeviceContext* dev;
+};
+
+struct dfcg_comm {
+  std::unique_ptr<Comm> comm;
 };
 
 struct dfcg_mc_solver {
@@ -45,6 +50,9 @@ int guard(F&& f) {
   } catch (const CudaError& e) {
     g_err = e.what();
     return DFCG_ECUDA;
+  } catch (const NcclError& e) {
+    g_err = e.what();
+    return DFCG_ENCCL;
   } catch (const std::bad_alloc& e) {
     g_err = "out of host memory";
     return DFCG_ENOMEM;
@@ -454,45 +462,121 @@ int dfcg_project_block(dfcg_ctx* ctx, const double* Ub, int64_t m, int64_t kb, c
   });
 }
 
+namespace {
+
+HostObs obs_from_c(const dfcg_obs* in) {
+  return HostObs::make(in->m, in->n, std::vector<long long>(in->row, in->row + in->nnz),
+                       std::vector<long long>(in->col, in->col + in->nnz),
+                       std::vector<double>(in->val, in->val + in->nnz));
+}
+
+DfcConfig dfc_cfg_from_c(const dfcg_dfc_cfg* c) {
+  DfcConfig cfg;
+  if (c->variant < 0 || c->variant > 2) throw std::invalid_argument("dfc_run: unknown variant");
+  cfg.variant = static_cast<DfcVariant>(c->variant);
+  cfg.ensemble = c->ensemble != 0;
+  cfg.t = c->t;
+  cfg.l = c->l;
+  cfg.d = c->d;
+  cfg.rp_p = c->rp_p;
+  cfg.rp_q = c->rp_q;
+  cfg.seed = c->seed;
+  cfg.solver_cfg = to_cfg(&c->solver);
+  cfg.task = c->task == 1 ? Task::RMF : Task::MC;
+  cfg.lambda = c->lambda;
+  cfg.workers = c->workers;
+  cfg.ensemble_anchors = c->ensemble_anchors;
+  return cfg;
+}
+
+void dfc_report_to_c(const DfcReport& r, dfcg_dfc_report* rep) {
+  if (!rep) return;
+  rep->divide_ms = r.divide_ms;
+  rep->factor_ms = r.factor_ms;
+  rep->combine_ms = r.combine_ms;
+  rep->total_ms = r.total_ms;
+  rep->chosen_k = r.chosen_k;
+  rep->k_clamped = r.k_clamped;
+  rep->rank_deficient = r.rank_deficient;
+  rep->n_sub = static_cast<int64_t>(r.subproblems.size());
+  rep->subproblems = static_cast<dfcg_solve_report*>(
+      std::malloc(sizeof(dfcg_solve_report) * std::max<size_t>(1, r.subproblems.size())));
+  if (!rep->subproblems) throw std::bad_alloc();
+  for (size_t i = 0; i < r.subproblems.size(); ++i) to_report(r.subproblems[i], &rep->subproblems[i]);
+}
+
+}  // namespace
+
 int dfcg_dfc_run(dfcg_ctx* ctx, const dfcg_obs* in, const dfcg_dfc_cfg* c, dfcg_lowrank* out, dfcg_dfc_report* rep) {
   return guard([&] {
     if (!ctx || !in || !c || !out) throw std::invalid_argument("dfcg_dfc_run: null argument");
-    HostObs obs = HostObs::make(in->m, in->n, std::vector<long long>(in->row, in->row + in->nnz),
-                                std::vector<long long>(in->col, in->col + in->nnz),
-                                std::vector<double>(in->val, in->val + in->nnz));
-    DfcConfig cfg;
-    if (c->variant < 0 || c->variant > 2) throw std::invalid_argument("dfc_run: unknown variant");
-    cfg.variant = static_cast<DfcVariant>(c->variant);
-    cfg.ensemble = c->ensemble != 0;
-    cfg.t = c->t;
-    cfg.l = c->l;
-    cfg.d = c->d;
-    cfg.rp_p = c->rp_p;
-    cfg.rp_q = c->rp_q;
-    cfg.seed = c->seed;
-    cfg.solver_cfg = to_cfg(&c->solver);
-    cfg.task = c->task == 1 ? Task::RMF : Task::MC;
-    cfg.lambda = c->lambda;
-    cfg.workers = c->workers;
-    cfg.ensemble_anchors = c->ensemble_anchors;
-    auto [est, r] = dfc_run(*ctx->dev, obs, cfg);
+    HostObs obs = obs_from_c(in);
+    auto [est, r] = dfc_run(*ctx->dev, obs, dfc_cfg_from_c(c));
     {
       CallStream cs(*ctx->dev);
       to_c(cs.s, est, out);
     }
-    if (rep) {
-      rep->divide_ms = r.divide_ms;
-      rep->factor_ms = r.factor_ms;
-      rep->combine_ms = r.combine_ms;
-      rep->total_ms = r.total_ms;
-      rep->chosen_k = r.chosen_k;
-      rep->k_clamped = r.k_clamped;
-      rep->rank_deficient = r.rank_deficient;
-      rep->n_sub = static_cast<int64_t>(r.subproblems.size());
-      rep->subproblems = static_cast<dfcg_solve_report*>(
-          std::malloc(sizeof(dfcg_solve_report) * std::max<size_t>(1, r.subproblems.size())));
-      for (size_t i = 0; i < r.subproblems.size(); ++i) to_report(r.subproblems[i], &rep->subproblems[i]);
+    dfc_report_to_c(r, rep);
+  });
+}
+
+// ---- multi-GPU
+int dfcg_nccl_unique_id(unsigned char id[128]) {
+  return guard([&] {
+    if (!id) throw std::invalid_argument("dfcg_nccl_unique_id: null argument");
+    nccl_unique_id(id);
+  });
+}
+
+int dfcg_comm_init_nccl(dfcg_ctx* ctx, int32_t nranks, int32_t rank, const unsigned char id[128], dfcg_comm** out) {
+  return guard([&] {
+    if (!ctx || !id || !out) throw std::invalid_argument("dfcg_comm_init_nccl: null argument");
+    auto c = std::make_unique<dfcg_comm>();
+    c->comm = make_nccl_comm(nranks, rank, id, ctx->dev->device);
+    *out = c.release();
+  });
+}
+
+int dfcg_comm_init_host(int32_t nranks, int32_t rank, const dfcg_host_transport* t, dfcg_comm** out) {
+  return guard([&] {
+    if (!t || !out) throw std::invalid_argument("dfcg_comm_init_host: null argument");
+    auto c = std::make_unique<dfcg_comm>();
+    c->comm = make_host_comm(nranks, rank, *t);
+    *out = c.release();
+  });
+}
+
+void dfcg_comm_destroy(dfcg_comm* comm) { delete comm; }
+
+int dfcg_comm_selftest(dfcg_comm* comm, int64_t* errors) {
+  return guard([&] {
+    if (!comm || !errors) throw std::invalid_argument("dfcg_comm_selftest: null argument");
+    *errors = comm->comm->selftest();
+  });
+}
+
+int dfcg_assign_blocks(int64_t count, const int64_t* nnz, int32_t nranks, int32_t* owner) {
+  return guard([&] {
+    if (count < 0 || (count > 0 && (!nnz || !owner))) throw std::invalid_argument("dfcg_assign_blocks: null argument");
+    const std::vector<int> o = assign_blocks_lpt(std::vector<i64>(nnz, nnz + count), nranks);
+    for (int64_t i = 0; i < count; ++i) owner[i] = o[static_cast<size_t>(i)];
+  });
+}
+
+int dfcg_dfc_run_dist(dfcg_ctx* ctx, dfcg_comm* comm, const dfcg_obs* in, const dfcg_dfc_cfg* c, dfcg_lowrank* out,
+                      dfcg_dfc_report* rep, int32_t* owner, int64_t owner_cap) {
+  return guard([&] {
+    if (!ctx || !comm || !in || !c || !out) throw std::invalid_argument("dfcg_dfc_run_dist: null argument");
+    HostObs obs = obs_from_c(in);
+    std::vector<int> own;
+    auto [est, r] = dfc_run_dist(*ctx->dev, *comm->comm, obs, dfc_cfg_from_c(c), &own);
+    {
+      CallStream cs(*ctx->dev);
+      to_c(cs.s, est, out);
     }
+    dfc_report_to_c(r, rep);
+    if (owner)
+      for (size_t i = 0; i < own.size() && static_cast<int64_t>(i) < owner_cap; ++i) owner[i] = own[i];
   });
 }
 

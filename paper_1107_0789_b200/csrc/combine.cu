@@ -214,14 +214,42 @@ void column_project(cudaStream_t s, const DevLowRank& basis, const std::vector<c
     const DevLowRank& B = *blocks[g];
     if (B.k == 0) continue;
     const i64 w = static_cast<i64>(groups[g].size());
-    DBuf<double> proj(kb * B.k, s), Rg(w * kb, s);
-    gemm(s, true, false, kb, B.k, m, 1.0, out.left.get(), kb, B.left.get(), B.k, 0.0, proj.get(), B.k);   // Ub^T left_g
-    gemm(s, false, true, w, kb, B.k, 1.0, B.right.get(), B.k, proj.get(), B.k, 0.0, Rg.get(), kb);       // right_g proj^T
-    DBuf<long long> idx = upload_idx(s, groups[g]);
-    scatter_rows_kernel<<<grid_for(w * kb), 256, 0, s>>>(w, kb, Rg.get(), kb, idx.get(), out.right.get(), kb);
-    DFCG_LAUNCH_CHECK();
+    DBuf<double> Rg(w * kb, s);
+    project_rows(s, out.left.get(), m, kb, B, Rg.get());
+    scatter_rows(s, Rg.get(), w, kb, groups[g], out.right.get());
   }
   DFCG_CUDA(cudaStreamSynchronize(s));
+}
+
+// One block of column_project (sketch.hpp:194-196): Rg = right_g (Ub^T left_g)^T, w_g x kb.
+// The multi-GPU combine runs it on the block's own rank; the arithmetic is the same GEMM pair.
+void project_rows(cudaStream_t s, const double* Ub, i64 m, i64 kb, const DevLowRank& B, double* Rg) {
+  if (B.m != m) throw std::invalid_argument("column_project: row count mismatch");
+  const i64 w = B.n;
+  if (B.k == 0) {
+    DFCG_CUDA(cudaMemsetAsync(Rg, 0, sizeof(double) * static_cast<size_t>(w * kb), s));
+    return;
+  }
+  DBuf<double> proj(kb * B.k, s);
+  gemm(s, true, false, kb, B.k, m, 1.0, Ub, kb, B.left.get(), B.k, 0.0, proj.get(), B.k);  // Ub^T left_g
+  gemm(s, false, true, w, kb, B.k, 1.0, B.right.get(), B.k, proj.get(), B.k, 0.0, Rg, kb);  // right_g proj^T
+}
+
+// dst[idx[p], :] = src[p, :] for the rows of one plan group (width c, row-major, ld c)
+void scatter_rows(cudaStream_t s, const double* src, i64 rows, i64 c, const std::vector<i64>& idx, double* dst) {
+  if (rows == 0 || c == 0) return;
+  DBuf<long long> d = upload_idx(s, idx);
+  scatter_rows_kernel<<<grid_for(rows * c), 256, 0, s>>>(rows, c, src, c, d.get(), dst, c);
+  DFCG_LAUNCH_CHECK();
+}
+
+// dst[p, :] = src[idx[p], :] (width c, row-major, ld c)
+void gather_rows(cudaStream_t s, const double* src, i64 c, const std::vector<i64>& idx, double* dst) {
+  const i64 l = static_cast<i64>(idx.size());
+  if (l == 0 || c == 0) return;
+  DBuf<long long> d = upload_idx(s, idx);
+  gather_rows_kernel<<<grid_for(l * c), 256, 0, s>>>(l, c, src, c, d.get(), dst, c);
+  DFCG_LAUNCH_CHECK();
 }
 
 // gen_nystrom (sketch.hpp:241-266): C W^+ R with W = C_hat restricted to the sampled rows.

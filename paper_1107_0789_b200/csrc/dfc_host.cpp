@@ -115,48 +115,135 @@ std::vector<std::vector<i64>> partition_columns(i64 n, i64 t, SeededRng& rng) {
   return groups;
 }
 
-// sampling.hpp:83-97 (entries stay column-major sorted: columns are relabelled monotonically)
-HostObs extract_columns(const HostObs& obs, const std::vector<i64>& idx) {
-  std::vector<i64> pos(static_cast<size_t>(obs.n), -1);
-  for (size_t p = 0; p < idx.size(); ++p) {
-    const i64 c = idx[p];
-    if (c < 0 || c >= obs.n) throw std::out_of_range("extract_columns: index out of range");
-    if (pos[static_cast<size_t>(c)] >= 0) throw std::invalid_argument("extract_columns: duplicate index");
-    pos[static_cast<size_t>(c)] = static_cast<i64>(p);
-  }
-  std::vector<long long> r, c;
-  std::vector<double> v;
-  for (i64 e = 0; e < obs.count(); ++e) {
-    const i64 p = pos[static_cast<size_t>(obs.col[e])];
-    if (p >= 0) {
-      r.push_back(obs.row[e]);
-      c.push_back(p);
-      v.push_back(obs.val[e]);
+// ---- D step (sampling.hpp:83-113): parallel stable bucketing of the triplets.
+// Every subproblem is a set of columns (extract_columns) or of rows (extract_rows) of the
+// observed matrix. One pass tags each entry with its subproblem and new index; chunks of the
+// entry array are counted in parallel, prefix-summed per (subproblem, chunk), and scattered in
+// parallel — each subproblem's entries keep the input's column-major order, and the column /
+// row relabelling is monotone, so every output is already a valid ObservedMatrix (sorted,
+// in range, no duplicates: inherited from the validated input) without a re-sort.
+// DFCG_DSTEP_THREADS bounds the host threads (default: hardware concurrency, at most 32).
+namespace {
+
+int dstep_threads(i64 work) {
+  static const int env = std::getenv("DFCG_DSTEP_THREADS") ? std::atoi(std::getenv("DFCG_DSTEP_THREADS")) : 0;
+  int t = env > 0 ? env : static_cast<int>(std::min(32u, std::max(1u, std::thread::hardware_concurrency())));
+  return static_cast<int>(std::max<i64>(1, std::min<i64>(t, work / (1 << 16) + 1)));
+}
+
+template <class Fn>
+void run_chunks(int nt, i64 total, Fn&& fn) {  // fn(chunk, begin, end)
+  std::vector<std::thread> th;
+  for (int c = 1; c < nt; ++c) th.emplace_back([&, c] { fn(c, total * c / nt, total * (c + 1) / nt); });
+  fn(0, 0, total / nt);
+  for (auto& x : th) x.join();
+}
+
+// subproblem definitions -> per-column / per-row (subproblem, new index) tables
+struct SubTables {
+  std::vector<int> col_sub;   // column -> column subproblem (-1: none)
+  std::vector<i64> col_pos;   // column -> index inside it
+  int row_sub = -1;           // the (single) row subproblem
+  std::vector<i64> row_pos;   // row -> index inside it (-1: not sampled)
+};
+
+SubTables make_tables(const HostObs& obs, const std::vector<std::vector<i64>>& col_groups,
+                      const std::vector<i64>* rows) {
+  SubTables t;
+  t.col_sub.assign(static_cast<size_t>(obs.n), -1);
+  t.col_pos.assign(static_cast<size_t>(obs.n), -1);
+  for (size_t g = 0; g < col_groups.size(); ++g)
+    for (size_t p = 0; p < col_groups[g].size(); ++p) {
+      const i64 c = col_groups[g][p];
+      if (c < 0 || c >= obs.n) throw std::out_of_range("extract_columns: index out of range");
+      if (t.col_sub[static_cast<size_t>(c)] >= 0) throw std::invalid_argument("extract_columns: duplicate index");
+      t.col_sub[static_cast<size_t>(c)] = static_cast<int>(g);
+      t.col_pos[static_cast<size_t>(c)] = static_cast<i64>(p);
+    }
+  if (rows) {
+    t.row_sub = static_cast<int>(col_groups.size());
+    t.row_pos.assign(static_cast<size_t>(obs.m), -1);
+    for (size_t p = 0; p < rows->size(); ++p) {
+      const i64 r = (*rows)[p];
+      if (r < 0 || r >= obs.m) throw std::out_of_range("extract_rows: index out of range");
+      if (t.row_pos[static_cast<size_t>(r)] >= 0) throw std::invalid_argument("extract_rows: duplicate index");
+      t.row_pos[static_cast<size_t>(r)] = static_cast<i64>(p);
     }
   }
-  return HostObs::make(obs.m, static_cast<i64>(idx.size()), std::move(r), std::move(c), std::move(v));
+  return t;
+}
+
+}  // namespace
+
+// Column groups (disjoint, e.g. a partition plan) and optionally one row sample, all in one
+// parallel pass. Output order: the column groups, then the row subproblem.
+std::vector<HostObs> extract_subproblems(const HostObs& obs, const std::vector<std::vector<i64>>& col_groups,
+                                         const std::vector<i64>* rows) {
+  const SubTables tb = make_tables(obs, col_groups, rows);
+  const size_t G = col_groups.size() + (rows ? 1 : 0);
+  const i64 N = obs.count();
+  const int nt = dstep_threads(N);
+  std::vector<i64> cnt(static_cast<size_t>(nt) * G, 0);  // [chunk][sub]
+  run_chunks(nt, N, [&](int c, i64 b, i64 e) {
+    i64* k = cnt.data() + static_cast<size_t>(c) * G;
+    for (i64 i = b; i < e; ++i) {
+      const int g = tb.col_sub[static_cast<size_t>(obs.col[i])];
+      if (g >= 0) ++k[g];
+      if (tb.row_sub >= 0 && tb.row_pos[static_cast<size_t>(obs.row[i])] >= 0) ++k[tb.row_sub];
+    }
+  });
+  std::vector<HostObs> out(G);
+  std::vector<i64> off(static_cast<size_t>(nt) * G);
+  for (size_t g = 0; g < G; ++g) {
+    i64 at = 0;
+    for (int c = 0; c < nt; ++c) {
+      off[static_cast<size_t>(c) * G + g] = at;
+      at += cnt[static_cast<size_t>(c) * G + g];
+    }
+    HostObs& o = out[g];
+    const bool is_row = tb.row_sub == static_cast<int>(g);
+    o.m = is_row ? static_cast<i64>(rows->size()) : obs.m;
+    o.n = is_row ? obs.n : static_cast<i64>(col_groups[g].size());
+    if (o.m < 1 || o.n < 1) throw std::invalid_argument("ObservedMatrix: dims must be positive");
+    o.row.resize(static_cast<size_t>(at));
+    o.col.resize(static_cast<size_t>(at));
+    o.val.resize(static_cast<size_t>(at));
+  }
+  run_chunks(nt, N, [&](int c, i64 b, i64 e) {
+    i64* w = off.data() + static_cast<size_t>(c) * G;
+    for (i64 i = b; i < e; ++i) {
+      const size_t col = static_cast<size_t>(obs.col[i]);
+      const int g = tb.col_sub[col];
+      if (g >= 0) {
+        HostObs& o = out[static_cast<size_t>(g)];
+        const size_t p = static_cast<size_t>(w[g]++);
+        o.row[p] = obs.row[i];
+        o.col[p] = tb.col_pos[col];
+        o.val[p] = obs.val[i];
+      }
+      if (tb.row_sub >= 0) {
+        const i64 rp = tb.row_pos[static_cast<size_t>(obs.row[i])];
+        if (rp >= 0) {
+          HostObs& o = out[static_cast<size_t>(tb.row_sub)];
+          const size_t p = static_cast<size_t>(w[tb.row_sub]++);
+          o.row[p] = rp;
+          o.col[p] = obs.col[i];
+          o.val[p] = obs.val[i];
+        }
+      }
+    }
+  });
+  return out;
+}
+
+// sampling.hpp:83-97
+HostObs extract_columns(const HostObs& obs, const std::vector<i64>& idx) {
+  return std::move(extract_subproblems(obs, {idx}, nullptr)[0]);
 }
 
 // sampling.hpp:99-113
 HostObs extract_rows(const HostObs& obs, const std::vector<i64>& idx) {
-  std::vector<i64> pos(static_cast<size_t>(obs.m), -1);
-  for (size_t p = 0; p < idx.size(); ++p) {
-    const i64 r = idx[p];
-    if (r < 0 || r >= obs.m) throw std::out_of_range("extract_rows: index out of range");
-    if (pos[static_cast<size_t>(r)] >= 0) throw std::invalid_argument("extract_rows: duplicate index");
-    pos[static_cast<size_t>(r)] = static_cast<i64>(p);
-  }
-  std::vector<long long> r, c;
-  std::vector<double> v;
-  for (i64 e = 0; e < obs.count(); ++e) {
-    const i64 p = pos[static_cast<size_t>(obs.row[e])];
-    if (p >= 0) {
-      r.push_back(p);
-      c.push_back(obs.col[e]);
-      v.push_back(obs.val[e]);
-    }
-  }
-  return HostObs::make(static_cast<i64>(idx.size()), obs.n, std::move(r), std::move(c), std::move(v));
+  return std::move(extract_subproblems(obs, {}, &idx)[0]);
 }
 
 // make_base_solver, dfc.hpp:70-78.
@@ -182,55 +269,6 @@ BaseSolver make_base_solver(DeviceContext& ctx, Task task, const ApgConfig& cfg,
 }
 
 namespace {
-
-// parallel_for, dfc.hpp:84-119 — each worker thread holds its own pooled stream.
-template <class Fn>
-void parallel_for(DeviceContext& ctx, std::size_t count, int workers, Fn&& fn) {
-  if (workers < 1) throw std::invalid_argument("parallel_for: workers must be >= 1");
-  const std::size_t nthreads = std::min<std::size_t>(static_cast<std::size_t>(workers), count);
-  std::vector<std::string> failures(count);
-  std::vector<char> failed(count, 0);
-  if (nthreads <= 1) {
-    CallStream cs(ctx);
-    for (std::size_t i = 0; i < count; ++i) {
-      try {
-        fn(i, cs.s);
-      } catch (const std::exception& e) {
-        throw BlockError(i, e.what());
-      }
-    }
-    return;
-  }
-  std::atomic<std::size_t> next{0};
-  auto worker = [&]() {
-    CallStream cs(ctx);
-    for (;;) {
-      const std::size_t i = next.fetch_add(1);
-      if (i >= count) return;
-      try {
-        fn(i, cs.s);
-      } catch (const std::exception& e) {
-        failures[i] = e.what();
-        failed[i] = 1;
-      }
-    }
-  };
-  std::vector<std::thread> pool;
-  for (std::size_t w = 0; w < nthreads; ++w) pool.emplace_back(worker);
-  for (auto& th : pool) th.join();
-  for (std::size_t i = 0; i < count; ++i)
-    if (failed[i]) throw BlockError(i, failures[i]);
-}
-
-struct PhaseClock {
-  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  double lap() {
-    const auto t1 = std::chrono::steady_clock::now();
-    const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-    t0 = t1;
-    return ms;
-  }
-};
 
 // solve_blocks, dfc.hpp:133-147.
 void solve_blocks(DeviceContext& ctx, const std::vector<HostObs>& blocks, const BaseSolver& solver, int workers,
@@ -265,6 +303,18 @@ std::vector<const DevLowRank*> ptrs(const std::vector<DevLowRank>& v) {
 
 }  // namespace
 
+// pair_deficient, dfc.hpp:272-280: rank(W) < max(rank C-hat, rank R-hat), W = C-hat's left factor
+// restricted to the sampled rows (gathered on the device) times its right factor.
+bool nys_pair_deficient(cudaStream_t s, const DevLowRank& C, const DevLowRank& R, const std::vector<i64>& row_idx) {
+  const i64 kmax = std::max(C.k, R.k);
+  if (kmax == 0 || C.k == 0) return kmax > 0;
+  const i64 d = static_cast<i64>(row_idx.size());
+  DBuf<double> W(d * C.k, s);
+  gather_rows(s, C.left.get(), C.k, row_idx, W.get());
+  SvdOfProduct f = svd_of_product(s, d, C.n, C.k, W.get(), C.right.get());
+  return f.r < kmax;
+}
+
 // median_rank, dfc.hpp:159-164.
 i64 median_rank(const std::vector<i64>& ranks) {
   if (ranks.empty()) throw std::invalid_argument("median_rank: empty list");
@@ -285,8 +335,7 @@ std::pair<DevLowRank, DfcReport> dfc_proj(DeviceContext& ctx, const HostObs& obs
   PhaseClock total, phase;
   SeededRng prng(cfg.seed, streams::partition);
   auto plan = partition_columns(obs.n, cfg.t, prng);
-  std::vector<HostObs> blocks;
-  for (const auto& g : plan) blocks.push_back(extract_columns(obs, g));
+  std::vector<HostObs> blocks = extract_subproblems(obs, plan, nullptr);
   report.divide_ms = phase.lap();
   std::vector<DevLowRank> ests;
   solve_blocks(ctx, blocks, solver, cfg.workers, ests, report.subproblems);
@@ -324,8 +373,7 @@ std::pair<DevLowRank, DfcReport> dfc_rp(DeviceContext& ctx, const HostObs& obs, 
   PhaseClock total, phase;
   SeededRng prng(cfg.seed, streams::partition);
   auto plan = partition_columns(obs.n, cfg.t, prng);
-  std::vector<HostObs> blocks;
-  for (const auto& g : plan) blocks.push_back(extract_columns(obs, g));
+  std::vector<HostObs> blocks = extract_subproblems(obs, plan, nullptr);
   report.divide_ms = phase.lap();
   std::vector<DevLowRank> ests;
   solve_blocks(ctx, blocks, solver, cfg.workers, ests, report.subproblems);
@@ -371,25 +419,13 @@ std::pair<DevLowRank, DfcReport> dfc_nys(DeviceContext& ctx, const HostObs& obs,
   std::vector<i64> row_idx = sample_without_replacement(m, cfg.d, row_rng);
   std::sort(row_idx.begin(), row_idx.end());
   auto pair_deficient = [&](cudaStream_t s, const DevLowRank& C, const DevLowRank& R) {
-    const i64 kmax = std::max(C.k, R.k);
-    if (kmax == 0 || C.k == 0) return kmax > 0;
-    const i64 d = static_cast<i64>(row_idx.size());
-    // Wleft = C.left[row_idx, :]
-    std::vector<double> hl(static_cast<size_t>(C.m * C.k)), hw(static_cast<size_t>(d * C.k));
-    DFCG_CUDA(cudaMemcpyAsync(hl.data(), C.left.get(), sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, s));
-    DFCG_CUDA(cudaStreamSynchronize(s));
-    for (i64 i = 0; i < d; ++i)
-      for (i64 c = 0; c < C.k; ++c) hw[static_cast<size_t>(i * C.k + c)] = hl[static_cast<size_t>(row_idx[i] * C.k + c)];
-    DBuf<double> W(d * C.k, s);
-    DFCG_CUDA(cudaMemcpyAsync(W.get(), hw.data(), sizeof(double) * hw.size(), cudaMemcpyHostToDevice, s));
-    SvdOfProduct f = svd_of_product(s, d, C.n, C.k, W.get(), C.right.get());
-    return f.r < kmax;
+    return nys_pair_deficient(s, C, R, row_idx);
   };
   if (!cfg.ensemble) {
     SeededRng col_rng(cfg.seed, streams::nys_cols);
     std::vector<i64> col_idx = sample_without_replacement(n, cfg.l, col_rng);
     std::sort(col_idx.begin(), col_idx.end());
-    std::vector<HostObs> blocks{extract_columns(obs, col_idx), extract_rows(obs, row_idx)};
+    std::vector<HostObs> blocks = extract_subproblems(obs, {col_idx}, &row_idx);
     report.divide_ms = phase.lap();
     std::vector<DevLowRank> ests;
     solve_blocks(ctx, blocks, solver, cfg.workers, ests, report.subproblems);
@@ -408,9 +444,7 @@ std::pair<DevLowRank, DfcReport> dfc_nys(DeviceContext& ctx, const HostObs& obs,
       std::clamp<i64>(static_cast<i64>(std::llround(static_cast<double>(n) / static_cast<double>(cfg.l))), 1, n);
   SeededRng prng(cfg.seed, streams::partition);
   auto plan = partition_columns(n, groups, prng);
-  std::vector<HostObs> blocks;
-  for (const auto& g : plan) blocks.push_back(extract_columns(obs, g));
-  blocks.push_back(extract_rows(obs, row_idx));
+  std::vector<HostObs> blocks = extract_subproblems(obs, plan, &row_idx);
   report.divide_ms = phase.lap();
   std::vector<DevLowRank> ests;
   solve_blocks(ctx, blocks, solver, cfg.workers, ests, report.subproblems);

@@ -3,7 +3,10 @@
 // device; estimates stay resident in HBM between the steps.
 #pragma once
 
+#include <atomic>
+#include <chrono>
 #include <functional>
+#include <thread>
 #include <string>
 #include <utility>
 #include <vector>
@@ -65,13 +68,75 @@ struct DfcReport {
 using BaseSolver = std::function<std::pair<DevLowRank, SolveReport>(const HostObs&, cudaStream_t)>;
 BaseSolver make_base_solver(DeviceContext& ctx, Task task, const ApgConfig& cfg, double lambda = 0.0);
 
+// parallel_for, dfc.hpp:84-119 — each worker thread holds its own pooled stream.
+template <class Fn>
+void parallel_for(DeviceContext& ctx, std::size_t count, int workers, Fn&& fn) {
+  if (workers < 1) throw std::invalid_argument("parallel_for: workers must be >= 1");
+  const std::size_t nthreads = std::min<std::size_t>(static_cast<std::size_t>(workers), count);
+  std::vector<std::string> failures(count);
+  std::vector<char> failed(count, 0);
+  if (nthreads <= 1) {
+    CallStream cs(ctx);
+    for (std::size_t i = 0; i < count; ++i) {
+      try {
+        fn(i, cs.s);
+      } catch (const std::exception& e) {
+        throw BlockError(i, e.what());
+      }
+    }
+    return;
+  }
+  std::atomic<std::size_t> next{0};
+  auto worker = [&]() {
+    CallStream cs(ctx);
+    for (;;) {
+      const std::size_t i = next.fetch_add(1);
+      if (i >= count) return;
+      try {
+        fn(i, cs.s);
+      } catch (const std::exception& e) {
+        failures[i] = e.what();
+        failed[i] = 1;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (std::size_t w = 0; w < nthreads; ++w) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  for (std::size_t i = 0; i < count; ++i)
+    if (failed[i]) throw BlockError(i, failures[i]);
+}
+
+struct PhaseClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double lap() {
+    const auto t1 = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t0 = t1;
+    return ms;
+  }
+};
+
 std::vector<i64> sample_without_replacement(i64 n, i64 l, SeededRng& rng);
 std::vector<std::vector<i64>> partition_columns(i64 n, i64 t, SeededRng& rng);
 HostObs extract_columns(const HostObs& obs, const std::vector<i64>& idx);
+// The D step's extraction of every subproblem in one parallel pass: disjoint column groups,
+// then (rows != nullptr) one row sample (extract_rows). Same outputs as the one-at-a-time calls.
+std::vector<HostObs> extract_subproblems(const HostObs& obs, const std::vector<std::vector<i64>>& col_groups,
+                                         const std::vector<i64>* rows);
 HostObs extract_rows(const HostObs& obs, const std::vector<i64>& idx);
 i64 median_rank(const std::vector<i64>& ranks);
+bool nys_pair_deficient(cudaStream_t s, const DevLowRank& C, const DevLowRank& R, const std::vector<i64>& row_idx);
 
 std::pair<DevLowRank, DfcReport> dfc_run(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg);
+
+// Multi-GPU dfc_run (one process per GPU, dist.hpp): every rank passes the same obs and cfg,
+// solves its LPT share of the subproblems and joins the combine's exchange; every rank returns
+// the final estimate. Same arithmetic as dfc_run, so the result matches it (P/tests/test_dfc.cpp:
+// 322-342's scheduling invariance, extended to ranks).
+class Comm;
+std::pair<DevLowRank, DfcReport> dfc_run_dist(DeviceContext& ctx, Comm& comm, const HostObs& obs, const DfcConfig& cfg,
+                                              std::vector<int>* owner_out = nullptr);
 std::pair<DevLowRank, DfcReport> dfc_proj(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg,
                                           const BaseSolver& solver);
 std::pair<DevLowRank, DfcReport> dfc_rp(DeviceContext& ctx, const HostObs& obs, const DfcConfig& cfg,

@@ -158,6 +158,37 @@ int dfcg_partition_columns(uint64_t seed, uint64_t stream, int64_t n, int64_t t,
   });
 }
 
+int dfcg_extract_subproblems(const dfcg_obs* in, int64_t ngroups, const int64_t* group_offsets,
+                             const int64_t* group_cols, int64_t nrows, const int64_t* rows, int64_t* counts,
+                             int64_t** out_rows, int64_t** out_cols, double** out_vals) {
+  return dfcg_guard_call([&] {
+    if (!in || !counts || !out_rows || !out_cols || !out_vals || (ngroups > 0 && (!group_offsets || !group_cols)) ||
+        (nrows > 0 && !rows))
+      throw std::invalid_argument("dfcg_extract_subproblems: null argument");
+    HostObs obs = HostObs::make(in->m, in->n, std::vector<long long>(in->row, in->row + in->nnz),
+                                std::vector<long long>(in->col, in->col + in->nnz),
+                                std::vector<double>(in->val, in->val + in->nnz));
+    std::vector<std::vector<i64>> groups(static_cast<size_t>(ngroups));
+    for (int64_t g = 0; g < ngroups; ++g) groups[g].assign(group_cols + group_offsets[g], group_cols + group_offsets[g + 1]);
+    std::vector<i64> r(rows, rows + std::max<int64_t>(nrows, 0));
+    std::vector<HostObs> subs = extract_subproblems(obs, groups, nrows > 0 ? &r : nullptr);
+    size_t total = 0;
+    for (const auto& o : subs) total += o.val.size();
+    *out_rows = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<size_t>(1, total)));
+    *out_cols = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<size_t>(1, total)));
+    *out_vals = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(1, total)));
+    if (!*out_rows || !*out_cols || !*out_vals) throw std::bad_alloc();
+    size_t at = 0;
+    for (size_t i = 0; i < subs.size(); ++i) {
+      counts[i] = static_cast<int64_t>(subs[i].val.size());
+      std::memcpy(*out_rows + at, subs[i].row.data(), sizeof(int64_t) * subs[i].val.size());
+      std::memcpy(*out_cols + at, subs[i].col.data(), sizeof(int64_t) * subs[i].val.size());
+      std::memcpy(*out_vals + at, subs[i].val.data(), sizeof(double) * subs[i].val.size());
+      at += subs[i].val.size();
+    }
+  });
+}
+
 // BASELINE configs[3] (c4) stand-in — recommender-shaped matrix completion, which the
 // reference's generators cannot produce: m x n with Zipf(s = 1) row and column
 // popularity (the Zipf ranks assigned by random permutations), cells drawn with probability

@@ -126,6 +126,9 @@ SvdOfProduct svd_of_product(cudaStream_t s, i64 m, i64 n, i64 k, const double* l
                             double rel_cutoff = 1e-12);
 void column_project(cudaStream_t s, const DevLowRank& basis, const std::vector<const DevLowRank*>& blocks,
                     const std::vector<std::vector<i64>>& groups, i64 n, DevLowRank& out);
+void project_rows(cudaStream_t s, const double* Ub, i64 m, i64 kb, const DevLowRank& block, double* Rg);
+void scatter_rows(cudaStream_t s, const double* src, i64 rows, i64 c, const std::vector<i64>& idx, double* dst);
+void gather_rows(cudaStream_t s, const double* src, i64 c, const std::vector<i64>& idx, double* dst);
 void gen_nystrom(cudaStream_t s, const DevLowRank& C, const DevLowRank& R, const std::vector<i64>& rows,
                  const std::vector<i64>& cols, DevLowRank& out);
 void average_estimates(cudaStream_t s, const std::vector<const DevLowRank*>& ests, std::optional<i64> recompress_to,

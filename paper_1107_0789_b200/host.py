@@ -56,6 +56,41 @@ def partition_columns(seed, stream, n, t):
     return [cols[offs[g]:offs[g + 1]].copy() for g in range(t)]
 
 
+def extract_subproblems(obs: Observed, groups, rows=None):
+    """libdfcg's D step (dfcg_extract_subproblems): the column groups, then the row sample, in
+    one parallel pass — what dfc_run extracts (P/include/dfc/sampling.hpp:83-113)."""
+    from ._lib import ObsC, _Keep, _obs_in
+
+    keep = _Keep()
+    o = _obs_in(obs, keep)
+    offs = np.zeros(len(groups) + 1, np.int64)
+    offs[1:] = np.cumsum([len(g) for g in groups])
+    cols = np.ascontiguousarray(np.concatenate([np.asarray(g, np.int64) for g in groups]) if groups else
+                                np.zeros(1, np.int64))
+    rr = np.ascontiguousarray(np.asarray(rows if rows is not None else [0], np.int64))
+    nsub = len(groups) + (rows is not None)
+    counts = np.zeros(max(nsub, 1), np.int64)
+    pr, pc, pv = i64ptr(), i64ptr(), C.POINTER(C.c_double)()
+    _check(lib().dfcg_extract_subproblems(C.byref(o), i64(len(groups)), _i(offs), _i(cols),
+                                          i64(len(rows) if rows is not None else 0), _i(rr), _i(counts),
+                                          C.byref(pr), C.byref(pc), C.byref(pv)))
+    total = int(counts[:nsub].sum())
+    R = np.ctypeslib.as_array(pr, (max(total, 1),))[:total].copy()
+    Cc = np.ctypeslib.as_array(pc, (max(total, 1),))[:total].copy()
+    V = np.ctypeslib.as_array(pv, (max(total, 1),))[:total].copy()
+    for p in (pr, pc, pv):
+        lib().dfcg_free(p)
+    out, at = [], 0
+    for i in range(nsub):
+        c = int(counts[i])
+        is_row = rows is not None and i == nsub - 1
+        m = len(rows) if is_row else obs.m
+        n = obs.n if is_row else len(groups[i])
+        out.append(Observed(m, n, R[at:at + c], Cc[at:at + c], V[at:at + c]))
+        at += c
+    return out
+
+
 def extract_columns(obs: Observed, idx) -> Observed:
     """extract_columns (P/include/dfc/sampling.hpp:83-97), vectorised."""
     idx = np.asarray(idx, np.int64)

@@ -20,7 +20,12 @@ Lᵀ·X (w x 16) for X = SeededRng(PROBE_SEED, 0) normals (m x 16, column-major)
 Frobenius norms. ||(L_gpu - L_oracle)ᵀ X||_F / ||L_oracleᵀ X||_F estimates the relative
 Frobenius error (E||EᵀX||² = 16 ||E||_F²) without committing the m x k factors.
 
-usage: python tests/golden/make_fixtures.py c2_window|c3_block [--iters N] [--threads T]
+  base_full: the reference's "Base" method (apg_mc on the WHOLE matrix, P/include/dfc/bench.hpp:
+             211-217) at BASELINE c2 (10000 x 10000, 1e7 observations), default ApgConfig, the
+             first ITERS iterations (ranks 1 .. ~1450; the next iteration jumps to k ~ 5800,
+             beyond what the oracle finishes in minutes).
+
+usage: python tests/golden/make_fixtures.py c2_window|c3_block|base_full [--iters N] [--threads T]
 """
 from __future__ import annotations
 
@@ -69,14 +74,17 @@ def fro_lowrank(left, right) -> float:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c2_window", "c3_block"])
+    ap.add_argument("which", choices=["c2_window", "c3_block", "base_full"])
     ap.add_argument("--iters", type=int, default=45)
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     O.lib().orc_set_blas_threads(args.threads)
     t0 = time.time()
-    if args.which == "c2_window":
-        blk = c2_block0()
+    if args.which in ("c2_window", "base_full"):
+        if args.which == "c2_window":
+            blk = c2_block0()
+        else:
+            L0, blk = O.gen_mc_instance(10000, 10000, 10, 10_000_000, 0.1, 1)
         run = O.McRun(blk)
         trace = []
         for i in range(args.iters):
@@ -85,12 +93,12 @@ def main():
                   f"k {trace[-1]['k_final']} calls {trace[-1]['svd_calls']}", flush=True)
         est, rep = run.finish()
         X = probes(blk.m)
-        out = dict(which="c2_window", m=blk.m, n=blk.n, nnz=blk.count, iters=args.iters, trace=trace,
+        out = dict(which=args.which, m=blk.m, n=blk.n, nnz=blk.count, iters=args.iters, trace=trace,
                    report=dict(iterations=rep.iterations, rank=rep.rank, objective=rep.objective,
                                residual=rep.residual),
                    fro_L=fro_lowrank(est.left, est.right),
                    sigma=np.linalg.norm(est.right, axis=0).tolist())
-        np.save(os.path.join(HERE, "c2_window_LtX.npy"), sketch(est.left, est.right, X))
+        np.save(os.path.join(HERE, f"{args.which}_LtX.npy"), sketch(est.left, est.right, X))
     else:
         M = c3_block0()
         lam = 1.0 / np.sqrt(max(M.shape))

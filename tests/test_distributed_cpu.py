@@ -1,13 +1,21 @@
-"""Multi-process (world_size 2, gloo, CPU) check of the sharded DFC-Proj host logic:
-blocks sharded over ranks, per-rank F step, basis broadcast, per-rank projection, row gather.
-Compute is the CPU oracle here (the GPU path plugs the C ABI into the same functions)."""
+"""Multi-rank host logic of libdfcg's distributed path on CPU (no GPU needed):
+
+* the LPT assignment every rank computes (dfcg_assign_blocks) against a plain restatement;
+* the host-callback transport (dfcg_comm_init_host) at world size 2 and 3 over gloo: every root
+  broadcasts, a ring of point-to-point messages — the traffic the distributed combine sends
+  through it (csrc/dist.cpp), driven through the C ABI from torch.distributed callbacks.
+
+The distributed dfc_run itself (same result as the single-process dfc_run) needs device
+memory: tests/test_gpu_dist.py runs it with two ranks sharing one GPU over this transport, and
+with NCCL at world size 1.
+"""
 import os
 import socket
 
 import numpy as np
 import pytest
 
-import oracle as O
+from paper_1107_0789_b200.distributed import Comm, assign_blocks
 
 
 def _free_port():
@@ -18,95 +26,57 @@ def _free_port():
     return port
 
 
-def _svd_basis(est):
-    # svd_of_product(left, right).U with the reference's numerical-rank cutoff (sketch.hpp:73-86)
-    if est.rank == 0:
-        return np.zeros((est.left.shape[0], 0))
-    ql, rl = np.linalg.qr(est.left)
-    qr, rr = np.linalg.qr(est.right)
-    u, s, _ = np.linalg.svd(rl @ rr.T)
-    keep = int(np.sum(s > 1e-12 * max(est.left.shape[0], est.right.shape[0]) * s[0]))
-    return ql @ u[:, :keep]
+def lpt_reference(nnz, nranks):
+    order = sorted(range(len(nnz)), key=lambda g: (-nnz[g], g))
+    load, count, owner = [0] * nranks, [0] * nranks, [0] * len(nnz)
+    for g in order:
+        best = min(range(nranks), key=lambda q: (load[q], count[q], q))
+        owner[g] = best
+        load[best] += max(nnz[g], 0)
+        count[best] += 1
+    return owner
 
 
-def _project(Ub, est):
-    if est.rank == 0:
-        return np.zeros((est.right.shape[0], Ub.shape[1]))
-    return est.right @ (Ub.T @ est.left).T
+def test_lpt_assignment_matches_restatement():
+    rng = np.random.default_rng(5)
+    cases = [[5, 5, 5, 5], [0, 0, 7], [1250000] * 8, list(rng.zipf(1.5, 64)), list(rng.integers(0, 10**7, 13))]
+    for nnz in cases:
+        for nranks in (1, 2, 3, 4, 8):
+            got = assign_blocks(nnz, nranks)
+            assert got == lpt_reference(list(map(int, nnz)), nranks), (nnz, nranks)
+            assert all(0 <= o < nranks for o in got)
+    # balanced c2 shape: 8 equal blocks over 8, 4, 2 ranks -> equal counts per rank
+    for nranks in (2, 4, 8):
+        got = assign_blocks([1250000] * 8, nranks)
+        assert sorted(np.bincount(got, minlength=nranks)) == [8 // nranks] * nranks
+    # Zipf-skewed blocks: LPT's makespan within 4/3 of the lower bound
+    nnz = [int(x) for x in np.random.default_rng(9).zipf(1.3, 64) * 1000]
+    for nranks in (2, 4, 8):
+        got = assign_blocks(nnz, nranks)
+        loads = np.bincount(got, weights=nnz, minlength=nranks)
+        assert loads.max() <= 4 / 3 * max(sum(nnz) / nranks, max(nnz)) + 1
+    with pytest.raises(ValueError):
+        assign_blocks([1, 2], 0)
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_dir):
     import torch.distributed as dist
-
-    from paper_1107_0789_b200.distributed import column_project_distributed, shard
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    L0, obs = O.gen_mc_instance(120, 90, 3, 5000, 0.1, 3, 0)
-    t, seed = 4, 5
-    groups = O.partition_columns(seed, 0xDFC0000000000001, 90, t)
-    local = {}
-    for g in shard(t, world, rank):
-        blk = O.extract_columns(obs, groups[g])
-        local[g], _ = O.apg_mc(blk)
-    res = column_project_distributed(dist, groups, local, 120, _svd_basis, _project)
-    if rank == 0:
-        ref, _ = O.dfc_run(obs, "proj", t=t, seed=seed)
-        got = res[0] @ res[1].T
-        err = np.linalg.norm(got - ref.dense()) / np.linalg.norm(ref.dense())
-        with open(out_path, "w") as f:
-            f.write(repr(float(err)))
+    comm = Comm.host()
+    bad = comm.selftest()
+    comm.close()
+    with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as f:
+        f.write(str(bad))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_sharded_dfc_proj_matches_single_process(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_transport_through_c_abi(tmp_path, world):
     import torch.multiprocessing as mp
 
-    out = str(tmp_path / "err.txt")
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
-    err = float(open(out).read())
-    assert err < 1e-10, err
-
-
-def _worker_nys(rank, world, port, out_path):
-    import torch.distributed as dist
-
-    from paper_1107_0789_b200.distributed import nystrom_distributed, shard
-
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    m, n, l, d, seed = 120, 90, 30, 40, 5
-    L0, obs = O.gen_mc_instance(m, n, 3, 5000, 0.1, 3, 0)
-    # dfc_nys's D step (P/include/dfc/dfc.hpp:250-290): sorted row / column samples
-    rows = np.sort(O.sample_without_replacement(seed, 0xDFC0000000000002, m, d))
-    cols = np.sort(O.sample_without_replacement(seed, 0xDFC0000000000003, n, l))
-    subs = {0: lambda: O.extract_columns(obs, cols), 1: lambda: O.extract_rows(obs, rows)}
-    local = {g: O.apg_mc(subs[g]())[0] for g in shard(2, world, rank)}
-    res = nystrom_distributed(dist, local, rows, cols, O.gen_nystrom, O.Estimate)
-    if rank == 0:
-        ref, _ = O.dfc_run(obs, "nys", l=l, d=d, seed=seed)
-        err = np.linalg.norm(res.dense() - ref.dense()) / np.linalg.norm(ref.dense())
-        with open(out_path, "w") as f:
-            f.write(repr(float(err)))
-    dist.barrier()
-    dist.destroy_process_group()
-
-
-def test_sharded_dfc_nys_matches_single_process(tmp_path):
-    """DFC-Nys with its two subproblems on two ranks (R-hat's factors broadcast to rank 0)."""
-    import torch.multiprocessing as mp
-
-    out = str(tmp_path / "err.txt")
-    mp.spawn(_worker_nys, args=(2, _free_port(), out), nprocs=2, join=True)
-    err = float(open(out).read())
-    assert err < 1e-10, err
-
-
-def test_shard_covers_blocks_once():
-    from paper_1107_0789_b200.distributed import shard
-
-    for t in (1, 4, 8, 64):
-        for world in (1, 2, 4, 8):
-            got = sorted(g for r in range(world) for g in shard(t, world, r))
-            assert got == list(range(t))
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert open(tmp_path / f"r{r}.txt").read() == "0", r

@@ -70,6 +70,7 @@ def test_bench_multi_rank_path_on_one_gpu():
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["gpu_launches"] > 0
+    assert sorted(set(line["e2e"]["owner"])) == [0, 1]  # LPT shares: both ranks solve blocks
 
 
 def test_device_normal_stream_matches_reference_rng():

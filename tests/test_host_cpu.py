@@ -192,3 +192,32 @@ def test_sample_without_replacement_sparse_path_identical(n, l, monkeypatch):
     sparse = P.sample_without_replacement(11, 3, n, l)
     assert np.array_equal(dense, sparse)
     assert np.array_equal(dense, O.sample_without_replacement(11, 3, n, l))
+
+
+def test_dstep_parallel_extraction_matches_oracle():
+    """libdfcg's D step (extract_subproblems: every column group of a partition plan plus a row
+    sample in one parallel stable pass) equals the oracle's extract_columns / extract_rows
+    (P/include/dfc/sampling.hpp:83-113), entry for entry and in order, at several thread counts."""
+    import os
+
+    L0, obs = P.gen_mc_instance(300, 260, 3, 30000, 0.1, 6)
+    oo = O.Observed(obs.m, obs.n, obs.rows, obs.cols, obs.vals)
+    groups = P.partition_columns(6, 0xDFC0000000000001, obs.n, 7)
+    rows = np.sort(P.sample_without_replacement(6, 0xDFC0000000000002, obs.m, 70))
+    for threads in ("1", "3", "8"):
+        os.environ["DFCG_DSTEP_THREADS"] = threads  # read once per process: first value wins
+        subs = P.extract_subproblems(obs, groups, rows)
+        assert len(subs) == 8
+        for g, s in enumerate(subs[:-1]):
+            ref = O.extract_columns(oo, groups[g])
+            assert (s.m, s.n) == (ref.m, ref.n)
+            assert np.array_equal(s.rows, ref.rows) and np.array_equal(s.cols, ref.cols)
+            assert np.array_equal(s.vals, ref.vals)
+        ref = O.extract_rows(oo, rows)
+        assert np.array_equal(subs[-1].rows, ref.rows) and np.array_equal(subs[-1].cols, ref.cols)
+        assert np.array_equal(subs[-1].vals, ref.vals)
+    assert sum(s.count for s in subs[:-1]) == obs.count
+    with pytest.raises(ValueError):
+        P.extract_subproblems(obs, [[0, 1], [1, 2]])  # overlapping groups
+    with pytest.raises(IndexError):
+        P.extract_subproblems(obs, [[0, obs.n]])
