@@ -222,6 +222,46 @@ def rmf_c3(P, device):
                      "shrink_kernel = the fused RMF elementwise pass (algorithmic bytes / event time)")
 
 
+def base_apg_window(P, obs, skip=26, win=20):
+    """The metric's second half, "base-APG iters/s at 10k x 10k": the reference's Base method
+    (apg_mc on the WHOLE matrix, no partition; P/include/dfc/bench.hpp:211-217) on the c2
+    instance, default ApgConfig, one GPU (one subproblem, replicas only). The
+    first `skip` iterations (ranks 1 -> ~3600, including the k ~ 7000 transients of iterations 14,
+    25 and 26) run untimed; iterations skip+1 .. skip+win (rank ~3500 -> ~3300, every iteration
+    on the dense operator 10^4 x 10^4) are timed with CUDA events, then one more iteration is
+    profiled per op class."""
+    import torch
+
+    sv = P.McSolver(obs)
+    t0 = time.perf_counter()
+    sv.step(skip)
+    torch.cuda.synchronize()
+    pro_s = time.perf_counter() - t0
+    w0 = P.work_counters()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    done, tr = sv.step(win, trace=True)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    roof = step_roofline(w0, P.work_counters(), ms, max(done, 1), *measured_peaks())
+    P.prof_enable(True)
+    sv.step(1)
+    prof = P.prof_collect()
+    P.prof_enable(False)
+    sv.close()
+    per_op = {k: dict(ms=round(v["ms"], 2), launches=v["launches"],
+                      tflops=round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 2))
+              for k, v in prof.items() if v["launches"] > 0}
+    return dict(value=done / (ms * 1e-3), unit="iterations/s", ms_per_iteration=ms / max(done, 1),
+                window=f"iterations {skip + 1}..{skip + done} of apg_mc on the full 10000x10000 c2 matrix "
+                       f"({obs.count} observations), default ApgConfig",
+                ranks=[t["rank"] for t in tr], prologue_s=round(pro_s, 1),
+                achieved_tflops=roof["achieved"], frac=roof["frac"], per_op_one_iteration=per_op,
+                note="one subproblem: the Base method (bench.hpp:211-217); frac = tensor-path FLOPs of the window / "
+                     "window device time against the measured FP64 DMMA peak")
+
+
 def lowrank_window(P, block, wl, skip=60, win=20):
     import math
 
@@ -534,9 +574,11 @@ def main():
     if rank == 0 and not args.no_lowrank:
         lowrank = lowrank_window(P, blocks[0], wl)
 
-    # the other BASELINE F-step configurations on this GPU (rank 0, N = 1): DFC-Nys at c2, c3
-    nys = rmf = None
+    # the other BASELINE F-step configurations on this GPU (rank 0, N = 1): base APG on the
+    # whole matrix, DFC-Nys at c2, c3
+    nys = rmf = base = None
     if rank == 0 and world == 1 and not args.no_extra and args.workload == "c2":
+        base = base_apg_window(P, obs)
         nys = nys_run(P, obs, wl)
         rmf = rmf_c3(P, local)
 
@@ -570,7 +612,7 @@ def main():
                                  note="DFC-Proj column_project of the 8 block estimates (N = 1: host factors in and "
                                       "out, device_ops = CUDA-event time per op class; N > 1: the combine phase of "
                                       "dfc_run_dist, basis broadcast + projected-row gather)"),
-                    lowrank=lowrank, nys_c2=nys, rmf_c3=rmf)
+                    lowrank=lowrank, base_apg=base, nys_c2=nys, rmf_c3=rmf)
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()

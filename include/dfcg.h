@@ -178,6 +178,13 @@ int dfcg_svd_of_product(dfcg_ctx* ctx, const dfcg_lowrank* in, dfcg_lowrank* out
  * (stream_id 0: apg_mc, 1: apg_rmf; P/include/dfc/solvers.hpp:263,344) copied to host out[n]. */
 int dfcg_normals_fetch(dfcg_ctx* ctx, int stream_id, int64_t pos, int64_t n, double* out);
 
+/* Diagnostics: the APG-MC iteration's sparse kernels on the observed set `in` with random dense
+ * operands — forward SpMM (R X, X n x b), transposed SpMM (R^T Q, Q m x b), SDDMM residual at
+ * rank kY — each timed over `reps` calls with CUDA events (ms3: ms per call) and the sum of its
+ * output (sum3). spmm_mode / sddmm_mode: 1 slab kernels, 0 the previous kernels, -1 default. */
+int dfcg_bench_sparse(dfcg_ctx* ctx, const dfcg_obs* in, int64_t b, int64_t kY, int32_t reps, int32_t spmm_mode,
+                      int32_t sddmm_mode, double* ms3, double* sum3);
+
 /* One block of the DFC-Proj combine, for the multi-GPU split of column_project
  * (sketch.hpp:194-196): Rg = block.right (Ub^T block.left)^T, Ub m x kb column-major, Rg
  * (block.n x kb, column-major) written to a caller buffer. */

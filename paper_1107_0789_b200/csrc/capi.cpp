@@ -206,6 +206,76 @@ int dfcg_normals_fetch(dfcg_ctx* ctx, int stream_id, int64_t pos, int64_t n, dou
   });
 }
 
+// Diagnostics: the per-iteration sparse kernels on one observed set, CUDA-event timed.
+int dfcg_bench_sparse(dfcg_ctx* ctx, const dfcg_obs* in, int64_t b, int64_t kY, int32_t reps, int32_t spmm_mode,
+                      int32_t sddmm_mode, double* ms3, double* sum3) {
+  return guard([&] {
+    if (!ctx || !in || !ms3 || !sum3 || b < 1 || kY < 1 || reps < 1)
+      throw std::invalid_argument("dfcg_bench_sparse: bad argument");
+    HostObs obs = HostObs::make(in->m, in->n, std::vector<long long>(in->row, in->row + in->nnz),
+                                std::vector<long long>(in->col, in->col + in->nnz),
+                                std::vector<double>(in->val, in->val + in->nnz));
+    CallStream cs(*ctx->dev);
+    const cudaStream_t s = cs.s;
+    DevOmega om;
+    om.build(s, obs.m, obs.n, obs.count(), obs.row.data(), obs.col.data(), obs.val.data());
+    auto fill = [&](i64 count, std::uint64_t seed) {
+      std::vector<double> h(static_cast<size_t>(count));
+      std::uint64_t x = seed;
+      for (auto& v : h) {
+        x = x * 6364136223846793005ULL + 1442695040888963407ULL;
+        v = static_cast<double>(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+      }
+      DBuf<double> d(count, s);
+      DFCG_CUDA(cudaMemcpyAsync(d.get(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
+      DFCG_CUDA(cudaStreamSynchronize(s));
+      return d;
+    };
+    DBuf<double> X = fill(obs.n * b, 1), Q = fill(obs.m * b, 2), Yl = fill(obs.m * kY, 3), Yr = fill(obs.n * kY, 4);
+    DBuf<double> outm(obs.m * b, s), outn(obs.n * b, s), r(std::max<i64>(1, obs.count()), s);
+    set_sparse_modes(spmm_mode, sddmm_mode);
+    cudaEvent_t e0, e1;
+    DFCG_CUDA(cudaEventCreate(&e0));
+    DFCG_CUDA(cudaEventCreate(&e1));
+    auto timed = [&](auto&& fn) {
+      fn();  // warm-up (and the one-time attribute opt-ins)
+      DFCG_CUDA(cudaEventRecord(e0, s));
+      for (int i = 0; i < reps; ++i) fn();
+      DFCG_CUDA(cudaEventRecord(e1, s));
+      DFCG_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      DFCG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      return static_cast<double>(ms) / reps;
+    };
+    auto total = [&](const DBuf<double>& d, i64 count) {
+      std::vector<double> h(static_cast<size_t>(count));
+      DFCG_CUDA(cudaMemcpyAsync(h.data(), d.get(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+      DFCG_CUDA(cudaStreamSynchronize(s));
+      double t = 0;
+      for (double v : h) t += v;
+      return t;
+    };
+    try {
+      ms3[0] = timed([&] { spmm(s, om, false, om.m_csr.get(), b, 1.0, X.get(), b, 0.0, outm.get(), b); });
+      sum3[0] = total(outm, obs.m * b);
+      ms3[1] = timed([&] {
+        spmm(s, om, true, om.m_csr.get(), b, 1.0, Q.get(), b, 0.0, outn.get(), b, om.m_csc.get());
+      });
+      sum3[1] = total(outn, obs.n * b);
+      ms3[2] = timed([&] { sddmm_residual(s, om, kY, Yl.get(), kY, Yr.get(), kY, om.m_csr.get(), r.get()); });
+      sum3[2] = total(r, obs.count());
+    } catch (...) {
+      set_sparse_modes(-1, -1);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
+    }
+    set_sparse_modes(-1, -1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
 void dfcg_ctx_destroy(dfcg_ctx* ctx) {
   if (!ctx) return;
   delete ctx->dev;

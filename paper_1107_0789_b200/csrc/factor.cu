@@ -18,6 +18,7 @@
 #include <numeric>
 
 #include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 
@@ -418,50 +419,26 @@ __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
 
 // In-place blocked Cholesky of G (n x n) -> upper R (lower part zeroed); Rinv = R^-1.
 // want_inverse == false: only R is produced and Rinv's contents are unspecified (scratch).
-// The look-ahead helper stream and its two events are leased from a per-device pool for the
-// duration of one factorisation (worker threads come and go with every dfc_run / combine;
-// the pool holds at most as many helpers as factorisations ever ran concurrently).
+// The look-ahead helper stream and its two events belong to the calling stream: one helper per
+// main stream, created on first use and kept for the process (main streams are pooled by the
+// DeviceContext and the solvers, so the helper count is bounded by theirs, whichever host threads
+// come and go). A helper shared between solves would queue one solve's potrf behind another's.
 struct AuxStream {
   cudaStream_t s = nullptr;
   cudaEvent_t updated = nullptr, factored = nullptr;
 };
-class AuxLease {
- public:
-  explicit AuxLease(int dev) : dev_(dev) {
-    {
-      std::lock_guard<std::mutex> lock(mu());
-      auto& fl = free_list(dev);
-      if (!fl.empty()) {
-        a_ = fl.back();
-        fl.pop_back();
-        return;
-      }
-    }
-    DFCG_CUDA(cudaStreamCreateWithFlags(&a_.s, cudaStreamNonBlocking));
-    DFCG_CUDA(cudaEventCreateWithFlags(&a_.updated, cudaEventDisableTiming));
-    DFCG_CUDA(cudaEventCreateWithFlags(&a_.factored, cudaEventDisableTiming));
+AuxStream& aux_for(cudaStream_t main) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, AuxStream> helpers;  // node-based: references stay valid
+  std::lock_guard<std::mutex> lock(mu);
+  AuxStream& a = helpers[main];
+  if (!a.s) {
+    DFCG_CUDA(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
+    DFCG_CUDA(cudaEventCreateWithFlags(&a.updated, cudaEventDisableTiming));
+    DFCG_CUDA(cudaEventCreateWithFlags(&a.factored, cudaEventDisableTiming));
   }
-  ~AuxLease() {
-    // work still queued on the helper stays ordered: the next lessee's launches queue behind it
-    std::lock_guard<std::mutex> lock(mu());
-    free_list(dev_).push_back(a_);
-  }
-  AuxLease(const AuxLease&) = delete;
-  AuxLease& operator=(const AuxLease&) = delete;
-  AuxStream& get() { return a_; }
-
- private:
-  static std::mutex& mu() {
-    static std::mutex m;
-    return m;
-  }
-  static std::vector<AuxStream>& free_list(int dev) {
-    static std::vector<AuxStream> lists[64];
-    return lists[dev_bit(dev) ? dev : 0];
-  }
-  int dev_;
-  AuxStream a_;
-};
+  return a;
+}
 
 void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol,
                           int* fail, bool want_inverse) {
@@ -486,8 +463,7 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   // Look-ahead: after the panel TRSM of block k, the next diagonal block is updated first and
   // factored on a helper stream while the rest of the trailing update runs on s, so the
   // latency-bound 64x64 potrf overlaps the trailing GEMM instead of following it.
-  AuxLease aux_lease(dev);
-  AuxStream& aux = aux_lease.get();
+  AuxStream& aux = aux_for(s);
   auto potrf = [&](cudaStream_t st, i64 k0, int kb) {
     prof::Scope scope(prof::kCholesky, st, kb * kb * kb / 3.0 + kb * kb * kb / 3.0, 16.0 * kb * kb);
     pdl_launch(potrf_diag_kernel, dim3(1), dim3(256), kPotrfSmem, st, kb, G + k0 * ldg + k0, ldg,

@@ -15,6 +15,10 @@ namespace dfcg {
 namespace {
 
 constexpr int kSpmmCpl = 4;
+constexpr int SLAB_WARPS = 16;  // warps per CTA of the slab SpMM / SDDMM kernels
+
+// kernel-choice overrides for the microbenchmark entry (dfcg_bench_sparse); -1: environment
+std::atomic<int> g_spmm_mode{-1}, g_sddmm_mode{-1};
 
 int pow2_at_least(i64 v) {
   int g = 1;
@@ -100,103 +104,146 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
   }
 }
 
-// Tiled SpMM (experimental, see spmm()) for sketches up to 64 columns: out[o, :] (+)= alpha sum_e v_e X[idx_e, :] over the
-// entries e of outer line o (a CSR row for R X, a CSC column for R^T X). One CTA per 128 outer
-// lines (16 warps x 8 lines, accumulators in registers: lane l holds columns l and l + 32) and
-// one chunk of the inner dimension; the chunk's X rows stream through shared memory 256 at a
-// time, so X is read from L2 once per 128 lines instead of once per entry (the segmented kernel
-// gathers a b-wide X row per entry: L2-bound, ~10% of the HBM roofline at the c5 block). Each
-// line's entries of a 256-row X slab are one contiguous range of the per-line 64-tile table.
-// Deterministic: a line's entries are summed in storage order; chunk partials (ws, when the
-// inner dimension is split for parallelism) are combined in chunk order by spmm_chunk_reduce.
-constexpr int TSP_LINES = 8, TSP_WARPS = 16, TSP_OB = TSP_LINES * TSP_WARPS, TSP_SLAB = 256;
-
-__global__ void __launch_bounds__(TSP_WARPS * 32)
-    spmm_tile_kernel(i64 n_outer, i64 n_inner, int nt, const int* __restrict__ tptr, const int* __restrict__ idx,
-                     const double* __restrict__ vals, int b, double alpha, const double* __restrict__ X, i64 ldx,
-                     double beta, double* __restrict__ out, i64 ldo, int chunk_tiles, double* __restrict__ ws) {
-  extern __shared__ double xs[];  // [TSP_SLAB][b]
+// Slab SpMM for sketches of b <= 64 columns: out[o, :] (+)= alpha sum_e v_e X[idx_e, :] over the
+// entries e of outer line o (a CSR row for R X, a CSC column for R^T X).
+//
+// Why: the segmented kernel gathers a b-wide row of X from L2 for every entry (N b 8 bytes of L2
+// reads, ~20x the algorithmic HBM bytes at b ~ 35; L2 throughput is only ~2x HBM on B200), so it
+// is L2-bound. Here X streams through shared memory in slabs of SB inner rows (double-buffered
+// cp.async), once per CTA of RB = 16 R outer lines, and every entry's X row is read from shared
+// memory: the X traffic from L2 drops by RB x density, the per-entry operand traffic moves to
+// shared memory (128 B/clk/SM), which bounds the kernel.
+//
+// Mapping: each warp owns R consecutive outer lines; its 32 lanes form gpw = 32 / G groups of
+// G = ceil(b / 4) lanes, lane (g, j) holding columns 4j .. 4j+3 (two 16-byte shared loads per
+// entry, conflict-free within a group). The entries of one line in the slab are loaded 32 at a
+// time, coalesced, and dealt round-robin to the groups by shuffles: group g accumulates entries
+// g, g + gpw, ... of every line (balanced to one entry; warp-uniform control flow). After the last
+// slab the groups' partial sums are added in group order (shuffles) and group 0 writes.
+// Deterministic: fixed slab order, fixed entry-to-group deal, fixed group reduction order.
+// Inner dimension split into gridDim.y chunks (whole slabs) when the outer lines alone do not
+// fill the GPU: partial results go to ws and spmm_chunk_reduce adds them in chunk order.
+template <int R>
+__global__ void __launch_bounds__(SLAB_WARPS * 32, 1)
+    spmm_slab_kernel(i64 n_outer, i64 n_inner, int nt, const int* __restrict__ tptr, const int* __restrict__ idx,
+                     const double* __restrict__ vals, int b, int G, int SB, double alpha,
+                     const double* __restrict__ X, i64 ldx, double beta, double* __restrict__ out, i64 ldo,
+                     int chunk_tiles, double* __restrict__ ws) {
+  extern __shared__ __align__(16) double xs[];  // [2][SB][BP]
+  const int BP = 4 * G;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const i64 o0 = static_cast<i64>(blockIdx.x) * TSP_OB + warp * TSP_LINES;
+  const int gpw = 32 / G, g = lane / G, j = lane - g * G;
+  const bool active = g < gpw;  // lanes past the last whole group idle in the FMA loop
+  const i64 o0 = (static_cast<i64>(blockIdx.x) * SLAB_WARPS + warp) * R;
   const int q_begin = blockIdx.y * chunk_tiles, q_end = min(nt, q_begin + chunk_tiles);
-  constexpr int TPS = TSP_SLAB / DevOmega::kTileCols;  // 64-tiles per slab
-  double acc[TSP_LINES][2];
+  const int TPS = SB / DevOmega::kTileCols;
+  const int nslab = (q_end - q_begin + TPS - 1) / TPS;
+  // lane j of a group owns columns {2j, 2j+1} and {2G+2j, 2G+2j+1}: each 16-byte shared load of a
+  // group covers one contiguous 16G-byte run of its X row (conflict-free within the group)
+  double acc[R][4];
 #pragma unroll
-  for (int r = 0; r < TSP_LINES; ++r) acc[r][0] = acc[r][1] = 0.0;
-  const bool c1 = lane + 32 < b;
-  for (int q0 = q_begin; q0 < q_end; q0 += TPS) {
-    const int q1 = min(q_end, q0 + TPS);
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+
+  auto stage = [&](int sl, int buf) {  // slab sl -> buffer buf (8-byte copies: any ldx)
+    const int q0 = q_begin + sl * TPS;
     const i64 in0 = static_cast<i64>(q0) * DevOmega::kTileCols;
-    const int rows_in = static_cast<int>(min(static_cast<i64>(q1 - q0) * DevOmega::kTileCols, n_inner - in0));
-    __syncthreads();  // the previous slab is consumed
-    // asynchronous 8-byte copies: no register round trip, every load in flight at once
-    for (int e = t; e < rows_in * b; e += blockDim.x) {
+    const int rows_in = static_cast<int>(min(static_cast<i64>(SB), n_inner - in0));
+    double* dst = xs + static_cast<size_t>(buf) * SB * BP;
+    for (int e = t; e < rows_in * b; e += SLAB_WARPS * 32) {
       const int r = e / b, c = e - r * b;
-      cp_async8(xs + e, X + (in0 + r) * ldx + c, true);
+      cp_async8(dst + r * BP + c, X + (in0 + r) * ldx + c, true);
     }
     cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    // the warp's 8 lines: slab ranges [e0, e1) via two table loads per line (lanes 0-15), and
-    // each line's first 32 entries loaded up front, one per lane (coalesced); the FMAs then take
-    // (index, value) by shuffle — no dependent global load inside the entry loop
+  };
+  if (nslab > 0) stage(0, 0);
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int q0 = q_begin + sl * TPS, q1 = min(q_end, q0 + TPS);
+    const i64 in0 = static_cast<i64>(q0) * DevOmega::kTileCols;
+    // the slab's entries of the warp's R lines, first 32 of each, loaded before the wait on the
+    // slab copy: R independent coalesced loads in flight at once
     int tv = 0;
-    if (lane < 2 * TSP_LINES) {
-      const i64 o = o0 + (lane & (TSP_LINES - 1));
-      tv = o < n_outer ? tptr[o * (nt + 1) + (lane < TSP_LINES ? q0 : q1)] : 0;
+    if (lane < 2 * R) {
+      const i64 o = o0 + (lane % R);
+      tv = o < n_outer ? tptr[o * (nt + 1) + (lane < R ? q0 : q1)] : 0;
     }
-    int e0[TSP_LINES], e1[TSP_LINES], ix0[TSP_LINES];
-    double v0[TSP_LINES];
+    int e0[R], e1[R], ix[R];
+    double v[R];
 #pragma unroll
-    for (int r = 0; r < TSP_LINES; ++r) {
+    for (int r = 0; r < R; ++r) {
       e0[r] = __shfl_sync(0xffffffffu, tv, r);
-      e1[r] = __shfl_sync(0xffffffffu, tv, TSP_LINES + r);
-      const int e = e0[r] + lane;
-      ix0[r] = 0;
-      v0[r] = 0.0;
-      if (e < e1[r]) {
-        ix0[r] = static_cast<int>(idx[e] - in0);
-        v0[r] = vals[e];
+      e1[r] = __shfl_sync(0xffffffffu, tv, R + r);
+      ix[r] = 0;
+      v[r] = 0.0;
+      if (lane < e1[r] - e0[r]) {
+        ix[r] = idx[e0[r] + lane] - static_cast<int>(in0);
+        v[r] = vals[e0[r] + lane];
       }
     }
+    if (sl + 1 < nslab) {
+      stage(sl + 1, (sl + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* xb = xs + static_cast<size_t>(sl & 1) * SB * BP + 2 * j;
 #pragma unroll
-    for (int r = 0; r < TSP_LINES; ++r) {
-      const int cnt_all = e1[r] - e0[r];
-      for (int base = 0; base < cnt_all; base += 32) {
-        int ixc = ix0[r];
-        double vc = v0[r];
-        if (base > 0) {  // lines with more than 32 entries in this slab
-          const int e = e0[r] + base + lane;
+    for (int r = 0; r < R; ++r) {
+      for (int base = e0[r]; base < e1[r]; base += 32) {
+        const int n_here = min(32, e1[r] - base);
+        int ixc = ix[r];
+        double vc = v[r];
+        if (base > e0[r]) {  // lines with more than 32 entries in this slab
           ixc = 0;
           vc = 0.0;
-          if (e < e1[r]) {
-            ixc = static_cast<int>(idx[e] - in0);
-            vc = vals[e];
+          if (lane < n_here) {
+            ixc = idx[base + lane] - static_cast<int>(in0);
+            vc = vals[base + lane];
           }
         }
-        const int cnt = min(32, cnt_all - base);
-        for (int jj = 0; jj < cnt; ++jj) {
-          const double* xr = xs + __shfl_sync(0xffffffffu, ixc, jj) * b;
-          const double v = __shfl_sync(0xffffffffu, vc, jj);
-          acc[r][0] = fma(v, lane < b ? xr[lane] : 0.0, acc[r][0]);
-          if (c1) acc[r][1] = fma(v, xr[lane + 32], acc[r][1]);
+        for (int jj = 0; jj < n_here; jj += gpw) {
+          const int src = jj + g;
+          const int ixs = __shfl_sync(0xffffffffu, ixc, src & 31);
+          const double vs = __shfl_sync(0xffffffffu, vc, src & 31);
+          if (active && src < n_here) {
+            const double* xr = xb + ixs * BP;
+            const double2 a = *reinterpret_cast<const double2*>(xr);
+            const double2 c2 = *reinterpret_cast<const double2*>(xr + 2 * G);
+            acc[r][0] = fma(vs, a.x, acc[r][0]);
+            acc[r][1] = fma(vs, a.y, acc[r][1]);
+            acc[r][2] = fma(vs, c2.x, acc[r][2]);
+            acc[r][3] = fma(vs, c2.y, acc[r][3]);
+          }
         }
       }
     }
+    __syncthreads();  // buffer (sl & 1) is refilled by the next iteration's stage
   }
+  // groups' partials in group order into group 0
 #pragma unroll
-  for (int r = 0; r < TSP_LINES; ++r) {
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double sum = acc[r][c];
+      for (int k = 1; k < gpw; ++k) sum += __shfl_sync(0xffffffffu, acc[r][c], (lane + k * G) & 31);
+      acc[r][c] = sum;
+    }
+  if (g != 0) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
     const i64 o = o0 + r;
     if (o >= n_outer) break;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = lane + 32 * h;
-      if (c >= b) continue;
+    for (int c = 0; c < 4; ++c) {
+      const int col = (c < 2 ? 2 * j : 2 * G + 2 * j) + (c & 1);
+      if (col >= b) continue;
       if (ws) {
-        ws[(static_cast<i64>(blockIdx.y) * n_outer + o) * b + c] = acc[r][h];
+        ws[(static_cast<i64>(blockIdx.y) * n_outer + o) * b + col] = acc[r][c];
       } else {
-        double* p = out + o * ldo + c;
-        *p = beta == 0.0 ? alpha * acc[r][h] : fma(beta, *p, alpha * acc[r][h]);
+        double* p = out + o * ldo + col;
+        *p = beta == 0.0 ? alpha * acc[r][c] : fma(beta, *p, alpha * acc[r][c]);
       }
     }
   }
@@ -379,6 +426,94 @@ __global__ void __launch_bounds__(SDD_T) sddmm_tile_kernel(i64 m, i64 n, i64 kY,
   }
 }
 
+// Slab SDDMM for kY <= 64: r_e = <Yl[i, :], Yr[j, :]> - sub_e over the CSR entries.
+// Each warp owns R consecutive rows; their Yl rows sit in registers for the whole kernel (group
+// lane j holds Yl[i][4j .. 4j+3]); Yr streams through shared memory in slabs of SB rows (double
+// buffered cp.async, each slab read from L2 once per CTA of 16 R rows). The entries of a row
+// inside the slab are loaded 32 at a time (coalesced) and dealt round-robin to the warp's 32 / G
+// groups (G = power of two >= kY / 4): a group forms its entry's dot product from two 16-byte
+// shared loads per lane and a log2(G)-step xor-shuffle reduction; the group leader writes r_e.
+// Per entry: 8 kY bytes of shared-memory operand traffic (the bound) instead of the entry-
+// parallel kernel's 16 kY bytes of L2 gathers.
+template <int R, int G>
+__global__ void __launch_bounds__(SLAB_WARPS * 32, 1)
+    sddmm_slab_kernel(i64 m, i64 n, int kY, int ntc, int SB, const int* __restrict__ tptr,
+                      const int* __restrict__ col, const double* __restrict__ Yl, i64 ldl,
+                      const double* __restrict__ Yr, i64 ldr, const double* __restrict__ sub,
+                      double* __restrict__ out) {
+  extern __shared__ __align__(16) double ys[];  // [2][SB][BP]
+  constexpr int BP = 4 * G, GPW = 32 / G;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int g = lane / G, j = lane % G;
+  const bool kact = 4 * j < kY;  // lanes past the k extent load nothing
+  const i64 r0 = (static_cast<i64>(blockIdx.x) * SLAB_WARPS + warp) * R;
+  double yl[R][4];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k = 4 * j + c;
+      yl[r][c] = (r0 + r < m && k < kY) ? Yl[(r0 + r) * ldl + k] : 0.0;
+    }
+  const int TPS = SB / DevOmega::kTileCols;
+  const int nslab = (ntc + TPS - 1) / TPS;
+  auto stage = [&](int sl, int buf) {
+    const i64 c0 = static_cast<i64>(sl) * SB;
+    const int rows_in = static_cast<int>(min(static_cast<i64>(SB), n - c0));
+    double* dst = ys + static_cast<size_t>(buf) * SB * BP;
+    for (int e = t; e < rows_in * BP; e += SLAB_WARPS * 32) {
+      const int rr = e / BP, k = e - rr * BP;
+      if (k < kY) cp_async8(dst + e, Yr + (c0 + rr) * ldr + k, true);
+      else dst[e] = 0.0;
+    }
+    cp_async_commit();
+  };
+  if (nslab > 0) stage(0, 0);
+  for (int sl = 0; sl < nslab; ++sl) {
+    if (sl + 1 < nslab) {
+      stage(sl + 1, (sl + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int q0 = sl * TPS, q1 = min(ntc, q0 + TPS);
+    const int c0 = sl * SB;
+    const double* yb = ys + static_cast<size_t>(sl & 1) * SB * BP + 4 * j;
+    int tv = 0;
+    if (lane < 2 * R) {
+      const i64 i = r0 + (lane % R);
+      tv = i < m ? tptr[i * (ntc + 1) + (lane < R ? q0 : q1)] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e0 = __shfl_sync(0xffffffffu, tv, r), e1 = __shfl_sync(0xffffffffu, tv, R + r);
+      for (int base = e0; base < e1; base += 32) {
+        const int n_here = min(32, e1 - base);
+        int cj = 0;
+        if (lane < n_here) cj = col[base + lane] - c0;
+        for (int jj = 0; jj < n_here; jj += GPW) {
+          const int src = jj + g;
+          const int cs = __shfl_sync(0xffffffffu, cj, src & 31);
+          double p = 0.0;
+          if (kact && src < n_here) {
+            const double2* yr = reinterpret_cast<const double2*>(yb + cs * BP);
+            const double2 a = yr[0], b2 = yr[1];
+            p = fma(yl[r][0], a.x, fma(yl[r][1], a.y, fma(yl[r][2], b2.x, yl[r][3] * b2.y)));
+          }
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+          if (j == 0 && src < n_here) {
+            const int e = base + src;
+            out[e] = sub ? p - sub[e] : p;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 int grid_for(i64 total, int threads = 256) {
   return static_cast<int>(std::max<i64>(1, std::min<i64>((total + threads - 1) / threads, 4096)));
 }
@@ -425,6 +560,11 @@ void upload(cudaStream_t s, DBuf<T>& d, const std::vector<T>& h) {
 }
 
 }  // namespace
+
+void set_sparse_modes(int spmm_mode, int sddmm_mode) {
+  g_spmm_mode.store(spmm_mode);
+  g_sddmm_mode.store(sddmm_mode);
+}
 
 void DevOmega::build(cudaStream_t s, i64 m_, i64 n_, i64 nnz_, const long long* rows, const long long* cols,
                      const double* vals) {
@@ -512,6 +652,41 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
   prof::Scope scope(prof::kSddmm, s, 2.0 * kY * om.nnz, 24.0 * om.nnz + 8.0 * (om.m + om.n) * kY);
   const char* tile_env = std::getenv("DFCG_SDDMM_TILE");  // 0 / 1 force the entry-parallel / tiled kernel
   const int tile_mode = tile_env ? std::atoi(tile_env) : -1;
+  // slab SDDMM: measured slower than the tiled kernel (tools/bench_sparse.py, profiles/
+  // r02_bench_sparse.txt: 1038 vs 439 us at the c5 block), so opt-in (DFCG_SDDMM_SLAB=1)
+  static const int slab_env0 = std::getenv("DFCG_SDDMM_SLAB") ? std::atoi(std::getenv("DFCG_SDDMM_SLAB")) : 0;
+  const int slab_env = g_sddmm_mode.load() >= 0 ? g_sddmm_mode.load() : slab_env0;
+  if (om.ntc > 0 && tile_mode == -1 && slab_env != 0 && kY >= 1 && kY <= 64) {
+    int G = 1;
+    while (4 * G < kY) G *= 2;
+    const int BP = 4 * G;
+    const int SB = std::max(64, std::min(1024, static_cast<int>((150 * 1024 / (2 * 8 * BP)) / 64 * 64)));
+    int dev = 0, nsm = 148;
+    DFCG_CUDA(cudaGetDevice(&dev));
+    DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int R = (om.m + 16 * 8 - 1) / (16 * 8) >= nsm ? 8 : 4;
+    const unsigned grid = static_cast<unsigned>((om.m + SLAB_WARPS * R - 1) / (SLAB_WARPS * R));
+    const size_t smem = sizeof(double) * 2 * SB * BP;
+    static std::atomic<std::uint64_t> configured{0};
+    if (!(configured.load() & dev_bit(dev))) {
+#define SDS_ATTR(r, g) \
+  DFCG_CUDA(cudaFuncSetAttribute(sddmm_slab_kernel<r, g>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      SDS_ATTR(4, 1) SDS_ATTR(4, 2) SDS_ATTR(4, 4) SDS_ATTR(4, 8) SDS_ATTR(4, 16)
+      SDS_ATTR(8, 1) SDS_ATTR(8, 2) SDS_ATTR(8, 4) SDS_ATTR(8, 8) SDS_ATTR(8, 16)
+#undef SDS_ATTR
+      configured.fetch_or(dev_bit(dev));
+    }
+#define SDS_CASE(r, g)                                                                                       \
+  if (R == r && G == g)                                                                                      \
+    sddmm_slab_kernel<r, g><<<grid, SLAB_WARPS * 32, smem, s>>>(om.m, om.n, static_cast<int>(kY), om.ntc, SB, \
+                                                                om.tile_csr.get(), om.csr_col.get(), Yl, ldl, Yr,  \
+                                                                ldr, sub, r_csr);
+    SDS_CASE(4, 1) SDS_CASE(4, 2) SDS_CASE(4, 4) SDS_CASE(4, 8) SDS_CASE(4, 16)
+    SDS_CASE(8, 1) SDS_CASE(8, 2) SDS_CASE(8, 4) SDS_CASE(8, 8) SDS_CASE(8, 16)
+#undef SDS_CASE
+    DFCG_LAUNCH_CHECK();
+    return;
+  }
   if (om.ntc > 0 && tile_mode != 0) {
     static std::atomic<std::uint64_t> configured{0};  // one bit per device
     int dev = 0;
@@ -585,36 +760,60 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   const i64 in_rows = transpose ? om.m : om.n;
   prof::Scope scope(prof::kSpmm, s, 2.0 * om.nnz * b,
                     (transpose ? 20.0 : 12.0) * om.nnz + 8.0 * b * (in_rows + out_rows * (beta != 0.0 ? 2 : 1)));
-  {  // tiled kernel: 2 <= b <= 64, the tile table of the walk, CSC values streamed (transpose)
-    // Experimental (DFCG_SPMM_TILE=1): measured slower than the segmented kernel at the c5 block
-    // (567 vs 273 us per call at b = 35, N = 1e7: one CTA per SM at 126 registers, slab staging
-    // and the per-slab barriers are not overlapped with the entry loop), so off by default.
-    static const bool tiled_env = std::getenv("DFCG_SPMM_TILE") && std::atoi(std::getenv("DFCG_SPMM_TILE")) == 1;
+  {  // slab kernel: b <= 64, the tile table of the walk, CSC values streamed (transpose)
+    // slab SpMM: measured slower than the segmented gather kernel (tools/bench_sparse.py,
+    // profiles/r02_bench_sparse.txt: 568 vs 280 us at the c5 block — 16 warps per SM with a
+    // dependent entry load per line and slab hide too little latency), so opt-in (DFCG_SPMM_SLAB=1)
+    static const int slab_env0 = std::getenv("DFCG_SPMM_SLAB") ? std::atoi(std::getenv("DFCG_SPMM_SLAB")) : 0;
+    const int slab_env = g_spmm_mode.load() >= 0 ? g_spmm_mode.load() : slab_env0;
     const int nt = transpose ? om.ntr : om.ntc;
     const double* tv = transpose ? vals_csc : vals_csr;
-    if (tiled_env && b >= 2 && b <= 64 && nt > 0 && tv) {
+    if (slab_env != 0 && b >= 1 && b <= 64 && nt > 0 && tv) {
       const int* tptr = transpose ? om.tile_csc.get() : om.tile_csr.get();
       const int* tidx = transpose ? om.csc_row.get() : om.csr_col.get();
-      const i64 outer_blocks = (out_rows + TSP_OB - 1) / TSP_OB;
-      // split the inner dimension until the grid covers ~2 CTAs per SM (chunks of >= one slab)
-      const int max_chunks = std::max(1, (nt + 3) / 4);
-      int chunks = static_cast<int>(std::min<i64>(max_chunks, std::max<i64>(1, (2 * 148 + outer_blocks - 1) / outer_blocks)));
-      const int chunk_tiles = (nt + chunks - 1) / chunks;
+      const int G = static_cast<int>((b + 3) / 4), BP = 4 * G;
+      // slab rows: two buffers within ~150 KB of shared memory, a multiple of the 64-row tiles
+      const int SB = std::max(64, std::min(512, static_cast<int>((150 * 1024 / (2 * 8 * BP)) / 64 * 64)));
+      int nsm = 148;
+      {
+        int dev = 0;
+        DFCG_CUDA(cudaGetDevice(&dev));
+        DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      }
+      // 4 lines per warp (64 per CTA, one CTA per SM); the inner dimension is split into chunks
+      // of whole slabs so the grid fills whole waves (>= 85% of the last) or reaches >= 4 waves
+      const int R = 4;
+      const i64 outer_blocks = (out_rows + SLAB_WARPS * R - 1) / (SLAB_WARPS * R);
+      const int TPS = SB / DevOmega::kTileCols;
+      const int max_chunks = std::max(1, (nt + TPS - 1) / TPS);
+      int chunks = 1;
+      {
+        double best = -1.0;
+        for (int c = 1; c <= std::min(max_chunks, 64); ++c) {
+          const i64 tot = outer_blocks * c;
+          const i64 waves = (tot + nsm - 1) / nsm;
+          const double eff = static_cast<double>(tot) / static_cast<double>(waves * nsm);
+          const double score = eff - (waves > 8 ? 0.01 * (waves - 8) : 0.0);
+          if (score > best + 1e-9) best = score, chunks = c;
+          if (waves >= 4 && eff >= 0.85) break;
+        }
+      }
+      const int chunk_tiles = ((nt + chunks - 1) / chunks + TPS - 1) / TPS * TPS;
       chunks = (nt + chunk_tiles - 1) / chunk_tiles;
-      const size_t smem = sizeof(double) * TSP_SLAB * b;
+      const size_t smem = sizeof(double) * 2 * SB * BP;
       static std::atomic<std::uint64_t> configured{0};
       int dev = 0;
       DFCG_CUDA(cudaGetDevice(&dev));
       if (!(configured.load() & dev_bit(dev))) {
-        DFCG_CUDA(cudaFuncSetAttribute(spmm_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sizeof(double) * TSP_SLAB * 64)));
+        DFCG_CUDA(cudaFuncSetAttribute(spmm_slab_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         configured.fetch_or(dev_bit(dev));
       }
       DBuf<double> ws;
       if (chunks > 1) ws.alloc(static_cast<i64>(chunks) * out_rows * b, s);
-      spmm_tile_kernel<<<dim3(static_cast<unsigned>(outer_blocks), static_cast<unsigned>(chunks)), TSP_WARPS * 32,
-                         smem, s>>>(out_rows, in_rows, nt, tptr, tidx, tv, static_cast<int>(b), alpha, X, ldx, beta,
-                                    out, ldo, chunk_tiles, chunks > 1 ? ws.get() : nullptr);
+      const dim3 grid(static_cast<unsigned>(outer_blocks), static_cast<unsigned>(chunks));
+      spmm_slab_kernel<4><<<grid, SLAB_WARPS * 32, smem, s>>>(out_rows, in_rows, nt, tptr, tidx, tv,
+                                                                 static_cast<int>(b), G, SB, alpha, X, ldx, beta, out,
+                                                                 ldo, chunk_tiles, chunks > 1 ? ws.get() : nullptr);
       DFCG_LAUNCH_CHECK();
       if (chunks > 1) {
         spmm_chunk_reduce<<<grid_for(out_rows * b), 256, 0, s>>>(out_rows, static_cast<int>(b), chunks, ws.get(),

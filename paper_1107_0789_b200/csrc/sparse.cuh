@@ -67,6 +67,10 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
 // vals_csc[p] = vals_csr[csc2csr[p]]
 void csr_to_csc(cudaStream_t s, const DevOmega& om, const double* vals_csr, double* vals_csc);
 
+// Microbenchmark override of the slab kernels (1 on, 0 off, -1 back to DFCG_SPMM_SLAB /
+// DFCG_SDDMM_SLAB): process-global, for dfcg_bench_sparse only.
+void set_sparse_modes(int spmm_mode, int sddmm_mode);
+
 // D[i, j] += alpha * vals[(i,j)] for the observed pattern (row-major m x n dense D).
 void scatter_add_dense(cudaStream_t s, const DevOmega& om, const double* vals_csr, double alpha, double* D, i64 ldd);
 
