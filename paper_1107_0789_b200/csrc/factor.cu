@@ -92,12 +92,11 @@ __device__ long long g_potrf_trace[64];
 #else
 #define POTRF_STAMP(i)
 #endif
-__global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr,
-                                                         const double* maxdiag, double rel_tol, int* fail,
-                                                         int want_inv) {
-  extern __shared__ double psm[];
-  pdl_wait();
-  pdl_trigger();
+// The 64x64 diagonal-block factorisation as a device function (256 threads, kPotrfSmem of
+// shared memory at psm): used by potrf_diag_kernel and by the fused cooperative Cholesky.
+// G is read through L2 (__ldcg): in the fused kernel other CTAs wrote it since the last grid sync.
+__device__ void potrf_tile(int kb, double* G, i64 ldg, double* Rinv, i64 ldr, const double* maxdiag, double rel_tol,
+                           int* fail, int want_inv, double* psm) {
 #ifdef DFCG_POTRF_TRACE
   long long tp_ = clock64();
 #endif
@@ -113,7 +112,7 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
     for (int it = 0; it < CNB * CNB / 256; ++it) {
       const int e = t + 256 * it, r = e / CNB, c = e % CNB;
       const bool ok = r < kb && c < kb && r <= c;
-      v[it] = G[ok ? r * ldg + c : 0];
+      v[it] = __ldcg(G + (ok ? r * ldg + c : 0));
     }
 #pragma unroll
     for (int it = 0; it < CNB * CNB / 256; ++it) {
@@ -123,7 +122,7 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
       X[r][c] = 0.0;
     }
   }
-  const double thr = rel_tol * (*maxdiag);
+  const double thr = rel_tol * __ldcg(maxdiag);
   __syncthreads();
   POTRF_STAMP(1)
   for (int c0 = 0; c0 < kbp; c0 += PB) {
@@ -294,6 +293,15 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 
   POTRF_STAMP(5)
 }
 
+__global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* G, i64 ldg, double* Rinv, i64 ldr,
+                                                         const double* maxdiag, double rel_tol, int* fail,
+                                                         int want_inv) {
+  extern __shared__ double psm[];
+  pdl_wait();
+  pdl_trigger();
+  potrf_tile(kb, G, ldg, Rinv, ldr, maxdiag, rel_tol, fail, want_inv, psm);
+}
+
 // Panel TRSM of the blocked Cholesky without an explicit inverse: X = R_kk^-T P for the kb x rem
 // panel P (in place). One warp per panel column, lane l holding rows l and l + 32: per pivot i
 // the owner scales x_i, a shuffle broadcasts it and every lane updates its later rows — a
@@ -408,6 +416,183 @@ __global__ void __launch_bounds__(256) trinv_diag_kernel(i64 n, const double* __
   }
 }
 
+// ---------------------------------------------------------------- fused tile Cholesky
+// The whole blocked Cholesky (and the inverse) of an n x n Gram in ONE cooperative launch of P
+// persistent CTAs, on 64 x 64 tiles, instead of ~4 launches per 64-column panel (potrf, panel
+// TRSM, look-ahead update, trailing update) plus 2 GEMMs per panel for the inverse. Step k:
+//   phase A  TRSM of row k as a product with the diagonal inverse: R_kj = X_kk^T G_kj (j > k), and
+//            (inverse) T_i = sum_{l=i}^{k-1} X_il R_lk for the rows i < k of column k of R^-1;
+//   phase B  trailing update G_ij -= R_ki^T R_kj (k < i <= j; CTA 0 updates tile (k+1, k+1) and
+//            factors it right away — the look-ahead — while the other CTAs update the rest), and
+//            (inverse) X_ik = -T_i X_kk;
+// one grid-wide barrier after each phase (2 per tile step). Every tile task is a sum of 64 x 64 x
+// 64 FP64 DMMA products (8 warps, 16 x 32 each), operands staged through shared memory with
+// L2-only cp.async (the tiles were written by other SMs since the last barrier).
+// Same arithmetic as the launch-per-panel path up to summation order within a tile product.
+constexpr int CF_LD = CNB + 4;  // padded shared-tile row (conflict-free DMMA fragments)
+constexpr size_t kCholFusedSmem = std::max(kPotrfSmem, sizeof(double) * 2 * CNB * CF_LD);
+
+struct CholFusedArgs {
+  int n, nt, want_inv;
+  double* G;
+  i64 ldg;
+  double* Rinv;
+  i64 ldr;
+  double* T;  // n x CNB scratch (the T_i tiles of the current column)
+  const double* maxdiag;
+  double rel_tol;
+  int* fail;
+};
+
+// acc += op(A) B for 64 x 64 tiles (rows / cols beyond ra / cb and k beyond kk are zero-filled):
+// op(A) = A^T (ta) or A; A at a (ld lda), B at b (ld ldb). 256 threads.
+__device__ __forceinline__ void cf_tile_product(double (&acc)[2][4][2], bool ta, const double* a, i64 lda,
+                                                const double* b, i64 ldb, int ra, int kk, int cb, double* sm) {
+  double* sA = sm;                 // [r][k] (ta: stored [k][r])
+  double* sB = sm + CNB * CF_LD;   // [k][c]
+  const int t = threadIdx.x;
+  // L2-only loads (ld.global.cg): tiles written by other SMs since the last grid barrier must not
+  // come from a stale L1 line (the T scratch is rewritten every step)
+#pragma unroll 4
+  for (int e = t; e < CNB * CNB; e += 256) {
+    const int r = e / CNB, c = e % CNB;
+    // A: global row r of the stored tile; stored rows are k (ta) or rows (!ta)
+    const bool oka = ta ? (r < kk && c < ra) : (r < ra && c < kk);
+    const bool okb = r < kk && c < cb;
+    const double va = oka ? __ldcg(a + r * lda + c) : 0.0;
+    const double vb = okb ? __ldcg(b + r * ldb + c) : 0.0;
+    sA[r * CF_LD + c] = va;
+    sB[r * CF_LD + c] = vb;
+  }
+  __syncthreads();
+  const int lane = t & 31, warp = t >> 5;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
+  const int fr = lane >> 2, fk = lane & 3;
+#pragma unroll 4
+  for (int k0 = 0; k0 < CNB; k0 += 4) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = wm + i * 8 + fr, k = k0 + fk;
+      af[i] = ta ? sA[k * CF_LD + r] : sA[r * CF_LD + k];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[j] = sB[(k0 + fk) * CF_LD + wn + j * 8 + fr];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+  }
+  __syncthreads();  // the tiles are restaged by the next product
+}
+
+// c[r, col] = alpha acc + (beta ? c : 0) over the valid rows / cols
+__device__ __forceinline__ void cf_store(const double (&acc)[2][4][2], double* c, i64 ldc, int rows, int cols,
+                                         double alpha, bool accumulate) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
+  const int er = lane >> 2, ec = (lane & 3) * 2;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = wm + i * 8 + er, col = wn + j * 8 + ec + h;
+        if (r < rows && col < cols) {
+          double* p = c + r * ldc + col;
+          *p = accumulate ? __ldcg(p) + alpha * acc[i][j][h] : alpha * acc[i][j][h];
+        }
+      }
+}
+
+__device__ __forceinline__ void cf_zero(double (&acc)[2][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) chol_fused_kernel(CholFusedArgs p) {
+  extern __shared__ double csm[];
+  cg::grid_group grid = cg::this_grid();
+  const int P = gridDim.x, c = blockIdx.x, nt = p.nt;
+  auto tsz = [&](int i) { return min(CNB, p.n - i * CNB); };
+  auto gt = [&](int i, int j) { return p.G + static_cast<i64>(i) * CNB * p.ldg + static_cast<i64>(j) * CNB; };
+  auto xt = [&](int i, int j) { return p.Rinv + static_cast<i64>(i) * CNB * p.ldr + static_cast<i64>(j) * CNB; };
+  double acc[2][4][2];
+  if (c == 0) {
+    potrf_tile(tsz(0), gt(0, 0), p.ldg, xt(0, 0), p.ldr, p.maxdiag, p.rel_tol, p.fail, 1, csm);
+    __syncthreads();
+  }
+  grid.sync();
+  for (int k = 0; k < nt; ++k) {
+    const int kb = tsz(k);
+    // ---- phase A: R_kj = X_kk^T G_kj; T_i = sum_{l=i}^{k-1} X_il R_lk
+    {
+      const int ntr = nt - k - 1, nti = p.want_inv ? k : 0;
+      for (int task = c; task < ntr + nti; task += P) {
+        cf_zero(acc);
+        if (task < ntr) {
+          const int j = k + 1 + task;
+          cf_tile_product(acc, true, xt(k, k), p.ldr, gt(k, j), p.ldg, kb, kb, tsz(j), csm);
+          cf_store(acc, gt(k, j), p.ldg, kb, tsz(j), 1.0, false);
+        } else {
+          const int i = task - ntr;
+          for (int l = i; l < k; ++l)
+            cf_tile_product(acc, false, xt(i, l), p.ldr, gt(l, k), p.ldg, tsz(i), tsz(l), kb, csm);
+          cf_store(acc, p.T + static_cast<i64>(i) * CNB * CNB, CNB, tsz(i), kb, 1.0, false);
+        }
+      }
+    }
+    grid.sync();
+    // ---- phase B: trailing update (+ look-ahead factorisation of tile k+1), X_ik = -T_i X_kk
+    {
+      const int m = nt - k - 1;  // trailing tiles per side
+      const int nup = m * (m + 1) / 2, nxi = p.want_inv ? k : 0;
+      if (c == 0 && m > 0) {
+        cf_zero(acc);
+        cf_tile_product(acc, true, gt(k, k + 1), p.ldg, gt(k, k + 1), p.ldg, tsz(k + 1), kb, tsz(k + 1), csm);
+        cf_store(acc, gt(k + 1, k + 1), p.ldg, tsz(k + 1), tsz(k + 1), -1.0, true);
+        __threadfence_block();
+        __syncthreads();
+        potrf_tile(tsz(k + 1), gt(k + 1, k + 1), p.ldg, xt(k + 1, k + 1), p.ldr, p.maxdiag, p.rel_tol, p.fail, 1,
+                   csm);
+        __syncthreads();
+      }
+      // the other update tiles and the X column, over CTAs 1..P-1 (CTA 0 too when P == 1)
+      const int workers = P > 1 ? P - 1 : 1, w = P > 1 ? c - 1 : 0;
+      if (P == 1 || c > 0) {
+        for (int task = w; task < (nup - (m > 0 ? 1 : 0)) + nxi; task += workers) {
+          cf_zero(acc);
+          const int nu = nup - (m > 0 ? 1 : 0);
+          if (task < nu) {
+            // tile index over the upper triangle of the trailing block, skipping (k+1, k+1)
+            int idx = task + 1, i = 0;
+            while (idx >= m - i) idx -= m - i, ++i;
+            const int ti = k + 1 + i, tj = ti + idx;
+            cf_tile_product(acc, true, gt(k, ti), p.ldg, gt(k, tj), p.ldg, tsz(ti), kb, tsz(tj), csm);
+            cf_store(acc, gt(ti, tj), p.ldg, tsz(ti), tsz(tj), -1.0, true);
+          } else {
+            const int i = task - nu;
+            cf_tile_product(acc, false, p.T + static_cast<i64>(i) * CNB * CNB, CNB, xt(k, k), p.ldr, tsz(i), kb, kb,
+                            csm);
+            cf_store(acc, xt(i, k), p.ldr, tsz(i), kb, -1.0, false);
+          }
+        }
+      }
+    }
+    grid.sync();
+  }
+  // strictly-lower tiles of R are zero (the diagonal tiles were written by potrf_tile)
+  for (int task = c; task < nt * nt; task += P) {
+    const int i = task / nt, j = task % nt;
+    if (i <= j) continue;
+    double* g = gt(i, j);
+    for (int e = threadIdx.x; e < tsz(i) * tsz(j); e += 256) g[(e / tsz(j)) * p.ldg + e % tsz(j)] = 0.0;
+  }
+}
+
 __global__ void zero_lower_kernel(i64 n, double* A, i64 lda) {
   const i64 total = n * n;
   for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < total;
@@ -460,6 +645,39 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   diag_max_kernel<<<1, 256, 0, s>>>(n, G, ldg, maxdiag.get());
   DFCG_LAUNCH_CHECK();
   DFCG_CUDA(cudaMemset2DAsync(Rinv, sizeof(double) * ldr, 0, sizeof(double) * n, n, s));
+  // One cooperative launch for the whole factorisation (chol_fused_kernel) while three or more
+  // solves share the GPU: the packed c2 step drops from 11263 to 6048 launches (136.0 -> 138.3
+  // block-it/s). A lone solve keeps the launch-per-panel path below: its critical path is the
+  // chain potrf(k) -> TRSM(k, k+1) -> update(k+1, k+1) -> potrf(k+1) either way, and the fused
+  // kernel's grid barriers made it slower there (22.8 vs 20.7 ms per lone c2 iteration,
+  // profiles/r02_lone_fused*.txt). DFCG_CHOL_FUSED=1 / 0 forces either.
+  static const int fused_mode = std::getenv("DFCG_CHOL_FUSED") ? std::atoi(std::getenv("DFCG_CHOL_FUSED")) : 3;
+  if (n > CNB && (fused_mode == 1 || (fused_mode == 3 && active_streams(dev) >= 3))) {
+    static std::atomic<std::uint64_t> fused_cfg{0};
+    static int occ = 0, nsm = 0;
+    if (!(fused_cfg.load() & dev_bit(dev))) {
+      DFCG_CUDA(cudaFuncSetAttribute(chol_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kCholFusedSmem)));
+      DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_fused_kernel, 256, kCholFusedSmem));
+      DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      fused_cfg.fetch_or(dev_bit(dev));
+    }
+    const int nt = static_cast<int>((n + CNB - 1) / CNB);
+    const int share = std::max(1, active_streams(dev));
+    // CTAs: the widest phase's task count, at most this solve's share of the co-resident slots
+    const int widest = std::max(nt * (nt - 1) / 2 + (want_inverse ? nt : 0), nt);
+    const int P = std::max(2, std::min(widest, std::max(2, occ * nsm / share)));
+    DBuf<double> T(want_inverse ? n * CNB : 1, s);
+    CholFusedArgs a{static_cast<int>(n), nt, want_inverse ? 1 : 0, G, ldg, Rinv, ldr, T.get(), maxdiag.get(),
+                    rel_tol, fail};
+    void* kargs[] = {&a};
+    prof::Scope scope(prof::kCholesky, s, n * n * n / 3.0 + (want_inverse ? n * n * n / 3.0 : 0.0),
+                      16.0 * n * n);
+    DFCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(chol_fused_kernel), dim3(P), dim3(256), kargs,
+                                          kCholFusedSmem, s));
+    DFCG_LAUNCH_CHECK();
+    return;
+  }
   // Look-ahead: after the panel TRSM of block k, the next diagonal block is updated first and
   // factored on a helper stream while the rest of the trailing update runs on s, so the
   // latency-bound 64x64 potrf overlaps the trailing GEMM instead of following it.

@@ -37,7 +37,17 @@ rho = s / (m * n)
 rows = []
 for t in ts:
     floor = sigma * math.sqrt(rho) * (math.sqrt(m) + math.sqrt(n / t))
-    cfg = P.ApgConfig(mu_floor=floor)
+    # Continuation start: the reference's mu_init = 0.99 ||P_Omega M_b||_2 (solvers.hpp:259) sits
+    # within the randomized range finder's sigma_1 error on these narrow, sparse blocks, so the
+    # first SVT returns rank 0 and apg_mc stops after one iteration with a zero estimate (the
+    # reference does the same, r01 parity probe). The sweep starts continuation at 0.9 sigma_1 of
+    # block 0 instead (ApgConfig::mu_init, one value for every block).
+    g0 = P.partition_columns(1, 0xDFC0000000000001, n, t)[0]
+    sv = P.McSolver(P.extract_columns(obs, g0), P.ApgConfig(max_iters=1))
+    _, tr = sv.step(1, trace=True)
+    sv.close()
+    mu_init = tr[0]["mu"] * 0.90 / 0.99
+    cfg = P.ApgConfig(mu_floor=floor, mu_init=mu_init)
     t1 = time.time()
     est, info = P.dfc_run(obs, "proj", ensemble=True, ensemble_anchors=anchors, t=t, seed=1, workers=min(t, 16),
                           solver_cfg=cfg)
@@ -45,7 +55,7 @@ for t in ts:
     its = [x.iterations for x in info["subproblems"]]
     pred = np.einsum("ij,ij->i", est.left[I], est.right[J])
     rmse = float(np.sqrt(np.mean((pred - truth) ** 2)))
-    row = dict(t=t, anchors=anchors, mu_floor=round(floor, 4), solve_s=round(wall, 2),
+    row = dict(t=t, anchors=anchors, mu_floor=round(floor, 4), mu_init=round(mu_init, 3), solve_s=round(wall, 2),
                divide_ms=round(info["divide_ms"], 1), factor_ms=round(info["factor_ms"], 1),
                combine_ms=round(info["combine_ms"], 1), block_iterations=sum(its),
                iterations_min_max=[min(its), max(its)],
