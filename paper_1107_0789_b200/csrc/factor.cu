@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdint>
 #include <cstring>
 #include <numeric>
 
@@ -451,19 +452,26 @@ __device__ __forceinline__ void cf_tile_product(double (&acc)[2][4][2], bool ta,
   double* sA = sm;                 // [r][k] (ta: stored [k][r])
   double* sB = sm + CNB * CF_LD;   // [k][c]
   const int t = threadIdx.x;
-  // L2-only loads (ld.global.cg): tiles written by other SMs since the last grid barrier must not
-  // come from a stale L1 line (the T scratch is rewritten every step)
-#pragma unroll 4
-  for (int e = t; e < CNB * CNB; e += 256) {
-    const int r = e / CNB, c = e % CNB;
-    // A: global row r of the stored tile; stored rows are k (ta) or rows (!ta)
-    const bool oka = ta ? (r < kk && c < ra) : (r < ra && c < kk);
-    const bool okb = r < kk && c < cb;
-    const double va = oka ? __ldcg(a + r * lda + c) : 0.0;
-    const double vb = okb ? __ldcg(b + r * ldb + c) : 0.0;
-    sA[r * CF_LD + c] = va;
-    sB[r * CF_LD + c] = vb;
+  // 16-byte L2-only copies (cp.async.cg: tiles written by other SMs since the last grid barrier
+  // must not come from a stale L1 line — the T scratch is rewritten every step), all in flight
+  // at once; pairs straddling the tile's valid extent copy 8 bytes and zero-fill the rest.
+  // Requires even leading dimensions and 16-byte aligned tiles (the host pads otherwise).
+  auto cp16n = [](double* dst, const double* src, int bytes) {
+    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(src), "r"(bytes));
+  };
+#pragma unroll
+  for (int it = 0; it < (CNB * CNB / 2) / 256; ++it) {
+    const int e = t + it * 256, r = e / (CNB / 2), c = 2 * (e % (CNB / 2));
+    // A: stored row r (= k for ta, = output row otherwise), stored cols c, c+1
+    const int arows = ta ? kk : ra, acols = ta ? ra : kk;
+    const int na = r < arows ? min(2, max(0, acols - c)) : 0;
+    cp16n(sA + r * CF_LD + c, na ? a + r * lda + c : a, 8 * na);
+    const int nb = r < kk ? min(2, max(0, cb - c)) : 0;
+    cp16n(sB + r * CF_LD + c, nb ? b + r * ldb + c : b, 8 * nb);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   const int lane = t & 31, warp = t >> 5;
   const int wm = (warp >> 1) * 16, wn = (warp & 1) * 32;
@@ -664,11 +672,29 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
     }
     const int nt = static_cast<int>((n + CNB - 1) / CNB);
     const int share = std::max(1, active_streams(dev));
+    // the tile copies are 16-byte cp.async: work on even-ld, aligned copies when the caller's
+    // layout is not (one 2-D copy in, one out)
+    auto aligned = [](const double* p, i64 ld) { return ld % 2 == 0 && reinterpret_cast<std::uintptr_t>(p) % 16 == 0; };
+    const bool in_place = aligned(G, ldg) && aligned(Rinv, ldr);
+    const i64 np = (n + 1) & ~i64{1};
+    DBuf<double> Gp, Rp;
+    double* Gf = G;
+    double* Rf = Rinv;
+    i64 ldgf = ldg, ldrf = ldr;
+    if (!in_place) {
+      Gp.alloc(n * np, s);
+      Rp.alloc(n * np, s);
+      copy2d(s, n, n, G, ldg, Gp.get(), np);
+      Rp.zero(s);
+      Gf = Gp.get();
+      Rf = Rp.get();
+      ldgf = ldrf = np;
+    }
     // CTAs: the widest phase's task count, at most this solve's share of the co-resident slots
     const int widest = std::max(nt * (nt - 1) / 2 + (want_inverse ? nt : 0), nt);
     const int P = std::max(2, std::min(widest, std::max(2, occ * nsm / share)));
     DBuf<double> T(want_inverse ? n * CNB : 1, s);
-    CholFusedArgs a{static_cast<int>(n), nt, want_inverse ? 1 : 0, G, ldg, Rinv, ldr, T.get(), maxdiag.get(),
+    CholFusedArgs a{static_cast<int>(n), nt, want_inverse ? 1 : 0, Gf, ldgf, Rf, ldrf, T.get(), maxdiag.get(),
                     rel_tol, fail};
     void* kargs[] = {&a};
     prof::Scope scope(prof::kCholesky, s, n * n * n / 3.0 + (want_inverse ? n * n * n / 3.0 : 0.0),
@@ -676,6 +702,10 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
     DFCG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(chol_fused_kernel), dim3(P), dim3(256), kargs,
                                           kCholFusedSmem, s));
     DFCG_LAUNCH_CHECK();
+    if (!in_place) {
+      copy2d(s, n, n, Gp.get(), np, G, ldg);
+      copy2d(s, n, n, Rp.get(), np, Rinv, ldr);
+    }
     return;
   }
   // Look-ahead: after the panel TRSM of block k, the next diagonal block is updated first and
