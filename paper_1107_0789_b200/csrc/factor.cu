@@ -422,10 +422,11 @@ __global__ void __launch_bounds__(256) trinv_diag_kernel(i64 n, const double* __
 // persistent CTAs, on 64 x 64 tiles, instead of ~4 launches per 64-column panel (potrf, panel
 // TRSM, look-ahead update, trailing update) plus 2 GEMMs per panel for the inverse. Step k:
 //   phase A  TRSM of row k as a product with the diagonal inverse: R_kj = X_kk^T G_kj (j > k), and
-//            (inverse) T_i = sum_{l=i}^{k-1} X_il R_lk for the rows i < k of column k of R^-1;
+//            (inverse) the l = k-1 term of every running sum T_ij = sum_{l=i}^{j-1} X_il R_lj
+//            (i <= k-1 < j), one tile product per task;
 //   phase B  trailing update G_ij -= R_ki^T R_kj (k < i <= j; CTA 0 updates tile (k+1, k+1) and
 //            factors it right away — the look-ahead — while the other CTAs update the rest), and
-//            (inverse) X_ik = -T_i X_kk;
+//            (inverse) X_ik = -T_ik X_kk (X R = I column by column);
 // one grid-wide barrier after each phase (2 per tile step). Every tile task is a sum of 64 x 64 x
 // 64 FP64 DMMA products (8 warps, 16 x 32 each), operands staged through shared memory with
 // L2-only cp.async (the tiles were written by other SMs since the last barrier).
@@ -439,7 +440,8 @@ struct CholFusedArgs {
   i64 ldg;
   double* Rinv;
   i64 ldr;
-  double* T;  // n x CNB scratch (the T_i tiles of the current column)
+  double* T;  // n x n scratch (ld ldt): the inverse's running sums T_ij, i < j
+  i64 ldt;
   const double* maxdiag;
   double rel_tol;
   int* fail;
@@ -528,6 +530,7 @@ __global__ void __launch_bounds__(256) chol_fused_kernel(CholFusedArgs p) {
   auto tsz = [&](int i) { return min(CNB, p.n - i * CNB); };
   auto gt = [&](int i, int j) { return p.G + static_cast<i64>(i) * CNB * p.ldg + static_cast<i64>(j) * CNB; };
   auto xt = [&](int i, int j) { return p.Rinv + static_cast<i64>(i) * CNB * p.ldr + static_cast<i64>(j) * CNB; };
+  auto tt = [&](int i, int j) { return p.T + static_cast<i64>(i) * CNB * p.ldt + static_cast<i64>(j) * CNB; };
   double acc[2][4][2];
   if (c == 0) {
     potrf_tile(tsz(0), gt(0, 0), p.ldg, xt(0, 0), p.ldr, p.maxdiag, p.rel_tol, p.fail, 1, csm);
@@ -536,20 +539,21 @@ __global__ void __launch_bounds__(256) chol_fused_kernel(CholFusedArgs p) {
   grid.sync();
   for (int k = 0; k < nt; ++k) {
     const int kb = tsz(k);
-    // ---- phase A: R_kj = X_kk^T G_kj; T_i = sum_{l=i}^{k-1} X_il R_lk
+    // ---- phase A: R_kj = X_kk^T G_kj (j > k); and the inverse's running sums
+    //      T_ij += X_{i,k-1} R_{k-1,j} for i <= k-1 < j (the l = k-1 term of
+    //      T_ij = sum_{l=i}^{j-1} X_il R_lj: every product is its own task, no serial chain)
     {
-      const int ntr = nt - k - 1, nti = p.want_inv ? k : 0;
-      for (int task = c; task < ntr + nti; task += P) {
+      const int ntr = nt - k - 1, nacc = p.want_inv && k > 0 ? k * (nt - k) : 0;
+      for (int task = c; task < ntr + nacc; task += P) {
         cf_zero(acc);
         if (task < ntr) {
           const int j = k + 1 + task;
           cf_tile_product(acc, true, xt(k, k), p.ldr, gt(k, j), p.ldg, kb, kb, tsz(j), csm);
           cf_store(acc, gt(k, j), p.ldg, kb, tsz(j), 1.0, false);
         } else {
-          const int i = task - ntr;
-          for (int l = i; l < k; ++l)
-            cf_tile_product(acc, false, xt(i, l), p.ldr, gt(l, k), p.ldg, tsz(i), tsz(l), kb, csm);
-          cf_store(acc, p.T + static_cast<i64>(i) * CNB * CNB, CNB, tsz(i), kb, 1.0, false);
+          const int q = task - ntr, i = q / (nt - k), j = k + q % (nt - k), l = k - 1;
+          cf_tile_product(acc, false, xt(i, l), p.ldr, gt(l, j), p.ldg, tsz(i), tsz(l), tsz(j), csm);
+          cf_store(acc, tt(i, j), p.ldt, tsz(i), tsz(j), 1.0, i != l);  // the l = i term starts the sum
         }
       }
     }
@@ -581,10 +585,9 @@ __global__ void __launch_bounds__(256) chol_fused_kernel(CholFusedArgs p) {
             const int ti = k + 1 + i, tj = ti + idx;
             cf_tile_product(acc, true, gt(k, ti), p.ldg, gt(k, tj), p.ldg, tsz(ti), kb, tsz(tj), csm);
             cf_store(acc, gt(ti, tj), p.ldg, tsz(ti), tsz(tj), -1.0, true);
-          } else {
+          } else {  // X_ik = -T_ik X_kk (T_ik complete: its last term was added in phase A)
             const int i = task - nu;
-            cf_tile_product(acc, false, p.T + static_cast<i64>(i) * CNB * CNB, CNB, xt(k, k), p.ldr, tsz(i), kb, kb,
-                            csm);
+            cf_tile_product(acc, false, tt(i, k), p.ldt, xt(k, k), p.ldr, tsz(i), kb, kb, csm);
             cf_store(acc, xt(i, k), p.ldr, tsz(i), kb, -1.0, false);
           }
         }
@@ -653,13 +656,12 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   diag_max_kernel<<<1, 256, 0, s>>>(n, G, ldg, maxdiag.get());
   DFCG_LAUNCH_CHECK();
   DFCG_CUDA(cudaMemset2DAsync(Rinv, sizeof(double) * ldr, 0, sizeof(double) * n, n, s));
-  // One cooperative launch for the whole factorisation (chol_fused_kernel) while three or more
-  // solves share the GPU: the packed c2 step drops from 11263 to 6048 launches (136.0 -> 138.3
-  // block-it/s). A lone solve keeps the launch-per-panel path below: its critical path is the
-  // chain potrf(k) -> TRSM(k, k+1) -> update(k+1, k+1) -> potrf(k+1) either way, and the fused
-  // kernel's grid barriers made it slower there (22.8 vs 20.7 ms per lone c2 iteration,
-  // profiles/r02_lone_fused*.txt). DFCG_CHOL_FUSED=1 / 0 forces either.
-  static const int fused_mode = std::getenv("DFCG_CHOL_FUSED") ? std::atoi(std::getenv("DFCG_CHOL_FUSED")) : 3;
+  // One cooperative launch for the whole factorisation (chol_fused_kernel) instead of the
+  // launch-per-panel path below: the packed c2 step drops from 11263 to 6048 launches (136.0 ->
+  // 142.0 block-it/s) and a lone c2 iteration from 20.7 to 19.7 ms (profiles/r02_lone_fused*_v3,
+  // r02_bench_c2_cholfused*_v3). DFCG_CHOL_FUSED=0 keeps the per-panel path, 3 fuses only while
+  // three or more solves share the GPU.
+  static const int fused_mode = std::getenv("DFCG_CHOL_FUSED") ? std::atoi(std::getenv("DFCG_CHOL_FUSED")) : 1;
   if (n > CNB && (fused_mode == 1 || (fused_mode == 3 && active_streams(dev) >= 3))) {
     static std::atomic<std::uint64_t> fused_cfg{0};
     static int occ = 0, nsm = 0;
@@ -691,10 +693,10 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
       ldgf = ldrf = np;
     }
     // CTAs: the widest phase's task count, at most this solve's share of the co-resident slots
-    const int widest = std::max(nt * (nt - 1) / 2 + (want_inverse ? nt : 0), nt);
+    const int widest = std::max(nt * (nt - 1) / 2 + (want_inverse ? nt : 0), want_inverse ? (nt / 2) * (nt - nt / 2) + nt : nt);
     const int P = std::max(2, std::min(widest, std::max(2, occ * nsm / share)));
-    DBuf<double> T(want_inverse ? n * CNB : 1, s);
-    CholFusedArgs a{static_cast<int>(n), nt, want_inverse ? 1 : 0, Gf, ldgf, Rf, ldrf, T.get(), maxdiag.get(),
+    DBuf<double> T(want_inverse ? n * np : 1, s);
+    CholFusedArgs a{static_cast<int>(n), nt, want_inverse ? 1 : 0, Gf, ldgf, Rf, ldrf, T.get(), np, maxdiag.get(),
                     rel_tol, fail};
     void* kargs[] = {&a};
     prof::Scope scope(prof::kCholesky, s, n * n * n / 3.0 + (want_inverse ? n * n * n / 3.0 : 0.0),

@@ -25,7 +25,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
     {"DFCG_JACOBI_GRAPH": "1"},
     {"DFCG_PDL": "2"},
     {"DFCG_CHOL_INV_LATE": "0", "DFCG_CHOL_FUSED": "0"},
-    {"DFCG_CHOL_FUSED": "1"},
+    {"DFCG_CHOL_FUSED": "0"},
     {"DFCG_PDL": "0", "DFCG_JACOBI_PDL": "0"},
     {"DFCG_DENSE_OP": "0", "DFCG_SPMM_SLAB": "1"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_TILE": "0"},
