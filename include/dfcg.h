@@ -185,6 +185,11 @@ int dfcg_normals_fetch(dfcg_ctx* ctx, int stream_id, int64_t pos, int64_t n, dou
 int dfcg_bench_sparse(dfcg_ctx* ctx, const dfcg_obs* in, int64_t b, int64_t kY, int32_t reps, int32_t spmm_mode,
                       int32_t sddmm_mode, double* ms3, double* sum3);
 
+/* Diagnostics: the CholeskyQR Cholesky (+ inverse) of a random SPD matrix of order n, ms per call
+ * over `reps` CUDA-event-timed calls, with max |R^T R - G| / max |G| and max |R Rinv - I|. */
+int dfcg_bench_cholesky(dfcg_ctx* ctx, int64_t n, int32_t reps, int32_t want_inverse, double* ms, double* relres,
+                        double* invres);
+
 /* One block of the DFC-Proj combine, for the multi-GPU split of column_project
  * (sketch.hpp:194-196): Rg = block.right (Ub^T block.left)^T, Ub m x kb column-major, Rg
  * (block.n x kb, column-major) written to a caller buffer. */

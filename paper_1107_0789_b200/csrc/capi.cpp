@@ -3,6 +3,7 @@
 #include "../../include/dfcg.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -273,6 +274,73 @@ int dfcg_bench_sparse(dfcg_ctx* ctx, const dfcg_obs* in, int64_t b, int64_t kY, 
     set_sparse_modes(-1, -1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+  });
+}
+
+// Diagnostics: cholesky_inverse (the Cholesky + inverse of CholeskyQR) of a random SPD Gram
+// (G = X^T X + n I, X 2n x n) of order n, CUDA-event timed over `reps` calls; relres = max
+// |R^T R - G| / max |G| and max |R Rinv - I| of the last call.
+extern "C++" {
+namespace dfcg {
+void cholesky_inverse_public(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol,
+                             int* fail, bool want_inverse, bool scale);
+}
+}
+int dfcg_bench_cholesky(dfcg_ctx* ctx, int64_t n, int32_t reps, int32_t want_inverse, double* ms, double* relres,
+                        double* invres) {
+  return guard([&] {
+    if (!ctx || !ms || n < 1 || reps < 1) throw std::invalid_argument("dfcg_bench_cholesky: bad argument");
+    CallStream cs(*ctx->dev);
+    const cudaStream_t s = cs.s;
+    std::vector<double> X(static_cast<size_t>(2 * n * n)), G(static_cast<size_t>(n * n), 0.0);
+    std::uint64_t x = 12345;
+    for (auto& v : X) {
+      x = x * 6364136223846793005ULL + 1442695040888963407ULL;
+      v = static_cast<double>(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    }
+    for (i64 i = 0; i < n; ++i)
+      for (i64 j = 0; j < n; ++j) {
+        double a = 0;
+        for (i64 r = 0; r < 2 * n; ++r) a += X[r * n + i] * X[r * n + j];
+        G[i * n + j] = a + (i == j ? n : 0.0);
+      }
+    DBuf<double> G0(n * n, s), Gw(n * n, s), Ri(n * n, s);
+    DBuf<int> fail(1, s);
+    DFCG_CUDA(cudaMemcpyAsync(G0.get(), G.data(), sizeof(double) * G.size(), cudaMemcpyHostToDevice, s));
+    cudaEvent_t e0, e1;
+    DFCG_CUDA(cudaEventCreate(&e0));
+    DFCG_CUDA(cudaEventCreate(&e1));
+    float total = 0;
+    for (int it = 0; it <= reps; ++it) {
+      DFCG_CUDA(cudaMemcpyAsync(Gw.get(), G0.get(), sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+      fail.zero(s);
+      DFCG_CUDA(cudaEventRecord(e0, s));
+      cholesky_inverse_public(s, n, Gw.get(), n, Ri.get(), n, 1e-11, fail.get(), want_inverse != 0, true);
+      DFCG_CUDA(cudaEventRecord(e1, s));
+      DFCG_CUDA(cudaEventSynchronize(e1));
+      float t = 0;
+      DFCG_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      if (it > 0) total += t;  // the first call is a warm-up
+    }
+    *ms = total / reps;
+    std::vector<double> R(static_cast<size_t>(n * n)), Rinv(static_cast<size_t>(n * n));
+    DFCG_CUDA(cudaMemcpyAsync(R.data(), Gw.get(), sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
+    DFCG_CUDA(cudaMemcpyAsync(Rinv.data(), Ri.get(), sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
+    DFCG_CUDA(cudaStreamSynchronize(s));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    double gmax = 0, rmax = 0, imax = 0;
+    for (i64 i = 0; i < n; ++i)
+      for (i64 j = 0; j < n; ++j) {
+        double a = 0, b = 0;
+        for (i64 l = 0; l <= std::min(i, j); ++l) a += R[l * n + i] * R[l * n + j];
+        for (i64 l = i; l <= j; ++l) b += R[i * n + l] * Rinv[l * n + j];
+        gmax = std::max(gmax, std::fabs(G[i * n + j]));
+        rmax = std::max(rmax, std::fabs(a - G[i * n + j]));
+        if (want_inverse) imax = std::max(imax, std::fabs(b - (i == j ? 1.0 : 0.0)));
+      }
+    if (relres) *relres = rmax / gmax;
+    if (invres) *invres = imax;
   });
 }
 

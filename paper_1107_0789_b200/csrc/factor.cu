@@ -694,7 +694,8 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
     }
     // CTAs: the widest phase's task count, at most this solve's share of the co-resident slots
     const int widest = std::max(nt * (nt - 1) / 2 + (want_inverse ? nt : 0), want_inverse ? (nt / 2) * (nt - nt / 2) + nt : nt);
-    const int P = std::max(2, std::min(widest, std::max(2, occ * nsm / share)));
+    int P = std::max(2, std::min(widest, std::max(2, occ * nsm / share)));
+    if (const char* pe = std::getenv("DFCG_CHOL_P")) P = std::max(2, std::min(std::atoi(pe), occ * nsm));  // tuning
     DBuf<double> T(want_inverse ? n * np : 1, s);
     CholFusedArgs a{static_cast<int>(n), nt, want_inverse ? 1 : 0, Gf, ldgf, Rf, ldrf, T.get(), np, maxdiag.get(),
                     rel_tol, fail};
@@ -2126,6 +2127,13 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     DFCG_LAUNCH_CHECK();
   }
   DFCG_CUDA(cudaStreamSynchronize(s));  // host vectors (perm, s_host, cperm) used by async copies
+}
+
+// Exported for the dfcg_bench_cholesky diagnostic (the internal entry lives in the anonymous
+// namespace above).
+void cholesky_inverse_public(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rinv, i64 ldr, double rel_tol,
+                             int* fail, bool want_inverse, bool scale) {
+  cholesky_inverse(s, n, G, ldg, Rinv, ldr, rel_tol, fail, want_inverse, scale);
 }
 
 }  // namespace dfcg
