@@ -137,6 +137,16 @@ def make_blocks(P, wl):
 
 
 
+def packed_shares():
+    """SM-time shares of the kernels in the packed timed step, from the committed ncu launch list
+    (profiles/ncu_packed_shares.json): which kernel dominates the step the value is measured on."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_packed_shares.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def roofline_entry(prof, peaks, peak_kind):
     ops = {k: v for k, v in prof.items() if v["launches"] > 0}
     if not ops:
@@ -147,9 +157,20 @@ def roofline_entry(prof, peaks, peak_kind):
     g = [ops[k] for k in ("gemm", "gemm_small") if k in ops]
     if g:
         kern["gemm_kernel"] = {f: sum(x[f] for x in g) for f in ("ms", "launches", "flops", "bytes")}
-    name, v = max(kern.items(), key=lambda kv: kv[1]["ms"])
+    # dominant in the PACKED timed step by SM-time (ncu launch list) when that record exists; the
+    # per-launch event times below come from one block run alone (events of eight concurrent
+    # streams would time each launch's wait for SMs, not the kernel)
+    shares = packed_shares()
+    basis = "largest event time on the lone-block step"
+    cand = {k: shares[k] for k in kern if shares and isinstance(shares.get(k), (int, float))}
+    if cand:
+        name = max(cand, key=cand.get)
+        v = kern[name]
+        basis = f"largest SM-time share of the packed timed step ({cand[name]:.3f}, {shares['source']})"
+    else:
+        name, v = max(kern.items(), key=lambda kv: kv[1]["ms"])
     per_launch_ms = v["ms"] / v["launches"]
-    share = v["ms"] / sum(x["ms"] for x in ops.values())
+    share = cand[name] if cand else v["ms"] / sum(x["ms"] for x in ops.values())
     if name in ("gemm_kernel", "jacobi", "cholesky", "qr_fallback"):
         achieved = v["flops"] / (v["ms"] * 1e-3) / 1e12
         peak = FP64_DMMA_PEAK_TFLOPS
@@ -161,6 +182,7 @@ def roofline_entry(prof, peaks, peak_kind):
         entry = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s",
                      peak_source=f"{peak_kind} MEASURED_PEAKS.json hbm_gbs")
     entry.update(frac=entry["achieved"] / entry["peak"], traffic=None, kernel=name, share_of_step=share,
+                 dominant_by=basis,
                  launches=v["launches"], avg_launch_ms=per_launch_ms,
                  per_op={k: dict(ms=round(x["ms"], 3), launches=x["launches"],
                                  tflops=round(x["flops"] / max(x["ms"], 1e-9) / 1e9, 3),

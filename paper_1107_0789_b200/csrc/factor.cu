@@ -523,7 +523,7 @@ __device__ __forceinline__ void cf_zero(double (&acc)[2][4][2]) {
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 }
 
-__global__ void __launch_bounds__(256) chol_fused_kernel(CholFusedArgs p) {
+__global__ void __launch_bounds__(256, 2) chol_fused_kernel(CholFusedArgs p) {
   extern __shared__ double csm[];
   cg::grid_group grid = cg::this_grid();
   const int P = gridDim.x, c = blockIdx.x, nt = p.nt;
@@ -694,7 +694,10 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
     }
     // CTAs: the widest phase's task count, at most this solve's share of the co-resident slots
     const int widest = std::max(nt * (nt - 1) / 2 + (want_inverse ? nt : 0), want_inverse ? (nt / 2) * (nt - nt / 2) + nt : nt);
-    int P = std::max(2, std::min(widest, std::max(2, occ * nsm / share)));
+    // at most 64 CTAs (the 1250-column factorisation gains nothing past it,
+    // profiles/r02_bench_cholesky.txt); 128 registers, two CTAs per SM, so a CTA waiting at a
+    // grid barrier holds half an SM, not all of it, while other solves' kernels run (packed F step)
+    int P = std::max(2, std::min({widest, 64, std::max(2, occ * nsm / share)}));
     if (const char* pe = std::getenv("DFCG_CHOL_P")) P = std::max(2, std::min(std::atoi(pe), occ * nsm));  // tuning
     DBuf<double> T(want_inverse ? n * np : 1, s);
     CholFusedArgs a{static_cast<int>(n), nt, want_inverse ? 1 : 0, Gf, ldgf, Rf, ldrf, T.get(), np, maxdiag.get(),

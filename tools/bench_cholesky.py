@@ -20,8 +20,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
     print(json.dumps(dict(n=n, inverse=inv, ms=round(ms.value, 4), relres=rr.value, invres=ir.value)))
     sys.exit(0)
 
+sweep = os.environ.get("CHOL_BENCH_P", "8,12,16,32,64,148")
 configs = [("per-panel", {"DFCG_CHOL_FUSED": "0"})] + \
-          [(f"fused P={p}", {"DFCG_CHOL_FUSED": "1", "DFCG_CHOL_P": str(p)}) for p in (8, 12, 16, 32, 64, 148)] + \
+          [(f"fused P={p}", {"DFCG_CHOL_FUSED": "1", "DFCG_CHOL_P": p}) for p in sweep.split(",") if p] + \
           [("fused default P", {"DFCG_CHOL_FUSED": "1"})]
 for n in (720, 1250):
     for inv in (1, 0):

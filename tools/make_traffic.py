@@ -6,7 +6,8 @@ import csv
 import json
 import sys
 
-CLASSES = [("jacobi", "jacobi"), ("potrf", "cholesky"), ("gemm_kernel", "gemm"), ("splitk_reduce", "gemm"),
+CLASSES = [("jacobi", "jacobi"), ("potrf", "cholesky"), ("chol_fused", "cholesky"), ("gemm_kernel", "gemm"),
+           ("splitk_reduce", "gemm"),
            ("spmm", "spmm"), ("seg_reduce", "spmm"), ("empty_rows", "spmm"), ("sddmm", "sddmm")]
 
 
@@ -27,7 +28,7 @@ def main(path, out):
         for key, cls in CLASSES:
             if key in name:
                 a = agg[cls]
-                if key in ("gemm_kernel", "jacobi", "potrf", "spmm", "sddmm"):
+                if key in ("gemm_kernel", "jacobi", "potrf", "chol_fused", "spmm", "sddmm"):
                     a[0] += 1
                 a[1] += m.get('dram__bytes_read.sum', 0.0) + m.get('dram__bytes_write.sum', 0.0)
                 break
