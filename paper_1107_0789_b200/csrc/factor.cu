@@ -434,6 +434,20 @@ __global__ void __launch_bounds__(256) trinv_diag_kernel(i64 n, const double* __
 constexpr int CF_LD = CNB + 4;  // padded shared-tile row (conflict-free DMMA fragments)
 constexpr size_t kCholFusedSmem = std::max(kPotrfSmem, sizeof(double) * 2 * CNB * CF_LD);
 
+#ifdef DFCG_CHOL_TRACE  // phase timestamps (globaltimer ns) of CTA 0 and CTA 1: tools/chol_trace.cu
+__device__ unsigned long long g_chol_trace[64][2][6];
+__device__ __forceinline__ void chol_stamp(int k, int who, int slot) {
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 1) && k < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_chol_trace[k][blockIdx.x][slot] = t;
+  }
+}
+#define CHOL_STAMP(k, slot) chol_stamp(k, 0, slot)
+#else
+#define CHOL_STAMP(k, slot)
+#endif
+
 struct CholFusedArgs {
   int n, nt, want_inv;
   double* G;
@@ -539,6 +553,7 @@ __global__ void __launch_bounds__(256, 2) chol_fused_kernel(CholFusedArgs p) {
   grid.sync();
   for (int k = 0; k < nt; ++k) {
     const int kb = tsz(k);
+    CHOL_STAMP(k, 0);
     // ---- phase A: R_kj = X_kk^T G_kj (j > k); and the inverse's running sums
     //      T_ij += X_{i,k-1} R_{k-1,j} for i <= k-1 < j (the l = k-1 term of
     //      T_ij = sum_{l=i}^{j-1} X_il R_lj: every product is its own task, no serial chain)
@@ -557,7 +572,9 @@ __global__ void __launch_bounds__(256, 2) chol_fused_kernel(CholFusedArgs p) {
         }
       }
     }
+    CHOL_STAMP(k, 1);
     grid.sync();
+    CHOL_STAMP(k, 2);
     // ---- phase B: trailing update (+ look-ahead factorisation of tile k+1), X_ik = -T_i X_kk
     {
       const int m = nt - k - 1;  // trailing tiles per side
@@ -568,9 +585,11 @@ __global__ void __launch_bounds__(256, 2) chol_fused_kernel(CholFusedArgs p) {
         cf_store(acc, gt(k + 1, k + 1), p.ldg, tsz(k + 1), tsz(k + 1), -1.0, true);
         __threadfence_block();
         __syncthreads();
+        CHOL_STAMP(k, 3);
         potrf_tile(tsz(k + 1), gt(k + 1, k + 1), p.ldg, xt(k + 1, k + 1), p.ldr, p.maxdiag, p.rel_tol, p.fail, 1,
                    csm);
         __syncthreads();
+        CHOL_STAMP(k, 4);
       }
       // the other update tiles and the X column, over CTAs 1..P-1 (CTA 0 too when P == 1)
       const int workers = P > 1 ? P - 1 : 1, w = P > 1 ? c - 1 : 0;
@@ -593,6 +612,7 @@ __global__ void __launch_bounds__(256, 2) chol_fused_kernel(CholFusedArgs p) {
         }
       }
     }
+    CHOL_STAMP(k, 5);
     grid.sync();
   }
   // strictly-lower tiles of R are zero (the diagonal tiles were written by potrf_tile)
