@@ -553,6 +553,61 @@ void build_plan(cudaStream_t s, SegPlan& p, i64 rows, const std::vector<int>& pt
   DFCG_CUDA(cudaStreamSynchronize(s));
 }
 
+// Chunked plan (see DevOmega::plan_csr_ck): tab is the walk's per-line 64-tile offset table
+// (lines x (nt + 1)); items in (chunk, line) order, segments <= seg_len entries, slots grouped per
+// line in chunk order (seg_reduce_kernel's layout); a line with a single run writes directly.
+void build_chunked_plan(cudaStream_t s, SegPlan& p, i64 rows, const std::vector<int>& tab, int nt, int seg_len) {
+  const int ct = DevOmega::kChunkTiles;
+  const int nchunks = (nt + ct - 1) / ct;
+  auto run = [&](i64 r, int c, long long& a, long long& b) {
+    a = tab[static_cast<size_t>(r * (nt + 1) + c * ct)];
+    b = tab[static_cast<size_t>(r * (nt + 1) + std::min(nt, (c + 1) * ct))];
+  };
+  std::vector<int> nseg(static_cast<size_t>(rows), 0);
+  for (int c = 0; c < nchunks; ++c)
+    for (i64 r = 0; r < rows; ++r) {
+      long long a, b;
+      run(r, c, a, b);
+      if (b > a) nseg[static_cast<size_t>(r)] += static_cast<int>((b - a + seg_len - 1) / seg_len);
+    }
+  std::vector<int> base(static_cast<size_t>(rows) + 1, 0), multi_rows, slot_ptr{0};
+  int slot = 0;
+  for (i64 r = 0; r < rows; ++r) {
+    base[static_cast<size_t>(r)] = slot;
+    if (nseg[static_cast<size_t>(r)] > 1) {
+      multi_rows.push_back(static_cast<int>(r));
+      slot += nseg[static_cast<size_t>(r)];
+      slot_ptr.push_back(slot);
+    }
+  }
+  std::vector<int> next(base.begin(), base.end() - 1);
+  std::vector<SegItem> items;
+  for (int c = 0; c < nchunks; ++c)
+    for (i64 r = 0; r < rows; ++r) {
+      long long a, b;
+      run(r, c, a, b);
+      for (long long e = a; e < b; e += seg_len) {
+        const int sl = nseg[static_cast<size_t>(r)] > 1 ? next[static_cast<size_t>(r)]++ : -1;
+        items.push_back({static_cast<int>(r), sl, e, std::min(b, e + seg_len)});
+      }
+    }
+  p.rows = rows;
+  p.n_items = static_cast<i64>(items.size());
+  p.n_slots = slot;
+  p.h_multi_rows = multi_rows;
+  p.items.alloc(std::max<i64>(1, p.n_items), s);
+  if (p.n_items)
+    DFCG_CUDA(cudaMemcpyAsync(p.items.get(), items.data(), sizeof(SegItem) * items.size(), cudaMemcpyHostToDevice, s));
+  p.multi_rows.alloc(std::max<size_t>(1, multi_rows.size()), s);
+  p.red_rowptr.alloc(static_cast<i64>(slot_ptr.size()), s);
+  if (!multi_rows.empty())
+    DFCG_CUDA(cudaMemcpyAsync(p.multi_rows.get(), multi_rows.data(), sizeof(int) * multi_rows.size(),
+                              cudaMemcpyHostToDevice, s));
+  DFCG_CUDA(cudaMemcpyAsync(p.red_rowptr.get(), slot_ptr.data(), sizeof(int) * slot_ptr.size(), cudaMemcpyHostToDevice,
+                            s));
+  DFCG_CUDA(cudaStreamSynchronize(s));  // host vectors must outlive the async copies
+}
+
 template <class T>
 void upload(cudaStream_t s, DBuf<T>& d, const std::vector<T>& h) {
   d.alloc(std::max<size_t>(1, h.size()), s);
@@ -625,6 +680,7 @@ void DevOmega::build(cudaStream_t s, i64 m_, i64 n_, i64 nnz_, const long long* 
     }
     upload(s, tile_csr, h);
     DFCG_CUDA(cudaStreamSynchronize(s));
+    if (ntc > 2 * kChunkTiles) build_chunked_plan(s, plan_csr_ck, m, h, ntc, seg_for(m, nnz));
   }
   // row-tile offsets of every CSC column (rows ascend within a column)
   const i64 rtiles = (m + kTileCols - 1) / kTileCols;
@@ -641,6 +697,7 @@ void DevOmega::build(cudaStream_t s, i64 m_, i64 n_, i64 nnz_, const long long* 
     }
     upload(s, tile_csc, h);
     DFCG_CUDA(cudaStreamSynchronize(s));
+    if (ntr > 2 * kChunkTiles) build_chunked_plan(s, plan_csc_ck, n, h, ntr, seg_for(n, nnz));
   }
   h_csc2csr = std::move(c2r);
 }
@@ -765,7 +822,7 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
     // profiles/r02_bench_sparse.txt: 568 vs 280 us at the c5 block — 16 warps per SM with a
     // dependent entry load per line and slab hide too little latency), so opt-in (DFCG_SPMM_SLAB=1)
     static const int slab_env0 = std::getenv("DFCG_SPMM_SLAB") ? std::atoi(std::getenv("DFCG_SPMM_SLAB")) : 0;
-    const int slab_env = g_spmm_mode.load() >= 0 ? g_spmm_mode.load() : slab_env0;
+    const int slab_env = g_spmm_mode.load() >= 0 ? (g_spmm_mode.load() == 1 ? 1 : 0) : slab_env0;
     const int nt = transpose ? om.ntr : om.ntc;
     const double* tv = transpose ? vals_csc : vals_csr;
     if (slab_env != 0 && b >= 1 && b <= 64 && nt > 0 && tv) {
@@ -828,11 +885,17 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
     DFCG_LAUNCH_CHECK();
   }
   if (p.n_items == 0) return;
+  // chunked (cache-blocked) plan of the same walk when it exists: DFCG_SPMM_CHUNK=0 disables
+  static const int chunk_env = std::getenv("DFCG_SPMM_CHUNK") ? std::atoi(std::getenv("DFCG_SPMM_CHUNK")) : 1;
+  const int mode = g_spmm_mode.load();
+  const SegPlan& pc = transpose ? om.plan_csc_ck : om.plan_csr_ck;
+  const bool chunked = pc.n_items > 0 && (mode >= 0 ? mode == 2 : chunk_env != 0);
+  const SegPlan& pp = chunked ? pc : p;
   DBuf<double> ws;
-  if (p.n_slots) ws.alloc(p.n_slots * b, s);
+  if (pp.n_slots) ws.alloc(pp.n_slots * b, s);
   // lanes per item: enough for one pass over the b columns at kSpmmCpl columns per lane
   const int G = pow2_at_least((b + kSpmmCpl - 1) / kSpmmCpl);
-  const i64 warps = (p.n_items + (32 / G) - 1) / (32 / G);
+  const i64 warps = (pp.n_items + (32 / G) - 1) / (32 / G);
   const int blocks = static_cast<int>((warps + 7) / 8);
   const int* idx = transpose ? om.csc_row.get() : om.csr_col.get();
   // the transposed walk streams CSC-ordered values when the caller has them, else it gathers
@@ -842,10 +905,10 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
 #define SPMM_CASE(g)                                                                                               \
   case g:                                                                                                          \
     if (transpose)                                                                                                 \
-      spmm_kernel<g, true><<<blocks, 256, 0, s>>>(p.n_items, p.items.get(), idx, perm, vals, b, alpha, X, ldx,     \
+      spmm_kernel<g, true><<<blocks, 256, 0, s>>>(pp.n_items, pp.items.get(), idx, perm, vals, b, alpha, X, ldx,     \
                                                    beta, out, ldo, ws.get());                                      \
     else                                                                                                           \
-      spmm_kernel<g, false><<<blocks, 256, 0, s>>>(p.n_items, p.items.get(), idx, perm, vals, b, alpha, X,         \
+      spmm_kernel<g, false><<<blocks, 256, 0, s>>>(pp.n_items, pp.items.get(), idx, perm, vals, b, alpha, X,         \
                                                     ldx, beta, out, ldo, ws.get());                                \
     break;
   switch (G) {
@@ -858,9 +921,9 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   }
 #undef SPMM_CASE
   DFCG_LAUNCH_CHECK();
-  if (!p.h_multi_rows.empty()) {
-    const i64 nr = static_cast<i64>(p.h_multi_rows.size());
-    seg_reduce_kernel<<<grid_for(nr * b), 256, 0, s>>>(nr, p.multi_rows.get(), p.red_rowptr.get(), b, ws.get(), alpha,
+  if (!pp.h_multi_rows.empty()) {
+    const i64 nr = static_cast<i64>(pp.h_multi_rows.size());
+    seg_reduce_kernel<<<grid_for(nr * b), 256, 0, s>>>(nr, pp.multi_rows.get(), pp.red_rowptr.get(), b, ws.get(), alpha,
                                                        beta, out, ldo);
     DFCG_LAUNCH_CHECK();
   }

@@ -35,6 +35,13 @@ struct DevOmega {
   DBuf<long long> csc2csr;  // CSC position -> CSR position
   DBuf<double> m_csc;
   SegPlan plan_csr, plan_csc;
+  // Cache-blocked variants of the two walks (the chunked SpMM): items ordered by a chunk of
+  // kChunkTiles 64-wide tiles of the INNER dimension, then by outer line, so the warps resident
+  // at any moment gather X rows from one chunk (~kChunkTiles * 64 * b * 8 bytes, L1-sized)
+  // instead of all of X (L2-bound); every (line, chunk) run is a workspace slot, summed per line
+  // in chunk order. Empty (n_items == 0) when the inner dimension spans <= 2 chunks.
+  static constexpr int kChunkTiles = 8;
+  SegPlan plan_csr_ck, plan_csc_ck;
   bool has_empty_csr = false, has_empty_csc = false;  // structure rows / columns without entries
   std::vector<long long> h_csc2csr;  // host copy (outputs in reference order)
   // Column-tile offsets of the CSR rows for the tiled SDDMM: the entries of row r in column
@@ -69,7 +76,7 @@ void csr_to_csc(cudaStream_t s, const DevOmega& om, const double* vals_csr, doub
 
 // Microbenchmark override of the slab kernels (1 on, 0 off, -1 back to DFCG_SPMM_SLAB /
 // DFCG_SDDMM_SLAB): process-global, for dfcg_bench_sparse only.
-void set_sparse_modes(int spmm_mode, int sddmm_mode);
+void set_sparse_modes(int spmm_mode, int sddmm_mode);  // spmm_mode: 0 gather, 1 slab, 2 chunked
 
 // D[i, j] += alpha * vals[(i,j)] for the observed pattern (row-major m x n dense D).
 void scatter_add_dense(cudaStream_t s, const DevOmega& om, const double* vals_csr, double alpha, double* D, i64 ldd);

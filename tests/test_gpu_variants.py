@@ -28,6 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
     {"DFCG_CHOL_FUSED": "0"},
     {"DFCG_PDL": "0", "DFCG_JACOBI_PDL": "0"},
     {"DFCG_DENSE_OP": "0", "DFCG_SPMM_SLAB": "1"},
+    {"DFCG_DENSE_OP": "0", "DFCG_SPMM_CHUNK": "0"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_TILE": "0"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_SLAB": "0", "DFCG_SDDMM_TW": "1"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_SLAB": "0", "DFCG_SDDMM_TW": "4"},

@@ -1,6 +1,6 @@
 """Microbenchmark of the APG-MC iteration's sparse kernels (dfcg_bench_sparse): forward SpMM R X,
-transposed SpMM R^T Q and the SDDMM residual, slab kernels (mode 1) against the previous
-segmented-gather SpMM / tiled SDDMM (mode 0), on the c5 block (40000 x 5000, N = 1e7) and the c2
+transposed SpMM R^T Q and the SDDMM residual; the segmented-gather SpMM / tiled SDDMM ("gather"),
+the slab kernels ("slab") and the cache-blocked (chunked) gather SpMM ("chunked"), on the c5 block (40000 x 5000, N = 1e7) and the c2
 block (10000 x 1250, N ~ 1.25e6) at their low-rank sketch widths. Rates are algorithmic bytes
 (the same accounting as the per-op profile) per CUDA-event time; sums compare the two modes."""
 import ctypes as C
@@ -33,17 +33,20 @@ for name, o, b, kY in cases:
     by = {"spmm": 12.0 * N + 8.0 * b * (n + m), "spmm_t": 12.0 * N + 8.0 * b * (m + n),
           "sddmm": 24.0 * N + 8.0 * (m + n) * kY}
     res = {}
-    for mode in (1, 0):
+    # (spmm mode, sddmm mode): 0 = gather SpMM / tiled SDDMM, 1 = slab kernels, 2 = chunked SpMM
+    for key, (ms_mode, sd_mode) in {"gather": (0, 0), "slab": (1, 1), "chunked": (2, 0)}.items():
         ms = (C.c_double * 3)()
         sm = (C.c_double * 3)()
         L._check(L.lib().dfcg_bench_sparse(L.context(0), C.byref(oc), C.c_int64(b), C.c_int64(kY), C.c_int32(reps),
-                                           C.c_int32(mode), C.c_int32(mode), ms, sm))
-        res[mode] = (list(ms), list(sm))
+                                           C.c_int32(ms_mode), C.c_int32(sd_mode), ms, sm))
+        res[key] = (list(ms), list(sm))
     row = dict(case=name, N=N, b=b, kY=kY)
     for i, k in enumerate(("spmm", "spmm_t", "sddmm")):
-        a, z = res[1][0][i], res[0][0][i]
-        row[k] = dict(slab_us=round(1e3 * a, 1), prev_us=round(1e3 * z, 1), speedup=round(z / a, 2),
-                      slab_gbs=round(by[k] / (a * 1e-3) / 1e9, 1), slab_frac=round(by[k] / (a * 1e-3) / 1e9 / peak, 3),
-                      sum_rel_diff=abs(res[1][1][i] - res[0][1][i]) / max(abs(res[0][1][i]), 1e-300))
+        row[k] = {}
+        for key in res:
+            t_ms = res[key][0][i]
+            row[k][key] = dict(us=round(1e3 * t_ms, 1), gbs=round(by[k] / (t_ms * 1e-3) / 1e9, 1),
+                               frac=round(by[k] / (t_ms * 1e-3) / 1e9 / peak, 3),
+                               sum_rel_diff=abs(res[key][1][i] - res["gather"][1][i]) / max(abs(res["gather"][1][i]), 1e-300))
     out.append(row)
     print(json.dumps(row), flush=True)
