@@ -24,6 +24,7 @@
 #include "common.cuh"
 
 #include <cooperative_groups.h>
+#include <map>
 namespace cg = cooperative_groups;
 
 namespace dfcg {
@@ -1340,14 +1341,16 @@ struct JacobiArgs {
   int p, prefetch_v;
 };
 
-template <int NB, int CS>
-__global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
-    jacobi_round_resident_kernel(const JacobiArgs* __restrict__ ja, int round, int inner_sweeps) {
+// The round body, shared by the launch-per-round kernel (PDL: griddepcontrol between rounds) and
+// the persistent sweep kernel (grid barriers between rounds). offmax: where this round's largest
+// pair cosine goes.
+template <int NB, int CS, bool PDL>
+__device__ __forceinline__ void jacobi_round_body(const JacobiArgs* __restrict__ ja, unsigned long long* offmax,
+                                                  int round, int inner_sweeps) {
   static_assert(NB == 8 || NB == 16, "8- or 16-column blocks (16 or 32 columns per pair)");
   const i64 rows_ = ja->rows, nv_ = ja->nv, ldw = ja->ldw, ldv = ja->ldv;
   double* W = ja->W;
   double* V = ja->V;
-  unsigned long long* offmax = ja->offmax;
   const double tol = ja->tol;
   const int p = ja->p, prefetch_v = ja->prefetch_v;
   constexpr int JW = 2 * NB, T = 256, NT = JW / 8, CH = JW / 2, KS = JW / 4;
@@ -1392,10 +1395,10 @@ __global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
   // Programmatic dependent launch (when the host enables it): everything above only reads the
   // argument block; the previous round's writes to W are visible after griddepcontrol.wait, and
   // the next round may start launching once every CTA of this one has issued its loads.
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if constexpr (PDL) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   stage(Wp, W, ldw, rows, rows4);
   asm volatile("cp.async.commit_group;\n" ::);
-  asm volatile("griddepcontrol.launch_dependents;\n" ::);
+  if constexpr (PDL) asm volatile("griddepcontrol.launch_dependents;\n" ::);
   if (prefetch_v) {  // second group: the V pair, consumed only after the rotation is known
     stage(Vp, V, ldv, nv, nv4);
     asm volatile("cp.async.commit_group;\n" ::);
@@ -1657,6 +1660,39 @@ __global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
   apply(Vp, V, ldv, nv, nv4);
+}
+
+template <int NB, int CS>
+__global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
+    jacobi_round_resident_kernel(const JacobiArgs* __restrict__ ja, int round, int inner_sweeps) {
+  jacobi_round_body<NB, CS, true>(ja, ja->offmax, round, inner_sweeps);
+}
+
+// Persistent Jacobi: every sweep of one SVD in ONE cooperative launch (the p - 1 rounds of a
+// sweep separated by grid barriers, the stop test on the device) instead of p - 1 launches per
+// sweep and a host round trip after each sweep. Same rounds, same pairing, same arithmetic: the
+// result is bitwise that of the launch-per-round path. Sweep s takes its largest cosine in
+// slot s % 3 of ja->offmax (three slots: CTA 0 clears slot (s + 1) % 3 at the start of sweep s,
+// whose last readers finished before the first barrier of sweep s - 1). sweeps_out: the sweeps
+// executed.
+template <int NB, int CS>
+__global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
+    jacobi_sweeps_kernel(const JacobiArgs* __restrict__ ja, double stop_tol, int max_sweeps, int* sweeps_out) {
+  cg::grid_group grid = cg::this_grid();
+  const int p = ja->p;
+  int sweep = 0;
+  while (sweep < max_sweeps) {
+    unsigned long long* slot = ja->offmax + sweep % 3;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(ja->offmax + (sweep + 1) % 3, 0ull);
+    for (int r = 0; r < p - 1; ++r) {
+      jacobi_round_body<NB, CS, false>(ja, slot, r, r == 0 ? 1 : 0);
+      grid.sync();
+    }
+    ++sweep;
+    const double off = __longlong_as_double(static_cast<long long>(__ldcg(slot)));
+    if (off <= stop_tol) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
 }
 
 // A[:, c] /= s[c] (columns with s[c] == 0 are zeroed)
@@ -2084,7 +2120,97 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
     DFCG_CUDA(cudaGraphDestroy(graph));
   }
   cudaGraphExec_t sweep_exec = sg ? sg->exec : nullptr;
-  for (int sweep = 0; sweep < 60 && !small; ++sweep) {
+  // Persistent sweeps (jacobi_sweeps_kernel): one cooperative launch per SVD, stop test on the
+  // device. DFCG_JACOBI_PERSIST=0 keeps the launch-per-round path, 1 always persists, 2 (default)
+  // persists while at most two solves share the GPU (the latency-bound lone-block regime).
+  static const int persist_env =
+      std::getenv("DFCG_JACOBI_PERSIST") ? std::atoi(std::getenv("DFCG_JACOBI_PERSIST")) : 2;
+  bool persist = resident && !small && !sweep_exec &&
+                 (persist_env == 1 || (persist_env == 2 && active_streams(dev) <= 2));
+  if (persist) {
+    auto fn = [&]() -> const void* {
+      if (NB == 8) {
+        if (CS == 1) return reinterpret_cast<const void*>(jacobi_sweeps_kernel<8, 1>);
+        if (CS == 2) return reinterpret_cast<const void*>(jacobi_sweeps_kernel<8, 2>);
+        return reinterpret_cast<const void*>(jacobi_sweeps_kernel<8, 4>);
+      }
+      if (CS == 1) return reinterpret_cast<const void*>(jacobi_sweeps_kernel<16, 1>);
+      if (CS == 2) return reinterpret_cast<const void*>(jacobi_sweeps_kernel<16, 2>);
+      return reinterpret_cast<const void*>(jacobi_sweeps_kernel<16, 4>);
+    }();
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> occ_cache;  // (kernel, device) -> co-resident CTAs per SM
+    int occ = 0, nsm = 0;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      auto it = occ_cache.find({fn, dev});
+      if (it == occ_cache.end()) {
+        const size_t cap = dyn_cap(CS);
+        DFCG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
+        DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+        occ_cache[{fn, dev}] = occ;
+      } else {
+        occ = it->second;
+      }
+    }
+    DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    persist = occ > 0 && static_cast<i64>(npairs) * CS <= static_cast<i64>(occ) * nsm;
+    if (persist) {
+      DBuf<unsigned long long> offs(3, s);
+      DBuf<int> nsw(1, s);
+      offs.zero(s);
+      const JacobiArgs pa{wrows, nj, np, np, W.get(), J.get(), offs.get(), tol, p, prefetch_v};
+      DFCG_CUDA(cudaMemcpyAsync(d_args, &pa, sizeof(JacobiArgs), cudaMemcpyHostToDevice, s));
+      const double per_sweep_flops = (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW;
+      const double per_sweep_bytes = (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW;
+      int h_sweeps = 0;
+      {
+        prof::Scope scope(prof::kJacobi, s, 0.0, 0.0, 0);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(npairs * CS));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        int na = 0;
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+        if (CS > 1) {
+          attr[na].id = cudaLaunchAttributeClusterDimension;
+          attr[na].val.clusterDim.x = static_cast<unsigned>(CS);
+          attr[na].val.clusterDim.y = 1;
+          attr[na].val.clusterDim.z = 1;
+          ++na;
+        }
+        cfg.attrs = attr;
+        cfg.numAttrs = na;
+        const JacobiArgs* ap = d_args;
+        const double stol = stop_tol;
+        const int maxsw = 60;
+        int* so = nsw.get();
+#define DFCG_JSWEEPS(nb, cs) DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_sweeps_kernel<nb, cs>, ap, stol, maxsw, so))
+        if (NB == 8) {
+          if (CS == 1) DFCG_JSWEEPS(8, 1);
+          else if (CS == 2) DFCG_JSWEEPS(8, 2);
+          else DFCG_JSWEEPS(8, 4);
+        } else {
+          if (CS == 1) DFCG_JSWEEPS(16, 1);
+          else if (CS == 2) DFCG_JSWEEPS(16, 2);
+          else DFCG_JSWEEPS(16, 4);
+        }
+#undef DFCG_JSWEEPS
+        DFCG_LAUNCH_CHECK();
+        DFCG_CUDA(cudaMemcpyAsync(&h_sweeps, so, sizeof(int), cudaMemcpyDeviceToHost, s));
+        DFCG_CUDA(cudaStreamSynchronize(s));
+        scope.add_work(h_sweeps * per_sweep_flops, h_sweeps * per_sweep_bytes, 1);
+      }
+      if (trace_svd)
+        std::fprintf(stderr, "[svd] %lldx%lld persistent: %d sweeps (CS %d)\n", (long long)rows, (long long)cols,
+                     h_sweeps, CS);
+    }
+  }
+  for (int sweep = 0; sweep < 60 && !small && !persist; ++sweep) {
     if (sweep_exec) {
       prof::Scope scope(prof::kJacobi, s, (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW,
                         (p - 1.0) * npairs * 16.0 * (wrows + nj) * JW, p - 1);

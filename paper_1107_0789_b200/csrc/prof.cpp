@@ -36,6 +36,15 @@ Scope::Scope(Op op, cudaStream_t s, double flops, double bytes, int launches)
   cudaEventRecord(e0_, s_);
 }
 
+void Scope::add_work(double flops, double bytes, int launches) {
+  g_work_flops[op_].fetch_add(static_cast<long long>(flops), std::memory_order_relaxed);
+  g_work_bytes[op_].fetch_add(static_cast<long long>(bytes), std::memory_order_relaxed);
+  g_work_launches[op_].fetch_add(launches, std::memory_order_relaxed);
+  flops_ += flops;
+  bytes_ += bytes;
+  launches_ += launches;
+}
+
 Scope::~Scope() {
   if (!on_) return;
   cudaEventRecord(e1_, s_);

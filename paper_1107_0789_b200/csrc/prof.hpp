@@ -41,6 +41,8 @@ class Scope {
   // rates stay per kernel without an event pair around every launch.
   Scope(Op op, cudaStream_t s, double flops, double bytes, int launches = 1);
   ~Scope();
+  // work known only after the launch (e.g. the sweeps a persistent Jacobi kernel executed)
+  void add_work(double flops, double bytes, int launches);
   Scope(const Scope&) = delete;
   Scope& operator=(const Scope&) = delete;
 

@@ -885,8 +885,11 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
     DFCG_LAUNCH_CHECK();
   }
   if (p.n_items == 0) return;
-  // chunked (cache-blocked) plan of the same walk when it exists: DFCG_SPMM_CHUNK=0 disables
-  static const int chunk_env = std::getenv("DFCG_SPMM_CHUNK") ? std::atoi(std::getenv("DFCG_SPMM_CHUNK")) : 1;
+  // chunked (cache-blocked) plan of the same walk when it exists: opt-in (DFCG_SPMM_CHUNK=1), it
+  // measured slower than the plain walk (c5 block: 305 vs 281 us forward, 334 vs 260 us
+  // transposed; profiles/r02_bench_sparse2.txt): the gather kernel is bound by L1 wavefronts per
+  // entry, not by L2 misses, so keeping the X chunk L1-resident does not help
+  static const int chunk_env = std::getenv("DFCG_SPMM_CHUNK") ? std::atoi(std::getenv("DFCG_SPMM_CHUNK")) : 0;
   const int mode = g_spmm_mode.load();
   const SegPlan& pc = transpose ? om.plan_csc_ck : om.plan_csr_ck;
   const bool chunked = pc.n_items > 0 && (mode >= 0 ? mode == 2 : chunk_env != 0);

@@ -1,6 +1,7 @@
 """The kernel variants selected by heuristics (or only by environment switches) must give the
 same parity: Jacobi rounds on 2- and 4-CTA clusters and with 16-column blocks, the 64x64 /
-64x48 GEMM tiles, the unscaled Cholesky, the Jacobi sweep replayed as a CUDA graph, the segmented (gather) SpMM, the tiled and the entry-parallel SDDMM (the slab kernels' fallbacks)
+64x48 GEMM tiles, the unscaled Cholesky, the Jacobi sweep replayed as a CUDA graph, the persistent (one cooperative launch per SVD) and
+launch-per-round Jacobi sweeps, the segmented (gather) SpMM, the tiled and the entry-parallel SDDMM (the slab kernels' fallbacks)
 under the factored operator. Each variant runs in a child process (the switches are
 read once per process)."""
 import os
@@ -28,12 +29,16 @@ HERE = os.path.dirname(os.path.abspath(__file__))
     {"DFCG_CHOL_FUSED": "0"},
     {"DFCG_PDL": "0", "DFCG_JACOBI_PDL": "0"},
     {"DFCG_DENSE_OP": "0", "DFCG_SPMM_SLAB": "1"},
-    {"DFCG_DENSE_OP": "0", "DFCG_SPMM_CHUNK": "0"},
+    {"DFCG_DENSE_OP": "0", "DFCG_SPMM_CHUNK": "1"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_TILE": "0"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_SLAB": "0", "DFCG_SDDMM_TW": "1"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_SLAB": "0", "DFCG_SDDMM_TW": "4"},
     {"DFCG_DENSE_OP": "0", "DFCG_SDDMM_SLAB": "1", "DFCG_SPMM_SLAB": "1"},
     {"DFCG_JACOBI_GRAPH": "1", "DFCG_JACOBI_CLUSTER": "1"},
+    {"DFCG_JACOBI_PERSIST": "0"},
+    {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_CLUSTER": "1"},
+    {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_CLUSTER": "4"},
+    {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_NB": "16"},
 ], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
 def test_variant_parity(env):
     r = subprocess.run([sys.executable, os.path.join(HERE, "_variant_case.py")], env={**os.environ, **env},
