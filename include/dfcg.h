@@ -42,7 +42,8 @@ enum {
   DFCG_ECUDA = -4,
   DFCG_ENOMEM = -5,
   DFCG_ENCCL = -6,
-  DFCG_EINTERNAL = -7
+  DFCG_EINTERNAL = -7,
+  DFCG_EPARSE = -8 /* ParseError (matrix_io.hpp:22-26); dfcg_last_error_line() is its line */
 };
 
 typedef struct dfcg_ctx dfcg_ctx;
@@ -131,6 +132,7 @@ int dfcg_ctx_create(int device, dfcg_ctx** out);
 void dfcg_ctx_destroy(dfcg_ctx* ctx);
 const char* dfcg_last_error(void);
 int64_t dfcg_last_error_block(void);
+int64_t dfcg_last_error_line(void); /* 1-based line of the last DFCG_EPARSE, else -1 */
 void dfcg_free(void* p);
 void dfcg_lowrank_free(dfcg_lowrank* e); /* frees left/right of a library-filled estimate */
 void dfcg_sparse_free(dfcg_sparse* s);

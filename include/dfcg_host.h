@@ -5,6 +5,7 @@
  *   SeededRng            P/include/dfc/rng.hpp:26-74
  *   sample_without_replacement / partition_columns / extract_*   P/include/dfc/sampling.hpp:15-113
  *   gen_mc_instance / gen_rmf_instance                            P/include/dfc/simgen.hpp:30-82
+ *   load_triplets / save_triplets                                 P/include/dfc/matrix_io.hpp:125-179
  * Nothing here runs on the GPU. Arrays returned through pointer-to-pointer arguments are
  * malloc'ed by the library; release them with dfcg_free (dfcg.h).
  */
@@ -56,6 +57,21 @@ int dfcg_gen_recsys_instance(int64_t m, int64_t n, int64_t r, double density, do
                              int64_t* count, int64_t** rows, int64_t** cols, double** vals);
 int dfcg_gen_rmf_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigma, uint64_t seed, uint64_t stream,
                           double lo, double hi, dfcg_lowrank* L0, dfcg_sparse* S0, double* M);
+
+/* ---- triplet text I/O (load_triplets / save_triplets, P/include/dfc/matrix_io.hpp:125-179) ----
+ * "% m n" header (optional; dims inferred from the data without it), one "i j v" line per
+ * observation, blank lines skipped, 0-based unless one_based. Parsed and sorted to the
+ * ObservedMatrix order (column-major, matrix_io.hpp:41-43) on DFCG_IO_THREADS host threads.
+ * Errors as the reference: DFCG_EPARSE (ParseError; dfcg_last_error_line() = its line, the
+ * first offending line in file order), DFCG_ERANGE (index outside the declared dims),
+ * DFCG_EINVAL (no header and no data; duplicate entry). Arrays are library-allocated. */
+int dfcg_load_triplets_text(const char* text, int64_t len, int32_t one_based, int64_t* m, int64_t* n, int64_t* count,
+                            int64_t** rows, int64_t** cols, double** vals);
+int dfcg_load_triplets_file(const char* path, int32_t one_based, int64_t* m, int64_t* n, int64_t* count,
+                            int64_t** rows, int64_t** cols, double** vals);
+/* "% m n" then "row col %.17g" per entry in the order given (lossless: load(save(x)) == x). */
+int dfcg_save_triplets_file(const char* path, const dfcg_obs* in);
+int dfcg_format_triplets(const dfcg_obs* in, char** text, int64_t* len); /* text: dfcg_free */
 
 /* ---- kernel accounting (bench / profiling; off by default) ---------------------------
  * Op classes, in order: 0 gemm (>= 2 GFLOP), 1 sddmm, 2 spmm, 3 cholesky, 4 qr_fallback,

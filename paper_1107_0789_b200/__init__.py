@@ -20,6 +20,7 @@ from ._lib import (  # noqa: F401,E402
     ApgConfig,
     BlockError,
     DfcError,
+    ParseError,
     Estimate,
     McSolver,
     Observed,
@@ -43,7 +44,11 @@ from .host import (  # noqa: F401,E402
     extract_columns,
     extract_subproblems,
     extract_rows,
+    format_triplets,
     gen_mc_instance,
+    load_triplets,
+    parse_triplets,
+    save_triplets,
     gen_recsys_instance,
     launch_count,
     work_counters,

@@ -103,6 +103,7 @@ def lib():
             L = C.CDLL(_SO)
             L.dfcg_last_error.restype = C.c_char_p
             L.dfcg_last_error_block.restype = i64
+            L.dfcg_last_error_line.restype = i64
             _lib = L
     return _lib
 
@@ -118,6 +119,8 @@ def _check(rc: int):
         raise IndexError(msg)
     if rc == -3:
         raise BlockError(int(L.dfcg_last_error_block()), msg)
+    if rc == -8:
+        raise ParseError(int(L.dfcg_last_error_line()), msg)
     raise DfcError(f"libdfcg error {rc}: {msg}")
 
 
@@ -135,6 +138,14 @@ def context(device: int = 0) -> C.c_void_p:
             _contexts[device] = h
         ctx = h
     return ctx
+
+
+class ParseError(RuntimeError):
+    """dfc::ParseError (P/include/dfc/matrix_io.hpp:22-26): "line N: what", with .line."""
+
+    def __init__(self, line: int, msg: str):
+        super().__init__(msg)  # libdfcg's message already carries the "line N: " prefix
+        self.line = line
 
 
 # ------------------------------------------------------------------ data model

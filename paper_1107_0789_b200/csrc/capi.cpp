@@ -12,6 +12,7 @@
 #include <string>
 
 #include "dfc_host.hpp"
+#include "triplet_io.hpp"
 #include "dist.hpp"
 
 using namespace dfcg;
@@ -34,14 +35,20 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int64_t g_err_block = -1;
+thread_local int64_t g_err_line = -1;
 
 template <class F>
 int guard(F&& f) {
   g_err.clear();
   g_err_block = -1;
+  g_err_line = -1;
   try {
     f();
     return DFCG_OK;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    g_err_line = static_cast<int64_t>(e.line);
+    return DFCG_EPARSE;
   } catch (const BlockError& e) {
     // the inner message: a caller rethrowing BlockError(dfcg_last_error_block(), msg) adds the
     // "block N: " prefix itself (P/include/dfc/dfc.hpp:50-54), exactly once
@@ -232,7 +239,9 @@ int dfcg_bench_sparse(dfcg_ctx* ctx, const dfcg_obs* in, int64_t b, int64_t kY, 
       DFCG_CUDA(cudaStreamSynchronize(s));
       return d;
     };
-    DBuf<double> X = fill(obs.n * b, 1), Q = fill(obs.m * b, 2), Yl = fill(obs.m * kY, 3), Yr = fill(obs.n * kY, 4);
+    // DFCG_BENCH_LDX: leading dimension of the gathered sketches (default b: packed rows)
+    const i64 ldx = std::getenv("DFCG_BENCH_LDX") ? std::max<i64>(b, std::atoll(std::getenv("DFCG_BENCH_LDX"))) : b;
+    DBuf<double> X = fill(obs.n * ldx, 1), Q = fill(obs.m * ldx, 2), Yl = fill(obs.m * kY, 3), Yr = fill(obs.n * kY, 4);
     DBuf<double> outm(obs.m * b, s), outn(obs.n * b, s), r(std::max<i64>(1, obs.count()), s);
     set_sparse_modes(spmm_mode, sddmm_mode);
     cudaEvent_t e0, e1;
@@ -257,10 +266,10 @@ int dfcg_bench_sparse(dfcg_ctx* ctx, const dfcg_obs* in, int64_t b, int64_t kY, 
       return t;
     };
     try {
-      ms3[0] = timed([&] { spmm(s, om, false, om.m_csr.get(), b, 1.0, X.get(), b, 0.0, outm.get(), b); });
+      ms3[0] = timed([&] { spmm(s, om, false, om.m_csr.get(), b, 1.0, X.get(), ldx, 0.0, outm.get(), b); });
       sum3[0] = total(outm, obs.m * b);
       ms3[1] = timed([&] {
-        spmm(s, om, true, om.m_csr.get(), b, 1.0, Q.get(), b, 0.0, outn.get(), b, om.m_csc.get());
+        spmm(s, om, true, om.m_csr.get(), b, 1.0, Q.get(), ldx, 0.0, outn.get(), b, om.m_csc.get());
       });
       sum3[1] = total(outn, obs.n * b);
       ms3[2] = timed([&] { sddmm_residual(s, om, kY, Yl.get(), kY, Yr.get(), kY, om.m_csr.get(), r.get()); });
@@ -352,6 +361,7 @@ void dfcg_ctx_destroy(dfcg_ctx* ctx) {
 
 const char* dfcg_last_error(void) { return g_err.c_str(); }
 int64_t dfcg_last_error_block(void) { return g_err_block; }
+int64_t dfcg_last_error_line(void) { return g_err_line; }
 void dfcg_free(void* p) { std::free(p); }
 
 void dfcg_lowrank_free(dfcg_lowrank* e) {

@@ -25,6 +25,7 @@
 
 #include <cooperative_groups.h>
 #include <map>
+#include <tuple>
 namespace cg = cooperative_groups;
 
 namespace dfcg {
@@ -2139,22 +2140,45 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       return reinterpret_cast<const void*>(jacobi_sweeps_kernel<16, 4>);
     }();
     static std::mutex mu;
-    static std::map<std::pair<const void*, int>, int> occ_cache;  // (kernel, device) -> co-resident CTAs per SM
-    int occ = 0, nsm = 0;
+    // (kernel, device, dynamic shared memory) -> CTAs that can be co-resident on the whole GPU.
+    // With clusters the bound is cudaOccupancyMaxActiveClusters x CS (cluster placement within
+    // GPCs leaves it below SMs x CTAs per SM: the full-matrix base APG's 187-pair SVD passed
+    // the per-SM bound at CS = 2 and the cooperative launch was refused).
+    static std::map<std::tuple<const void*, int, size_t>, i64> occ_cache;
+    i64 co_resident = 0;
     {
       std::lock_guard<std::mutex> lock(mu);
-      auto it = occ_cache.find({fn, dev});
+      const auto key = std::make_tuple(fn, dev, smem);
+      auto it = occ_cache.find(key);
       if (it == occ_cache.end()) {
         const size_t cap = dyn_cap(CS);
         DFCG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)));
+        int occ = 0, nsm = 0;
         DFCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
-        occ_cache[{fn, dev}] = occ;
+        DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        co_resident = static_cast<i64>(occ) * nsm;
+        if (CS > 1) {
+          cudaLaunchConfig_t qc = {};
+          qc.gridDim = dim3(static_cast<unsigned>(CS) * 1024u);
+          qc.blockDim = dim3(256);
+          qc.dynamicSmemBytes = smem;
+          cudaLaunchAttribute qa[1];
+          qa[0].id = cudaLaunchAttributeClusterDimension;
+          qa[0].val.clusterDim.x = static_cast<unsigned>(CS);
+          qa[0].val.clusterDim.y = 1;
+          qa[0].val.clusterDim.z = 1;
+          qc.attrs = qa;
+          qc.numAttrs = 1;
+          int ncl = 0;
+          DFCG_CUDA(cudaOccupancyMaxActiveClusters(&ncl, fn, &qc));
+          co_resident = std::min<i64>(co_resident, static_cast<i64>(ncl) * CS);
+        }
+        occ_cache[key] = co_resident;
       } else {
-        occ = it->second;
+        co_resident = it->second;
       }
     }
-    DFCG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    persist = occ > 0 && static_cast<i64>(npairs) * CS <= static_cast<i64>(occ) * nsm;
+    persist = static_cast<i64>(npairs) * CS <= co_resident;
     if (persist) {
       DBuf<unsigned long long> offs(3, s);
       DBuf<int> nsw(1, s);
@@ -2189,7 +2213,8 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
         const double stol = stop_tol;
         const int maxsw = 60;
         int* so = nsw.get();
-#define DFCG_JSWEEPS(nb, cs) DFCG_CUDA(cudaLaunchKernelEx(&cfg, jacobi_sweeps_kernel<nb, cs>, ap, stol, maxsw, so))
+        cudaError_t lerr = cudaSuccess;
+#define DFCG_JSWEEPS(nb, cs) lerr = cudaLaunchKernelEx(&cfg, jacobi_sweeps_kernel<nb, cs>, ap, stol, maxsw, so)
         if (NB == 8) {
           if (CS == 1) DFCG_JSWEEPS(8, 1);
           else if (CS == 2) DFCG_JSWEEPS(8, 2);
@@ -2200,12 +2225,20 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
           else DFCG_JSWEEPS(16, 4);
         }
 #undef DFCG_JSWEEPS
-        DFCG_LAUNCH_CHECK();
-        DFCG_CUDA(cudaMemcpyAsync(&h_sweeps, so, sizeof(int), cudaMemcpyDeviceToHost, s));
-        DFCG_CUDA(cudaStreamSynchronize(s));
-        scope.add_work(h_sweeps * per_sweep_flops, h_sweeps * per_sweep_bytes, 1);
+        if (lerr == cudaErrorCooperativeLaunchTooLarge) {
+          // the occupancy query overestimated (e.g. another context's carve-out): nothing was
+          // launched; fall back to one launch per round below
+          (void)cudaGetLastError();
+          persist = false;
+        } else {
+          DFCG_CUDA(lerr);
+          DFCG_LAUNCH_CHECK();
+          DFCG_CUDA(cudaMemcpyAsync(&h_sweeps, so, sizeof(int), cudaMemcpyDeviceToHost, s));
+          DFCG_CUDA(cudaStreamSynchronize(s));
+          scope.add_work(h_sweeps * per_sweep_flops, h_sweeps * per_sweep_bytes, 1);
+        }
       }
-      if (trace_svd)
+      if (trace_svd && persist)
         std::fprintf(stderr, "[svd] %lldx%lld persistent: %d sweeps (CS %d)\n", (long long)rows, (long long)cols,
                      h_sweeps, CS);
     }

@@ -10,6 +10,7 @@
 
 #include "../../include/dfcg_host.h"
 #include "dfc_host.hpp"
+#include "triplet_io.hpp"
 
 using namespace dfcg;
 
@@ -332,6 +333,67 @@ int dfcg_gen_mc_instance(int64_t m, int64_t n, int64_t r, int64_t s, double sigm
     *rows = dup(std::vector<int64_t>(obs.row.begin(), obs.row.end()));
     *cols = dup(std::vector<int64_t>(obs.col.begin(), obs.col.end()));
     *vals = dup(obs.val);
+  });
+}
+
+// load_triplets / save_triplets, matrix_io.hpp:125-179 (parallel; triplet_io.cpp).
+namespace {
+void triplets_out(TripletFile& f, int64_t* m, int64_t* n, int64_t* count, int64_t** rows, int64_t** cols,
+                  double** vals) {
+  *m = f.m;
+  *n = f.n;
+  *count = static_cast<int64_t>(f.val.size());
+  *rows = dup(std::vector<int64_t>(f.row.begin(), f.row.end()));
+  std::vector<long long>().swap(f.row);
+  *cols = dup(std::vector<int64_t>(f.col.begin(), f.col.end()));
+  std::vector<long long>().swap(f.col);
+  *vals = dup(f.val);
+}
+}  // namespace
+
+int dfcg_load_triplets_text(const char* text, int64_t len, int32_t one_based, int64_t* m, int64_t* n, int64_t* count,
+                            int64_t** rows, int64_t** cols, double** vals) {
+  return dfcg_guard_call([&] {
+    if ((!text && len > 0) || len < 0 || !m || !n || !count || !rows || !cols || !vals)
+      throw std::invalid_argument("dfcg_load_triplets_text: bad argument");
+    TripletFile f = load_triplets_text(text ? text : "", static_cast<size_t>(len), one_based != 0);
+    triplets_out(f, m, n, count, rows, cols, vals);
+  });
+}
+
+int dfcg_load_triplets_file(const char* path, int32_t one_based, int64_t* m, int64_t* n, int64_t* count,
+                            int64_t** rows, int64_t** cols, double** vals) {
+  return dfcg_guard_call([&] {
+    if (!path || !m || !n || !count || !rows || !cols || !vals)
+      throw std::invalid_argument("dfcg_load_triplets_file: bad argument");
+    TripletFile f = load_triplets_file(path, one_based != 0);
+    triplets_out(f, m, n, count, rows, cols, vals);
+  });
+}
+
+int dfcg_save_triplets_file(const char* path, const dfcg_obs* in) {
+  return dfcg_guard_call([&] {
+    if (!path || !in || in->nnz < 0 || (in->nnz > 0 && (!in->row || !in->col || !in->val)))
+      throw std::invalid_argument("dfcg_save_triplets_file: bad argument");
+    static_assert(sizeof(long long) == sizeof(int64_t), "index width");
+    save_triplets_file(path, in->m, in->n, static_cast<size_t>(in->nnz), reinterpret_cast<const long long*>(in->row),
+                       reinterpret_cast<const long long*>(in->col), in->val);
+  });
+}
+
+int dfcg_format_triplets(const dfcg_obs* in, char** text, int64_t* len) {
+  return dfcg_guard_call([&] {
+    if (!in || !text || !len || in->nnz < 0 || (in->nnz > 0 && (!in->row || !in->col || !in->val)))
+      throw std::invalid_argument("dfcg_format_triplets: bad argument");
+    const std::string s = format_triplets(in->m, in->n, static_cast<size_t>(in->nnz),
+                                          reinterpret_cast<const long long*>(in->row),
+                                          reinterpret_cast<const long long*>(in->col), in->val);
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    if (!p) throw std::bad_alloc();
+    std::memcpy(p, s.data(), s.size());
+    p[s.size()] = 0;
+    *text = p;
+    *len = static_cast<int64_t>(s.size());
   });
 }
 

@@ -145,6 +145,69 @@ def gen_mc_instance(m, n, r, s, sigma, seed, stream=0):
     return _lowrank_out(L0), Observed(m, n, R, Cc, V)
 
 
+def _triplets_out(m, n, count, rows, cols, vals) -> Observed:
+    N = int(count.value)
+    if N:
+        R = np.ctypeslib.as_array(rows, shape=(N,)).copy()
+        Cc = np.ctypeslib.as_array(cols, shape=(N,)).copy()
+        V = np.ctypeslib.as_array(vals, shape=(N,)).copy()
+    else:
+        R, Cc, V = np.empty(0, np.int64), np.empty(0, np.int64), np.empty(0, np.float64)
+    for p in (rows, cols, vals):
+        lib().dfcg_free(C.cast(p, C.c_void_p))
+    return Observed(int(m.value), int(n.value), R, Cc, V)
+
+
+def parse_triplets(text, one_based=False) -> Observed:
+    """load_triplets (P/include/dfc/matrix_io.hpp:125-170) on in-memory text: optional "% m n"
+    header, one "i j v" line per observation; raises ParseError (.line), IndexError (outside the
+    declared dims) or ValueError (no header and no data, duplicates) as the reference throws
+    ParseError, std::out_of_range and std::invalid_argument."""
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    m, n, count = i64(), i64(), i64()
+    rows, cols, vals = i64ptr(), i64ptr(), C.POINTER(C.c_double)()
+    _check(lib().dfcg_load_triplets_text(C.c_char_p(raw), i64(len(raw)), C.c_int32(1 if one_based else 0),
+                                         C.byref(m), C.byref(n), C.byref(count), C.byref(rows), C.byref(cols),
+                                         C.byref(vals)))
+    return _triplets_out(m, n, count, rows, cols, vals)
+
+
+def load_triplets(path, one_based=False) -> Observed:
+    """load_triplets on a file (memory-mapped, parsed and sorted on DFCG_IO_THREADS threads)."""
+    m, n, count = i64(), i64(), i64()
+    rows, cols, vals = i64ptr(), i64ptr(), C.POINTER(C.c_double)()
+    _check(lib().dfcg_load_triplets_file(C.c_char_p(str(path).encode()), C.c_int32(1 if one_based else 0),
+                                         C.byref(m), C.byref(n), C.byref(count), C.byref(rows), C.byref(cols),
+                                         C.byref(vals)))
+    return _triplets_out(m, n, count, rows, cols, vals)
+
+
+def _obs_c(obs: Observed):
+    from ._lib import ObsC
+
+    R = np.ascontiguousarray(obs.rows, np.int64)
+    Cc = np.ascontiguousarray(obs.cols, np.int64)
+    V = np.ascontiguousarray(obs.vals, np.float64)
+    return ObsC(obs.m, obs.n, len(V), _i(R), _i(Cc), _d(V)), (R, Cc, V)
+
+
+def save_triplets(path, obs: Observed) -> None:
+    """save_triplets (matrix_io.hpp:172-179): "% m n" then "row col %.17g" per entry."""
+    oc, keep = _obs_c(obs)
+    _check(lib().dfcg_save_triplets_file(C.c_char_p(str(path).encode()), C.byref(oc)))
+    del keep
+
+
+def format_triplets(obs: Observed) -> str:
+    oc, keep = _obs_c(obs)
+    text, n = C.c_void_p(), i64()
+    _check(lib().dfcg_format_triplets(C.byref(oc), C.byref(text), C.byref(n)))
+    out = C.string_at(text, n.value).decode()
+    lib().dfcg_free(text)
+    del keep
+    return out
+
+
 def gen_recsys_instance(m, n, r, density, seed, stream=0, cols=None, fsd=None, noise=0.8):
     """BASELINE c4 stand-in (dfcg_gen_recsys_instance): Zipf row/column popularity, values
     clip(round(3.6 + A B^T + N(0, noise^2)), 1, 5), A, B iid N(0, 0.3^2 / r); `cols` restricts the
