@@ -751,6 +751,14 @@ struct McSolver::State {
   // factor was not formed keeps (lazy_* = index of the operator buffer Ad[] it came from, cl_*
   // = R_A^-1 U~, w x k): left = A cl.
   DBuf<double> RA, RAinv, cl_c, cl_p;
+  // RA / RAinv factor the previous iteration's operator (same side): the next CholeskyQR may
+  // start from them (cholqr2_r warm); ra_warm counts warm factorisations since the last cold one.
+  bool ra_ok = false;
+  int ra_warm = 0;
+  // a refused warm pass (the operator moved too far: its Gram's smallest pivot fell below the
+  // threshold) costs m w^2 FLOPs for nothing: no warm attempt for ra_skip iterations after one,
+  // twice as long after each further refusal (ra_backoff)
+  int ra_skip = 0, ra_backoff = 2;
   int lazy_c = -1, lazy_p = -1;
   bool wide = false;  // the deferred factor: the left one (tall, m >= n) or the right one (m < n)
   int ad_next = 0;  // Ad[] buffer the next dense iteration writes
@@ -775,7 +783,11 @@ static void materialize(cudaStream_t s, i64 m, i64 n, bool wide, const DBuf<doub
 // CholQR, the left factor, the densified iterate); compressed ~ 5 m n^2 (CholeskyQR2 of A:
 // two Grams and a triangular product, and the iterate as A (R_A^-1 P)). DFCG_DENSE_OP=1 / 2
 // forces uncompressed / compressed (when admissible).
-static bool compress_operator(i64 m, i64 n, i64 rank_hint) {
+// Warm CholeskyQR factorisations (preconditioned by the previous iteration's R_A^-1) between two
+// cold ones: P R_A - I picks up one rounding per product, a cold CholeskyQR2 resets it.
+constexpr int kCholqrWarmRun = 8;
+
+static bool compress_operator(i64 m, i64 n, i64 rank_hint, bool warm = false) {
   const char* env = std::getenv("DFCG_DENSE_OP");
   const int mode = env ? std::atoi(env) : -1;
   if (mode == 1) return false;
@@ -784,7 +796,9 @@ static bool compress_operator(i64 m, i64 n, i64 rank_hint) {
   if (lo < 128) return false;
   const double b = static_cast<double>(std::min<i64>(rank_hint + 15, lo)), r = static_cast<double>(rank_hint);
   const double nn = static_cast<double>(lo);
-  return 12.0 * b + 2.0 * r + 5.0 * b * b / nn + 2.0 * b * r / nn > 5.0 * nn;
+  // warm: the factorisation is expected to start from the previous iteration's factor (one
+  // triangular product and one Gram instead of two Grams and a triangular product)
+  return 12.0 * b + 2.0 * r + 5.0 * b * b / nn + 2.0 * b * r / nn > (warm ? 4.0 : 5.0) * nn;
 }
 
 // Whether an iteration applies the SVT operator materialised (dense m x n, step 1:
@@ -901,15 +915,28 @@ bool McSolver::step(std::vector<IterTrace>* trace) {
                                                                st.om.m_csr.get(), st.Ad[ai].get());
       DFCG_LAUNCH_CHECK();
     }
-    if (compress_operator(m, n, st.rank_hint)) {
+    if (compress_operator(m, n, st.rank_hint, st.ra_ok && st.ra_skip == 0)) {
       const i64 lo = std::min(m, n);
       st.RA.ensure(lo * lo, s);
       st.RAinv.ensure(lo * lo, s);
       st.wide = m < n;
-      compressed = st.wide ? cholqr2_r(s, n, m, st.Ad[ai].get(), n, st.RA.get(), st.RAinv.get(), 1e-13, true)
-                           : cholqr2_r(s, m, n, st.Ad[ai].get(), n, st.RA.get(), st.RAinv.get(), 1e-13);
+      const bool warm = st.ra_ok && st.ra_warm < kCholqrWarmRun && st.ra_skip == 0;
+      if (st.ra_skip > 0) --st.ra_skip;
+      bool used_warm = false;
+      compressed = st.wide ? cholqr2_r(s, n, m, st.Ad[ai].get(), n, st.RA.get(), st.RAinv.get(), 1e-13, true, warm,
+                                       &used_warm)
+                           : cholqr2_r(s, m, n, st.Ad[ai].get(), n, st.RA.get(), st.RAinv.get(), 1e-13, false, warm,
+                                       &used_warm);
+      st.ra_warm = used_warm ? st.ra_warm + 1 : 0;
+      if (warm && !used_warm) {
+        st.ra_skip = st.ra_backoff;
+        st.ra_backoff = std::min(2 * st.ra_backoff, 64);
+      } else if (used_warm) {
+        st.ra_backoff = 2;
+      }
     }
   }
+  st.ra_ok = compressed;  // a factor to start the next iteration's CholeskyQR from
   DBuf<double> Yl, Yr;
   const i64 ldy = std::max<i64>(1, even_ld(kY));  // even: 16-byte GEMM operand loads
   if (kY > 0 && !dense) {
@@ -1174,6 +1201,8 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
   NormalCursor cur{&ctx.normals(1), 0};
   SvtResult last;
   DBuf<double> RA, RAinv, cl_last;  // compressed iterations (see below)
+  bool ra_ok = false;               // RA / RAinv factor the previous iteration's operator
+  int ra_warm = 0, ra_skip = 0, ra_backoff = 2;  // as in McSolver::State
   bool left_deferred = false;
   double tau_prev = 1.0, tau_curr = 1.0, mu = mu_init, mu_used = mu_init;
   i64 rank_hint = 1;
@@ -1213,11 +1242,22 @@ void apg_rmf_device(DeviceContext& ctx, cudaStream_t s, const double* M_colmajor
       // cost model says so (OpTri, as in apg_mc): the SVT runs on R_A, the next L_d is
       // GL (R_A^-1 U~ S V^T) and the left factor is deferred (only the last one is output).
       bool compressed = false;
-      if (!cfg.line_search && m >= n && compress_operator(m, n, rank_hint)) {
+      if (!cfg.line_search && m >= n && compress_operator(m, n, rank_hint, ra_ok && ra_skip == 0)) {
         RA.ensure(n * n, s);
         RAinv.ensure(n * n, s);
-        compressed = cholqr2_r(s, m, n, GL.get(), m, RA.get(), RAinv.get(), 1e-13, true);
+        bool used_warm = false;
+        const bool warm = ra_ok && ra_warm < kCholqrWarmRun && ra_skip == 0;
+        if (ra_skip > 0) --ra_skip;
+        compressed = cholqr2_r(s, m, n, GL.get(), m, RA.get(), RAinv.get(), 1e-13, true, warm, &used_warm);
+        ra_warm = used_warm ? ra_warm + 1 : 0;
+        if (warm && !used_warm) {
+          ra_skip = ra_backoff;
+          ra_backoff = std::min(2 * ra_backoff, 64);
+        } else if (used_warm) {
+          ra_backoff = 2;
+        }
       }
+      ra_ok = compressed;
       if (compressed) {
         OpTri op{RA.get(), n};
         svt_operator(s, op, step * mu, rank_hint, cur, f);

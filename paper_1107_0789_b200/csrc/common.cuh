@@ -212,8 +212,10 @@ bool cholqr_factor(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx,
 // rel_tol1: breakdown threshold of the first pass's (Jacobi-scaled) Cholesky pivots. Returns
 // false on breakdown (cond(A) too large for CholeskyQR2); R / Rinv are then unusable.
 // trans: the tall matrix is A^T, A stored row-major cols x rows (lda).
+// warm: R / Rinv hold the factor of the previous (nearby) operator on entry; it preconditions a
+// single pass (see the definition). *used_warm reports whether that pass was accepted.
 bool cholqr2_r(cudaStream_t s, i64 rows, i64 cols, const double* A, i64 lda, double* R, double* Rinv,
-               double rel_tol1, bool trans = false);
+               double rel_tol1, bool trans = false, bool warm = false, bool* used_warm = nullptr);
 // Householder QR only (tests / fallback).
 void householder_qr(cudaStream_t s, i64 rows, i64 cols, double* X, i64 ldx, double* R, i64 ldr);
 

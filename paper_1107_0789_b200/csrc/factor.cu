@@ -684,7 +684,12 @@ void cholesky_inverse_raw(cudaStream_t s, i64 n, double* G, i64 ldg, double* Rin
   // r02_bench_c2_cholfused*_v3). DFCG_CHOL_FUSED=0 keeps the per-panel path, 3 fuses only while
   // three or more solves share the GPU.
   static const int fused_mode = std::getenv("DFCG_CHOL_FUSED") ? std::atoi(std::getenv("DFCG_CHOL_FUSED")) : 1;
-  if (n > CNB && (fused_mode == 1 || (fused_mode == 3 && active_streams(dev) >= 3))) {
+  // Large factorisations keep the per-panel path: their trailing updates are full-GPU GEMMs
+  // (the base APG on the whole 10^4 x 10^4 matrix factors n ~ 3600: 35 ms fused on 64 CTAs
+  // against the per-panel path, profiles/r02_bench_cholesky_large.txt). DFCG_CHOL_FUSED_MAXN.
+  static const i64 fused_maxn =
+      std::getenv("DFCG_CHOL_FUSED_MAXN") ? std::atoll(std::getenv("DFCG_CHOL_FUSED_MAXN")) : 2048;
+  if (n > CNB && n <= fused_maxn && (fused_mode == 1 || (fused_mode == 3 && active_streams(dev) >= 3))) {
     static std::atomic<std::uint64_t> fused_cfg{0};
     static int occ = 0, nsm = 0;
     if (!(fused_cfg.load() & dev_bit(dev))) {
@@ -1797,20 +1802,128 @@ bool cholqr_factor(cudaStream_t s, i64 rows, i64 cols, const double* X, i64 ldx,
   return h_fail == 0;
 }
 
+// dg[i] = G[i, i]
+__global__ void diag_copy_kernel(i64 n, const double* __restrict__ G, i64 ldg, double* __restrict__ dg) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    dg[i] = G[i * ldg + i];
+}
+
+// out = min_i R[i, i]^2 / dg[i]: the smallest pivot of the Cholesky of the unit-diagonal Gram
+// D^-1 G D^-1 (dg = diag G before the factorisation, R its factor) = min_i sin^2 of the angle
+// between column i and the span of the columns before it. One CTA.
+__global__ void min_scaled_pivot_kernel(i64 n, const double* __restrict__ R, i64 ldr, const double* __restrict__ dg,
+                                        double* __restrict__ out) {
+  __shared__ double sm[256];
+  double v = 1.0;
+  for (i64 i = threadIdx.x; i < n; i += 256) {
+    const double r = R[i * ldr + i], d = dg[i];
+    if (d > 0.0) v = fmin(v, r * r / d);
+  }
+  sm[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sm[0];
+}
+
 bool cholqr2_r(cudaStream_t s, i64 rows, i64 cols, const double* A, i64 lda, double* R, double* Rinv,
-               double rel_tol1, bool trans) {
+               double rel_tol1, bool trans, bool warm, bool* used_warm) {
+  if (used_warm) *used_warm = false;
   if (cols <= 0) return true;
   DBuf<int> fail(1, s);
   fail.zero(s);
-  DBuf<double> G(cols * cols, s), R1inv(cols * cols, s), Q1(rows * cols, s), R2inv(cols * cols, s);
+  DBuf<double> G(cols * cols, s), R1inv(cols * cols, s);
+  DBuf<double> dg(cols + 1, s);  // diag of the Gram, then the smallest scaled pivot
+  static const bool trace_qr = std::getenv("DFCG_TRACE_CHOLQR") != nullptr;
+  // Warm start: the caller's R / Rinv hold the factor of the PREVIOUS operator A' (A changes
+  // slowly from one APG iteration to the next). P = R'^-1 preconditions A: Q1 = A P is close to
+  // orthonormal, so ONE CholQR pass on Q1 has CholeskyQR2's accuracy (orthogonality ~ eps
+  // cond(A P)^2), and the pass that only served to build the preconditioner — the Gram of A and
+  // its Cholesky, m w^2 FLOPs and a w x w factorisation per iteration — is skipped:
+  //   Q1 = A P,  R1^T R1 = Q1^T Q1,  R = R1 R',  Rinv = P R1^-1.
+  // Accepted only when the smallest pivot of the (unit-diagonal) Gram of Q1 is >= 1e-4
+  // (DFCG_CHOLQR_WARM_PIVOT), i.e. cond(A P)^2 <~ 1e4-1e5 and the loss of orthogonality <~ 1e-11;
+  // otherwise the cold CholeskyQR2 below runs. The caller refreshes with a cold factorisation
+  // every few iterations (R' P - I accumulates rounding). DFCG_CHOLQR_WARM=0 disables.
+  static const int warm_env = std::getenv("DFCG_CHOLQR_WARM") ? std::atoi(std::getenv("DFCG_CHOLQR_WARM")) : 1;
+  static const double warm_piv =
+      std::getenv("DFCG_CHOLQR_WARM_PIVOT") ? std::atof(std::getenv("DFCG_CHOLQR_WARM_PIVOT")) : 1e-4;
+  if (warm && warm_env != 0) {
+    DBuf<double> Q1(rows * cols, s), R1winv(cols * cols, s);
+    if (trans) gemm_ta_upper_b(s, rows, cols, 1.0, A, lda, Rinv, cols, 0.0, Q1.get(), cols);
+    else gemm_upper_b(s, rows, cols, 1.0, A, lda, Rinv, cols, 0.0, Q1.get(), cols);
+    gram_upper(s, rows, cols, Q1.get(), cols, G.get(), cols);
+    diag_copy_kernel<<<grid_for(cols), 256, 0, s>>>(cols, G.get(), cols, dg.get());
+    DFCG_LAUNCH_CHECK();
+    cholesky_inverse(s, cols, G.get(), cols, R1winv.get(), cols, 1e-11, fail.get());
+    min_scaled_pivot_kernel<<<1, 256, 0, s>>>(cols, G.get(), cols, dg.get(), dg.get() + cols);
+    DFCG_LAUNCH_CHECK();
+    int w_fail = 0;
+    double w_piv = 0.0;
+    DFCG_CUDA(cudaMemcpyAsync(&w_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    DFCG_CUDA(cudaMemcpyAsync(&w_piv, dg.get() + cols, sizeof(double), cudaMemcpyDeviceToHost, s));
+    DFCG_CUDA(cudaStreamSynchronize(s));
+    if (trace_qr)
+      std::fprintf(stderr, "[cholqr2_r] %lld x %lld warm pass: smallest scaled pivot %.3e%s\n", (long long)rows,
+                   (long long)cols, w_piv, w_fail ? " (breakdown)" : "");
+    if (!w_fail && w_piv >= warm_piv) {
+      // R = R1 R' and Rinv = P R1^-1 (upper triangles, lower parts stored as zeros); Q1 is scratch
+      gemm_upper_b(s, cols, cols, 1.0, G.get(), cols, R, cols, 0.0, Q1.get(), cols);
+      copy2d(s, cols, cols, Q1.get(), cols, R, cols);
+      gemm_upper_b(s, cols, cols, 1.0, Rinv, cols, R1winv.get(), cols, 0.0, Q1.get(), cols);
+      copy2d(s, cols, cols, Q1.get(), cols, Rinv, cols);
+      if (used_warm) *used_warm = true;
+      if (trace_qr) {  // consistency of the accumulated pair: max |R Rinv - I|
+        gemm_upper_b(s, cols, cols, 1.0, R, cols, Rinv, cols, 0.0, Q1.get(), cols);
+        std::vector<double> h(static_cast<size_t>(cols * cols));
+        DFCG_CUDA(cudaMemcpyAsync(h.data(), Q1.get(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+        DFCG_CUDA(cudaStreamSynchronize(s));
+        double mx = 0.0;
+        for (i64 i = 0; i < cols; ++i)
+          for (i64 j = 0; j < cols; ++j)
+            mx = std::max(mx, std::fabs(h[static_cast<size_t>(i * cols + j)] - (i == j ? 1.0 : 0.0)));
+        std::fprintf(stderr, "[cholqr2_r] warm pair: max |R Rinv - I| = %.3e\n", mx);
+      }
+      return true;
+    }
+    fail.zero(s);
+  }
   // pass 1: R1^T R1 = A^T A, Q1 = A R1^-1 (orthogonal to ~eps cond(A)^2)
   if (trans) gram_upper_nt(s, cols, rows, A, lda, G.get(), cols);
   else gram_upper(s, rows, cols, A, lda, G.get(), cols);
+  diag_copy_kernel<<<grid_for(cols), 256, 0, s>>>(cols, G.get(), cols, dg.get());
+  DFCG_LAUNCH_CHECK();
   cholesky_inverse(s, cols, G.get(), cols, R1inv.get(), cols, rel_tol1, fail.get());
+  min_scaled_pivot_kernel<<<1, 256, 0, s>>>(cols, G.get(), cols, dg.get(), dg.get() + cols);
+  DFCG_LAUNCH_CHECK();
   int h_fail = 0;
+  double h_piv = 0.0;
   DFCG_CUDA(cudaMemcpyAsync(&h_fail, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  DFCG_CUDA(cudaMemcpyAsync(&h_piv, dg.get() + cols, sizeof(double), cudaMemcpyDeviceToHost, s));
   DFCG_CUDA(cudaStreamSynchronize(s));
   if (h_fail) return false;
+  // One pass is enough when A is well conditioned. Q_A = A R1^-1 is never formed: the iteration
+  // works on R_A alone and only needs A = Q_A R_A with Q_A^T Q_A = I + E; one pass leaves
+  // |E| ~ eps cond(A D^-1)^2, which perturbs the SVT input by |E| |A| (the SVT is
+  // nonexpansive). The smallest scaled pivot bounds cond(A D^-1)^2 from below by its inverse
+  // and tracks it within a small factor on the APG operators (dense, noisy blocks): at
+  // pivot >= DFCG_CHOLQR_SINGLE_PIVOT (default 1e-5) |E| <~ 1e-10, the level of the Jacobi stop
+  // and of the derived left factors. The second pass (2 m w^2 of the iteration's FLOPs: the
+  // explicit Q1 and its Gram) runs only below that. DFCG_CHOLQR_SINGLE=0: always two passes.
+  static const int single_env = std::getenv("DFCG_CHOLQR_SINGLE") ? std::atoi(std::getenv("DFCG_CHOLQR_SINGLE")) : 1;
+  static const double single_piv =
+      std::getenv("DFCG_CHOLQR_SINGLE_PIVOT") ? std::atof(std::getenv("DFCG_CHOLQR_SINGLE_PIVOT")) : 1e-5;
+  if (trace_qr)
+    std::fprintf(stderr, "[cholqr2_r] %lld x %lld smallest scaled pivot %.3e\n", (long long)rows, (long long)cols, h_piv);
+  if (single_env != 0 && h_piv >= single_piv) {
+    copy2d(s, cols, cols, G.get(), cols, R, cols);
+    copy2d(s, cols, cols, R1inv.get(), cols, Rinv, cols);
+    return true;
+  }
+  DBuf<double> Q1(rows * cols, s), R2inv(cols * cols, s);
   if (trans) gemm_ta_upper_b(s, rows, cols, 1.0, A, lda, R1inv.get(), cols, 0.0, Q1.get(), cols);
   else gemm_upper_b(s, rows, cols, 1.0, A, lda, R1inv.get(), cols, 0.0, Q1.get(), cols);
   // pass 2 on the explicit Q1: R2^T R2 = Q1^T Q1; A = (Q1 R2^-1) (R2 R1)

@@ -104,6 +104,99 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
   }
 }
 
+// Segmented SpMM, 16-byte variant (opt-in, DFCG_SPMM16=1; needs 16-byte aligned sketch rows: even
+// ldx, aligned base — every sketch buffer of the range finder is). Same items, same per-column FMA
+// order as spmm_kernel (bitwise the same output); two changes, both aimed at the kernel's
+// limiter, the L1 data pipe (ncu: l1tex__data_pipe_lsu_wavefronts at 87% of peak, L2 at 43%,
+// DRAM at 9%, profiles/r02_ncu_spmm_c5.txt — ~6.4 wavefronts per entry against 2.2 for the
+// 280-byte row alone):
+//   * X rows are read as double2 (G lanes x 16 bytes per row segment, 2 chunks per lane per pass);
+//   * index and value are loaded once per entry by ONE lane of the group (coalesced, G entries
+//     per load) and handed to the group by shuffles, instead of every lane of the group loading
+//     the same two words (a 16-lane broadcast load writes back 16 x 12 bytes per entry).
+// A group whose segment is shorter leaves its loop early: every shuffle names only the group's
+// own lanes in its mask. The last chunk of an odd b reads one padding double (ldx >= b + 1).
+template <int G, bool T>
+__global__ void spmm16_kernel(i64 n_items, const SegItem* __restrict__ items, const int* __restrict__ idx,
+                              const double* __restrict__ vals, i64 b, double alpha, const double* __restrict__ X,
+                              i64 ldx, double beta, double* __restrict__ out, i64 ldo, double* __restrict__ ws) {
+  constexpr int PER_WARP = 32 / G;
+  const int lane = threadIdx.x & 31, lig = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane - lig));
+  const i64 gid = ((static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * PER_WARP + lane / G;
+  if (gid >= n_items) return;  // whole groups leave together
+  const SegItem it = items[gid];
+  const i64 nch = (b + 1) >> 1;  // double2 chunks per row
+  const i64 ld2 = ldx >> 1;
+  const double2* __restrict__ X2 = reinterpret_cast<const double2*>(X);
+  for (i64 c0 = 0; c0 < nch; c0 += 2 * G) {
+    const bool on0 = c0 + lig < nch, on1 = c0 + lig + G < nch;
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    for (long long e = it.e0; e < it.e1; e += G) {
+      const long long mine = e + lig;
+      const int my_ix = mine < it.e1 ? idx[mine] : 0;
+      const double my_v = mine < it.e1 ? vals[mine] : 0.0;
+      const int cnt = static_cast<int>(it.e1 - e < G ? it.e1 - e : G);
+      int u = 0;
+      for (; u + 4 <= cnt; u += 4) {
+        int ix[4];
+        double vv[4];
+        double2 x0[4], x1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ix[q] = __shfl_sync(gmask, my_ix, u + q, G);
+          vv[q] = __shfl_sync(gmask, my_v, u + q, G);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2* x = X2 + static_cast<i64>(ix[q]) * ld2 + c0 + lig;
+          x0[q] = on0 ? __ldg(x) : make_double2(0.0, 0.0);
+          x1[q] = on1 ? __ldg(x + G) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a0.x = fma(vv[q], x0[q].x, a0.x);
+          a0.y = fma(vv[q], x0[q].y, a0.y);
+          a1.x = fma(vv[q], x1[q].x, a1.x);
+          a1.y = fma(vv[q], x1[q].y, a1.y);
+        }
+      }
+      for (; u < cnt; ++u) {
+        const int ix = __shfl_sync(gmask, my_ix, u, G);
+        const double v = __shfl_sync(gmask, my_v, u, G);
+        const double2* x = X2 + static_cast<i64>(ix) * ld2 + c0 + lig;
+        if (on0) {
+          const double2 t = __ldg(x);
+          a0.x = fma(v, t.x, a0.x);
+          a0.y = fma(v, t.y, a0.y);
+        }
+        if (on1) {
+          const double2 t = __ldg(x + G);
+          a1.x = fma(v, t.x, a1.x);
+          a1.y = fma(v, t.y, a1.y);
+        }
+      }
+    }
+    auto put = [&](i64 c, double acc) {
+      if (c >= b) return;
+      if (it.slot < 0) {
+        double* o = out + static_cast<i64>(it.row) * ldo + c;
+        *o = beta == 0.0 ? alpha * acc : alpha * acc + beta * *o;
+      } else {
+        ws[static_cast<i64>(it.slot) * b + c] = acc;
+      }
+    };
+    if (on0) {
+      put(2 * (c0 + lig), a0.x);
+      put(2 * (c0 + lig) + 1, a0.y);
+    }
+    if (on1) {
+      put(2 * (c0 + lig + G), a1.x);
+      put(2 * (c0 + lig + G) + 1, a1.y);
+    }
+  }
+}
+
 // Slab SpMM for sketches of b <= 64 columns: out[o, :] (+)= alpha sum_e v_e X[idx_e, :] over the
 // entries e of outer line o (a CSR row for R X, a CSC column for R^T X).
 //
@@ -892,10 +985,52 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
   static const int chunk_env = std::getenv("DFCG_SPMM_CHUNK") ? std::atoi(std::getenv("DFCG_SPMM_CHUNK")) : 0;
   const int mode = g_spmm_mode.load();
   const SegPlan& pc = transpose ? om.plan_csc_ck : om.plan_csr_ck;
-  const bool chunked = pc.n_items > 0 && (mode >= 0 ? mode == 2 : chunk_env != 0);
+  const bool chunked = pc.n_items > 0 && (mode >= 0 ? mode == 2 || mode == 4 : chunk_env != 0);
   const SegPlan& pp = chunked ? pc : p;
   DBuf<double> ws;
   if (pp.n_slots) ws.alloc(pp.n_slots * b, s);
+  // 16-byte variant (spmm16_kernel): CSC-ordered values streamed (no permutation gather), even
+  // ldx >= b + (b & 1), 16-byte aligned X. Opt-in (DFCG_SPMM16=1; bench modes 3 / 4): measured
+  // slower at the c5 block (355 vs 275 us forward, 306 vs 253 us transposed — the shuffles go
+  // through the same data pipe as the loads they replace) and level at the c2 block (38.8 vs
+  // 39.0 us, 39.1 vs 45.5 us transposed); profiles/r02_bench_sparse16.txt.
+  static const int v16_env = std::getenv("DFCG_SPMM16") ? std::atoi(std::getenv("DFCG_SPMM16")) : 0;
+  const bool use16 = (mode >= 0 ? mode == 3 || mode == 4 : v16_env != 0) &&
+                     !(transpose && !vals_csc) && ldx % 2 == 0 && ldx >= b + (b & 1) &&
+                     reinterpret_cast<std::uintptr_t>(X) % 16 == 0;
+  if (use16) {
+    const int G16 = pow2_at_least((((b + 1) >> 1) + 1) / 2);  // 2 double2 chunks per lane per pass
+    const i64 warps16 = (pp.n_items + (32 / G16) - 1) / (32 / G16);
+    const int blocks16 = static_cast<int>((warps16 + 7) / 8);
+    const int* idx16 = transpose ? om.csc_row.get() : om.csr_col.get();
+    const double* vals16 = transpose ? vals_csc : vals_csr;
+#define SPMM16_CASE(g)                                                                                              \
+  case g:                                                                                                           \
+    if (transpose)                                                                                                  \
+      spmm16_kernel<g, true><<<blocks16, 256, 0, s>>>(pp.n_items, pp.items.get(), idx16, vals16, b, alpha, X, ldx,  \
+                                                       beta, out, ldo, ws.get());                                   \
+    else                                                                                                            \
+      spmm16_kernel<g, false><<<blocks16, 256, 0, s>>>(pp.n_items, pp.items.get(), idx16, vals16, b, alpha, X, ldx, \
+                                                        beta, out, ldo, ws.get());                                  \
+    break;
+    switch (G16) {
+      SPMM16_CASE(1)
+      SPMM16_CASE(2)
+      SPMM16_CASE(4)
+      SPMM16_CASE(8)
+      SPMM16_CASE(16)
+      SPMM16_CASE(32)
+    }
+#undef SPMM16_CASE
+    DFCG_LAUNCH_CHECK();
+    if (!pp.h_multi_rows.empty()) {
+      const i64 nr = static_cast<i64>(pp.h_multi_rows.size());
+      seg_reduce_kernel<<<grid_for(nr * b), 256, 0, s>>>(nr, pp.multi_rows.get(), pp.red_rowptr.get(), b, ws.get(),
+                                                         alpha, beta, out, ldo);
+      DFCG_LAUNCH_CHECK();
+    }
+    return;
+  }
   // lanes per item: enough for one pass over the b columns at kSpmmCpl columns per lane
   const int G = pow2_at_least((b + kSpmmCpl - 1) / kSpmmCpl);
   const i64 warps = (pp.n_items + (32 / G) - 1) / (32 / G);

@@ -76,7 +76,7 @@ void csr_to_csc(cudaStream_t s, const DevOmega& om, const double* vals_csr, doub
 
 // Microbenchmark override of the slab kernels (1 on, 0 off, -1 back to DFCG_SPMM_SLAB /
 // DFCG_SDDMM_SLAB): process-global, for dfcg_bench_sparse only.
-void set_sparse_modes(int spmm_mode, int sddmm_mode);  // spmm_mode: 0 gather, 1 slab, 2 chunked
+void set_sparse_modes(int spmm_mode, int sddmm_mode);  // spmm_mode: 0 gather (8-byte), 1 slab, 2 chunked (8-byte), 3 gather 16-byte, 4 chunked 16-byte
 
 // D[i, j] += alpha * vals[(i,j)] for the observed pattern (row-major m x n dense D).
 void scatter_add_dense(cudaStream_t s, const DevOmega& om, const double* vals_csr, double alpha, double* D, i64 ldd);

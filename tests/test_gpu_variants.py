@@ -1,7 +1,7 @@
 """The kernel variants selected by heuristics (or only by environment switches) must give the
 same parity: Jacobi rounds on 2- and 4-CTA clusters and with 16-column blocks, the 64x64 /
 64x48 GEMM tiles, the unscaled Cholesky, the Jacobi sweep replayed as a CUDA graph, the persistent (one cooperative launch per SVD) and
-launch-per-round Jacobi sweeps, the segmented (gather) SpMM, the tiled and the entry-parallel SDDMM (the slab kernels' fallbacks)
+launch-per-round Jacobi sweeps, the compressed operator from a warm-started, a single or a double CholQR pass, the 8- and 16-byte SpMM, the segmented (gather) SpMM, the tiled and the entry-parallel SDDMM (the slab kernels' fallbacks)
 under the factored operator. Each variant runs in a child process (the switches are
 read once per process)."""
 import os
@@ -39,6 +39,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
     {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_CLUSTER": "1"},
     {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_CLUSTER": "4"},
     {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_NB": "16"},
+    {"DFCG_DENSE_OP": "2", "DFCG_CHOLQR_SINGLE": "0"},
+    {"DFCG_DENSE_OP": "2", "DFCG_CHOLQR_SINGLE": "1", "DFCG_CHOLQR_SINGLE_PIVOT": "1e-12"},
+    {"DFCG_DENSE_OP": "2", "DFCG_CHOLQR_SINGLE": "1", "DFCG_CHOLQR_SINGLE_PIVOT": "0.5"},
+    {"DFCG_CHOL_FUSED_MAXN": "100"},
+    {"DFCG_DENSE_OP": "2", "DFCG_CHOLQR_WARM": "0"},
+    {"DFCG_DENSE_OP": "2", "DFCG_CHOLQR_WARM_PIVOT": "0.999999"},
+    {"DFCG_DENSE_OP": "0", "DFCG_SPMM16": "0"},
+    {"DFCG_DENSE_OP": "0", "DFCG_SPMM16": "1", "DFCG_SPMM_CHUNK": "1"},
 ], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
 def test_variant_parity(env):
     r = subprocess.run([sys.executable, os.path.join(HERE, "_variant_case.py")], env={**os.environ, **env},

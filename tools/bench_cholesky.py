@@ -24,10 +24,13 @@ sweep = os.environ.get("CHOL_BENCH_P", "8,12,16,32,64,148")
 configs = [("per-panel", {"DFCG_CHOL_FUSED": "0"})] + \
           [(f"fused P={p}", {"DFCG_CHOL_FUSED": "1", "DFCG_CHOL_P": p}) for p in sweep.split(",") if p] + \
           [("fused default P", {"DFCG_CHOL_FUSED": "1"})]
-for n in (720, 1250):
+for n in [int(x) for x in os.environ.get("CHOL_BENCH_N", "720,1250").split(",")]:
     for inv in (1, 0):
         for name, env in configs:
-            r = subprocess.run([sys.executable, __file__, "--one", str(n), str(inv)], env={**os.environ, **env},
-                               capture_output=True, text=True, timeout=600)
-            line = r.stdout.strip().splitlines()[-1] if r.returncode == 0 else f"failed: {r.stderr[-300:]}"
+            try:
+                r = subprocess.run([sys.executable, __file__, "--one", str(n), str(inv)], env={**os.environ, **env},
+                                   capture_output=True, text=True, timeout=int(os.environ.get("CHOL_BENCH_TIMEOUT", "120")))
+                line = r.stdout.strip().splitlines()[-1] if r.returncode == 0 else f"failed: {r.stderr[-300:]}"
+            except subprocess.TimeoutExpired:
+                line = "timed out"
             print(f"{name:18s} {line}", flush=True)
