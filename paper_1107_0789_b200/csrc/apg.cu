@@ -785,7 +785,8 @@ static void materialize(cudaStream_t s, i64 m, i64 n, bool wide, const DBuf<doub
 // forces uncompressed / compressed (when admissible).
 // Warm CholeskyQR factorisations (preconditioned by the previous iteration's R_A^-1) between two
 // cold ones: P R_A - I picks up one rounding per product, a cold CholeskyQR2 resets it.
-constexpr int kCholqrWarmRun = 8;
+static const int kCholqrWarmRun =
+    std::getenv("DFCG_CHOLQR_WARM_RUN") ? std::max(0, std::atoi(std::getenv("DFCG_CHOLQR_WARM_RUN"))) : 8;
 
 static bool compress_operator(i64 m, i64 n, i64 rank_hint, bool warm = false) {
   const char* env = std::getenv("DFCG_DENSE_OP");

@@ -50,7 +50,7 @@ __global__ void sddmm_kernel(i64 N, i64 kY, const int* __restrict__ row, const i
 
 // Segmented SpMM. transpose=false: items walk CSR rows, structure idx = csr_col, value t.
 // transpose=true: items walk CSC columns, idx = csc_row, value csc2csr[e].
-template <int G, bool T>
+template <int G, bool T, int CPL = kSpmmCpl>
 __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, const int* __restrict__ idx,
                             const long long* __restrict__ perm, const double* __restrict__ vals, i64 b, double alpha,
                             const double* __restrict__ X, i64 ldx, double beta, double* __restrict__ out, i64 ldo,
@@ -60,7 +60,7 @@ __global__ void spmm_kernel(i64 n_items, const SegItem* __restrict__ items, cons
   const i64 gid = ((static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * PER_WARP + lane / G;
   if (gid >= n_items) return;
   const SegItem it = items[gid];
-  constexpr int CPL = kSpmmCpl;  // columns per lane per pass: one walk of the segment covers CPL G columns
+  // CPL columns per lane per pass: one walk of the segment covers CPL G columns
   for (i64 c0 = 0; c0 < b; c0 += CPL * G) {
     double acc[CPL];
 #pragma unroll
@@ -1022,6 +1022,43 @@ void spmm(cudaStream_t s, const DevOmega& om, bool transpose, const double* vals
       SPMM16_CASE(32)
     }
 #undef SPMM16_CASE
+    DFCG_LAUNCH_CHECK();
+    if (!pp.h_multi_rows.empty()) {
+      const i64 nr = static_cast<i64>(pp.h_multi_rows.size());
+      seg_reduce_kernel<<<grid_for(nr * b), 256, 0, s>>>(nr, pp.multi_rows.get(), pp.red_rowptr.get(), b, ws.get(),
+                                                         alpha, beta, out, ldo);
+      DFCG_LAUNCH_CHECK();
+    }
+    return;
+  }
+  // Wide variant (bench mode 5 / DFCG_SPMM_WIDE=1): 2 columns per lane, so b = 35 takes one item per
+  // warp (32 contiguous lanes on the row's first 256 bytes) instead of two half-warp items.
+  static const int wide_env = std::getenv("DFCG_SPMM_WIDE") ? std::atoi(std::getenv("DFCG_SPMM_WIDE")) : 0;
+  if (mode >= 0 ? mode == 5 : wide_env != 0) {
+    const int GW = pow2_at_least((b + 1) / 2);
+    const i64 warpsw = (pp.n_items + (32 / GW) - 1) / (32 / GW);
+    const int blocksw = static_cast<int>((warpsw + 7) / 8);
+    const int* idxw = transpose ? om.csc_row.get() : om.csr_col.get();
+    const double* valsw = transpose && vals_csc ? vals_csc : vals_csr;
+    const long long* permw = transpose && !vals_csc ? om.csc2csr.get() : nullptr;
+#define SPMMW_CASE(g)                                                                                              \
+  case g:                                                                                                          \
+    if (transpose)                                                                                                 \
+      spmm_kernel<g, true, 2><<<blocksw, 256, 0, s>>>(pp.n_items, pp.items.get(), idxw, permw, valsw, b, alpha, X,  \
+                                                       ldx, beta, out, ldo, ws.get());                             \
+    else                                                                                                           \
+      spmm_kernel<g, false, 2><<<blocksw, 256, 0, s>>>(pp.n_items, pp.items.get(), idxw, permw, valsw, b, alpha, X, \
+                                                        ldx, beta, out, ldo, ws.get());                            \
+    break;
+    switch (GW) {
+      SPMMW_CASE(1)
+      SPMMW_CASE(2)
+      SPMMW_CASE(4)
+      SPMMW_CASE(8)
+      SPMMW_CASE(16)
+      SPMMW_CASE(32)
+    }
+#undef SPMMW_CASE
     DFCG_LAUNCH_CHECK();
     if (!pp.h_multi_rows.empty()) {
       const i64 nr = static_cast<i64>(pp.h_multi_rows.size());

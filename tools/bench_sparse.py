@@ -34,7 +34,7 @@ for name, o, b, kY in cases:
           "sddmm": 24.0 * N + 8.0 * (m + n) * kY}
     res = {}
     # (spmm mode, sddmm mode): 0 = gather SpMM / tiled SDDMM, 1 = slab kernels, 2 = chunked SpMM
-    for key, (ms_mode, sd_mode) in {"gather": (0, 0), "slab": (1, 1), "chunked": (2, 0), "gather16": (3, 0), "chunked16": (4, 0)}.items():
+    for key, (ms_mode, sd_mode) in {"gather": (0, 0), "slab": (1, 1), "chunked": (2, 0), "gather16": (3, 0), "chunked16": (4, 0), "wide": (5, 0)}.items():
         ms = (C.c_double * 3)()
         sm = (C.c_double * 3)()
         L._check(L.lib().dfcg_bench_sparse(L.context(0), C.byref(oc), C.c_int64(b), C.c_int64(kY), C.c_int32(reps),
