@@ -869,9 +869,25 @@ void sddmm_residual(cudaStream_t s, const DevOmega& om, i64 kY, const double* Yl
       ldl = ldr = k2;
     }
     static const int tw_env = std::getenv("DFCG_SDDMM_TW") ? std::atoi(std::getenv("DFCG_SDDMM_TW")) : 0;
-    const bool wide = tw_env ? tw_env == 4 : k2 <= 32;
+    const bool wide = tw_env == 4;
     const unsigned gy = static_cast<unsigned>((om.m + STR - 1) / STR);
-    if (wide)
+    // Tile width at kY <= 32 (16-wide k chunks): 64 x 128 tiles (49 KB of shared memory, four CTAs
+    // per SM) — the tiled kernel is latency-bound (ncu: no pipe above 45 %, occupancy 24 % with
+    // the 82 KB 64 x 256 tiles, profiles/r02_ncu_sddmm_c5.txt), and the narrower tile measured
+    // 336 vs 435 us at the c5 block and 26.8 vs 34.9 us at the c2 block; 64 x 64 tiles (434 /
+    // 28.8 us), 64 x 192 (461 / 35.6 us) and single-buffered 32-wide chunks (406-502 us) are
+    // slower (profiles/r02_bench_sddmm_tiles.txt). DFCG_SDDMM_TW=4 keeps 64 x 256, 1 forces
+    // the 64 x 64 / 32-wide kernel of kY > 32.
+    if (tw_env ? tw_env == 2 : k2 <= 32) {
+      static std::atomic<std::uint64_t> cfg2{0};
+      if (!(cfg2.load() & dev_bit(dev))) {
+        DFCG_CUDA(cudaFuncSetAttribute(sddmm_tile_kernel<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sddmm_smem<2, 16>())));
+        cfg2.fetch_or(dev_bit(dev));
+      }
+      sddmm_tile_kernel<2, 16><<<dim3((om.ntc + 1) / 2, gy), SDD_T, sddmm_smem<2, 16>(), s>>>(
+          om.m, om.n, k2, om.ntc, om.tile_csr.get(), om.csr_col.get(), Yl, ldl, Yr, ldr, sub, r_csr);
+    } else if (wide)
       sddmm_tile_kernel<4, 16><<<dim3((om.ntc + 3) / 4, gy), SDD_T, sddmm_smem<4, 16>(), s>>>(
           om.m, om.n, k2, om.ntc, om.tile_csr.get(), om.csr_col.get(), Yl, ldl, Yr, ldr, sub, r_csr);
     else
