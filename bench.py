@@ -377,15 +377,26 @@ def run_reference(args, wl):
                 warmup=args.warmup, ms_per_step=1e3 * dt / max(done, 1), higher_is_better=True,
                 scaling="strong", vs_baseline=None, dtype="f64",
                 data="synthetic (oracle restatement of the reference generator gen_mc_instance, seed 1)",
-                config=dict(workload=f"{args.workload}: DFC-Proj MC {wl['m']}x{wl['n']} r={wl['r']} "
-                                     f"{wl['s']} obs sigma={wl['sigma']} t={wl['t']} default ApgConfig",
-                            window=window, prologue_s=round(pro_s, 1),
-                            ranks=[t["rank"] for t in tr]),
+                config=bench_config(args, wl),
+                execution=dict(blocks="block 0 (10000x1250) alone: a bounded sample of the workload, the unit "
+                                      "is one APG iteration on one block", window=window,
+                               prologue_s=round(pro_s, 1), ranks=[t["rank"] for t in tr]),
                 cpu_baseline=dict(value=value, unit=UNIT, cores=threads, kind="port",
                                   sample=f"{window}; oracle/ restatement of apg_mc (single-threaded sparse "
                                          f"ops as in the reference, OpenBLAS/LAPACK with {threads} threads)"),
                 e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
+
+
+def bench_config(args, wl):
+    """The `config` of the JSON line: the same dict in both arms (the reference arm measures the
+    GPU arm's workload and window; what differs between the arms is under `execution`)."""
+    first = args.prologue + args.warmup + 1
+    return dict(workload=f"{args.workload}: DFC-Proj MC {wl['m']}x{wl['n']} r={wl['r']} "
+                         f"{wl['s']} obs sigma={wl['sigma']} t={wl['t']} default ApgConfig",
+                window=f"APG iterations {first}..{first + args.steps - 1} of a block (one step = one "
+                       f"iteration; the unit is one iteration of one {wl['m']}x{wl['n'] // wl['t']} block)",
+                l2="inputs > L2 (no flush)")
 
 
 def step_roofline(w0, w1, ms, steps, peaks, peak_kind):
@@ -620,14 +631,11 @@ def main():
         line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
                     ms_per_step=ms / max(args.steps, 1), higher_is_better=True, scaling="strong", vs_baseline=None,
                     dtype="f64", data="synthetic (reference generator gen_mc_instance, seed 1)",
-                    config=dict(workload=f"{args.workload}: DFC-Proj MC {wl['m']}x{wl['n']} r={wl['r']} "
-                                         f"{wl['s']} obs sigma={wl['sigma']} t={wl['t']} default ApgConfig",
-                                window=f"APG iterations {args.prologue + args.warmup + 1}.."
-                                       f"{args.prologue + args.warmup + args.steps} of every block",
-                                blocks_per_gpu=len(mine), l2="inputs > L2 (no flush)",
-                                parallelism=f"{wl['t']} blocks over {world} GPU(s) (LPT by nnz), one CUDA "
-                                            f"stream per block; combine over libdfcg's "
-                                            f"{'NCCL' if backend == 'nccl' or world == 1 else 'host'} transport"),
+                    config=bench_config(args, wl),
+                    execution=dict(blocks="every block", blocks_per_gpu=len(mine),
+                                   parallelism=f"{wl['t']} blocks over {world} GPU(s) (LPT by nnz), one CUDA "
+                                               f"stream per block; combine over libdfcg's "
+                                               f"{'NCCL' if backend == 'nccl' or world == 1 else 'host'} transport"),
                     roofline=roof, roofline_step=roof_step, roofline_gemm=roof_gemm, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
                     clocks=clocks.summary(), combine_ms=combine_ms,
                     combine=dict(ms=combine_ms, device_ops=combine_ops,
