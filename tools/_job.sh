@@ -1,3 +1,4 @@
 set -x
-timeout 1500 python tools/probe_c5_sweep.py > gpurun_out/s4_c5_sweep.txt 2>&1; grep -v '"config"' gpurun_out/s4_c5_sweep.txt | cut -c1-420
-timeout 1200 python tools/probe_c4_full.py > gpurun_out/s4_c4_full.txt 2>&1; tail -2 gpurun_out/s4_c4_full.txt | cut -c1-600
+timeout 1800 python -m pytest tests -m gpu -q --durations=5 > gpurun_out/s4_gputest_final2.log 2>&1; tail -4 gpurun_out/s4_gputest_final2.log
+timeout 900 python bench.py > gpurun_out/s4_bench_final2.json 2> gpurun_out/s4_bench_final2.err; tail -c 300 gpurun_out/s4_bench_final2.err
+python -c "import __graft_entry__ as g; g.smoke()"
