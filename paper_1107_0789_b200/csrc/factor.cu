@@ -1910,12 +1910,13 @@ bool cholqr2_r(cudaStream_t s, i64 rows, i64 cols, const double* A, i64 lda, dou
   // |E| ~ eps cond(A D^-1)^2, which perturbs the SVT input by |E| |A| (the SVT is
   // nonexpansive). The smallest scaled pivot bounds cond(A D^-1)^2 from below by its inverse
   // and tracks it within a small factor on the APG operators (dense, noisy blocks): at
-  // pivot >= DFCG_CHOLQR_SINGLE_PIVOT (default 1e-5) |E| <~ 1e-10, the level of the Jacobi stop
-  // and of the derived left factors. The second pass (2 m w^2 of the iteration's FLOPs: the
-  // explicit Q1 and its Gram) runs only below that. DFCG_CHOLQR_SINGLE=0: always two passes.
+  // pivot >= DFCG_CHOLQR_SINGLE_PIVOT (default 1e-4, the warm pass's threshold) |E| <~ 1e-11. The
+  // second pass (2 m w^2 of the iteration's FLOPs: the explicit Q1 and its Gram) runs only below
+  // that — always at a c2 block, whose operator's smallest pivot is ~1e-8 (the warm start above is
+  // what saves the pass there). DFCG_CHOLQR_SINGLE=0: always two passes.
   static const int single_env = std::getenv("DFCG_CHOLQR_SINGLE") ? std::atoi(std::getenv("DFCG_CHOLQR_SINGLE")) : 1;
   static const double single_piv =
-      std::getenv("DFCG_CHOLQR_SINGLE_PIVOT") ? std::atof(std::getenv("DFCG_CHOLQR_SINGLE_PIVOT")) : 1e-5;
+      std::getenv("DFCG_CHOLQR_SINGLE_PIVOT") ? std::atof(std::getenv("DFCG_CHOLQR_SINGLE_PIVOT")) : 1e-4;
   if (trace_qr)
     std::fprintf(stderr, "[cholqr2_r] %lld x %lld smallest scaled pivot %.3e\n", (long long)rows, (long long)cols, h_piv);
   if (single_env != 0 && h_piv >= single_piv) {
