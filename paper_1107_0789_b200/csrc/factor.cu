@@ -1683,17 +1683,51 @@ __global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
 // executed.
 template <int NB, int CS>
 __global__ void __launch_bounds__(256, NB == 8 ? 2 : 1)
-    jacobi_sweeps_kernel(const JacobiArgs* __restrict__ ja, double stop_tol, int max_sweeps, int* sweeps_out) {
+    jacobi_sweeps_kernel(const JacobiArgs* __restrict__ ja, double stop_tol, int max_sweeps, int* sweeps_out,
+                         unsigned* __restrict__ ver) {
   cg::grid_group grid = cg::this_grid();
   const int p = ja->p;
   int sweep = 0;
+  // ver != nullptr: point-to-point ordering between rounds instead of a grid barrier. ver[b]
+  // counts the CTAs that have finished a round on column block b (CS per round): the CTA that
+  // takes (bi, bj) in a round waits until both blocks carry every earlier round, and publishes
+  // them when its own writes are out. A block is touched by one cluster per round, so this is
+  // the only ordering the rounds need; the grid barrier stays at the end of each sweep (the
+  // sweep's largest cosine must be complete before the stop test).
+  unsigned gen = 0;  // rounds finished so far
+  const int pk = static_cast<int>(blockIdx.x / CS);
   while (sweep < max_sweeps) {
     unsigned long long* slot = ja->offmax + sweep % 3;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(ja->offmax + (sweep + 1) % 3, 0ull);
     for (int r = 0; r < p - 1; ++r) {
-      jacobi_round_body<NB, CS, false>(ja, slot, r, r == 0 ? 1 : 0);
-      grid.sync();
+      if (ver) {
+        auto ring = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 - r) % (p - 1) + (p - 1)) % (p - 1); };
+        const int bi = ring(pk), bj = ring(p - 1 - pk);
+        if (threadIdx.x == 0) {
+          const unsigned need = static_cast<unsigned>(CS) * gen;
+          unsigned v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ver + bi) : "memory");
+          } while (v < need);
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ver + bj) : "memory");
+          } while (v < need);
+        }
+        __syncthreads();
+        jacobi_round_body<NB, CS, false>(ja, slot, r, r == 0 ? 1 : 0);
+        __syncthreads();  // every thread's stores of this round are issued
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(ver + bi, 1u);
+          atomicAdd(ver + bj, 1u);
+        }
+        ++gen;
+      } else {
+        jacobi_round_body<NB, CS, false>(ja, slot, r, r == 0 ? 1 : 0);
+        grid.sync();
+      }
     }
+    if (ver) grid.sync();
     ++sweep;
     const double off = __longlong_as_double(static_cast<long long>(__ldcg(slot)));
     if (off <= stop_tol) break;
@@ -2297,6 +2331,15 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       DBuf<unsigned long long> offs(3, s);
       DBuf<int> nsw(1, s);
       offs.zero(s);
+      // point-to-point round ordering (block version counters) instead of a grid barrier per
+      // round; DFCG_JACOBI_P2P=0 keeps the barriers
+      static const int p2p_env = std::getenv("DFCG_JACOBI_P2P") ? std::atoi(std::getenv("DFCG_JACOBI_P2P")) : 1;
+      DBuf<unsigned> vers;
+      if (p2p_env != 0) {
+        vers.alloc(p, s);
+        vers.zero(s);
+      }
+      unsigned* verp = p2p_env != 0 ? vers.get() : nullptr;
       const JacobiArgs pa{wrows, nj, np, np, W.get(), J.get(), offs.get(), tol, p, prefetch_v};
       DFCG_CUDA(cudaMemcpyAsync(d_args, &pa, sizeof(JacobiArgs), cudaMemcpyHostToDevice, s));
       const double per_sweep_flops = (p - 1.0) * npairs * (2.0 * wrows + 2.0 * (wrows + nj)) * JW * JW;
@@ -2328,7 +2371,7 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
         const int maxsw = 60;
         int* so = nsw.get();
         cudaError_t lerr = cudaSuccess;
-#define DFCG_JSWEEPS(nb, cs) lerr = cudaLaunchKernelEx(&cfg, jacobi_sweeps_kernel<nb, cs>, ap, stol, maxsw, so)
+#define DFCG_JSWEEPS(nb, cs) lerr = cudaLaunchKernelEx(&cfg, jacobi_sweeps_kernel<nb, cs>, ap, stol, maxsw, so, verp)
         if (NB == 8) {
           if (CS == 1) DFCG_JSWEEPS(8, 1);
           else if (CS == 2) DFCG_JSWEEPS(8, 2);
