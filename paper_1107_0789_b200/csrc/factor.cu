@@ -2331,9 +2331,11 @@ void thin_svd(cudaStream_t s, i64 rows, i64 cols, double* A, i64 lda, double* U,
       DBuf<unsigned long long> offs(3, s);
       DBuf<int> nsw(1, s);
       offs.zero(s);
-      // point-to-point round ordering (block version counters) instead of a grid barrier per
-      // round; DFCG_JACOBI_P2P=0 keeps the barriers
-      static const int p2p_env = std::getenv("DFCG_JACOBI_P2P") ? std::atoi(std::getenv("DFCG_JACOBI_P2P")) : 1;
+      // DFCG_JACOBI_P2P=1: point-to-point round ordering (block version counters) instead of a
+      // grid barrier per round. Measured level with the barriers (8.47 vs 8.43 ms of Jacobi per
+      // lone c2 iteration, profiles/r02_lone_jacobi_p2p.txt): the round's own serial chain, not
+      // the barrier, is what a sweep waits for. Opt-in.
+      static const int p2p_env = std::getenv("DFCG_JACOBI_P2P") ? std::atoi(std::getenv("DFCG_JACOBI_P2P")) : 0;
       DBuf<unsigned> vers;
       if (p2p_env != 0) {
         vers.alloc(p, s);

@@ -39,8 +39,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
     {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_CLUSTER": "1"},
     {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_CLUSTER": "4"},
     {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_NB": "16"},
-    {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_P2P": "0"},
-    {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_P2P": "0", "DFCG_JACOBI_CLUSTER": "2"},
+    {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_P2P": "1"},
+    {"DFCG_JACOBI_PERSIST": "1", "DFCG_JACOBI_P2P": "1", "DFCG_JACOBI_CLUSTER": "2"},
     {"DFCG_DENSE_OP": "2", "DFCG_CHOLQR_SINGLE": "0"},
     {"DFCG_DENSE_OP": "2", "DFCG_CHOLQR_SINGLE": "1", "DFCG_CHOLQR_SINGLE_PIVOT": "1e-12"},
     {"DFCG_DENSE_OP": "2", "DFCG_CHOLQR_SINGLE": "1", "DFCG_CHOLQR_SINGLE_PIVOT": "0.5"},
