@@ -858,6 +858,7 @@ McSolver::~McSolver() = default;
 bool McSolver::step(std::vector<IterTrace>* trace) {
   if (stopped_ || iters_ >= cfg_.max_iters) return false;
   ActiveSolve busy(ctx_.device);
+  prof::NvtxRange nvtx_iteration("apg_mc iteration");
   // ncu --profile-from-start off: DFCG_PROFILE_ITER=k brackets iteration k of every solve.
   static const int profile_iter = std::getenv("DFCG_PROFILE_ITER") ? std::atoi(std::getenv("DFCG_PROFILE_ITER")) : -1;
   struct ProfRange {

@@ -1,6 +1,9 @@
 // Kernel accounting (see prof.hpp) and its C ABI (dfcg_prof_*, declared in include/dfcg_host.h).
 #include "prof.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -24,8 +27,23 @@ std::mutex g_mu;
 std::vector<Rec> g_recs;
 }  // namespace
 
+// DFCG_NVTX=1: every scope is also an NVTX range named after its op class (and every APG
+// iteration one, see nvtx_push / nvtx_pop), so an nsys / ncu timeline shows the phases of each
+// solve on its host thread. Header-only NVTX v3: a no-op unless a tool injects itself.
+static const bool g_nvtx = std::getenv("DFCG_NVTX") && std::atoi(std::getenv("DFCG_NVTX")) != 0;
+static const char* const kOpNames[kNumOps] = {"gemm",   "sddmm",       "spmm",   "cholesky", "qr_fallback",
+                                              "jacobi", "elementwise", "reduce", "other",    "gemm_small"};
+
+void nvtx_push(const char* name) {
+  if (g_nvtx) nvtxRangePushA(name);
+}
+void nvtx_pop() {
+  if (g_nvtx) nvtxRangePop();
+}
+
 Scope::Scope(Op op, cudaStream_t s, double flops, double bytes, int launches)
     : op_(op), s_(s), flops_(flops), bytes_(bytes), launches_(launches) {
+  if (g_nvtx) nvtxRangePushA(kOpNames[op]);
   g_work_flops[op].fetch_add(static_cast<long long>(flops), std::memory_order_relaxed);
   g_work_bytes[op].fetch_add(static_cast<long long>(bytes), std::memory_order_relaxed);
   g_work_launches[op].fetch_add(launches, std::memory_order_relaxed);
@@ -46,6 +64,7 @@ void Scope::add_work(double flops, double bytes, int launches) {
 }
 
 Scope::~Scope() {
+  if (g_nvtx) nvtxRangePop();
   if (!on_) return;
   cudaEventRecord(e1_, s_);
   std::lock_guard<std::mutex> lock(g_mu);

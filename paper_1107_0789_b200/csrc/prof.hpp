@@ -32,6 +32,16 @@ extern std::atomic<long long> g_launches;
 // no events): bench.py reads them around its timed window for the packed-step roofline.
 extern std::atomic<long long> g_work_flops[kNumOps], g_work_bytes[kNumOps], g_work_launches[kNumOps];
 
+// NVTX ranges on the calling host thread when DFCG_NVTX=1 (no-ops otherwise)
+void nvtx_push(const char* name);
+void nvtx_pop();
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtx_push(name); }
+  ~NvtxRange() { nvtx_pop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // RAII scope: records start/stop events on `s` when profiling is enabled.
