@@ -784,9 +784,11 @@ static void materialize(cudaStream_t s, i64 m, i64 n, bool wide, const DBuf<doub
 // two Grams and a triangular product, and the iterate as A (R_A^-1 P)). DFCG_DENSE_OP=1 / 2
 // forces uncompressed / compressed (when admissible).
 // Warm CholeskyQR factorisations (preconditioned by the previous iteration's R_A^-1) between two
-// cold ones: P R_A - I picks up one rounding per product, a cold CholeskyQR2 resets it.
+// cold ones: P R_A - I picks up one rounding per product, a cold CholeskyQR2 resets it. Over a
+// whole c2 block solve (496 iterations, profiles/r02_warmqr_full_solve.txt): runs of 8 leave
+// max |R_A R_A^-1 - I| = 4.9e-11, runs of 16 6.3e-11 (no warm pass refused, smallest pivot 4.9e-3).
 static const int kCholqrWarmRun =
-    std::getenv("DFCG_CHOLQR_WARM_RUN") ? std::max(0, std::atoi(std::getenv("DFCG_CHOLQR_WARM_RUN"))) : 8;
+    std::getenv("DFCG_CHOLQR_WARM_RUN") ? std::max(0, std::atoi(std::getenv("DFCG_CHOLQR_WARM_RUN"))) : 16;
 
 static bool compress_operator(i64 m, i64 n, i64 rank_hint, bool warm = false) {
   const char* env = std::getenv("DFCG_DENSE_OP");
