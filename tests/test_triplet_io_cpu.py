@@ -217,3 +217,92 @@ def test_load_feeds_the_d_step(tmp_path):
 def test_missing_file():
     with pytest.raises(P.DfcError, match="cannot open"):
         P.load_triplets("/nonexistent/dir/x.txt")
+
+
+# ---- fuzz: the parser against a character-level restatement of the istream extraction
+import random  # noqa: E402
+import re  # noqa: E402
+
+def _istream_int(s, pos):
+    # mimic istream >> long: skip ws, optional sign, digits
+    n=len(s)
+    while pos<n and s[pos] in ' \t\r\v\f\n': pos+=1
+    q=pos
+    if q<n and s[q] in '+-': q+=1
+    d=q
+    while q<n and s[q].isdigit(): q+=1
+    if q==d: return None,pos
+    return int(s[pos:q]), q
+def _istream_dbl(s,pos):
+    n=len(s)
+    while pos<n and s[pos] in ' \t\r\v\f\n': pos+=1
+    m=re.match(r'[+-]?(\d+\.?\d*|\.\d+)([eE][+-]?\d+)?', s[pos:])
+    if not m: return None,pos
+    # "1e" -> failure
+    rest=s[pos+m.end():]
+    if re.match(r'[eE]', rest): return None,pos
+    v=float(m.group(0))
+    if v in (float('inf'),float('-inf')): return None,pos
+    return v,pos+m.end()
+def _fuzz_ref(text, one_based):
+    base=1 if one_based else 0
+    m=n=-1; obs=[]; seen=False
+    for ln,line in enumerate(text.split('\n'),1):
+        toks=line.split()
+        if not toks: continue
+        if toks[0]=='%':
+            if seen or m>=0: return ('parse',ln)
+            p=line.index('%')+1
+            a,p=_istream_int(line,p)
+            if a is None: return ('parse',ln)
+            b,p=_istream_int(line,p)
+            if b is None or a<1 or b<1: return ('parse',ln)
+            if line[p:].strip(): return ('parse',ln)
+            m,n=a,b; continue
+        i,p=_istream_int(line,0)
+        if i is None: return ('parse',ln)
+        j,p=_istream_int(line,p)
+        if j is None: return ('parse',ln)
+        v,p=_istream_dbl(line,p)
+        if v is None: return ('parse',ln)
+        if line[p:].strip(): return ('parse',ln)
+        i-=base; j-=base
+        if i<0 or j<0: return ('parse',ln)
+        if m>=0 and (i>=m or j>=n): return ('range',ln)
+        seen=True; obs.append((j,i,v))
+    if m<0:
+        if not obs: return ('inval',0)
+        m=max(o[1] for o in obs)+1; n=max(o[0] for o in obs)+1
+    obs.sort(key=lambda o:(o[0],o[1]))
+    for a,b in zip(obs,obs[1:]):
+        if a[0]==b[0] and a[1]==b[1]: return ('inval',0)
+    return ('ok',(m,n,[(i,j,v) for j,i,v in obs]))
+
+
+def _fuzz_ours(text, one_based):
+    try:
+        o = P.parse_triplets(text, one_based)
+        return ('ok', (o.m, o.n, entries(o)))
+    except P.ParseError as e:
+        return ('parse', e.line)
+    except IndexError as e:
+        return ('range', int(re.match(r'line (\d+)', str(e)).group(1)))
+    except ValueError:
+        return ('inval', 0)
+
+
+def test_fuzz_error_class_and_line_match_restatement():
+    """Random small inputs built from valid and malformed fragments: the same outcome (matrix,
+    or error class and line number) as load_triplets' istream logic (matrix_io.hpp:127-170)."""
+    random.seed(1)
+    frag = ['0', '1', '2', '3', '7', '-1', '+2', '1.5', '-.5', '2.', '1e2', '1e', 'x', '%', '% 4 4', '% 3', '  ',
+            '\t', '9 9', 'inf', '0x1', '1e400', '3 3 3', '4 0 1 z', '']
+    for _ in range(4000):
+        lines = []
+        for _ in range(random.randint(0, 6)):
+            k = random.randint(0, 4)
+            sep = random.choice([' ', '\t', '']) if random.random() < 0.5 else ' '
+            lines.append(sep.join(random.choice(frag) for _ in range(k)))
+        text = '\n'.join(lines) + random.choice(['', '\n'])
+        ob = random.random() < 0.3
+        assert _fuzz_ref(text, ob) == _fuzz_ours(text, ob), repr(text)
